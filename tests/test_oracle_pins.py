@@ -1,0 +1,599 @@
+"""Pins of the CPU oracle against values fixed by the paper / SPEC worked examples, closed
+forms, invariants and brute force (task rule ③).  Pure CPU; no GPU.
+
+Each test names the pin (SURVEY §8(c) "What pins each part", P1..P19) and the passage.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+
+def one(pos, log_scale=(math.log(0.05),) * 3, rot=(1, 0, 0, 0), logit=0.0, sh=None):
+    sh = np.zeros((1, 16, 3)) if sh is None else np.asarray(sh, np.float64).reshape(1, 16, 3)
+    return synth.Scene(np.array([pos], np.float32), np.array([log_scale], np.float32),
+                       np.array([rot], np.float32), np.array([logit], np.float32),
+                       sh.astype(np.float32))
+
+
+CAM100 = synth.identity_camera(100, 100, 32, 32, 64, 64)
+
+
+# ---------------------------------------------------------------- R10 exp
+def test_exp_rn_accuracy():
+    """R10: exp_rn is within ~1 ulp of exp (Cephes-quality) over the clamp range."""
+    xs = np.linspace(-80, 80, 20001).astype(np.float32)
+    got = np.array([oracle.exp_rn(float(x)) for x in xs[::7]], np.float64)
+    ref = np.exp(xs[::7].astype(np.float64))
+    ulp = np.spacing(got.astype(np.float32)).astype(np.float64)
+    assert np.max(np.abs(got - ref) / ulp) < 1.5
+    assert oracle.exp_rn(0.0) == 1.0
+
+
+# ---------------------------------------------------------------- P1, P2
+@pytest.mark.parametrize("which", ["f32", "f64"])
+def test_p1_p2_on_axis_isotropic(which):
+    sc = one((0, 0, 5))
+    if which == "f32":
+        mb = oracle.membership(sc, CAM100)
+        assert mb["vis"][0] == 1
+        assert (mb["mx"][0], mb["my"][0], mb["depth"][0]) == (32.0, 32.0, 5.0)
+        a, b, c = mb["cov"][0]
+        r = mb["radius"][0]
+    else:
+        out, _ = oracle.project64(sc, CAM100)
+        assert out[0, 0] == 1 and abs(out[0, 1] - 32) < 1e-12 and abs(out[0, 3] - 5) < 1e-12
+        a, b, c, r = out[0, 4], out[0, 5], out[0, 6], out[0, 15]
+    # (fx s / z)^2 + 0.3 = (100*0.05/5)^2 + 0.3 = 1.3
+    assert abs(a - 1.3) < 2e-6 and abs(c - 1.3) < 2e-6 and abs(b) < 1e-7
+    assert r == 4  # ceil(3 sqrt(1.3)) = ceil(3.42)
+
+
+# ---------------------------------------------------------------- P3 axis-aligned
+def test_p3_axis_aligned_independent_of_sz():
+    for sz in (0.001, 0.05, 0.3):
+        sc = one((0, 0, 4), (math.log(0.02), math.log(0.06), math.log(sz)))
+        out, _ = oracle.project64(sc, CAM100)
+        sx, sy = (math.exp(float(np.float32(math.log(v)))) for v in (0.02, 0.06))
+        assert abs(out[0, 4] - ((100 * sx / 4) ** 2 + 0.3)) < 1e-12
+        assert abs(out[0, 6] - ((100 * sy / 4) ** 2 + 0.3)) < 1e-12
+        assert abs(out[0, 5]) < 1e-12
+
+
+# ---------------------------------------------------------------- P4 isotropic off-axis
+def test_p4_isotropic_off_axis_closed_form():
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        x, y, z, s = rng.uniform(-1, 1), rng.uniform(-1, 1), rng.uniform(2, 6), rng.uniform(.01, .1)
+        fx, fy = 80.0, 120.0
+        cam = synth.identity_camera(fx, fy, 500, 500, 1000, 1000)
+        sc = one((x, y, z), (math.log(s),) * 3, rot=tuple(rng.normal(size=4)))
+        xf, yf, zf = (float(np.float32(v)) for v in (x, y, z))
+        sf = math.exp(float(np.float32(math.log(s))))
+        out, _ = oracle.project64(sc, cam)
+        a = sf ** 2 * fx ** 2 / zf ** 2 * (1 + xf ** 2 / zf ** 2) + 0.3
+        b = sf ** 2 * fx * fy * xf * yf / zf ** 4
+        c = sf ** 2 * fy ** 2 / zf ** 2 * (1 + yf ** 2 / zf ** 2) + 0.3
+        np.testing.assert_allclose(out[0, 4:7], [a, b, c], rtol=1e-9, atol=1e-12)
+        # and the fp32 chain agrees to fp32 rounding
+        mb = oracle.membership(sc, cam)
+        np.testing.assert_allclose(mb["cov"][0], [a, b, c], rtol=2e-5, atol=1e-6)
+
+
+# ---------------------------------------------------------------- P5 culling
+def test_p5_culling():
+    for pos in [(0, 0, -1), (0, 0, 0.005), (1000, 0, 5), (0, -50, 5)]:
+        sc = one(pos)
+        assert oracle.membership(sc, CAM100)["vis"][0] == 0
+        assert oracle.project64(sc, CAM100)[0][0, 0] == 0
+
+
+# ---------------------------------------------------------------- P6 SH
+def _sh_Y(dirs):
+    """Y_k(dir) recovered from the oracle's colour: set one coefficient to 0.1."""
+    n = len(dirs)
+    Y = np.zeros((n, 16))
+    cam = synth.identity_camera(100, 100, 32, 32, 64, 64)
+    for k in range(16):
+        sh = np.zeros((n, 16, 3))
+        sh[:, k, 0] = 0.1
+        sc = synth.Scene(dirs.astype(np.float32) * 3, np.zeros((n, 3), np.float32),
+                         np.tile(np.array([1, 0, 0, 0], np.float32), (n, 1)),
+                         np.zeros(n, np.float32), sh.astype(np.float32))
+        out, _ = oracle.project64(sc, cam)
+        pos = sc.pos.astype(np.float64)
+        assert np.all(out[:, 14] == 0)
+        Y[:, k] = (out[:, 11] - 0.5) / 0.1
+    return Y, pos / np.linalg.norm(pos, axis=1, keepdims=True)
+
+
+def test_p6_sh_constants_and_zero():
+    sc = one((0.3, -0.2, 4))
+    assert np.allclose(oracle.project64(sc, CAM100)[0][0, 11:14], 0.5, atol=1e-15)
+    sh = np.zeros((16, 3))
+    sh[0] = [0.7, -0.3, 1.1]
+    out = oracle.project64(one((0.3, -0.2, 4), sh=sh), CAM100)[0][0]
+    np.testing.assert_allclose(out[11:14], 0.5 + 0.28209479177387814 * sh[0], atol=1e-6)
+
+
+def test_p6_sh_gram_and_parity():
+    """Quadrature: Gauss-Legendre (cos theta) x uniform phi is exact for degree <= 6,
+    so the Gram matrix of the 16 basis functions must be the identity; Y(-d)=(-1)^l Y(d)."""
+    xg, wg = np.polynomial.legendre.leggauss(12)
+    nphi = 24
+    phi = 2 * np.pi * np.arange(nphi) / nphi
+    ct, ph = np.meshgrid(xg, phi, indexing="ij")
+    st = np.sqrt(1 - ct ** 2)
+    d = np.stack([st * np.cos(ph), st * np.sin(ph), ct], -1).reshape(-1, 3)
+    # positions are stored in float32: use the float32 direction actually rendered
+    Y, dd = _sh_Y(d)
+    w = (wg[:, None] * np.full(nphi, 2 * np.pi / nphi)[None, :]).reshape(-1)
+    # directions are float32-rounded; recompute weights' error budget ~1e-6
+    gram = (Y * w[:, None]).T @ Y
+    assert np.max(np.abs(gram - np.eye(16))) < 1e-5
+    Yn, _ = _sh_Y(-d)
+    lvals = np.array([0, 1, 1, 1, 2, 2, 2, 2, 2, 3, 3, 3, 3, 3, 3, 3])
+    np.testing.assert_allclose(Yn, Y * (-1.0) ** lvals, atol=1e-6)
+
+
+# ---------------------------------------------------------------- P7 tile membership
+def test_p7_rect_single_and_corner():
+    # minimum radius is ceil(3 sqrt(0.3)) = 2 (dilation): r=2 centred at (8,8) -> tile (0,0)
+    cam = synth.identity_camera(100, 100, 8, 8, 64, 64)
+    sc = one((0, 0, 5), (math.log(0.001),) * 3)
+    mb = oracle.membership(sc, cam)
+    assert mb["radius"][0] == 2 and list(mb["rect"][0]) == [0, 0, 0, 0]
+    cam = synth.identity_camera(100, 100, 16, 16, 64, 64)
+    mb = oracle.membership(sc, cam)
+    assert list(mb["rect"][0]) == [0, 1, 0, 1]
+
+
+def test_p7_rect_equals_pixel_bruteforce():
+    """Tile t is in rect iff some integer pixel of t (px in [16t, 16t+15]) lies within the
+    square |px - m| <= r (R1 pixel centres, R2), clipped to the tile grid."""
+    sc = synth.scene_c0(3)
+    cam = synth.cameras_c0()[0]
+    mb = oracle.membership(sc, cam)
+    Wt = Ht = 4
+    for i in range(sc.n):
+        m = (float(mb["mx"][i]), float(mb["my"][i]))
+        r = float(mb["radius"][i])
+        if not mb["vis"][i]:
+            if mb["radius"][i] == 0:
+                continue
+        tiles = set()
+        for ty in range(Ht):
+            for tx in range(Wt):
+                okx = any(abs(px - m[0]) <= r for px in range(16 * tx, 16 * tx + 16)) if mb["vis"][i] else False
+                oky = any(abs(py - m[1]) <= r for py in range(16 * ty, 16 * ty + 16)) if mb["vis"][i] else False
+                if okx and oky:
+                    tiles.add((tx, ty))
+        tx0, tx1, ty0, ty1 = mb["rect"][i]
+        want = {(tx, ty) for tx in range(tx0, tx1 + 1) for ty in range(ty0, ty1 + 1)}
+        assert tiles == want, i
+
+
+# ---------------------------------------------------------------- P8 / O11 lists
+def test_p8_depth_order_and_stable_sort():
+    sc = synth.scene_c0(0)
+    cams = synth.cameras_c0()
+    recs = oracle.make_records(sc, cams)
+    off, ent = oracle.tile_lists(recs, 0, 16, 4, 4)
+    # library routine: lexsort by (block, depth, gid) over brute-force (record, block) pairs
+    pairs = []
+    for j in range(recs.n):
+        _, v, tx0, tx1, ty0, ty1 = recs.rec_i[j]
+        for ty in range(ty0, ty1 + 1):
+            for tx in range(tx0, tx1 + 1):
+                pairs.append((ty * 4 + tx, recs.rec_f[j, 2], recs.rec_i[j, 0], j))
+    pairs = np.array(pairs)
+    order = np.lexsort((pairs[:, 2], pairs[:, 1], pairs[:, 0]))
+    np.testing.assert_array_equal(ent, pairs[order, 3].astype(np.int64))
+    np.testing.assert_array_equal(np.diff(off), np.bincount(pairs[:, 0].astype(int), minlength=16))
+
+
+def test_p8_two_depths():
+    sc = synth.Scene(np.array([[0, 0, 2.0], [0, 0, 1.0]], np.float32), np.full((2, 3), math.log(0.01), np.float32),
+                     np.tile(np.array([1, 0, 0, 0], np.float32), (2, 1)), np.zeros(2, np.float32),
+                     np.zeros((2, 16, 3), np.float32))
+    recs = oracle.make_records(sc, [CAM100])
+    off, ent = oracle.tile_lists(recs, 0, 16, 4, 4)
+    blk = 2 * 4 + 2
+    assert list(recs.rec_i[ent[off[blk]:off[blk + 1]], 0]) == [1, 0]
+
+
+def test_p8_permutation_invariance():
+    sc = synth.scene_c0(1)
+    cams = synth.cameras_c0()
+    perm = np.random.default_rng(5).permutation(sc.n)
+    sp = synth.Scene(sc.pos[perm], sc.log_scale[perm], sc.rot[perm], sc.opac_logit[perm], sc.sh[perm])
+    # gids follow the permutation (tie-break by gid is then also permuted) -> same image
+    # up to ties; C0 has no depth ties, so the images are bit-identical.
+    f0 = oracle.render_batch(sc, cams)[3]
+    f1 = oracle.render_batch(sp, cams)[3]
+    np.testing.assert_array_equal(f0["c"], f1["c"])
+
+
+# ---------------------------------------------------------------- P9 compositing
+def _stack(alphas_o, rgbs, W=16, H=16, pix=(5, 5), bg=(0, 0, 0)):
+    """Hand-built records centred exactly on pixel `pix` (G = 1 there), depth order given."""
+    n = len(alphas_o)
+    rec_f = np.zeros((n, 10))
+    rec_f[:, 0], rec_f[:, 1] = pix
+    rec_f[:, 2] = np.arange(1, n + 1, dtype=np.float64)
+    rec_f[:, 3] = rec_f[:, 5] = 1.0
+    rec_f[:, 6] = alphas_o
+    rec_f[:, 7:10] = rgbs
+    rec_i = np.zeros((n, 6), np.int64)
+    rec_i[:, 0] = np.arange(n)
+    rec_i[:, 3] = rec_i[:, 5] = 0
+    recs = oracle.Records(rec_f, rec_i, None, None)
+    off, ent = oracle.tile_lists(recs, 0, 1, 1, 1)
+    f = oracle.render_fwd(recs, off, ent, 0, 1, W, H, bg)
+    p = pix[1] * 16 + pix[0]
+    return f["c"][0, p], f["T"][0, p], f["nlast"][0, p], f
+
+
+def test_p9a_empty():
+    recs = oracle.Records(np.zeros((0, 10)), np.zeros((0, 6), np.int64), None, None)
+    f = oracle.render_fwd(recs, np.zeros(2, np.int64), np.zeros(0, np.int64), 0, 1, 16, 16, (0.2, 0.5, 0.8))
+    assert np.all(f["c"][0] == [0.2, 0.5, 0.8]) and np.all(f["T"][0] == 1)
+
+
+def test_p9b_single_centre():
+    c, T, nl, _ = _stack([0.6], [[0.2, 0.4, 1.0]])
+    np.testing.assert_allclose(c, 0.6 * np.array([0.2, 0.4, 1.0]), atol=1e-15)
+    assert nl == 1 and abs(T - 0.4) < 1e-15
+
+
+def test_p9c_stop_rule():
+    """alpha = (0.99, 0.1, 0.99), grey levels (0, 0, 1): 0.0 under R3 (stop before
+    compositing); SPEC's literal reading would give 0.00891."""
+    c, T, nl, f = _stack([0.99, 0.1, 0.99], [[0] * 3, [0] * 3, [1] * 3])
+    assert np.all(c == 0.0) and nl == 2
+    assert abs(T - 0.01 * 0.9) < 1e-15
+    assert f["counts"][0, 5 * 16 + 5, 3] == 1
+
+
+def test_p9d_cap_and_p9e_threshold():
+    c, T, _, _ = _stack([1.0], [[1, 1, 1]])
+    np.testing.assert_allclose(c, 0.99, atol=1e-15)
+    c, T, nl, _ = _stack([1 / 255 * 0.999], [[1, 1, 1]])
+    assert np.all(c == 0) and T == 1 and nl == 0
+
+
+def test_p9f_two_term():
+    c, _, _, _ = _stack([0.5, 1.0], [[1, 0, 0], [0, 0, 1]])
+    np.testing.assert_allclose(c, [0.5, 0, 0.495], atol=1e-15)
+
+
+def test_p10_energy_bound():
+    rng = np.random.default_rng(3)
+    n = 300
+    rec_f = np.zeros((n, 10))
+    rec_f[:, 0:2] = rng.uniform(0, 32, (n, 2))
+    rec_f[:, 2] = rng.uniform(1, 5, n)
+    rec_f[:, 3] = rec_f[:, 5] = rng.uniform(0.05, 1, n)
+    rec_f[:, 4] = 0
+    rec_f[:, 6] = rng.uniform(0, 1, n)
+    rec_f[:, 7:10] = rng.uniform(0, 1, (n, 3))
+    rec_i = np.zeros((n, 6), np.int64)
+    rec_i[:, 0] = np.arange(n)
+    rec_i[:, 3] = rec_i[:, 5] = 1
+    recs = oracle.Records(rec_f, rec_i, None, None)
+    off, ent = oracle.tile_lists(recs, 0, 4, 2, 2)
+    f = oracle.render_fwd(recs, off, ent, 0, 4, 32, 32)
+    assert f["c"].min() >= 0 and f["c"].max() <= 1
+
+
+# ---------------------------------------------------------------- P11/P16 exchange sets (O10)
+def test_p16_exchange_sets_and_partition():
+    sc = synth.scene_c0(0)
+    cams = synth.cameras_c0()
+    mb = oracle.membership(sc, cams[0])
+    B = 16
+    full = oracle.make_records(sc, cams)
+    offf, entf = oracle.tile_lists(full, 0, B, 4, 4)
+    rng = np.random.default_rng(1)
+    for G in (1, 2, 4, 8, 16):
+        cuts = np.sort(rng.integers(0, B + 1, G - 1))
+        dp = np.concatenate([[0], cuts, [B]]).astype(np.int64)
+        mask = oracle.exchange_sets(mb["vis"], mb["rect"], 0, 4, 4, dp)
+        if G == 1:
+            assert np.all(mask[mb["vis"] == 1] == 1)
+        # no false deliveries, completeness: per rank, records sent to g give the same lists
+        for g in range(G):
+            sent = np.nonzero(mask >> g & 1)[0]
+            for i in sent:
+                tx0, tx1, ty0, ty1 = mb["rect"][i]
+                blocks = [ty * 4 + tx for ty in range(ty0, ty1 + 1) for tx in range(tx0, tx1 + 1)]
+                assert any(dp[g] <= b < dp[g + 1] for b in blocks)
+            sel = np.isin(full.rec_i[:, 0], sent)
+            sub = oracle.Records(full.rec_f[sel], full.rec_i[sel], None, None)
+            off, ent = oracle.tile_lists(sub, dp[g], dp[g + 1], 4, 4)
+            ids = np.nonzero(sel)[0]
+            for k in range(dp[g], dp[g + 1]):
+                a = ids[ent[off[k - dp[g]]:off[k - dp[g] + 1]]]
+                np.testing.assert_array_equal(a, entf[offf[k]:offf[k + 1]])
+        # conservation: total deliveries = sum_i |D(i)|, and below the dense bound G*N
+        tot = sum(int(np.sum(mask >> g & 1)) for g in range(G))
+        assert tot == sum(bin(int(m)).count("1") for m in mask)
+        assert tot <= G * sc.n
+
+
+# ---------------------------------------------------------------- P12 render backward FD
+def _fd_scene(seed, n=8, opaque=False):
+    rng = np.random.default_rng(seed)
+    rec_f = np.zeros((n, 10))
+    rec_f[:, 0:2] = rng.uniform(2, 14, (n, 2))
+    rec_f[:, 2] = rng.permutation(n) + 1.0
+    L = rng.normal(0, 0.15, (n, 2, 2)) + np.eye(2) * 0.3
+    con = L @ L.transpose(0, 2, 1)
+    rec_f[:, 3], rec_f[:, 4], rec_f[:, 5] = con[:, 0, 0], con[:, 0, 1], con[:, 1, 1]
+    rec_f[:, 6] = rng.uniform(0.5, 0.98, n) if opaque else rng.uniform(0.1, 0.9, n)
+    rec_f[:, 7:10] = rng.uniform(0, 1, (n, 3))
+    rec_i = np.zeros((n, 6), np.int64)
+    rec_i[:, 0] = np.arange(n)
+    return oracle.Records(rec_f, rec_i, None, None)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_p12_render_bwd_finite_difference(seed):
+    recs = _fd_scene(seed, opaque=seed % 2 == 1)
+    bg = (0.2, 0.5, 0.8)
+    off, ent = oracle.tile_lists(recs, 0, 1, 1, 1)
+    w = synth.upstream_grad(seed, (1, 256, 3)).astype(np.float64)
+    base = oracle.render_fwd(recs, off, ent, 0, 1, 16, 16, bg)
+    g = oracle.render_bwd(recs, off, ent, 0, 1, 16, 16, w, bg)
+    checked = 0
+    for j in range(recs.n):
+        for k in range(9):
+            col = [0, 1, 3, 4, 5, 6, 7, 8, 9][k]
+            h = 1e-6 * max(1.0, abs(recs.rec_f[j, col]))
+            vals = []
+            ok = True
+            for sgn_ in (1, -1):
+                rf = recs.rec_f.copy()
+                rf[j, col] += sgn_ * h
+                r2 = oracle.Records(rf, recs.rec_i, None, None)
+                f = oracle.render_fwd(r2, off, ent, 0, 1, 16, 16, bg)
+                if not (np.array_equal(f["nlast"], base["nlast"]) and np.array_equal(f["counts"], base["counts"])):
+                    ok = False  # probe crosses a discontinuity (1/255 skip, T cut-off, cap)
+                vals.append(np.sum(f["c"] * w))
+            if not ok:
+                continue
+            fd = (vals[0] - vals[1]) / (2 * h)
+            assert abs(fd - g[j, k]) <= 1e-5 * max(abs(fd), 1e-3) + 1e-7, (j, k, fd, g[j, k])
+            checked += 1
+    assert checked > 30
+
+
+def test_p12_zero_upstream_and_occluded():
+    recs = _fd_scene(4)
+    off, ent = oracle.tile_lists(recs, 0, 1, 1, 1)
+    assert np.all(oracle.render_bwd(recs, off, ent, 0, 1, 16, 16, np.zeros((1, 256, 3))) == 0)
+    # a fully opaque wall in front stops every pixel before the Gaussians behind it
+    n = 4
+    rec_f = np.zeros((n, 10))
+    rec_f[:, 0:2] = 8.0
+    rec_f[:, 2] = [1, 2, 3, 4]
+    rec_f[:2, 3] = rec_f[:2, 5] = 1e-6  # huge flat walls -> alpha 0.99 everywhere
+    rec_f[2:, 3] = rec_f[2:, 5] = 0.1
+    rec_f[:, 6] = 1.0
+    rec_f[:, 7:] = 0.5
+    rec_i = np.zeros((n, 6), np.int64)
+    rec_i[:, 0] = np.arange(n)
+    r = oracle.Records(rec_f, rec_i, None, None)
+    off, ent = oracle.tile_lists(r, 0, 1, 1, 1)
+    g = oracle.render_bwd(r, off, ent, 0, 1, 16, 16, np.ones((1, 256, 3)))
+    assert np.all(g[2:] == 0) and np.any(g[:2] != 0)
+
+
+# ---------------------------------------------------------------- P13 projection backward FD
+def _small_scene(seed, n=12):
+    rng = np.random.default_rng(seed)
+    sc = synth.Scene(np.stack([rng.uniform(-1, 1, n), rng.uniform(-1, 1, n), rng.uniform(3, 5, n)], 1),
+                     math.log(0.1) + rng.normal(0, 0.4, (n, 3)), rng.normal(0, 1, (n, 4)),
+                     rng.normal(0, 1, n), rng.normal(0, 0.3, (n, 16, 3)))
+    return sc  # float64 arrays (project64 / project_bwd take fp64 parameters)
+
+
+def _cams2():
+    return [synth.look_at((0.3, -0.2, 0.0), (0, 0, 4), (0, -1, 0), 60, 70, 64, 64),
+            synth.look_at((-0.5, 0.4, 0.5), (0.1, 0, 4), (0, -1, 0), 55, 55, 64, 48)]
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_p13_project_bwd_finite_difference(seed):
+    sc = _small_scene(seed)
+    cams = _cams2()
+    rng = np.random.default_rng(100 + seed)
+    fields = [1, 2, 7, 8, 9, 10, 11, 12, 13]  # mx my A B C opacity r g b
+    W = rng.normal(0, 1, (len(cams), sc.n, 9))
+
+    def loss(s):
+        tot = 0.0
+        for v, cam in enumerate(cams):
+            out, _ = oracle.project64(s, cam)
+            vis = out[:, 0] > 0
+            tot += np.sum((out[:, fields] * W[v])[vis])
+        return tot
+
+    gv = np.zeros((len(cams), sc.n, 9))
+    for v, cam in enumerate(cams):
+        out, _ = oracle.project64(sc, cam)
+        gv[v][out[:, 0] > 0] = W[v][out[:, 0] > 0]
+    recs_vi = []
+    for v in range(len(cams)):
+        for i in range(sc.n):
+            recs_vi.append((v, i))
+    recs = oracle.Records(None, None, np.array(recs_vi), None)
+    g = oracle.project_bwd(sc, cams, recs, gv.reshape(-1, 9))
+    flat = oracle.flatten_params(sc)
+    checked = 0
+    for i in range(sc.n):
+        for k in range(59):
+            h = 1e-6 * max(1.0, abs(flat[i, k]))
+
+            def setp(delta):
+                f = flat.copy()
+                f[i, k] += delta
+                return synth.Scene(f[:, 0:3], f[:, 3:6], f[:, 6:10], f[:, 10], f[:, 11:].reshape(-1, 16, 3))
+            fd = (loss(setp(h)) - loss(setp(-h))) / (2 * h)
+            assert abs(fd - g[i, k]) <= 1e-5 * max(abs(fd), abs(g[i, k])) + 2e-6 * max(1, np.abs(g[i]).max()), (i, k, fd, g[i, k])
+            checked += 1
+    assert checked == sc.n * 59
+
+
+def test_p13_degree0_dc_gradient():
+    sc = _small_scene(7, n=3)
+    cam = _cams2()[0]
+    gv = np.zeros((1, 3, 9))
+    gv[0, :, 6:9] = [[1.0, 2.0, -3.0]] * 3
+    recs = oracle.Records(None, None, np.array([(0, i) for i in range(3)]), None)
+    out, _ = oracle.project64(sc, cam)
+    g = oracle.project_bwd(sc, [cam], recs, gv.reshape(-1, 9))
+    for i in range(3):
+        if out[i, 0] > 0:
+            want = 0.28209479177387814 * np.array([1.0, 2.0, -3.0]) * (1 - (int(out[i, 14]) >> np.arange(3) & 1))
+            np.testing.assert_allclose(g[i, 11:14], want, rtol=1e-14)
+
+
+# ---------------------------------------------------------------- P14 Adam (Eq. 1-2)
+def test_p14_scaling_rules():
+    th = np.array([1.0])
+    g = np.array([0.3])
+    # b=4, lr=0.0025 -> lr' = 0.005 (Eq. 1): first step is -lr' * sign(g) up to eps
+    t, m, v = oracle.adam(th, np.zeros(1), np.zeros(1), g, 0.0025, batch=4)
+    assert abs((t[0] - 1.0) + 0.005) < 1e-12
+    # beta1=0.9, b=2 -> 0.81 (Eq. 2): m = (1 - 0.81) g
+    t, m, v = oracle.adam(th, np.zeros(1), np.zeros(1), g, 0.001, batch=2)
+    assert abs(m[0] - 0.19 * 0.3) < 1e-15
+    assert abs(v[0] - (1 - 0.999 ** 2) * 0.09) < 1e-15
+    # zero gradient from a fresh state leaves parameters unchanged
+    t, m, v = oracle.adam(np.array([2.0, -1.0]), np.zeros(2), np.zeros(2), np.zeros(2), 0.1, batch=3)
+    assert np.all(t == [2.0, -1.0])
+
+
+@pytest.mark.parametrize("batch", [1, 4, 16])
+def test_p14_matches_torch_adam(batch):
+    import torch
+    rng = np.random.default_rng(batch)
+    theta = rng.normal(size=50)
+    lr = 1.6e-4
+    p = torch.tensor(theta, dtype=torch.float64, requires_grad=True)
+    opt = torch.optim.Adam([p], lr=lr * math.sqrt(batch), betas=(0.9 ** batch, 0.999 ** batch), eps=1e-15)
+    th, m, v = theta.copy(), np.zeros(50), np.zeros(50)
+    for step in range(1, 6):
+        g = rng.normal(size=50) * 1e-3
+        p.grad = torch.tensor(g)
+        opt.step()
+        th, m, v = oracle.adam(th, m, v, g, lr, batch=batch, step=step)
+    np.testing.assert_allclose(th, p.detach().numpy(), rtol=1e-12, atol=1e-15)
+
+
+# ---------------------------------------------------------------- P15 Algorithm 1
+@pytest.mark.parametrize("et,G,want", [
+    ([1, 1, 1, 1], 2, [0, 2, 4]),
+    ([3, 1, 1, 1, 2], 2, [0, 2, 5]),
+    ([5, 1, 1, 1], 2, [0, 0, 4]),
+    ([4, 2, 7], 1, [0, 3]),
+    ([0, 0, 1, 1], 2, [0, 3, 4]),
+    ([0, 0, 0, 0, 0], 2, [0, 2, 5]),
+])
+def test_p15_traces(et, G, want):
+    assert list(oracle.division_points(et, G)) == want
+
+
+def test_p15_random_load_bound():
+    """Load bound max_g load <= tot/G + max(ET), monotone DP, and DP[g] is the
+    largest prefix whose cumulative cost stays within g*tot/G (exact rational check)."""
+    rng = np.random.default_rng(0)
+    from fractions import Fraction
+    for _ in range(2000):
+        B, G = int(rng.integers(1, 257)), int(rng.integers(1, 17))
+        et = rng.integers(0, 1000, B) * (rng.random(B) < 0.8)
+        dp = oracle.division_points(et, G)
+        assert dp[0] == 0 and dp[-1] == B and np.all(np.diff(dp) >= 0)
+        ct = np.cumsum(et)
+        tot = int(ct[-1]) if B else 0
+        if tot == 0:
+            continue
+        loads = [int(et[dp[g]:dp[g + 1]].sum()) for g in range(G)]
+        assert max(loads) <= Fraction(tot, G) + int(et.max())
+        for g in range(1, G):
+            th = Fraction(g * tot, G)
+            k = int(dp[g])
+            assert (k == 0 or ct[k - 1] <= th) and (k == B or ct[k] > th)
+
+
+# ---------------------------------------------------------------- P18 cost modes
+def test_p18_paper_avg():
+    dp = np.array([0, 2, 4])
+    et = oracle.costs_to_et(2, dp, [1500, 500, 700, 300], [256, 256, 256, 256])
+    assert list(et) == [1000, 1000, 500, 500]
+    assert list(oracle.costs_to_et(1, dp, [1, 2, 3, 4], [256] * 4)) == [1, 2, 3, 4]
+
+
+# ---------------------------------------------------------------- P19 L1 loss
+def test_p19_l1():
+    recs = oracle.Records(np.zeros((0, 10)), np.zeros((0, 6), np.int64), None, None)
+    off = np.zeros(2, np.int64)
+    gt = np.full((1, 16, 16, 3), 255, np.uint8)
+    f = oracle.render_fwd(recs, off, np.zeros(0, np.int64), 0, 1, 16, 16, (1, 1, 1), gt)
+    assert f["loss"] == 0 and np.all(f["dl_dc"] == 0)
+    gt = np.zeros((1, 16, 16, 3), np.uint8)
+    f = oracle.render_fwd(recs, off, np.zeros(0, np.int64), 0, 1, 16, 16, (0.5, 0.5, 0.5), gt)
+    assert abs(f["loss"] - 0.5) < 1e-12
+    assert np.allclose(f["dl_dc"], 1 / (3 * 256))
+
+
+# ---------------------------------------------------------------- C0 calibration
+def test_c0_shape():
+    sc = synth.scene_c0(0)
+    mb = oracle.membership(sc, synth.cameras_c0()[0])
+    assert 950 <= mb["vis"].sum() <= 1000
+    r = mb["radius"][mb["vis"] == 1]
+    assert 3 <= np.median(r) <= 10
+    # fp32 chain vs fp64: same visibility and means to fp32 rounding
+    out, _ = oracle.project64(sc, synth.cameras_c0()[0])
+    same = (out[:, 0] > 0) == (mb["vis"] == 1)
+    assert same.mean() > 0.99
+    v = mb["vis"] == 1
+    np.testing.assert_allclose(mb["mx"][v], out[v, 1], rtol=1e-5, atol=1e-4)
+
+
+# ---------------------------------------------------------------- golden fixtures
+def _golden():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")) as f:
+        return json.load(f)
+
+
+def test_golden_worked_examples():
+    g = _golden()
+    for ex in g["division_points"]:
+        assert list(oracle.division_points(ex["ET"], ex["G"])) == ex["DP"], ex["cite"]
+    ex = g["adam_scaling"][0]
+    t, _, _ = oracle.adam(np.array([0.0]), np.zeros(1), np.zeros(1), np.array([1.0]), ex["lr"], batch=ex["batch"])
+    assert abs(-t[0] - ex["lr_scaled"]) < 1e-12, ex["cite"]
+    ex = g["adam_scaling"][1]
+    _, m, _ = oracle.adam(np.array([0.0]), np.zeros(1), np.zeros(1), np.array([1.0]), 0.1, beta1=ex["beta1"], batch=ex["batch"])
+    assert abs(m[0] - (1 - ex["beta1_scaled"])) < 1e-15, ex["cite"]
+    for ex in g["projection"]:
+        sc = one(tuple(ex["pos"]), (math.log(ex.get("scale", 0.05)),) * 3)
+        cam = synth.identity_camera(ex["fx"], ex["fx"], ex["cx"], ex["cx"], 64, 64)
+        mb = oracle.membership(sc, cam)
+        if "mean2d" in ex:
+            assert [float(mb["mx"][0]), float(mb["my"][0])] == ex["mean2d"] and mb["depth"][0] == ex["depth"]
+        if "radius" in ex:
+            assert mb["radius"][0] == ex["radius"], ex["cite"]
+    for ex in g["compositing"]:
+        if not ex["alphas"]:
+            continue
+        c, _, _, _ = _stack(ex["alphas"], ex["rgb"])
+        np.testing.assert_allclose(c, ex["C"], atol=1e-15, err_msg=ex["cite"])
