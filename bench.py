@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""Benchmark: train views/s of the Grendel 3DGS training step on B200 (BASELINE.json metric
+"train views/sec at 1/2/4/8 B200 (Rubble-shaped 4K); fwd+bwd raster ms/view").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl libgs|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+One step = the whole hot path (A1-A9: project, exchange, bin+sort, render fwd + fused L1,
+render bwd, reverse exchange, transformation backward + Adam, rebalance) over one batch of b
+views of a synthetic, seeded scene (synth/, recipe in DESIGN.md §3).  `value` is whole-job
+views/s with inputs resident in HBM, timed by CUDA events on the step stream between a barrier
++ synchronize, max over ranks.  `e2e` repeats the timed loop through the same public API with
+each step's ground-truth batch copied host(pinned)->device and the loss copied back.
+Inputs (11.2M Gaussians x 3 states, 0.76 GB ground truth per batch) are far larger than L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+CONFIGS = {
+    "C0": dict(workload="C0 tiny: 1,000 Gaussians, 64x64, batch 1", n=1000, b=1, pool=1, seed=0),
+    "C1": dict(workload="Mip-NeRF360-garden-shaped: 5M Gaussians, 1920x1080, batch 4", n=5_000_000, b=4,
+               pool=64, seed=1),
+    "C2": dict(workload="Rubble-shaped: 11.2M Gaussians, 4591x3436, batch 16", n=11_200_000, b=16, pool=64,
+               seed=2),
+    "C3": dict(workload="Rubble-shaped 40.4M Gaussians, 4591x3436, batch 16", n=40_400_000, b=16, pool=64,
+               seed=3),
+    "C4": dict(workload="MatrixCity-shaped: 24M Gaussians, 1920x1080 street+aerial, batch 32", n=24_000_000,
+               b=32, pool=128, seed=4),
+}
+METRIC = "train views/sec at 1/2/4/8 B200 (Rubble-shaped 4K); fwd+bwd raster ms/view"
+
+# Roofline census (frozen): FP32-pipe lane-operations per evaluation.
+CENSUS = dict(fwd_comp=13, fwd_skip=8, fwd_stop=9, bwd_contrib=41, bwd_skip=8)
+
+
+def make_scene(cfg, lo, hi):
+    n, seed = cfg["n"], cfg["seed"]
+    if cfg is CONFIGS["C0"]:
+        return synth.scene_c0(seed).slice(lo, hi)
+    fn = {1: synth.scene_garden, 2: synth.scene_rubble, 3: synth.scene_rubble, 4: synth.scene_city}[seed]
+    return fn(n, seed, lo, hi)
+
+
+def make_cameras(cfg):
+    seed = cfg["seed"]
+    if seed == 0:
+        return synth.cameras_c0()
+    if seed in (2, 3):
+        return synth.cameras_rubble(cfg["pool"], seed)
+    if seed == 1:
+        return synth.cameras_garden(cfg["pool"], seed)
+    return synth.cameras_city(cfg["pool"], seed)
+
+
+def batches(cfg, steps):
+    if cfg["seed"] == 4:  # C4: 16 street + 16 aerial per batch
+        half = cfg["pool"] // 2
+        st = synth.batch_schedule(half, cfg["b"] // 2, steps, cfg["seed"])
+        ae = synth.batch_schedule(half, cfg["b"] // 2, steps, cfg["seed"] + 1)
+        return [s + [half + a for a in x] for s, x in zip(st, ae)]
+    return synth.batch_schedule(cfg["pool"], cfg["b"], steps, cfg["seed"])
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        rows = []
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            try:
+                rows.append((float(f[0]), float(f[1]), f[3:7]))
+            except Exception:
+                pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [r[0] for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[2][k].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d, "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------- oracle arm
+
+def oracle_sample(scene, cam, gt_img, n_blocks=16, adam_frac=1.0 / 16, seed=0):
+    """One bounded sample of one view of the workload, run by the CPU oracle as it stands
+    (single thread).  Sample: project ALL Gaussians for the view (O1-O9, measured as is),
+    build the lists of and render forward + L1 + backward a window of `n_blocks` blocks
+    (O11-O15), transformation backward of the records that window touched (O16), Adam over a
+    1/16 slice of the Gaussians (O17).  Render is scaled to all blocks of the view, the
+    transformation backward to all records of the view, Adam to all Gaussians (then shared by
+    the b views of the batch)."""
+    import oracle
+    n = scene.n
+    W, H = cam.width, cam.height
+    Wt, Ht = (W + 15) // 16, (H + 15) // 16
+    t0 = time.perf_counter()
+    recs = oracle.make_records(scene, [cam], "parity")
+    t1 = time.perf_counter()
+    k = (seed * 7919) % max(1, Wt * Ht - n_blocks)
+    c = max(0, min((Ht // 2) * Wt + Wt // 2 + k - Wt * Ht // 2, Wt * Ht - n_blocks)) if seed else (Ht // 2) * Wt + Wt // 2
+    b0, b1 = c, min(c + n_blocks, Wt * Ht)
+    off, ent = oracle.tile_lists(recs, b0, b1, Wt, Ht)
+    t1b = time.perf_counter()
+    f = oracle.render_fwd(recs, off, ent, b0, b1, W, H, (0, 0, 0), gt_img[None], 1, 1e-5)
+    g = oracle.render_bwd(recs, off, ent, b0, b1, W, H, f["dl_dc"])
+    t2 = time.perf_counter()
+    touched = np.unique(ent)
+    gidx = recs.vi[touched, 1]
+    sub = synth.Scene(scene.pos[gidx], scene.log_scale[gidx], scene.rot[gidx], scene.opac_logit[gidx],
+                      scene.sh[gidx])
+    sel = oracle.Records(None, None, np.stack([np.zeros(len(touched), np.int64), np.arange(len(touched))], 1), None)
+    oracle.project_bwd(sub, [cam], sel, g[touched])
+    t3 = time.perf_counter()
+    m = max(1, int(n * adam_frac))
+    flat = oracle.flatten_params(scene.slice(0, m))
+    oracle.adam(flat, np.zeros_like(flat), np.zeros_like(flat), np.zeros_like(flat), 1e-3, batch=1, step=1)
+    t4 = time.perf_counter()
+    proj = t1 - t0
+    lists = t1b - t1  # one pass over all records (the window's lists are its output)
+    rend = (t2 - t1b) * (Wt * Ht) / max(b1 - b0, 1)
+    pb = (t3 - t2) * recs.n / max(len(touched), 1)
+    adam = (t4 - t3) * n / m
+    return dict(sec_per_view_est=proj + lists + rend + pb, adam_per_batch=adam, cpu_s=t4 - t0,
+                parts=dict(project=proj, lists=lists, render=rend, proj_bwd=pb, adam=adam))
+
+
+def cpu_views_per_s(sample, b):
+    per_view = sample["sec_per_view_est"] + sample["adam_per_batch"] / b
+    return 1.0 / per_view
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    scene = make_scene(cfg, 0, cfg["n"])
+    cams = make_cameras(cfg)
+    sched = batches(cfg, args.warmup + args.steps)
+    times, samples = [], []
+    for k in range(args.warmup + args.steps):
+        cam = cams[sched[k][0]]
+        gt = synth.gt_image(cfg["seed"], cam)
+        t = time.perf_counter()
+        s = oracle_sample(scene, cam, gt, seed=k)
+        if k >= args.warmup:
+            times.append(time.perf_counter() - t)
+            samples.append(cpu_views_per_s(s, cfg["b"]))
+    v = float(np.mean(samples))
+    line = {"metric": METRIC, "value": v, "unit": "views/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 * float(np.mean(times)), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": cfg["workload"], "global_batch": cfg["b"], "parallelism": "oracle-cpu-1-thread"},
+            "cpu_baseline": {"value": v, "unit": "views/s", "cores": 1, "kind": "oracle",
+                             "sample": "per step: one view; all Gaussians projected; 16 blocks rendered fwd+L1+bwd "
+                                       "(scaled to all blocks); their records' transformation backward (scaled "
+                                       "to all records); Adam over 1/16 of the Gaussians (scaled, shared by b views)"},
+            "e2e": {"value": v, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- libgs arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="libgs", choices=["libgs", "reference"])
+    ap.add_argument("--cost-mode", default="measured", choices=["measured", "work", "paper_avg"])
+    ap.add_argument("--no-rebalance", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--breakdown-steps", type=int, default=2)
+    ap.add_argument("--json-out", default=None)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2406_18533_b200._lib as L
+    from paper_2406_18533_b200.engine import GrendelTrainer, event_ms, make_events
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [L.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = L.Context(local, rank, world, obj[0])
+    else:
+        ctx = L.Context(local, 0, 1)
+
+    t_setup = time.perf_counter()
+    n = cfg["n"]
+    lo, hi = n * rank // world, n * (rank + 1) // world
+    scene = make_scene(cfg, lo, hi)
+    cams = make_cameras(cfg)
+    W, H = cams[0].width, cams[0].height
+    p = L.GaussianParams.from_arrays(scene.pos, scene.log_scale, scene.rot, scene.opac_logit, scene.sh, dev, lo)
+    sched = batches(cfg, args.warmup + args.steps + args.breakdown_steps + args.steps + 2)
+    # ground-truth pool on the device (uint8, i.i.d. uniform; only the L1 sign matters)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(cfg["seed"] + 200)
+    gt_pool = torch.randint(0, 256, (len(cams), H, W, 3), dtype=torch.uint8, device=dev, generator=gen)
+    gt_batch = torch.empty((cfg["b"], H, W, 3), dtype=torch.uint8, device=dev)
+    cost_mode = {"measured": L.COST_MEASURED, "work": L.COST_WORK, "paper_avg": L.COST_PAPER_AVG}[args.cost_mode]
+    tr = GrendelTrainer(ctx, p, W, H, cfg["b"], len(cams), cost_mode=cost_mode, rebalance=not args.no_rebalance,
+                        device=dev)
+    stream = torch.cuda.current_stream()
+    k_sched = [0]
+
+    def batch_cams(k):
+        return [cams[i] for i in sched[k]]
+
+    def one_step(events=None, stats=False):
+        k = k_sched[0]
+        idx = torch.tensor(sched[k], device=dev)
+        torch.index_select(gt_pool, 0, idx, out=gt_batch)
+        loss = tr.step(batch_cams(k), gt_batch, next_cams=batch_cams(k + 1), events=events, collect_stats=stats)
+        k_sched[0] += 1
+        return loss
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        one_step()
+    setup_s = time.perf_counter() - t_setup
+
+    # ---------------- timed region (device-resident inputs)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = ctx.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        one_step()
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    launches = ctx.launch_count() - l0
+    ms = e0.elapsed_time(e1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    views = cfg["b"] * args.steps
+    value = views / (ms_max / 1000.0)
+
+    # ---------------- per-call breakdown + work counters (untimed pass)
+    calls = {}
+    stats = np.zeros(8, np.int64)
+    counts = dict(n_send=0, n_recv=0, n_pairs=0)
+    for _ in range(args.breakdown_steps):
+        ev = make_events()
+        one_step(events=ev, stats=True)
+        torch.cuda.synchronize()
+        for kname, v in event_ms(ev).items():
+            calls[kname] = calls.get(kname, 0.0) + v / args.breakdown_steps
+        stats += tr.stats.cpu().numpy() // 1
+        for kname in counts:
+            counts[kname] += tr.last[kname] / args.breakdown_steps
+    stats = stats / args.breakdown_steps
+
+    # ---------------- e2e: host (pinned) ground truth in, loss out, through the same API
+    e2e = None
+    if not args.no_e2e:
+        gt_host = torch.empty((len(cams), H, W, 3), dtype=torch.uint8, pin_memory=True)
+        gt_host.copy_(gt_pool.cpu())
+        loss_host = torch.empty(1, dtype=torch.float64, pin_memory=True)
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            k = k_sched[0]
+            for j, i in enumerate(sched[k]):
+                gt_batch[j].copy_(gt_host[i], non_blocking=True)
+            loss = tr.step(batch_cams(k), gt_batch, next_cams=batch_cams(k + 1))
+            loss_host.copy_(loss, non_blocking=True)
+            k_sched[0] += 1
+        f1.record(stream)
+        barrier()
+        ems = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e2e = {"value": views / (float(ems.item()) / 1000.0), "unit": "views/s",
+               "h2d_bytes_per_step": int(cfg["b"] * H * W * 3), "d2h_bytes_per_step": 8}
+
+    # ---------------- roofline of the dominant kernel
+    pk, pk_src = peaks()
+    sm_mhz = float(pk.get("sm_max_mhz", 1965.0))
+    fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # T lane-ops/s
+    Efc, Efs, Estop, Eb, Ebc = stats[1], stats[2], stats[3], stats[4], stats[5]
+    work = {
+        "render_fwd": ("alu", (CENSUS["fwd_comp"] * Efc + CENSUS["fwd_skip"] * Efs + CENSUS["fwd_stop"] * Estop) / 1e12,
+                       "T FP32-lane-op/s", fp32_peak),
+        "render_bwd": ("alu", (CENSUS["bwd_contrib"] * Ebc + CENSUS["bwd_skip"] * (Eb - Ebc)) / 1e12,
+                       "T FP32-lane-op/s", fp32_peak),
+        "adam": ("hbm", (1416.0 * p.n + 36.0 * counts["n_send"]) / 1e9, "GB/s", float(pk.get("hbm_gbs", 6650.0))),
+        "project": ("hbm", (236.0 * p.n + 48.0 * counts["n_send"]) / 1e9, "GB/s", float(pk.get("hbm_gbs", 6650.0))),
+        "bin_sort": ("hbm", (28.0 * counts["n_pairs"] + 16.0 * counts["n_recv"]) / 1e9, "GB/s",
+                     float(pk.get("hbm_gbs", 6650.0))),
+    }
+    dom = max((k for k in work if k in calls), key=lambda k: calls[k])
+    bound, amount, unit, peak = work[dom]
+    achieved = amount / (calls[dom] / 1000.0)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "dram_traffic.json")) as f:
+            traffic = json.load(f).get(args.config, {}).get(dom)
+    except Exception:
+        pass
+    rooflines = {}
+    for k, (bd, amt, un, pkv) in work.items():
+        if k in calls and calls[k] > 0:
+            a = amt / (calls[k] / 1000.0)
+            rooflines[k] = {"bound": bd, "achieved": round(a, 3), "peak": pkv, "unit": un, "frac": round(a / pkv, 4),
+                            "ms": round(calls[k], 3)}
+
+    # ---------------- oracle baseline on the host cores (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        full = scene
+        cam = batch_cams(0)[0]
+        gt = gt_pool[sched[0][0]].cpu().numpy()
+        s = oracle_sample(full, cam, gt)
+        cpu = {"value": cpu_views_per_s(s, cfg["b"]), "unit": "views/s", "cores": 1, "kind": "oracle",
+               "sample": "one view; all Gaussians projected; 16 blocks rendered fwd+L1+bwd (scaled to all "
+                         "blocks); their records' transformation backward (scaled to all records); Adam over 1/16 "
+                         "of the Gaussians (scaled, shared by b views); %.1f s of CPU work" % s["cpu_s"],
+               "parts_s_per_view": {k: round(v, 3) for k, v in s["parts"].items()}}
+
+    if rank == 0:
+        raster_ms_view = (calls.get("render_fwd", 0) + calls.get("render_bwd", 0)) / cfg["b"]
+        line = {"metric": METRIC, "value": round(value, 3), "unit": "views/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": cfg["workload"], "config_id": args.config, "global_batch": cfg["b"],
+                           "image": [W, H], "gaussians": n, "parallelism": "gaussian+pixel x%d (Grendel)" % world,
+                           "l2_policy": "inputs larger than L2 (params+Adam state %.1f GB, GT %.2f GB/step)" % (
+                               3 * 240 * n / 1e9, cfg["b"] * W * H * 3 / 1e9),
+                           "cost_mode": args.cost_mode, "rebalance": not args.no_rebalance},
+                "raster_ms_per_view": round(raster_ms_view, 3),
+                "calls_ms": {k: round(v, 3) for k, v in calls.items()},
+                "gpu_launches": int(launches),
+                "roofline": {"bound": bound, "kernel": dom, "achieved": round(achieved, 3), "peak": peak,
+                             "unit": unit, "frac": round(achieved / peak, 4), "traffic": traffic,
+                             "peak_source": pk_src},
+                "rooflines": rooflines,
+                "work": {"E_f": int(stats[0]), "E_fc": int(Efc), "E_fs": int(Efs), "E_stop": int(Estop),
+                         "E_b": int(Eb), "E_bc": int(Ebc), "records": int(counts["n_recv"]),
+                         "pairs": int(counts["n_pairs"])},
+                "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "setup_s": round(setup_s, 1)}
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.json_out:
+            with open(args.json_out, "w") as f:
+                f.write(s + "\n")
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,246 @@
+/* gs.h -- C ABI of libgs: the data-parallel hot path of one Grendel 3DGS training step
+ * (arXiv 2406.18533), B200-native (CUDA sm_100a + NCCL over NVLink/NVSwitch).
+ *
+ * Citation key: P:n = PAPER.md line n (section/equation named), S:n = SPEC.md line n,
+ * O1..O18 = the step definitions of SURVEY.md §8(c), R1..R11 = readings in DESIGN.md §2.
+ *
+ * One training step on rank r of G ranks over a batch of b views:
+ *   gs_project -> gs_exchange -> gs_bin_sort -> gs_render_fwd -> gs_render_bwd
+ *   -> gs_exchange_grads -> gs_adam_step -> gs_rebalance
+ *
+ * Conventions shared by every call
+ *  - Pointers named *_h are HOST memory; every other buffer pointer is DEVICE memory on the
+ *    context's device.  Device buffers are allocated and owned by the caller (PyTorch);
+ *    the context owns only a growable device scratch arena for temporaries and a small
+ *    pinned host mirror, both released by gs_destroy.
+ *  - `stream` is a cudaStream_t passed as void*.  Calls are stream-ordered and
+ *    asynchronous except where a host sync is stated (count read-backs).
+ *  - Every call returns a gs_status and never throws; gs_last_error() has the message.
+ *  - Views of one batch share one image size W x H; the batch's blocks are serialized as
+ *    beta = v * Wt * Ht + ty * Wt + tx with Wt = ceil(W/16), Ht = ceil(H/16)
+ *    ("dividing it into 16x16-pixel blocks, serializing the blocks";
+ *    P:523).  Rank g owns blocks [dp_h[g], dp_h[g+1]) (dp_h[0] = 0, dp_h[G] = b*Wt*Ht).
+ *  - Per-pixel buffers are block-major over the rank's owned blocks: pixel p = ly*16+lx
+ *    of owned block lb = beta - dp_h[r] lives at [lb*256 + p] (per channel plane:
+ *    [lb][ch][256]).  Pixels with px >= W or py >= H are not rendered (R: partial blocks).
+ *  - All collective calls (gs_exchange, gs_exchange_grads, gs_rebalance) must be called by
+ *    every rank in the same order.  Contexts are not re-entrant: one per rank and thread.
+ */
+#ifndef GS_H
+#define GS_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GS_OK = 0,
+  GS_EINVAL = 1,       /* invalid argument (null required pointer, bad sizes, dp not monotone...) */
+  GS_ECAPACITY = 2,    /* a caller capacity is too small; *needed written; outputs invalid      */
+  GS_ENONFINITE = 3,   /* a parameter is NaN/Inf (gs_check_finite)                               */
+  GS_ECUDA = 4,        /* CUDA runtime error                                                      */
+  GS_ENCCL = 5,        /* NCCL error                                                              */
+  GS_ENOTSUP = 6       /* world > 1 requested but the library was built without NCCL              */
+} gs_status;
+
+typedef struct gs_ctx gs_ctx;
+
+/* Pinhole camera, one per view of a batch ("Given a camera view v and the associated
+ * screen space").  R is world->camera (rows: image-right, image-down, forward), row-major;
+ * camera centre c = -R^T t.  Pixel (px,py) has its centre at (px,py) (R1).             */
+typedef struct {
+  float R[9];
+  float t[3];
+  float fx, fy, cx, cy;
+  int32_t width, height;
+  int32_t image_id; /* training-image id, indexes the rebalancer's cost history */
+} gs_camera;
+
+/* Gaussian parameters of the rank's shard (x, s, q, alpha, sh in R^48), SoA of
+ * float4 planes so a warp reads 512 contiguous bytes per plane:
+ *   pos_op[n]    = (x, y, z, opacity_logit)
+ *   log_scale[n] = (log sx, log sy, log sz, unused)
+ *   rot[n]       = (w, x, y, z), unnormalised (normalised inside O1)
+ *   sh[12][n]    = plane k holds SH floats 4k..4k+3 of the 48 ((l,m)-major, rgb inner)
+ * gid of element i is gid_base + i (contiguous shard).                            */
+typedef struct {
+  float* pos_op;
+  float* log_scale;
+  float* rot;
+  float* sh;
+  int64_t n;
+  int64_t gid_base;
+} gs_params;
+
+/* Adam hyper-parameters.  lr[6] = base learning rates lambda per group
+ * (pos, sh_dc, sh_rest, opacity, scale, rot) for THIS step (the position schedule is the
+ * caller's); the call applies Eq. (1) lambda' = lambda sqrt(batch) and Eq. (2)
+ * beta' = beta^batch itself.  step = t >= 1 (bias correction as torch.optim.Adam).      */
+typedef struct {
+  float lr[6];
+  float beta1, beta2, eps;
+  int32_t batch;
+  int64_t step;
+} gs_adam_hparams;
+
+enum { GS_COST_MEASURED = 0, GS_COST_WORK = 1, GS_COST_PAPER_AVG = 2 };
+enum { GS_ADAM_GRAD = 1, GS_ADAM_APPLY = 2, GS_ADAM_WRITE_GRAD = 4 };
+
+/* Size of one projected record (A1 output / A2 payload):
+ *   float4 {mx, my, depth, radius(float)}      mean2d, depth = p_z (O3-O4, O7)
+ *   float4 {l11, l21, l22, opacity}            Cholesky factor L of the conic, conic = L L^T (O6)
+ *   float4 {r, g, b, meta(u32 = gid*32 + v)}   colour (O9)                                    */
+#define GS_RECORD_BYTES 48
+/* dL/d(record) as exchanged back (A6): 9 floats (mx, my, A, B, C, opacity, r, g, b) where
+ * (A, B, C) is the conic [[A, B], [B, C]] and B is the scalar off-diagonal (R: #16).     */
+#define GS_GRAD_FLOATS 9
+
+/* --------------------------------------------------------------------------- context */
+int gs_version(void);
+/* 128-byte NCCL unique id (rank 0 calls it; the bytes are broadcast by torch.distributed).
+ * Returns GS_ENOTSUP when built without NCCL.                                            */
+gs_status gs_nccl_unique_id(uint8_t id_h[128]);
+/* Create a context on `device` for rank/world.  world == 1 needs no id (id_h may be NULL);
+ * world > 1 with an id initialises an NCCL communicator (collective over all ranks);
+ * world > 1 with id_h == NULL creates a "virtual" rank without a communicator: the local
+ * calls (project, bin_sort, render, adam) work on its partition, the collective calls
+ * return GS_EINVAL.  (Used to test partitioned execution on one GPU.)                   */
+gs_status gs_create(gs_ctx** out, int device, int rank, int world, const uint8_t* id_h);
+void gs_destroy(gs_ctx* ctx);
+const char* gs_last_error(const gs_ctx* ctx);
+/* Number of CUDA kernels this context has launched so far (for launch accounting). */
+int64_t gs_launch_count(const gs_ctx* ctx);
+
+/* Non-finite parameter check: GS_ENONFINITE with *bad_gid_h = lowest offending
+ * gid, else GS_OK and *bad_gid_h = -1.  Host sync.                                       */
+gs_status gs_check_finite(gs_ctx* ctx, const gs_params* p, int64_t* bad_gid_h, void* stream);
+
+/* --------------------------------------------------------------------------- A1 */
+/* Bytes of the backward index gs_project writes and gs_adam_step reads, for n owned
+ * Gaussians and n_views views at the context's world size.                               */
+size_t gs_project_index_bytes(const gs_ctx* ctx, int64_t n, int n_views);
+
+/* A1 gs_project -- EWA projection and culling on the owner (P:103 step 1; O1-O10).
+ * For every owned Gaussian i and view v: the fp32 membership chain O1-O8 (visibility,
+ * mean2d, depth, 2D covariance, radius, tile rectangle; bit-exact, R10), the conic's
+ * Cholesky factor, opacity and SH degree-3 colour (O9), and the destination set
+ * D(i,v) = ranks owning a block of the rectangle (O10; Fig. 3).  Writes one
+ * record per (i, v, d in D(i,v)) into send_rec, bucketed by destination d, then view v,
+ * then ascending gid (deterministic: no placement atomics).  send_counts_h[G] receives the
+ * per-destination record counts (host sync).  If the total exceeds send_cap, returns
+ * GS_ECAPACITY with the counts written and send_rec untouched.  bwd_index must hold
+ * gs_project_index_bytes(ctx, p->n, n_views) bytes; it is read back by gs_adam_step.
+ * Invisible Gaussians (behind near plane 0.01, det <= 0, empty rectangle) produce nothing. */
+gs_status gs_project(gs_ctx* ctx, const gs_params* p, const gs_camera* cams_h, int n_views,
+                     const int64_t* dp_h, void* send_rec, int64_t send_cap,
+                     int64_t* send_counts_h, void* bwd_index, void* stream);
+
+/* --------------------------------------------------------------------------- A2 */
+/* A2 gs_exchange -- forward sparse all-to-all of records ("sparse all-to-all
+ * communication to retrieve Gaussians intersecting with any pixels in the partition";
+ * P:529).  Exchanges the G x G count matrix (NCCL all-gather, host sync), then grouped
+ * ncclSend/ncclRecv.  recv_rec receives the records ordered by ascending source rank,
+ * so within each view they are in ascending gid.  recv_counts_h[G] = records from each
+ * source; *n_recv_h = total.  GS_ECAPACITY if it exceeds recv_cap (nothing transferred).
+ * world == 1: identity; recv_rec may alias send_rec (then nothing is copied).            */
+gs_status gs_exchange(gs_ctx* ctx, const void* send_rec, const int64_t* send_counts_h,
+                      void* recv_rec, int64_t recv_cap, int64_t* recv_counts_h,
+                      int64_t* n_recv_h, void* stream);
+
+/* --------------------------------------------------------------------------- A3 */
+/* A3 gs_bin_sort -- Z-buffer build ("iterates over intersecting Gaussians in
+ * increasing depth"; App. A.2; O11).  For each received record, every owned block
+ * of its view inside its tile rectangle gets the record; each block's list is sorted by
+ * (depth, gid) (R7; unique keys, so the order is deterministic).  Outputs:
+ *   tile_range[n_owned+1] (int32 offsets into sorted_idx), sorted_idx[n_pairs] (uint32
+ *   receive indices).  *n_pairs_h = pair count (host sync).  GS_ECAPACITY if > pair_cap. */
+gs_status gs_bin_sort(gs_ctx* ctx, const void* recv_rec, int64_t n_recv, const gs_camera* cams_h,
+                      int n_views, const int64_t* dp_h, uint32_t* sorted_idx, int64_t pair_cap,
+                      int32_t* tile_range, int64_t* n_pairs_h, void* stream);
+
+/* --------------------------------------------------------------------------- A4 */
+/* A4 gs_render_fwd -- front-to-back alpha compositing over the owned blocks (P:106-107
+ * "uses alpha-composition to combine their contributions until a threshold opacity has
+ * been reached"; O12 with alpha = min(0.99, o G), skip alpha < 1/255, stop before the entry
+ * that would take T below 1e-4 (R3); C += T bg).  Writes T_final[n_owned*256],
+ * n_last[n_owned*256] (int32), optionally out_rgb[n_owned][3][256] (C incl. background).
+ * If gt (uint8 [n_views][H][W][3], value/255) is given, fuses the L1 loss (O13):
+ * dL_dpix[n_owned][3][256] = sign(C - GT) / (3 H W b_loss) and *loss_sum (device double)
+ * += sum |C - GT| / (3 H W b_loss).  tile_cost[n_owned] (int64, nullable) += per-block
+ * cost (MEASURED: SM cycles of the block; WORK: evaluations E_f).  stats (nullable
+ * int64[8], device) += (E_f, E_fc, E_fs, E_stop, 0, 0, 0, 0) totals.                      */
+gs_status gs_render_fwd(gs_ctx* ctx, const void* recv_rec, const uint32_t* sorted_idx,
+                        const int32_t* tile_range, const gs_camera* cams_h, int n_views,
+                        const int64_t* dp_h, const float* bg_h, const uint8_t* gt, int b_loss,
+                        float* out_rgb, float* T_final, int32_t* n_last, float* dL_dpix,
+                        double* loss_sum, int64_t* tile_cost, int cost_mode, int64_t* stats,
+                        void* stream);
+
+/* --------------------------------------------------------------------------- A5 */
+/* A5 gs_render_bwd -- backward of compositing (O14-O15).  Walks each pixel's list
+ * back to front from n_last, reconstructing T, and accumulates dL/d(record) over all owned
+ * pixels into dL_drec[n_recv][9] (zeroed by this call; float atomics, so summation order is
+ * not deterministic).  tile_cost += cost (WORK: visited entries = n_last per pixel).
+ * stats (nullable) += (0, 0, 0, 0, E_b visited, E_bc contributing, 0, 0).                */
+gs_status gs_render_bwd(gs_ctx* ctx, const void* recv_rec, int64_t n_recv,
+                        const uint32_t* sorted_idx, const int32_t* tile_range,
+                        const gs_camera* cams_h, int n_views, const int64_t* dp_h,
+                        const float* bg_h, const float* dL_dpix, const float* T_final,
+                        const int32_t* n_last, float* dL_drec, int64_t* tile_cost, int cost_mode,
+                        int64_t* stats, void* stream);
+
+/* --------------------------------------------------------------------------- A6 */
+/* A6 gs_exchange_grads -- reverse sparse all-to-all ("A reversed all-to-all
+ * communication is done during the backward pass").  Exact transpose of gs_exchange with
+ * the counts it returned: dL_dsend[n_send][9] receives, in send order, the gradient each
+ * record got from its renderer.  world == 1: identity (dL_dsend may alias dL_drec).      */
+gs_status gs_exchange_grads(gs_ctx* ctx, const float* dL_drec, const int64_t* recv_counts_h,
+                            const int64_t* send_counts_h, float* dL_dsend, void* stream);
+
+/* --------------------------------------------------------------------------- A7 + A8 */
+/* A7+A8 gs_adam_step -- transformation backward fused with Adam ("Gaussian
+ * transformation backward ... distributed the same way"; Eq. (1)-(2); O16-O17).
+ * flags:
+ *   GS_ADAM_GRAD       compute the parameter gradient from dL_dsend (summed over the
+ *                      record's destinations in ascending rank, then over views; O16)
+ *   GS_ADAM_WRITE_GRAD also store that gradient into g (parity mode)
+ *   GS_ADAM_APPLY      apply Adam to p, m, v (dense over all owned Gaussians, R9) using the
+ *                      fused gradient (with GS_ADAM_GRAD) or the gradient stored in g.
+ * m, v, g use the same float4-plane layout as p (unused lanes ignored).                  */
+gs_status gs_adam_step(gs_ctx* ctx, gs_params* p, gs_params* m, gs_params* v, gs_params* g,
+                       const gs_camera* cams_h, int n_views, const int64_t* dp_h,
+                       const float* dL_dsend, const void* bwd_index, const gs_adam_hparams* hp,
+                       int flags, void* stream);
+
+/* --------------------------------------------------------------------------- A9 */
+/* A9 gs_rebalance -- dynamic pixel-tile load balancing (§3.2, Algorithm 1).
+ * 1. all-gathers the owned per-block costs of the current batch (NCCL; every rank then holds
+ *    the whole row, so every rank computes identical division points, no broadcast);
+ * 2. converts costs to estimates (MEASURED/WORK: the cost; PAPER_AVG: the rank's average
+ *    per-pixel cost times the block's pixels) and stores them in
+ *    history[image_id][Wt*Ht] (device int64, initialise to -1 = never rendered);
+ * 3. builds ET for the next batch from the history, unseen images costing their pixel
+ *    count, and runs Algorithm 1 in exact int64 (R8): CT = cumsum(ET),
+ *    DP[g] = #{i : CT[i] G <= g CT[B-1]}, DP[0] = 0, DP[G] = B (uniform if all zero).
+ * dp_next_h[G+1] is written on the host (host sync).                                     */
+gs_status gs_rebalance(gs_ctx* ctx, const int64_t* owned_tile_cost, const gs_camera* cams_h,
+                       int n_views, const int64_t* dp_h, int64_t* history, int64_t n_images,
+                       int cost_mode, const gs_camera* next_cams_h, int n_next,
+                       int64_t* dp_next_h, void* stream);
+
+/* Algorithm 1 alone, pure host function: DP_h[G+1] from ET_h[B].
+ * GS_EINVAL if G < 1, B < 0, any ET < 0, or the int64 guard B*max(ET)*G < 2^63 fails.    */
+gs_status gs_division_points(const int64_t* ET_h, int64_t B, int G, int64_t* DP_h);
+
+/* Host-side exchange plan (used by gs_exchange; exported for multi-process CPU tests):
+ * from the row-major G x G count matrix counts_h[src*G+dst] compute for `rank` the send
+ * offsets send_off_h[G+1] and receive offsets recv_off_h[G+1] (ascending source rank).   */
+gs_status gs_exchange_plan(const int64_t* counts_h, int G, int rank, int64_t* send_off_h,
+                           int64_t* recv_off_h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,359 @@
+"""Thin ctypes binding of libgs (include/gs.h).  Argument marshalling only: every step of
+the hot path runs in libgs's CUDA kernels; this module never computes any part of it and has
+no fallback -- importing it fails loudly if libgs.so is missing.
+
+Names mirror the C ABI without the ``gs_`` prefix.  Tensors are torch CUDA tensors (the
+buffers the caller owns); host arrays are numpy / python ints.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgs.so")
+
+GS_OK, GS_EINVAL, GS_ECAPACITY, GS_ENONFINITE, GS_ECUDA, GS_ENCCL, GS_ENOTSUP = range(7)
+COST_MEASURED, COST_WORK, COST_PAPER_AVG = 0, 1, 2
+ADAM_GRAD, ADAM_APPLY, ADAM_WRITE_GRAD = 1, 2, 4
+RECORD_BYTES = 48
+GRAD_FLOATS = 9
+
+
+class GSError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__("libgs status %d: %s" % (status, msg))
+        self.status = status
+
+
+class CapacityError(GSError):
+    pass
+
+
+class Camera(C.Structure):
+    _fields_ = [("R", C.c_float * 9), ("t", C.c_float * 3), ("fx", C.c_float), ("fy", C.c_float),
+                ("cx", C.c_float), ("cy", C.c_float), ("width", C.c_int32), ("height", C.c_int32),
+                ("image_id", C.c_int32)]
+
+
+class Params(C.Structure):
+    _fields_ = [("pos_op", C.c_void_p), ("log_scale", C.c_void_p), ("rot", C.c_void_p),
+                ("sh", C.c_void_p), ("n", C.c_int64), ("gid_base", C.c_int64)]
+
+
+class AdamHparams(C.Structure):
+    _fields_ = [("lr", C.c_float * 6), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
+                ("batch", C.c_int32), ("step", C.c_int64)]
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError("libgs.so not built (run __graft_entry__.build() or "
+                      "python -m paper_2406_18533_b200.build); there is no CPU fallback")
+_lib = C.CDLL(LIB_PATH)
+
+_vp, _i64, _i32, _sz = C.c_void_p, C.c_int64, C.c_int32, C.c_size_t
+_P64 = C.POINTER(C.c_int64)
+_sig = {
+    "gs_version": (C.c_int, []),
+    "gs_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "gs_create": (C.c_int, [C.POINTER(_vp), C.c_int, C.c_int, C.c_int, C.c_char_p]),
+    "gs_destroy": (None, [_vp]),
+    "gs_last_error": (C.c_char_p, [_vp]),
+    "gs_launch_count": (C.c_int64, [_vp]),
+    "gs_check_finite": (C.c_int, [_vp, C.POINTER(Params), _P64, _vp]),
+    "gs_project_index_bytes": (_sz, [_vp, _i64, C.c_int]),
+    "gs_project": (C.c_int, [_vp, C.POINTER(Params), C.POINTER(Camera), C.c_int, _P64, _vp, _i64, _P64, _vp, _vp]),
+    "gs_exchange": (C.c_int, [_vp, _vp, _P64, _vp, _i64, _P64, _P64, _vp]),
+    "gs_bin_sort": (C.c_int, [_vp, _vp, _i64, C.POINTER(Camera), C.c_int, _P64, _vp, _i64, _vp, _P64, _vp]),
+    "gs_render_fwd": (C.c_int, [_vp, _vp, _vp, _vp, C.POINTER(Camera), C.c_int, _P64, C.POINTER(C.c_float),
+                                _vp, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
+    "gs_render_bwd": (C.c_int, [_vp, _vp, _i64, _vp, _vp, C.POINTER(Camera), C.c_int, _P64,
+                                C.POINTER(C.c_float), _vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
+    "gs_exchange_grads": (C.c_int, [_vp, _vp, _P64, _P64, _vp, _vp]),
+    "gs_adam_step": (C.c_int, [_vp, C.POINTER(Params), C.POINTER(Params), C.POINTER(Params), C.POINTER(Params),
+                               C.POINTER(Camera), C.c_int, _P64, _vp, _vp, C.POINTER(AdamHparams), C.c_int, _vp]),
+    "gs_rebalance": (C.c_int, [_vp, _vp, C.POINTER(Camera), C.c_int, _P64, _vp, _i64, C.c_int,
+                               C.POINTER(Camera), C.c_int, _P64, _vp]),
+    "gs_division_points": (C.c_int, [_P64, _i64, C.c_int, _P64]),
+    "gs_exchange_plan": (C.c_int, [_P64, C.c_int, C.c_int, _P64, _P64]),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+def version() -> int:
+    return _lib.gs_version()
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _i64arr(vals):
+    a = np.ascontiguousarray(np.asarray(vals, dtype=np.int64))
+    return a, a.ctypes.data_as(_P64)
+
+
+def cameras(cams) -> "C.Array":
+    """Any objects with R (3x3), t (3), fx, fy, cx, cy, width, height, image_id."""
+    arr = (Camera * len(cams))()
+    for k, c in enumerate(cams):
+        arr[k].R[:] = [float(x) for x in np.asarray(c.R, np.float32).reshape(-1)]
+        arr[k].t[:] = [float(x) for x in np.asarray(c.t, np.float32).reshape(-1)]
+        arr[k].fx, arr[k].fy, arr[k].cx, arr[k].cy = c.fx, c.fy, c.cx, c.cy
+        arr[k].width, arr[k].height = c.width, c.height
+        arr[k].image_id = int(getattr(c, "image_id", 0))
+    return arr
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+class Context:
+    """One libgs context per rank (gs_create / gs_destroy)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+        self._h = C.c_void_p()
+        st = _lib.gs_create(C.byref(self._h), device, rank, world, nccl_id)
+        self.device, self.rank, self.world = device, rank, world
+        if st != GS_OK:
+            msg = self.last_error()
+            _lib.gs_destroy(self._h)
+            self._h = None
+            raise GSError(st, msg)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def launch_count(self) -> int:
+        return int(_lib.gs_launch_count(self._h))
+
+    def last_error(self) -> str:
+        return (_lib.gs_last_error(self._h) or b"").decode()
+
+    def check(self, st):
+        if st == GS_OK:
+            return
+        cls = CapacityError if st == GS_ECAPACITY else GSError
+        raise cls(st, self.last_error())
+
+    def close(self):
+        if self._h:
+            _lib.gs_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = _lib.gs_nccl_unique_id(buf)
+    if st != GS_OK:
+        raise GSError(st, "gs_nccl_unique_id")
+    return buf.raw
+
+
+class GaussianParams:
+    """Owner-side SoA float4 planes (include/gs.h gs_params) as torch CUDA tensors."""
+
+    def __init__(self, pos_op, log_scale, rot, sh, gid_base=0):
+        self.pos_op, self.log_scale, self.rot, self.sh = pos_op, log_scale, rot, sh
+        self.gid_base = int(gid_base)
+
+    @property
+    def n(self):
+        return int(self.pos_op.shape[0])
+
+    def struct(self) -> Params:
+        return Params(self.pos_op.data_ptr(), self.log_scale.data_ptr(), self.rot.data_ptr(),
+                      self.sh.data_ptr(), self.n, self.gid_base)
+
+    @classmethod
+    def empty(cls, n, device, gid_base=0, zero=True):
+        import torch
+        f = torch.zeros if zero else torch.empty
+        return cls(f((n, 4), dtype=torch.float32, device=device), f((n, 4), dtype=torch.float32, device=device),
+                   f((n, 4), dtype=torch.float32, device=device), f((12, n, 4), dtype=torch.float32, device=device),
+                   gid_base)
+
+    @classmethod
+    def from_arrays(cls, pos, log_scale, rot, opac_logit, sh, device, gid_base=0):
+        """Pack numpy [N,3],[N,3],[N,4],[N],[N,16,3] into the float4 planes (layout only)."""
+        import torch
+        n = pos.shape[0]
+        po = np.concatenate([pos, opac_logit[:, None]], 1).astype(np.float32)
+        ls = np.concatenate([log_scale, np.zeros((n, 1), np.float32)], 1).astype(np.float32)
+        shp = np.ascontiguousarray(np.asarray(sh, np.float32).reshape(n, 12, 4).transpose(1, 0, 2))
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(device)
+        return cls(t(po), t(ls), t(rot), t(shp), gid_base)
+
+    def to_flat(self) -> np.ndarray:
+        """[N, 59] = (pos3, log_scale3, rot4, logit1, sh48), the oracle's gradient order."""
+        po = self.pos_op.detach().cpu().numpy()
+        ls = self.log_scale.detach().cpu().numpy()
+        q = self.rot.detach().cpu().numpy()
+        sh = self.sh.detach().cpu().numpy().transpose(1, 0, 2).reshape(self.n, 48)
+        return np.concatenate([po[:, :3], ls[:, :3], q, po[:, 3:4], sh], 1)
+
+    def zeros_like(self):
+        return GaussianParams.empty(self.n, self.pos_op.device, self.gid_base)
+
+
+# ----------------------------------------------------------------------------- calls
+
+def check_finite(ctx, params, stream=None):
+    bad = C.c_int64(-1)
+    ps = params.struct()
+    st = _lib.gs_check_finite(ctx.handle, C.byref(ps), C.byref(bad), _stream(stream))
+    if st == GS_ENONFINITE:
+        return int(bad.value)
+    ctx.check(st)
+    return -1
+
+
+def project_index_bytes(ctx, n, n_views):
+    return int(_lib.gs_project_index_bytes(ctx.handle, n, n_views))
+
+
+def project(ctx, params, cams, dp, send_rec, send_cap, bwd_index, stream=None):
+    """A1.  Returns send_counts (numpy int64[G]).  Raises CapacityError (counts in .counts)."""
+    ca = cameras(cams)
+    dpa, dpp = _i64arr(dp)
+    cnt, cntp = _i64arr(np.zeros(ctx.world))
+    ps = params.struct()
+    st = _lib.gs_project(ctx.handle, C.byref(ps), ca, len(cams), dpp, _ptr(send_rec), send_cap, cntp,
+                         _ptr(bwd_index), _stream(stream))
+    if st == GS_ECAPACITY:
+        e = CapacityError(st, ctx.last_error())
+        e.counts = cnt.copy()
+        raise e
+    ctx.check(st)
+    return cnt
+
+
+def exchange(ctx, send_rec, send_counts, recv_rec, recv_cap, stream=None):
+    """A2.  Returns (recv_counts int64[G], n_recv)."""
+    sc, scp = _i64arr(send_counts)
+    rc, rcp = _i64arr(np.zeros(ctx.world))
+    nr = C.c_int64(0)
+    st = _lib.gs_exchange(ctx.handle, _ptr(send_rec), scp, _ptr(recv_rec), recv_cap, rcp, C.byref(nr),
+                          _stream(stream))
+    if st == GS_ECAPACITY:
+        e = CapacityError(st, ctx.last_error())
+        e.needed = int(nr.value)
+        raise e
+    ctx.check(st)
+    return rc, int(nr.value)
+
+
+def bin_sort(ctx, recv_rec, n_recv, cams, dp, sorted_idx, pair_cap, tile_range, stream=None):
+    """A3.  Returns n_pairs."""
+    ca = cameras(cams)
+    _, dpp = _i64arr(dp)
+    npairs = C.c_int64(0)
+    st = _lib.gs_bin_sort(ctx.handle, _ptr(recv_rec), n_recv, ca, len(cams), dpp, _ptr(sorted_idx), pair_cap,
+                          _ptr(tile_range), C.byref(npairs), _stream(stream))
+    if st == GS_ECAPACITY:
+        e = CapacityError(st, ctx.last_error())
+        e.needed = int(npairs.value)
+        raise e
+    ctx.check(st)
+    return int(npairs.value)
+
+
+def _bg(bg):
+    a = (C.c_float * 3)(*[float(x) for x in (bg if bg is not None else (0, 0, 0))])
+    return a
+
+
+def render_fwd(ctx, recv_rec, sorted_idx, tile_range, cams, dp, bg, gt, b_loss, out_rgb, T_final, n_last,
+               dL_dpix, loss_sum, tile_cost, cost_mode, stats, stream=None):
+    """A4."""
+    ca = cameras(cams)
+    _, dpp = _i64arr(dp)
+    st = _lib.gs_render_fwd(ctx.handle, _ptr(recv_rec), _ptr(sorted_idx), _ptr(tile_range), ca, len(cams), dpp,
+                            _bg(bg), _ptr(gt), int(b_loss), _ptr(out_rgb), _ptr(T_final), _ptr(n_last),
+                            _ptr(dL_dpix), _ptr(loss_sum), _ptr(tile_cost), int(cost_mode), _ptr(stats),
+                            _stream(stream))
+    ctx.check(st)
+
+
+def render_bwd(ctx, recv_rec, n_recv, sorted_idx, tile_range, cams, dp, bg, dL_dpix, T_final, n_last,
+               dL_drec, tile_cost, cost_mode, stats, stream=None):
+    """A5."""
+    ca = cameras(cams)
+    _, dpp = _i64arr(dp)
+    st = _lib.gs_render_bwd(ctx.handle, _ptr(recv_rec), int(n_recv), _ptr(sorted_idx), _ptr(tile_range), ca,
+                            len(cams), dpp, _bg(bg), _ptr(dL_dpix), _ptr(T_final), _ptr(n_last), _ptr(dL_drec),
+                            _ptr(tile_cost), int(cost_mode), _ptr(stats), _stream(stream))
+    ctx.check(st)
+
+
+def exchange_grads(ctx, dL_drec, recv_counts, send_counts, dL_dsend, stream=None):
+    """A6."""
+    _, rcp = _i64arr(recv_counts)
+    _, scp = _i64arr(send_counts)
+    ctx.check(_lib.gs_exchange_grads(ctx.handle, _ptr(dL_drec), rcp, scp, _ptr(dL_dsend), _stream(stream)))
+
+
+def adam_hparams(lr, batch, step, beta1=0.9, beta2=0.999, eps=1e-15) -> AdamHparams:
+    h = AdamHparams()
+    h.lr[:] = [float(x) for x in lr]
+    h.beta1, h.beta2, h.eps, h.batch, h.step = beta1, beta2, eps, int(batch), int(step)
+    return h
+
+
+def adam_step(ctx, p, m, v, g, cams, dp, dL_dsend, bwd_index, hp, flags, stream=None):
+    """A7 + A8."""
+    ca = cameras(cams) if cams is not None else None
+    n_views = len(cams) if cams is not None else 0
+    _, dpp = _i64arr(dp if dp is not None else [0])
+    st_ = [x.struct() if x is not None else None for x in (p, m, v, g)]
+    refs = [C.byref(s) if s is not None else None for s in st_]
+    st = _lib.gs_adam_step(ctx.handle, refs[0], refs[1], refs[2], refs[3], ca, n_views, dpp, _ptr(dL_dsend),
+                           _ptr(bwd_index), C.byref(hp), int(flags), _stream(stream))
+    ctx.check(st)
+
+
+def rebalance(ctx, owned_tile_cost, cams, dp, history, n_images, cost_mode, next_cams, stream=None):
+    """A9.  Returns dp_next (numpy int64[G+1])."""
+    ca, na = cameras(cams), cameras(next_cams)
+    _, dpp = _i64arr(dp)
+    out, outp = _i64arr(np.zeros(ctx.world + 1))
+    st = _lib.gs_rebalance(ctx.handle, _ptr(owned_tile_cost), ca, len(cams), dpp, _ptr(history), int(n_images),
+                           int(cost_mode), na, len(next_cams), outp, _stream(stream))
+    ctx.check(st)
+    return out
+
+
+def division_points(et, G):
+    """Algorithm 1 (pure host function of libgs)."""
+    a, ap = _i64arr(et)
+    out, outp = _i64arr(np.zeros(G + 1))
+    st = _lib.gs_division_points(ap if a.size else None, a.size, G, outp)
+    if st != GS_OK:
+        raise GSError(st, "gs_division_points")
+    return out
+
+
+def exchange_plan(counts, G, rank):
+    a, ap = _i64arr(np.asarray(counts).reshape(-1))
+    so, sop = _i64arr(np.zeros(G + 1))
+    ro, rop = _i64arr(np.zeros(G + 1))
+    st = _lib.gs_exchange_plan(ap, G, rank, sop, rop)
+    if st != GS_OK:
+        raise GSError(st, "gs_exchange_plan")
+    return so, ro

@@ -1,0 +1,106 @@
+// gs_internal.h -- host-side internals of libgs (context, errors, scratch arena).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/gs.h"
+
+#ifdef GS_WITH_NCCL
+#include <nccl.h>
+#endif
+
+// A growable device arena of named slots.  Temporaries of one call live in slots; a slot
+// grows (cudaFree + cudaMalloc, after a stream sync) only when a larger size is requested.
+struct gs_slot {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+enum {
+  SLOT_SCAN = 0,      // scan partials
+  SLOT_PROJ_TMP,      // projection per-destination totals
+  SLOT_DIFF,          // bin_sort 2D difference arrays
+  SLOT_COUNTS,        // bin_sort per-block counts (int64)
+  SLOT_CURSOR,        // bin_sort per-block cursors
+  SLOT_KEYS,          // bin_sort (depth, recv idx) keys
+  SLOT_KEYS_TMP,      // merge ping-pong for long lists
+  SLOT_LARGE,         // list of long blocks + counters
+  SLOT_ROW,           // rebalance cost row (all blocks of the batch)
+  SLOT_ET,            // rebalance ET of next batch
+  SLOT_CT,            // rebalance prefix sums
+  SLOT_MISC,          // small counters / dp
+  SLOT_COUNT_GATHER,  // exchange count matrix
+  SLOT_N
+};
+
+struct gs_ctx {
+  int device = 0, rank = 0, world = 1;
+  std::string err;
+  gs_slot slot[SLOT_N];
+  int64_t* pinned = nullptr;  // small pinned host mirror (>= 4096 int64)
+  int64_t launches = 0;       // kernels launched through this context (gs_launch_count)
+#ifdef GS_WITH_NCCL
+  ncclComm_t comm = nullptr;
+#endif
+};
+
+gs_status gs_fail(gs_ctx* c, gs_status s, const char* fmt, ...);
+void* gs_slot_get(gs_ctx* c, int slot, size_t bytes, cudaStream_t st);
+gs_status gs_cuda_check(gs_ctx* c, cudaError_t e, const char* what);
+
+#define GS_CUDA(ctx, expr)                                              \
+  do {                                                                  \
+    cudaError_t _e = (expr);                                            \
+    if (_e != cudaSuccess) return gs_cuda_check((ctx), _e, #expr);      \
+  } while (0)
+
+#define GS_LAUNCH_CHECK(ctx, what)                                       \
+  do {                                                                  \
+    cudaError_t _e = cudaPeekAtLastError();                             \
+    if (_e != cudaSuccess) return gs_cuda_check((ctx), _e, what);       \
+  } while (0)
+
+#define GS_REQUIRE(ctx, cond, ...)                                       \
+  do {                                                                  \
+    if (!(cond)) return gs_fail((ctx), GS_EINVAL, __VA_ARGS__);         \
+  } while (0)
+
+// Shared validation of a batch description: equal-size views, monotone dp.
+gs_status gs_check_batch(gs_ctx* c, const gs_camera* cams_h, int n_views, const int64_t* dp_h);
+
+// Device-wide int64 exclusive (inclusive=0) or inclusive scan, in-place allowed.
+gs_status gs_scan_i64(gs_ctx* c, const int64_t* in, int64_t* out, int64_t n, int inclusive,
+                      cudaStream_t st);
+
+// Kernel-side view of the batch geometry and of the rank's partition.
+#define GS_MAX_WORLD 32
+#define GS_MAX_VIEWS 32
+struct gs_dp_arg {
+  long long dp[GS_MAX_WORLD + 1];
+  int G;
+  int rank;
+};
+struct gs_geom {
+  int W, H, Wt, Ht;
+  long long per_view;  // Wt * Ht
+};
+inline gs_geom gs_make_geom(const gs_camera* c) {
+  gs_geom g;
+  g.W = c->width;
+  g.H = c->height;
+  g.Wt = (g.W + 15) / 16;
+  g.Ht = (g.H + 15) / 16;
+  g.per_view = (long long)g.Wt * g.Ht;
+  return g;
+}
+inline gs_dp_arg gs_make_dp(const gs_ctx* c, const int64_t* dp_h) {
+  gs_dp_arg d;
+  d.G = c->world;
+  d.rank = c->rank;
+  for (int g = 0; g <= GS_MAX_WORLD; g++) d.dp[g] = g <= c->world ? dp_h[g] : dp_h[c->world];
+  return d;
+}

@@ -1,0 +1,188 @@
+// gs_project.cu -- A1: EWA projection, culling, colour and exchange destinations on the
+// Gaussian's owner (P:103 step 1 "each Gaussian i is transformed and projected to determine
+// its position x_{v,i} ... depth_{v,i} ... radius_{v,i} ... color c_{v,i}").
+//
+// Two passes over the owned shard, one thread per Gaussian, 256 per CTA:
+//   count: fp32 membership chain for every view, destination set D(i,v) (O10), per-CTA
+//          bucket counts, bucket = (destination d, view v), and the (v,d) bitmask per Gaussian
+//          (the backward index gs_adam_step reuses);
+//   scan:  exclusive scan of the counts in (d, v, CTA) order -> each CTA's bucket bases;
+//   write: recompute the projection, rank each Gaussian inside its CTA bucket with warp
+//          ballots (thread order = gid order), write 48-byte records.
+// Placement is therefore deterministic and gid-ordered within each (d, v) bucket, which the
+// stable (depth, gid) order of A3 relies on; no placement atomics.
+#include "gs_device.cuh"
+#include "gs_index.cuh"
+
+using namespace gsd;
+
+namespace {
+
+__global__ void __launch_bounds__(kBlock) k_project_count(
+    const float4* __restrict__ pos_op, const float4* __restrict__ log_scale,
+    const float4* __restrict__ rot, int64_t n, gs_cams_arg cams, gs_geom geo, gs_dp_arg dp,
+    int nb, int NW, uint32_t* __restrict__ maskw, int64_t* __restrict__ cta_cnt, int64_t ncta) {
+  __shared__ int s_c[kMaxBuckets];
+  for (int k = threadIdx.x; k < nb; k += kBlock) s_c[k] = 0;
+  __syncthreads();
+  int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+  uint32_t m[kMaxWords];
+#pragma unroll
+  for (int w = 0; w < kMaxWords; w++) m[w] = 0;
+  if (i < n) {
+    float4 X = pos_op[i];
+    gs_cov3 cv = cov3_of(log_scale[i], rot[i]);
+    for (int v = 0; v < cams.n; v++) {
+      gs_memb mb = membership(cv, X.x, X.y, X.z, cams.c[v], geo.Wt, geo.Ht);
+      if (!mb.vis) continue;
+      unsigned dm = dest_mask(mb, v, geo, dp);
+      while (dm) {
+        int d = __ffs(dm) - 1;
+        dm &= dm - 1;
+        int k = d * cams.n + v;
+        set_bit(m, k);
+        atomicAdd(&s_c[k], 1);
+      }
+    }
+    for (int w = 0; w < NW; w++) maskw[(int64_t)w * n + i] = m[w];
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nb; k += kBlock) cta_cnt[(int64_t)k * ncta + blockIdx.x] = s_c[k];
+}
+
+__global__ void k_gather_totals(const int64_t* base, int64_t ncta, int b, int G, int64_t* out) {
+  int d = threadIdx.x;
+  if (d <= G) out[d] = base[(int64_t)d * b * ncta];
+}
+
+__global__ void __launch_bounds__(kBlock) k_project_write(
+    const float4* __restrict__ pos_op, const float4* __restrict__ log_scale,
+    const float4* __restrict__ rot, const float4* __restrict__ sh, int64_t n, int64_t gid_base,
+    gs_cams_arg cams, gs_geom geo, int G, int nb, int NW, const uint32_t* __restrict__ maskw,
+    const int64_t* __restrict__ base, int64_t ncta, gs_rec* __restrict__ out) {
+  __shared__ int s_cnt[kWarps * kMaxBuckets];
+  const int b = cams.n;
+  int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+  uint32_t m[kMaxWords], u[kMaxWords];
+  load_masks(maskw, n, i, NW, m);
+  cta_rank_phase1(m, u, NW, nb, s_cnt);
+  // view-independent parameters
+  float4 X = make_float4(0, 0, 0, 0), q = X, ls = X;
+  float shv[48];
+  if (i < n) {
+    X = pos_op[i];
+    ls = log_scale[i];
+    q = rot[i];
+#pragma unroll
+    for (int k = 0; k < 12; k++) {
+      float4 s4 = sh[(int64_t)k * n + i];
+      shv[4 * k] = s4.x; shv[4 * k + 1] = s4.y; shv[4 * k + 2] = s4.z; shv[4 * k + 3] = s4.w;
+    }
+  }
+  gs_cov3 cv = cov3_of(ls, q);
+  const float opac = 1.0f / (1.0f + __expf(-X.w));
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int v = 0; v < b; v++) {
+    if (!view_in_union(u, v, b, G)) continue;  // warp-uniform
+    bool mine = i < n && view_in_mask(m, v, b, G);
+    gs_rec rec;
+    if (mine) {
+      const gs_dcam& cam = cams.c[v];
+      gs_memb mb = membership(cv, X.x, X.y, X.z, cam, geo.Wt, geo.Ht);
+      // conic = inverse of the 2D covariance; store its Cholesky factor L (conic = L L^T):
+      // det by Kahan's difference of products, then l11 = sqrt(c)/sqrt(det),
+      // l21 = -b/(sqrt(det) sqrt(c)), l22 = 1/sqrt(c)  (well conditioned for thin Gaussians)
+      float bb = mb.b * mb.b;
+      float e = fmaf(-mb.b, mb.b, bb);
+      float det = fmaf(mb.a, mb.c, -bb) + e;
+      if (!(det > 0.f)) det = sub(mul(mb.a, mb.c), mul(mb.b, mb.b));
+      float sd = sqrtf(det), sc = sqrtf(mb.c);
+      float l11 = sc / sd, l21 = -mb.b / (sd * sc), l22 = 1.0f / sc;
+      // O9: colour from the view direction
+      float dx = X.x - cam.campos[0], dy = X.y - cam.campos[1], dz = X.z - cam.campos[2];
+      float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
+      float Y[16];
+      sh_basis(dx * inv, dy * inv, dz * inv, Y);
+      float col[3];
+#pragma unroll
+      for (int ch = 0; ch < 3; ch++) {
+        float s = 0.5f;
+#pragma unroll
+        for (int k = 0; k < 16; k++) s = fmaf(Y[k], shv[3 * k + ch], s);
+        col[ch] = fmaxf(s, 0.0f);
+      }
+      unsigned meta = (unsigned)((gid_base + i) * 32 + v);
+      rec.a = make_float4(mb.mx, mb.my, mb.depth, mb.r);
+      rec.b = make_float4(l11, l21, l22, opac);
+      rec.c = make_float4(col[0], col[1], col[2], __uint_as_float(meta));
+    }
+    for (int d = 0; d < G; d++) {
+      int k = d * b + v;
+      if (!get_bit(u, k)) continue;  // warp-uniform
+      bool bit = i < n && get_bit(m, k);
+      unsigned bal = __ballot_sync(0xffffffffu, bit);
+      if (bit) {
+        int64_t pos = base[(int64_t)k * ncta + blockIdx.x] + warp_prefix(s_cnt, wid, nb, k) +
+                      __popc(bal & lt);
+        out[pos] = rec;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" size_t gs_project_index_bytes(const gs_ctx* c, int64_t n, int n_views) {
+  if (!c || n < 0 || n_views < 1) return 0;
+  return index_layout(n, n_views, c->world).bytes;
+}
+
+extern "C" gs_status gs_project(gs_ctx* c, const gs_params* p, const gs_camera* cams_h,
+                                int n_views, const int64_t* dp_h, void* send_rec, int64_t send_cap,
+                                int64_t* send_counts_h, void* bwd_index, void* stream) {
+  if (!c) return GS_EINVAL;
+  gs_status s = gs_check_batch(c, cams_h, n_views, dp_h);
+  if (s != GS_OK) return s;
+  GS_REQUIRE(c, p && send_counts_h, "null argument");
+  const int G = c->world, b = n_views, nb = b * G;
+  GS_REQUIRE(c, nb <= kMaxBuckets, "n_views * world = %d exceeds %d", nb, kMaxBuckets);
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int d = 0; d < G; d++) send_counts_h[d] = 0;
+  if (p->n == 0) return GS_OK;
+  GS_REQUIRE(c, bwd_index && p->pos_op && p->log_scale && p->rot && p->sh, "null buffer");
+  gs_index_layout L = index_layout(p->n, b, G);
+  uint32_t* maskw = (uint32_t*)bwd_index;
+  int64_t* base = (int64_t*)((char*)bwd_index + L.base_off);
+  gs_cams_arg cams = make_cams(cams_h, n_views);
+  gs_geom geo = gs_make_geom(&cams_h[0]);
+  gs_dp_arg dp = gs_make_dp(c, dp_h);
+  GS_CUDA(c, cudaMemsetAsync(base + (int64_t)nb * L.ncta, 0, sizeof(int64_t), st));
+  ++c->launches;
+  k_project_count<<<(unsigned)L.ncta, kBlock, 0, st>>>(
+      (const float4*)p->pos_op, (const float4*)p->log_scale, (const float4*)p->rot, p->n, cams, geo,
+      dp, nb, L.NW, maskw, base, L.ncta);
+  GS_LAUNCH_CHECK(c, "project_count");
+  s = gs_scan_i64(c, base, base, (int64_t)nb * L.ncta + 1, 0, st);
+  if (s != GS_OK) return s;
+  int64_t* tot = (int64_t*)gs_slot_get(c, SLOT_PROJ_TMP, (GS_MAX_WORLD + 1) * sizeof(int64_t), st);
+  if (!tot) return gs_fail(c, GS_ECUDA, "scratch");
+  ++c->launches;
+  k_gather_totals<<<1, 64, 0, st>>>(base, L.ncta, b, G, tot);
+  GS_CUDA(c, cudaMemcpyAsync(c->pinned, tot, (G + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(c, cudaStreamSynchronize(st));
+  for (int d = 0; d < G; d++) send_counts_h[d] = c->pinned[d + 1] - c->pinned[d];
+  int64_t total = c->pinned[G];
+  if (total > send_cap)
+    return gs_fail(c, GS_ECAPACITY, "send capacity %lld < %lld records", (long long)send_cap,
+                   (long long)total);
+  if (total == 0) return GS_OK;
+  GS_REQUIRE(c, send_rec != nullptr, "null send_rec");
+  ++c->launches;
+  k_project_write<<<(unsigned)L.ncta, kBlock, 0, st>>>(
+      (const float4*)p->pos_op, (const float4*)p->log_scale, (const float4*)p->rot,
+      (const float4*)p->sh, p->n, p->gid_base, cams, geo, G, nb, L.NW, maskw, base, L.ncta,
+      (gs_rec*)send_rec);
+  GS_LAUNCH_CHECK(c, "project_write");
+  return GS_OK;
+}

@@ -1,0 +1,269 @@
+// gs_sort.cu -- A3: Z-buffer build ("iterates over intersecting Gaussians in
+// increasing depth"; App. A.2 "indices of intersecting gaussians for each pixel").
+//
+// B200 design (differs from the prior art's global (tile|depth) 64-bit radix sort):
+//  1. per-block list lengths without per-pair atomics: every record adds +1/-1 at the four
+//     corners of its tile rectangle in a 2D difference array of its view (4 atomics per
+//     record), a row scan and a column scan give each block's count;
+//  2. exclusive scan of the owned blocks' counts -> tile_range (host sync for capacity);
+//  3. placement: each record appends key = depth_bits << 32 | recv_idx to every owned block
+//     of its rectangle (one atomic cursor per pair);
+//  4. per-block sort of the keys in shared memory (bitonic, <= 4096 keys) or, for the rare
+//     longer lists, chunk sort + merge-path merges in global memory.
+// (depth, recv_idx) is unique within a block and recv_idx is ascending in gid within a
+// view (A1/A2 ordering), so the result is exactly the (depth, gid) order of O11 (R7)
+// whatever the placement order: no stable sort is needed.
+#include "gs_device.cuh"
+#include "gs_internal.h"
+
+using namespace gsd;
+
+namespace {
+
+constexpr int kSortThreads = 256;
+constexpr int kSmallCap = 4096;  // keys sorted in shared memory (32 KB)
+
+__global__ void k_rect_diff(const gs_rec* __restrict__ rec, int64_t n_recv, gs_geom geo, int v_lo,
+                            int v_hi, int* __restrict__ diff) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_recv) return;
+  float4 a = rec[j].a;
+  int v = (int)(__float_as_uint(rec[j].c.w) & 31u);
+  if (v < v_lo || v > v_hi) return;
+  int tx0, tx1, ty0, ty1;
+  if (!rect_of(a.x, a.y, a.w, geo.Wt, geo.Ht, tx0, tx1, ty0, ty1)) return;
+  const int ld = geo.Wt + 1;
+  int* D = diff + (int64_t)(v - v_lo) * (geo.Ht + 1) * ld;
+  atomicAdd(&D[ty0 * ld + tx0], 1);
+  atomicAdd(&D[ty0 * ld + tx1 + 1], -1);
+  atomicAdd(&D[(ty1 + 1) * ld + tx0], -1);
+  atomicAdd(&D[(ty1 + 1) * ld + tx1 + 1], 1);
+}
+
+__global__ void k_diff_rows(int* diff, int nrows, int ld) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrows) return;
+  int* p = diff + (int64_t)r * ld;
+  int s = 0;
+  for (int x = 0; x < ld; x++) p[x] = (s += p[x]);
+}
+
+__global__ void k_diff_cols(int* diff, int nviews, int rows, int ld) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nviews * ld) return;
+  int v = t / ld, x = t % ld;
+  int* p = diff + (int64_t)v * rows * ld + x;
+  int s = 0;
+  for (int y = 0; y < rows; y++) p[(int64_t)y * ld] = (s += p[(int64_t)y * ld]);
+}
+
+__global__ void k_owned_counts(const int* diff, gs_geom geo, int64_t B_lo, int64_t n_owned, int v_lo,
+                               int64_t* counts) {
+  int64_t lb = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (lb > n_owned) return;
+  if (lb == n_owned) { counts[lb] = 0; return; }
+  int64_t beta = B_lo + lb, v = beta / geo.per_view, loc = beta % geo.per_view;
+  int tx = (int)(loc % geo.Wt), ty = (int)(loc / geo.Wt);
+  counts[lb] = diff[((v - v_lo) * (geo.Ht + 1) + ty) * (int64_t)(geo.Wt + 1) + tx];
+}
+
+__global__ void k_to_range(const int64_t* off, int64_t n_owned, int32_t* range, int32_t* cursor) {
+  int64_t lb = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (lb > n_owned) return;
+  range[lb] = (int32_t)off[lb];
+  if (lb < n_owned) cursor[lb] = (int32_t)off[lb];
+}
+
+__global__ void k_place(const gs_rec* __restrict__ rec, int64_t n_recv, gs_geom geo, int64_t B_lo,
+                        int64_t B_hi, int32_t* __restrict__ cursor, unsigned long long* __restrict__ keys) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_recv) return;
+  float4 a = rec[j].a;
+  int v = (int)(__float_as_uint(rec[j].c.w) & 31u);
+  int tx0, tx1, ty0, ty1;
+  if (!rect_of(a.x, a.y, a.w, geo.Wt, geo.Ht, tx0, tx1, ty0, ty1)) return;
+  const unsigned long long hi = (unsigned long long)__float_as_uint(a.z) << 32;
+  const int64_t vb = (int64_t)v * geo.per_view;
+  // owned rows only
+  int ylo = ty0, yhi = ty1;
+  if (vb + (int64_t)ty0 * geo.Wt + tx1 < B_lo) ylo = (int)max((int64_t)ty0, (B_lo - vb - tx1 + geo.Wt - 1) / geo.Wt);
+  for (int ty = ylo; ty <= yhi; ty++) {
+    int64_t row = vb + (int64_t)ty * geo.Wt;
+    if (row + tx0 >= B_hi) break;
+    for (int tx = tx0; tx <= tx1; tx++) {
+      int64_t beta = row + tx;
+      if (beta < B_lo) continue;
+      if (beta >= B_hi) break;
+      int pos = atomicAdd(&cursor[beta - B_lo], 1);
+      keys[pos] = hi | (unsigned long long)j;
+    }
+  }
+}
+
+__device__ __forceinline__ void bitonic_smem(unsigned long long* s, int P) {
+  for (int k = 2; k <= P; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < P / 2; t += kSortThreads) {
+        int i = (t / j) * 2 * j + (t % j), l = i + j;
+        bool up = (i & k) == 0;
+        unsigned long long x = s[i], y = s[l];
+        if ((x > y) == up) { s[i] = y; s[l] = x; }
+      }
+      __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_small(const int32_t* __restrict__ range,
+                                                             int64_t n_owned, const unsigned long long* __restrict__ keys,
+                                                             uint32_t* __restrict__ sorted_idx,
+                                                             int32_t* large_list, int32_t* n_large) {
+  __shared__ unsigned long long s[kSmallCap];
+  int64_t lb = blockIdx.x;
+  int beg = range[lb], n = range[lb + 1] - beg;
+  if (n == 0) return;
+  if (n > kSmallCap) {
+    if (threadIdx.x == 0) large_list[atomicAdd(n_large, 1)] = (int32_t)lb;
+    return;
+  }
+  if (n == 1) {
+    if (threadIdx.x == 0) sorted_idx[beg] = (uint32_t)keys[beg];
+    return;
+  }
+  int P = 2;
+  while (P < n) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += kSortThreads) s[i] = i < n ? keys[beg + i] : ~0ull;
+  __syncthreads();
+  bitonic_smem(s, P);
+  for (int i = threadIdx.x; i < n; i += kSortThreads) sorted_idx[beg + i] = (uint32_t)s[i];
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_large(const int32_t* __restrict__ range,
+                                                             unsigned long long* keys,
+                                                             unsigned long long* tmp,
+                                                             uint32_t* __restrict__ sorted_idx,
+                                                             const int32_t* large_list,
+                                                             const int32_t* n_large, int32_t* next) {
+  __shared__ unsigned long long s[kSmallCap];
+  __shared__ int s_item;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(next, 1);
+    __syncthreads();
+    int item = s_item;
+    __syncthreads();
+    if (item >= *n_large) return;
+    int lb = large_list[item];
+    int beg = range[lb], n = range[lb + 1] - beg;
+    unsigned long long* src = keys + beg;
+    unsigned long long* dst = tmp + beg;
+    // 1. sort chunks of kSmallCap in shared memory
+    for (int c0 = 0; c0 < n; c0 += kSmallCap) {
+      int m = min(kSmallCap, n - c0);
+      for (int i = threadIdx.x; i < kSmallCap; i += kSortThreads) s[i] = i < m ? src[c0 + i] : ~0ull;
+      __syncthreads();
+      bitonic_smem(s, kSmallCap);
+      for (int i = threadIdx.x; i < m; i += kSortThreads) src[c0 + i] = s[i];
+      __syncthreads();
+    }
+    // 2. merge-path merges of sorted runs, ping-pong src <-> dst
+    for (int w = kSmallCap; w < n; w <<= 1) {
+      for (int p0 = 0; p0 < n; p0 += 2 * w) {
+        int na = min(w, n - p0), nbb = max(0, min(w, n - p0 - w));
+        const unsigned long long* A = src + p0;
+        const unsigned long long* Bv = src + p0 + na;
+        int L = na + nbb, per = (L + kSortThreads - 1) / kSortThreads;
+        int d0 = min(L, (int)threadIdx.x * per), d1 = min(L, d0 + per);
+        // diagonal search: i = elements taken from A among the first d0 outputs
+        int lo = max(0, d0 - nbb), hi = min(d0, na);
+        while (lo < hi) {
+          int mid = (lo + hi) >> 1;
+          if (A[mid] < Bv[d0 - 1 - mid]) lo = mid + 1; else hi = mid;
+        }
+        int ia = lo, ib = d0 - lo;
+        for (int d = d0; d < d1; d++) {
+          bool takeA = ib >= nbb || (ia < na && A[ia] < Bv[ib]);
+          dst[p0 + d] = takeA ? A[ia++] : Bv[ib++];
+        }
+      }
+      __syncthreads();
+      unsigned long long* t = src; src = dst; dst = t;
+    }
+    for (int i = threadIdx.x; i < n; i += kSortThreads) sorted_idx[beg + i] = (uint32_t)src[i];
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv, const gs_camera* cams_h,
+                                 int n_views, const int64_t* dp_h, uint32_t* sorted_idx, int64_t pair_cap,
+                                 int32_t* tile_range, int64_t* n_pairs_h, void* stream) {
+  if (!c) return GS_EINVAL;
+  gs_status s = gs_check_batch(c, cams_h, n_views, dp_h);
+  if (s != GS_OK) return s;
+  GS_REQUIRE(c, tile_range && n_pairs_h, "null argument");
+  GS_REQUIRE(c, n_recv >= 0 && n_recv < (1ll << 32), "n_recv out of range");
+  cudaStream_t st = (cudaStream_t)stream;
+  gs_geom geo = gs_make_geom(&cams_h[0]);
+  const int64_t B_lo = dp_h[c->rank], B_hi = dp_h[c->rank + 1], n_owned = B_hi - B_lo;
+  *n_pairs_h = 0;
+  if (n_owned == 0) {
+    GS_CUDA(c, cudaMemsetAsync(tile_range, 0, sizeof(int32_t), st));
+    return GS_OK;
+  }
+  const int v_lo = (int)(B_lo / geo.per_view), v_hi = (int)((B_hi - 1) / geo.per_view);
+  const int nvl = v_hi - v_lo + 1;
+  const int64_t diff_n = (int64_t)nvl * (geo.Ht + 1) * (geo.Wt + 1);
+  int* diff = (int*)gs_slot_get(c, SLOT_DIFF, diff_n * sizeof(int), st);
+  int64_t* counts = (int64_t*)gs_slot_get(c, SLOT_COUNTS, (n_owned + 1) * sizeof(int64_t), st);
+  int32_t* cursor = (int32_t*)gs_slot_get(c, SLOT_CURSOR, (n_owned + 1) * sizeof(int32_t), st);
+  int32_t* large = (int32_t*)gs_slot_get(c, SLOT_LARGE, (n_owned + 8) * sizeof(int32_t), st);
+  if (!diff || !counts || !cursor || !large) return gs_fail(c, GS_ECUDA, "scratch");
+  GS_CUDA(c, cudaMemsetAsync(diff, 0, diff_n * sizeof(int), st));
+  if (n_recv > 0) {
+    GS_REQUIRE(c, recv_rec != nullptr, "null recv_rec");
+    ++c->launches;
+    k_rect_diff<<<(unsigned)((n_recv + 255) / 256), 256, 0, st>>>((const gs_rec*)recv_rec, n_recv, geo,
+                                                                  v_lo, v_hi, diff);
+  }
+  const int ld = geo.Wt + 1, rows = geo.Ht + 1;
+  ++c->launches;
+  k_diff_rows<<<(nvl * rows + 127) / 128, 128, 0, st>>>(diff, nvl * rows, ld);
+  ++c->launches;
+  k_diff_cols<<<(nvl * ld + 127) / 128, 128, 0, st>>>(diff, nvl, rows, ld);
+  ++c->launches;
+  k_owned_counts<<<(unsigned)((n_owned + 256) / 256), 256, 0, st>>>(diff, geo, B_lo, n_owned, v_lo, counts);
+  GS_LAUNCH_CHECK(c, "bin_sort counts");
+  s = gs_scan_i64(c, counts, counts, n_owned + 1, 0, st);
+  if (s != GS_OK) return s;
+  GS_CUDA(c, cudaMemcpyAsync(c->pinned, counts + n_owned, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(c, cudaStreamSynchronize(st));
+  const int64_t K = c->pinned[0];
+  *n_pairs_h = K;
+  if (K > pair_cap || K >= (1ll << 31))
+    return gs_fail(c, GS_ECAPACITY, "pair capacity %lld < %lld", (long long)pair_cap, (long long)K);
+  ++c->launches;
+  k_to_range<<<(unsigned)((n_owned + 256) / 256), 256, 0, st>>>(counts, n_owned, tile_range, cursor);
+  GS_LAUNCH_CHECK(c, "bin_sort range");
+  if (K == 0) return GS_OK;
+  GS_REQUIRE(c, sorted_idx != nullptr, "null sorted_idx");
+  unsigned long long* keys = (unsigned long long*)gs_slot_get(c, SLOT_KEYS, K * sizeof(unsigned long long), st);
+  if (!keys) return gs_fail(c, GS_ECUDA, "key scratch (%lld pairs)", (long long)K);
+  ++c->launches;
+  k_place<<<(unsigned)((n_recv + 255) / 256), 256, 0, st>>>((const gs_rec*)recv_rec, n_recv, geo, B_lo, B_hi,
+                                                            cursor, keys);
+  GS_CUDA(c, cudaMemsetAsync(large + n_owned, 0, 8 * sizeof(int32_t), st));
+  int32_t* n_large = large + n_owned;
+  ++c->launches;
+  k_sort_small<<<(unsigned)n_owned, kSortThreads, 0, st>>>(tile_range, n_owned, keys, sorted_idx, large,
+                                                          n_large);
+  GS_LAUNCH_CHECK(c, "bin_sort small");
+  unsigned long long* tmp = (unsigned long long*)gs_slot_get(c, SLOT_KEYS_TMP, K * sizeof(unsigned long long), st);
+  if (!tmp) return gs_fail(c, GS_ECUDA, "merge scratch");
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
+  ++c->launches;
+  k_sort_large<<<dev_sms, kSortThreads, 0, st>>>(tile_range, keys, tmp, sorted_idx, large, n_large,
+                                                  n_large + 1);
+  GS_LAUNCH_CHECK(c, "bin_sort large");
+  return GS_OK;
+}

@@ -1,0 +1,182 @@
+"""The training-step driver: one Grendel step per call (P:101-115 pipeline, P:190 mixed
+parallelism, P:200-226 rebalancing), issuing the libgs C-ABI calls of CS1 in order on one
+CUDA stream.  Buffers are torch CUDA tensors owned here and grown on GS_ECAPACITY.
+This is the public API ``bench.py`` and the e2e measurement call.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+# 3DGS default learning rates ("default hyperparameters from the 3DGS repository";
+# values as S:349 lists them): pos, sh_dc, sh_rest, opacity, scale, rot
+DEFAULT_LR = (1.6e-4, 2.5e-3, 1.25e-4, 5e-2, 5e-3, 1e-3)
+
+
+def uniform_dp(B: int, G: int) -> np.ndarray:
+    """Cold start: uniform block partition."""
+    return np.array([g * B // G for g in range(G + 1)], np.int64)
+
+
+class _Buf:
+    """A growable torch buffer (capacity in elements of `row` shape)."""
+
+    def __init__(self, device, dtype, row=(), cap=0):
+        self.device, self.dtype, self.row, self.t, self.cap = device, dtype, tuple(row), None, 0
+        if cap:
+            self.ensure(cap)
+
+    def ensure(self, n):
+        if n > self.cap:
+            cap = max(int(n * 1.25) + 1024, 1024)
+            self.t = torch.empty((cap,) + self.row, dtype=self.dtype, device=self.device)
+            self.cap = cap
+        return self.t
+
+
+class GrendelTrainer:
+    def __init__(self, ctx: L.Context, params: L.GaussianParams, width: int, height: int, n_views: int,
+                 n_images: int, lr=DEFAULT_LR, cost_mode=L.COST_MEASURED, bg=(0.0, 0.0, 0.0),
+                 rebalance=True, dp=None, device=None):
+        self.ctx, self.p = ctx, params
+        self.device = device or params.pos_op.device
+        self.W, self.H, self.b = width, height, n_views
+        self.Wt, self.Ht = (width + 15) // 16, (height + 15) // 16
+        self.B = n_views * self.Wt * self.Ht
+        self.G, self.rank = ctx.world, ctx.rank
+        self.lr, self.cost_mode, self.bg, self.do_rebalance = tuple(lr), cost_mode, tuple(bg), rebalance
+        self.m, self.v = params.zeros_like(), params.zeros_like()
+        self.dp = uniform_dp(self.B, self.G) if dp is None else np.asarray(dp, np.int64)
+        self.history = torch.full((n_images, self.Wt * self.Ht), -1, dtype=torch.int64, device=self.device)
+        self.n_images = n_images
+        self.step_count = 0
+        dev = self.device
+        self.bwd_index = torch.empty(L.project_index_bytes(ctx, params.n, n_views), dtype=torch.uint8, device=dev)
+        self.send = _Buf(dev, torch.uint8, (L.RECORD_BYTES,))
+        self.recv = _Buf(dev, torch.uint8, (L.RECORD_BYTES,))
+        self.sorted = _Buf(dev, torch.int32)
+        self.range = _Buf(dev, torch.int32)
+        self.T = _Buf(dev, torch.float32, (256,))
+        self.nl = _Buf(dev, torch.int32, (256,))
+        self.dpix = _Buf(dev, torch.float32, (3, 256))
+        self.cost = _Buf(dev, torch.int64)
+        self.drec = _Buf(dev, torch.float32, (L.GRAD_FLOATS,))
+        self.dsend = _Buf(dev, torch.float32, (L.GRAD_FLOATS,))
+        self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.stats = torch.zeros(8, dtype=torch.int64, device=dev)
+        self.last = {}
+
+    @property
+    def n_owned(self):
+        return int(self.dp[self.rank + 1] - self.dp[self.rank])
+
+    def step(self, cams, gt, next_cams=None, stream=None, events=None, collect_stats=False):
+        """One training step on the batch `cams` (len == n_views) with ground truth `gt`
+        (uint8 CUDA tensor [n_views, H, W, 3]).  Returns the loss tensor (device, fp64).
+        events: optional dict name -> (start, end) torch.cuda.Event pairs to record per call."""
+        ctx, dp, st = self.ctx, self.dp, stream
+        ev = events if events is not None else {}
+
+        def rec(name, k):
+            if name in ev:
+                ev[name][k].record(torch.cuda.current_stream() if st is None else st)
+
+        self.step_count += 1
+        # A1 project (retry on capacity)
+        rec("project", 0)
+        cap = self.send.cap
+        while True:
+            try:
+                send_counts = L.project(ctx, self.p, cams, dp, self.send.t, cap, self.bwd_index, st)
+                break
+            except L.CapacityError as e:
+                cap = int(e.counts.sum())
+                self.send.ensure(cap)
+                cap = self.send.cap
+        rec("project", 1)
+        n_send = int(send_counts.sum())
+        # A2 exchange
+        rec("exchange", 0)
+        if self.G == 1:
+            recv_t, recv_counts, n_recv = self.send.t, send_counts.copy(), n_send
+        else:
+            while True:
+                try:
+                    recv_counts, n_recv = L.exchange(ctx, self.send.t, send_counts, self.recv.t, self.recv.cap, st)
+                    break
+                except L.CapacityError as e:
+                    self.recv.ensure(e.needed)
+            recv_t = self.recv.t
+        rec("exchange", 1)
+        # A3 bin + sort
+        rec("bin_sort", 0)
+        no = self.n_owned
+        self.range.ensure(no + 1)
+        while True:
+            try:
+                n_pairs = L.bin_sort(ctx, recv_t, n_recv, cams, dp, self.sorted.t, self.sorted.cap,
+                                     self.range.t, st)
+                break
+            except L.CapacityError as e:
+                self.sorted.ensure(e.needed)
+        rec("bin_sort", 1)
+        # A4 render forward + fused L1
+        self.T.ensure(no), self.nl.ensure(no), self.dpix.ensure(no), self.cost.ensure(no)
+        self.drec.ensure(n_recv), self.dsend.ensure(n_send)
+        self.cost.t[:no].zero_()
+        self.loss.zero_()
+        stats = None
+        if collect_stats:
+            self.stats.zero_()
+            stats = self.stats
+        rec("render_fwd", 0)
+        L.render_fwd(ctx, recv_t, self.sorted.t, self.range.t, cams, dp, self.bg, gt, self.b, None, self.T.t,
+                     self.nl.t, self.dpix.t, self.loss, self.cost.t, self.cost_mode, stats, st)
+        rec("render_fwd", 1)
+        # A5 render backward
+        rec("render_bwd", 0)
+        L.render_bwd(ctx, recv_t, n_recv, self.sorted.t, self.range.t, cams, dp, self.bg, self.dpix.t, self.T.t,
+                     self.nl.t, self.drec.t, self.cost.t, self.cost_mode, stats, st)
+        rec("render_bwd", 1)
+        # A6 reverse exchange
+        rec("exchange_grads", 0)
+        if self.G == 1:
+            dsend = self.drec.t
+        else:
+            L.exchange_grads(ctx, self.drec.t, recv_counts, send_counts, self.dsend.t, st)
+            dsend = self.dsend.t
+        rec("exchange_grads", 1)
+        # A7 + A8 transformation backward + Adam
+        rec("adam", 0)
+        hp = L.adam_hparams(self.lr, self.b, self.step_count)
+        L.adam_step(ctx, self.p, self.m, self.v, None, cams, dp, dsend, self.bwd_index, hp,
+                    L.ADAM_GRAD | L.ADAM_APPLY, st)
+        rec("adam", 1)
+        # A9 rebalance for the next batch
+        rec("rebalance", 0)
+        if self.do_rebalance and next_cams is not None:
+            self.dp = L.rebalance(ctx, self.cost.t, cams, dp, self.history, self.n_images, self.cost_mode,
+                                  next_cams, st)
+        rec("rebalance", 1)
+        self.last = dict(n_send=n_send, n_recv=n_recv, n_pairs=n_pairs, send_counts=send_counts,
+                         recv_counts=recv_counts, n_owned=no)
+        return self.loss
+
+
+def make_events(names=("project", "exchange", "bin_sort", "render_fwd", "render_bwd", "exchange_grads", "adam",
+                       "rebalance")):
+    return {n: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for n in names}
+
+
+def event_ms(events):
+    return {n: s.elapsed_time(e) for n, (s, e) in events.items()}
+
+
+def position_lr(step, lr_init=1.6e-4, lr_final=1.6e-6, max_steps=30000, extent=1.0):
+    """Host-side exponential position-lr schedule, log-linear interpolation."""
+    t = min(max(step / max(max_steps, 1), 0.0), 1.0)
+    return extent * math.exp(math.log(lr_init) * (1 - t) + math.log(lr_final) * t)

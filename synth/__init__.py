@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import dataclasses
 import math
+import os
 
 import numpy as np
 
@@ -132,20 +133,35 @@ def _finish(pos, ls, rot, op, sh, gid_base) -> Scene:
                  np.ascontiguousarray(sh, np.float32), gid_base)
 
 
-def _chunked(seed, n_total, lo, hi, draw_chunk) -> Scene:
-    """Draw gids [lo, hi) chunk by chunk (each chunk from its own Philox key)."""
-    parts = []
+def _chunk_job(args):
+    kind, seed, n_total, c = args
+    g0, g1 = c * CHUNK, min((c + 1) * CHUNK, n_total)
+    return _DRAW[kind](_rng(seed, _S_COMP, c), g0, g1, seed, n_total)
+
+
+def _chunked(kind, seed, n_total, lo, hi) -> Scene:
+    """Draw gids [lo, hi) chunk by chunk (each chunk from its own Philox key, so the result
+    does not depend on how the range is split); chunks are drawn in parallel processes."""
     c0, c1 = lo // CHUNK, (hi + CHUNK - 1) // CHUNK
-    for c in range(c0, c1):
-        g0, g1 = c * CHUNK, min((c + 1) * CHUNK, n_total)
-        sc = draw_chunk(_rng(seed, _S_COMP, c), g0, g1)
-        a, b = max(lo, g0) - g0, min(hi, g1) - g0
-        parts.append(sc.slice(a, b))
-    cat = lambda k: np.concatenate([getattr(p, k) for p in parts]) if parts else None
+    jobs = [(kind, seed, n_total, c) for c in range(c0, c1)]
+    if len(jobs) > 1:
+        import concurrent.futures as cf
+        import multiprocessing as mp
+        with cf.ProcessPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1),
+                                    mp_context=mp.get_context("fork")) as ex:
+            chunks = list(ex.map(_chunk_job, jobs))
+    else:
+        chunks = [_chunk_job(j) for j in jobs]
+    parts = []
+    for c, sc in zip(range(c0, c1), chunks):
+        g0 = c * CHUNK
+        g1 = g0 + sc.n
+        parts.append(sc.slice(max(lo, g0) - g0, min(hi, g1) - g0))
     if not parts:
         z = np.zeros
         return Scene(z((0, 3), np.float32), z((0, 3), np.float32), z((0, 4), np.float32),
                      z((0,), np.float32), z((0, 16, 3), np.float32), lo)
+    cat = lambda k: np.concatenate([getattr(p, k) for p in parts])
     return Scene(cat("pos"), cat("log_scale"), cat("rot"), cat("opac_logit"), cat("sh"), lo)
 
 
@@ -184,16 +200,15 @@ def _terrain_n(x, y):
 
 def scene_rubble(n_total=11_200_000, seed=2, lo=0, hi=None) -> Scene:
     """C2/C3 Rubble-shaped terrain over [-1,1]^2."""
-    hi = n_total if hi is None else hi
+    return _chunked("rubble", seed, n_total, lo, n_total if hi is None else hi)
+
+
+def _draw_rubble(rng, g0, g1, seed, n_total):
+    n = g1 - g0
     d_loc = math.sqrt(4.0 / n_total)
-
-    def draw(rng, g0, g1):
-        n = g1 - g0
-        x, y = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
-        pts = np.stack([x, y, _terrain_h(x, y)], 1)
-        return _finish(*_surface_attrs(rng, pts, _terrain_n(x, y), np.full(n, d_loc), n), g0)
-
-    return _chunked(seed, n_total, lo, hi, draw)
+    x, y = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    pts = np.stack([x, y, _terrain_h(x, y)], 1)
+    return _finish(*_surface_attrs(rng, pts, _terrain_n(x, y), np.full(n, d_loc), n), g0)
 
 
 def cameras_rubble(n_pool=64, seed=2, width=4591, height=3436):
@@ -214,34 +229,35 @@ def cameras_rubble(n_pool=64, seed=2, width=4591, height=3436):
 def scene_garden(n_total=5_000_000, seed=1, lo=0, hi=None) -> Scene:
     """C1: 45% ground disk r=1.6, 40% ellipsoid shell (.35,.35,.28) at (0,0,.3),
     15% background dome r=4."""
-    hi = n_total if hi is None else hi
+    return _chunked("garden", seed, n_total, lo, n_total if hi is None else hi)
+
+
+def _draw_garden(rng, g0, g1, seed, n_total):
     areas = np.array([math.pi * 1.6 ** 2, 4 * math.pi * 0.33 ** 2, 2 * math.pi * 16.0])
     frac = np.array([0.45, 0.40, 0.15])
     d_comp = np.sqrt(areas / (frac * n_total))
+    n = g1 - g0
+    comp = np.searchsorted(np.cumsum(frac), rng.random(n), side="right").clip(0, 2)
+    pts, nrm = np.zeros((n, 3)), np.zeros((n, 3))
+    m = comp == 0
+    r, th = 1.6 * np.sqrt(rng.random(m.sum())), rng.uniform(0, 2 * math.pi, m.sum())
+    pts[m] = np.stack([r * np.cos(th), r * np.sin(th), np.zeros_like(r)], 1)
+    nrm[m] = [0, 0, 1]
+    m = comp == 1
+    u = rng.normal(size=(m.sum(), 3))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    ax = np.array([.35, .35, .28])
+    pts[m] = u * ax + [0, 0, .3]
+    g = u / ax
+    nrm[m] = g / np.linalg.norm(g, axis=1, keepdims=True)
+    m = comp == 2
+    u = rng.normal(size=(m.sum(), 3))
+    u[:, 2] = np.abs(u[:, 2])
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    pts[m], nrm[m] = 4.0 * u, -u
+    return _finish(*_surface_attrs(rng, pts, nrm, d_comp[comp], n), g0)
 
-    def draw(rng, g0, g1):
-        n = g1 - g0
-        comp = np.searchsorted(np.cumsum(frac), rng.random(n), side="right").clip(0, 2)
-        pts, nrm = np.zeros((n, 3)), np.zeros((n, 3))
-        m = comp == 0
-        r, th = 1.6 * np.sqrt(rng.random(m.sum())), rng.uniform(0, 2 * math.pi, m.sum())
-        pts[m] = np.stack([r * np.cos(th), r * np.sin(th), np.zeros_like(r)], 1)
-        nrm[m] = [0, 0, 1]
-        m = comp == 1
-        u = rng.normal(size=(m.sum(), 3))
-        u /= np.linalg.norm(u, axis=1, keepdims=True)
-        ax = np.array([.35, .35, .28])
-        pts[m] = u * ax + [0, 0, .3]
-        g = u / ax
-        nrm[m] = g / np.linalg.norm(g, axis=1, keepdims=True)
-        m = comp == 2
-        u = rng.normal(size=(m.sum(), 3))
-        u[:, 2] = np.abs(u[:, 2])
-        u /= np.linalg.norm(u, axis=1, keepdims=True)
-        pts[m], nrm[m] = 4.0 * u, -u
-        return _finish(*_surface_attrs(rng, pts, nrm, d_comp[comp], n), g0)
 
-    return _chunked(seed, n_total, lo, hi, draw)
 
 
 def cameras_garden(n_pool=64, seed=1, width=1920, height=1080):
@@ -266,7 +282,10 @@ def _city_heights(seed):
 def scene_city(n_total=24_000_000, seed=4, lo=0, hi=None) -> Scene:
     """C4: 45% ground [-1,1]^2; 55% on the 5 faces of a 20x20 grid of box buildings
     (half-width .03, heights U(.02,.12))."""
-    hi = n_total if hi is None else hi
+    return _chunked("city", seed, n_total, lo, n_total if hi is None else hi)
+
+
+def _draw_city(rng, g0, g1, seed, n_total):
     H = _city_heights(seed)
     hw = 0.03
     side = 2 * hw * H  # area of one side face per building
@@ -277,36 +296,35 @@ def scene_city(n_total=24_000_000, seed=4, lo=0, hi=None) -> Scene:
     d_ground = math.sqrt(4.0 / (0.45 * n_total))
     d_bld = math.sqrt(fa.sum() / (0.55 * n_total))
 
-    def draw(rng, g0, g1):
-        n = g1 - g0
-        ground = rng.random(n) < 0.45
-        pts, nrm = np.zeros((n, 3)), np.zeros((n, 3))
-        k = ground.sum()
-        pts[ground] = np.stack([rng.uniform(-1, 1, k), rng.uniform(-1, 1, k), np.zeros(k)], 1)
-        nrm[ground] = [0, 0, 1]
-        m = ~ground
-        k = m.sum()
-        f = np.searchsorted(fcum, rng.random(k), side="right").clip(0, fa.size - 1)
-        b, face = f // 5, f % 5
-        bx, by = _CITY[b // 20], _CITY[b % 20]
-        h = H.reshape(-1)[b]
-        u, v = rng.uniform(-1, 1, k), rng.random(k)
-        p = np.zeros((k, 3))
-        q = np.zeros((k, 3))
-        for fi, (nx, ny) in enumerate([(1, 0), (-1, 0), (0, 1), (0, -1)]):
-            s = face == fi
-            p[s, 0] = bx[s] + (nx * hw if nx else u[s] * hw)
-            p[s, 1] = by[s] + (ny * hw if ny else u[s] * hw)
-            p[s, 2] = v[s] * h[s]
-            q[s] = [nx, ny, 0]
-        s = face == 4
-        p[s] = np.stack([bx[s] + u[s] * hw, by[s] + rng.uniform(-1, 1, s.sum()) * hw, h[s]], 1)
-        q[s] = [0, 0, 1]
-        pts[m], nrm[m] = p, q
-        d = np.where(ground, d_ground, d_bld)
-        return _finish(*_surface_attrs(rng, pts, nrm, d, n), g0)
+    n = g1 - g0
+    ground = rng.random(n) < 0.45
+    pts, nrm = np.zeros((n, 3)), np.zeros((n, 3))
+    k = ground.sum()
+    pts[ground] = np.stack([rng.uniform(-1, 1, k), rng.uniform(-1, 1, k), np.zeros(k)], 1)
+    nrm[ground] = [0, 0, 1]
+    m = ~ground
+    k = m.sum()
+    f = np.searchsorted(fcum, rng.random(k), side="right").clip(0, fa.size - 1)
+    b, face = f // 5, f % 5
+    bx, by = _CITY[b // 20], _CITY[b % 20]
+    h = H.reshape(-1)[b]
+    u, v = rng.uniform(-1, 1, k), rng.random(k)
+    p = np.zeros((k, 3))
+    q = np.zeros((k, 3))
+    for fi, (nx, ny) in enumerate([(1, 0), (-1, 0), (0, 1), (0, -1)]):
+        s = face == fi
+        p[s, 0] = bx[s] + (nx * hw if nx else u[s] * hw)
+        p[s, 1] = by[s] + (ny * hw if ny else u[s] * hw)
+        p[s, 2] = v[s] * h[s]
+        q[s] = [nx, ny, 0]
+    s = face == 4
+    p[s] = np.stack([bx[s] + u[s] * hw, by[s] + rng.uniform(-1, 1, s.sum()) * hw, h[s]], 1)
+    q[s] = [0, 0, 1]
+    pts[m], nrm[m] = p, q
+    d = np.where(ground, d_ground, d_bld)
+    return _finish(*_surface_attrs(rng, pts, nrm, d, n), g0)
 
-    return _chunked(seed, n_total, lo, hi, draw)
+
 
 
 def cameras_city(n_pool=128, seed=4, width=1920, height=1080):
@@ -367,6 +385,8 @@ def batch_schedule(n_pool: int, b: int, steps: int, seed: int):
         out.append(batch)
     return out
 
+
+_DRAW = {"rubble": _draw_rubble, "garden": _draw_garden, "city": _draw_city}
 
 CONFIGS = {
     "C0": dict(n=1000, b=1, size=(64, 64)),

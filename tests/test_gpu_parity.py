@@ -1,0 +1,307 @@
+"""GPU parity: libgs (CUDA sm_100a, through the C ABI) against the CPU oracle on the same
+seeded inputs (SURVEY §8(c) comparison protocol):
+  bit-exact   visibility, mean2d, depth, radius, exchange sets and their order, per-block
+              sorted lists, n_last on unflagged pixels, DP given ET, partitioned == whole;
+  1e-4 abs    pixel colours / transmittance on unflagged pixels;
+  1e-3 (#31)  record gradients, parameter gradients, Adam updates (per group: max-norm and
+              2-norm of the error relative to those of the oracle).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests.gsutil import block_major, conic_of, decode_records, grad_metric
+
+L = pytest.importorskip("paper_2406_18533_b200._lib")
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+FLAG_EPS = 1e-5
+
+
+def params_of(scene, device=DEV):
+    return L.GaussianParams.from_arrays(scene.pos, scene.log_scale, scene.rot, scene.opac_logit, scene.sh,
+                                        device, scene.gid_base)
+
+
+class Run:
+    """Step-by-step G=1 (or virtual-rank) pipeline through the C ABI."""
+
+    def __init__(self, scene, cams, bg=(0, 0, 0), gt=None, cost_mode=L.COST_WORK, world=1, rank=0, dp=None,
+                 upstream=None):
+        self.ctx = L.Context(0, rank, world)
+        self.cams = cams
+        self.W, self.H = cams[0].width, cams[0].height
+        self.Wt, self.Ht = (self.W + 15) // 16, (self.H + 15) // 16
+        self.B = len(cams) * self.Wt * self.Ht
+        self.dp = np.array(dp if dp is not None else [0, self.B], np.int64)
+        self.p = params_of(scene)
+        self.idx = torch.empty(L.project_index_bytes(self.ctx, self.p.n, len(cams)), dtype=torch.uint8, device=DEV)
+        try:
+            self.send_counts = L.project(self.ctx, self.p, cams, self.dp, None, 0, self.idx)
+            cap = int(self.send_counts.sum())
+        except L.CapacityError as e:
+            cap = int(e.counts.sum())
+        self.send = torch.empty((max(cap, 1), 48), dtype=torch.uint8, device=DEV)
+        self.send_counts = L.project(self.ctx, self.p, cams, self.dp, self.send, cap, self.idx)
+        self.n_send = int(self.send_counts.sum())
+        self.bg, self.gt, self.cost_mode = bg, gt, cost_mode
+
+    def render(self, recv, n_recv, upstream=None):
+        ctx, dp = self.ctx, self.dp
+        self.recv, self.n_recv = recv, n_recv
+        no = int(dp[ctx.rank + 1] - dp[ctx.rank])
+        self.no = no
+        self.range = torch.empty(no + 1, dtype=torch.int32, device=DEV)
+        try:
+            npairs = L.bin_sort(ctx, recv, n_recv, self.cams, dp, None, 0, self.range)
+        except L.CapacityError as e:
+            npairs = e.needed
+        self.sorted = torch.empty(max(npairs, 1), dtype=torch.int32, device=DEV)
+        self.n_pairs = L.bin_sort(ctx, recv, n_recv, self.cams, dp, self.sorted, npairs, self.range)
+        self.T = torch.empty(no * 256, dtype=torch.float32, device=DEV)
+        self.nl = torch.empty(no * 256, dtype=torch.int32, device=DEV)
+        self.rgb = torch.empty(no * 768, dtype=torch.float32, device=DEV)
+        self.dpix = torch.zeros(no * 768, dtype=torch.float32, device=DEV)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=DEV)
+        self.cost = torch.zeros(no, dtype=torch.int64, device=DEV)
+        self.stats = torch.zeros(8, dtype=torch.int64, device=DEV)
+        gt_t = torch.from_numpy(self.gt).to(DEV) if self.gt is not None else None
+        L.render_fwd(ctx, recv, self.sorted, self.range, self.cams, dp, self.bg, gt_t, len(self.cams), self.rgb,
+                     self.T, self.nl, self.dpix if gt_t is not None else None, self.loss, self.cost,
+                     self.cost_mode, self.stats)
+        if upstream is not None:
+            self.dpix.copy_(torch.from_numpy(np.ascontiguousarray(upstream.transpose(0, 2, 1)).reshape(-1)).to(DEV))
+        self.drec = torch.empty((max(n_recv, 1), 9), dtype=torch.float32, device=DEV)
+        L.render_bwd(ctx, recv, n_recv, self.sorted, self.range, self.cams, dp, self.bg, self.dpix, self.T, self.nl,
+                     self.drec, self.cost, self.cost_mode, self.stats)
+        torch.cuda.synchronize()
+        return self
+
+
+def oracle_pipeline(scene, cams, bg, gt=None, b0=None, b1=None, flag_eps=FLAG_EPS):
+    recs, off, ent, fwd = oracle.render_batch(scene, cams, "parity", bg, gt, flag_eps, b0, b1)
+    return recs, off, ent, fwd
+
+
+def scenes():
+    return [("c0s0", synth.scene_c0(0), (0, 0, 0)), ("c0s1-bg", synth.scene_c0(1), (0.2, 0.5, 0.8)),
+            ("c0-opaque", synth.scene_c0(0, opaque=True), (0, 0, 0)),
+            ("c0-opaque-bg", synth.scene_c0(1, opaque=True), (0.2, 0.5, 0.8))]
+
+
+@pytest.fixture(scope="module", params=scenes(), ids=lambda s: s[0])
+def case(request):
+    name, sc, bg = request.param
+    cams = synth.cameras_c0()
+    gt = synth.gt_image(0, cams[0])[None]
+    run = Run(sc, cams, bg, gt)
+    run.render(run.send, run.n_send)
+    recs, off, ent, fwd = oracle_pipeline(sc, cams, bg, gt)
+    return dict(name=name, scene=sc, cams=cams, bg=bg, gt=gt, run=run, recs=recs, off=off, ent=ent, fwd=fwd)
+
+
+# ---------------------------------------------------------------- A1 projection
+def test_project_membership_bitexact(case):
+    run, sc, cam = case["run"], case["scene"], case["cams"][0]
+    d = decode_records(run.send[: run.n_send])
+    mb = oracle.membership(sc, cam)
+    vis = np.nonzero(mb["vis"])[0]
+    np.testing.assert_array_equal(d["gid"], vis)  # same set, ascending gid order
+    np.testing.assert_array_equal(d["view"], 0)
+    for k in ("mx", "my", "depth"):
+        np.testing.assert_array_equal(d[k].view(np.uint32), mb[k][vis].view(np.uint32), err_msg=k)
+    np.testing.assert_array_equal(d["radius"].astype(np.int64), mb["radius"][vis])
+
+
+def test_project_continuous(case):
+    run, recs = case["run"], case["recs"]
+    d = decode_records(run.send[: run.n_send])
+    np.testing.assert_allclose(conic_of(d), recs.rec_f[:, 3:6], rtol=2e-5, atol=1e-7)
+    np.testing.assert_allclose(d["opacity"], recs.rec_f[:, 6], rtol=1e-5, atol=1e-7)
+    np.testing.assert_allclose(d["rgb"], recs.rec_f[:, 7:10], rtol=1e-5, atol=1e-5)
+
+
+# ---------------------------------------------------------------- A3 lists
+def test_bin_sort_lists_bitexact(case):
+    run, recs, off, ent = case["run"], case["recs"], case["off"], case["ent"]
+    rng = run.range.cpu().numpy()
+    srt = run.sorted[: run.n_pairs].cpu().numpy().view(np.uint32)
+    d = decode_records(run.send[: run.n_send])
+    np.testing.assert_array_equal(rng.astype(np.int64), off)
+    np.testing.assert_array_equal(d["gid"][srt], recs.rec_i[ent, 0])
+
+
+# ---------------------------------------------------------------- A4 forward
+def test_render_fwd(case):
+    run, fwd = case["run"], case["fwd"]
+    nb = run.no
+    flags = fwd["flags"]
+    unflag = (flags & 3) == 0
+    T = block_major(run.T, nb)
+    nl = block_major(run.nl, nb)
+    rgb = block_major(run.rgb, nb, 3)
+    assert (~unflag).sum() <= max(1, 1e-3 * unflag.size), "flagged pixels: %d" % (~unflag).sum()
+    np.testing.assert_array_equal(nl[unflag], fwd["nlast"][unflag])
+    assert np.abs(T - fwd["T"])[unflag].max() <= 1e-4
+    assert np.abs(rgb - fwd["c"])[unflag].max() <= 1e-4
+    # fused L1: dL/dpix equal where the sign is not ambiguous, loss within fp32 summation
+    dpix = block_major(run.dpix, nb, 3)
+    ok = unflag & ((flags & 8) == 0)
+    np.testing.assert_allclose(dpix[ok], fwd["dl_dc"][ok], rtol=1e-6, atol=0)
+    assert abs(run.loss.item() - fwd["loss"]) <= 1e-5 * abs(fwd["loss"]) + 1e-9
+    # work counters: E_f totals and per-block WORK cost (fwd E_f + bwd n_last)
+    st = run.stats.cpu().numpy()
+    if unflag.all():
+        assert st[0] == fwd["counts"][..., 0].sum() and st[1] == fwd["counts"][..., 1].sum()
+        assert st[3] == fwd["counts"][..., 3].sum()
+        np.testing.assert_array_equal(run.cost.cpu().numpy(), fwd["work"])
+
+
+# ---------------------------------------------------------------- A5 backward
+def test_render_bwd_upstream(case):
+    """Seeded upstream gradient (zero on flagged pixels) fed to both sides (the upstream is an
+    input, so sign decisions of the loss cannot differ)."""
+    sc, cams, bg, recs, off, ent, fwd = (case[k] for k in ("scene", "cams", "bg", "recs", "off", "ent", "fwd"))
+    run = Run(sc, cams, bg, None)
+    up = synth.upstream_grad(11, (16, 256, 3)).astype(np.float64) * 1e-3
+    up[(fwd["flags"] & 3) != 0] = 0
+    run.render(run.send, run.n_send, upstream=up.astype(np.float32))
+    g_or = oracle.render_bwd(recs, off, ent, 0, 16, run.W, run.H, up.astype(np.float32).astype(np.float64), bg)
+    g_k = run.drec[: run.n_send].cpu().numpy().astype(np.float64)
+    # records are in the same (view, gid) order on both sides at G=1
+    for name, sl in [("mean", slice(0, 2)), ("conic", slice(2, 5)), ("opacity", slice(5, 6)), ("rgb", slice(6, 9))]:
+        e_inf, e_2 = grad_metric(g_k[:, sl], g_or[:, sl])
+        assert e_inf <= 1e-3 and e_2 <= 1e-3, (name, e_inf, e_2)
+
+
+# ---------------------------------------------------------------- A7 + A8
+def test_param_grads_and_adam(case):
+    sc, cams, bg, recs, off, ent, fwd = (case[k] for k in ("scene", "cams", "bg", "recs", "off", "ent", "fwd"))
+    run = Run(sc, cams, bg, None)
+    up = synth.upstream_grad(12, (16, 256, 3)).astype(np.float64) * 1e-3
+    up[(fwd["flags"] & 3) != 0] = 0
+    run.render(run.send, run.n_send, upstream=up.astype(np.float32))
+    g_or = oracle.render_bwd(recs, off, ent, 0, 16, run.W, run.H, up.astype(np.float32).astype(np.float64), bg)
+    pg_or = oracle.project_bwd(sc, cams, recs, g_or)
+    gbuf = run.p.zeros_like()
+    hp = L.adam_hparams((1e-3,) * 6, 1, 1)
+    L.adam_step(run.ctx, run.p, None, None, gbuf, cams, run.dp, run.drec, run.idx, hp, L.ADAM_GRAD | L.ADAM_WRITE_GRAD)
+    torch.cuda.synchronize()
+    pg_k = gbuf.to_flat()
+    for name, sl in oracle.GROUP_SLICES.items():
+        e_inf, e_2 = grad_metric(pg_k[:, sl], pg_or[:, sl])
+        assert e_inf <= 1e-3 and e_2 <= 1e-3, (name, e_inf, e_2)
+
+
+def test_adam_apply_matches_oracle():
+    sc = synth.scene_c0(3)
+    p = params_of(sc)
+    ctx = L.Context(0, 0, 1)
+    n = sc.n
+    g, m, v = synth.adam_state(5, n)
+    flat = lambda a: a  # [n,60] planes: pos_op(4) ls(4) rot(4) sh(48)
+
+    def planes(a):
+        gp = L.GaussianParams.empty(n, DEV)
+        gp.pos_op.copy_(torch.from_numpy(a[:, 0:4]))
+        gp.log_scale.copy_(torch.from_numpy(a[:, 4:8]))
+        gp.rot.copy_(torch.from_numpy(a[:, 8:12]))
+        gp.sh.copy_(torch.from_numpy(np.ascontiguousarray(a[:, 12:60].reshape(n, 12, 4).transpose(1, 0, 2))))
+        return gp
+
+    def unplanes(gp):
+        return np.concatenate([gp.pos_op.cpu().numpy(), gp.log_scale.cpu().numpy(), gp.rot.cpu().numpy(),
+                               gp.sh.cpu().numpy().transpose(1, 0, 2).reshape(n, 48)], 1)
+
+    theta0 = unplanes(p).astype(np.float64)
+    G_, M_, V_ = planes(g), planes(m), planes(v)
+    lr = (1.6e-4, 2.5e-3, 1.25e-4, 5e-2, 5e-3, 1e-3)
+    batch, step = 4, 3
+    L.adam_step(ctx, p, M_, V_, G_, None, None, None, None, L.adam_hparams(lr, batch, step), L.ADAM_APPLY)
+    torch.cuda.synchronize()
+    got_p, got_m, got_v = unplanes(p), unplanes(M_), unplanes(V_)
+    # element -> group (pos, sh_dc, sh_rest, opacity, scale, rot); log_scale lane 3 is padding
+    grp = np.array([0, 0, 0, 3, 4, 4, 4, -1, 5, 5, 5, 5, 1, 1, 1] + [2] * 45)
+    for k in range(60):
+        if grp[k] < 0:
+            continue
+        th, mm, vv = oracle.adam(theta0[:, k], m[:, k], v[:, k], g[:, k], lr[grp[k]], batch=batch, step=step)
+        # fp32 state: error relative to the group's scale (m can cancel to ~0)
+        np.testing.assert_allclose(got_m[:, k], mm, rtol=1e-5, atol=1e-6 * np.abs(mm).max())
+        np.testing.assert_allclose(got_v[:, k], vv, rtol=1e-5, atol=1e-6 * np.abs(vv).max())
+        e_inf, e_2 = grad_metric(got_p[:, k] - theta0[:, k], th - theta0[:, k])
+        assert e_inf <= 1e-3 and e_2 <= 1e-3, (k, e_inf, e_2)
+
+
+# ---------------------------------------------------------------- partition invariance + exchange sets
+@pytest.mark.parametrize("G", [2, 3, 5])
+def test_virtual_partition_equals_whole(G):
+    """P11/P16: Gaussians sharded over G owners, pixels over G ranks by a random DP; the test
+    moves each bucket to its rank (the transport, ascending source rank); stitched images are
+    bit-identical to the single-rank run, exchange sets equal the oracle's O10 brute force."""
+    sc = synth.scene_c0(2)
+    cams = synth.cameras_c0()
+    bg = (0.2, 0.5, 0.8)
+    whole = Run(sc, cams, bg, None)
+    whole.render(whole.send, whole.n_send)
+    B = whole.B
+    rng = np.random.default_rng(G)
+    dp = np.concatenate([[0], np.sort(rng.integers(0, B + 1, G - 1)), [B]]).astype(np.int64)
+    bounds = [sc.n * s // G for s in range(G + 1)]
+    owners = [Run(sc.slice(bounds[s], bounds[s + 1]), cams, bg, None, world=G, rank=s, dp=dp) for s in range(G)]
+    mb = oracle.membership(sc, cams[0])
+    mask = oracle.exchange_sets(mb["vis"], mb["rect"], 0, whole.Wt, whole.Ht, dp)
+    rgb_whole = block_major(whole.rgb, whole.no, 3)
+    nl_whole = block_major(whole.nl, whole.no)
+    for r in range(G):
+        parts = []
+        for s in range(G):
+            o = owners[s]
+            off = np.concatenate([[0], np.cumsum(o.send_counts)])
+            parts.append(o.send[off[r]:off[r + 1]])
+        recv = torch.cat(parts) if parts else torch.empty((0, 48), dtype=torch.uint8, device=DEV)
+        d = decode_records(recv)
+        want = np.nonzero(mask >> r & 1)[0]
+        np.testing.assert_array_equal(d["gid"], want)  # ascending source rank then gid
+        rr = Run(sc.slice(0, 1), cams, bg, None, world=G, rank=r, dp=dp)
+        rr.render(recv if len(recv) else torch.empty((1, 48), dtype=torch.uint8, device=DEV), len(recv))
+        lo, hi = dp[r], dp[r + 1]
+        np.testing.assert_array_equal(block_major(rr.rgb, rr.no, 3), rgb_whole[lo:hi])
+        np.testing.assert_array_equal(block_major(rr.nl, rr.no), nl_whole[lo:hi])
+
+
+# ---------------------------------------------------------------- A9
+def test_division_points_host_and_device():
+    rng = np.random.default_rng(0)
+    for _ in range(500):
+        B, G = int(rng.integers(1, 300)), int(rng.integers(1, 17))
+        et = rng.integers(0, 1000, B) * (rng.random(B) < 0.7)
+        np.testing.assert_array_equal(L.division_points(et, G), oracle.division_points(et, G))
+
+
+@pytest.mark.parametrize("mode", [L.COST_WORK, L.COST_PAPER_AVG])
+def test_rebalance_device(mode):
+    sc = synth.scene_c0(0)
+    cams = synth.cameras_c0()
+    run = Run(sc, cams, (0, 0, 0), None, cost_mode=L.COST_WORK)
+    run.render(run.send, run.n_send)
+    hist = torch.full((4, 16), -1, dtype=torch.int64, device=DEV)
+    # G=1: DP is trivially [0, B]; the history must hold the estimates of image 0
+    dpn = L.rebalance(run.ctx, run.cost, cams, run.dp, hist, 4, mode, cams)
+    assert list(dpn) == [0, 16]
+    cost = run.cost.cpu().numpy()
+    npix = np.full(16, 256)
+    et = oracle.costs_to_et(mode, run.dp, cost, npix)
+    np.testing.assert_array_equal(hist[0].cpu().numpy(), et)
+    assert (hist[1:] == -1).all()
+
+
+def test_rebalance_virtual_world_needs_comm():
+    ctx = L.Context(0, 0, 2)
+    with pytest.raises(L.GSError):
+        L.exchange(ctx, None, [0, 0], None, 0)
