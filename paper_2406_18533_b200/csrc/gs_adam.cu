@@ -47,31 +47,26 @@ inline planes mk(const gs_params* p) {
   return planes{(float4*)p->pos_op, (float4*)p->log_scale, (float4*)p->rot, (float4*)p->sh};
 }
 
-__device__ __forceinline__ void sh_basis_grad(float x, float y, float z, float dY[16][3]) {
+// Gradient of P(d) = sum_k c_k Y_k(d) with respect to d (d treated as free; the unit-norm
+// constraint is applied by the caller's (I - d d^T)/|x - c| projection).
+__device__ __forceinline__ void sh_poly_grad(float x, float y, float z, const float c[16], float& gx, float& gy,
+                                             float& gz) {
   const float C1 = 0.4886025119029199f;
   const float a0 = 1.0925484305920792f, a1 = -1.0925484305920792f, a2 = 0.31539156525252005f,
               a3 = -1.0925484305920792f, a4 = 0.5462742152960396f;
   const float c0 = -0.5900435899266435f, c1 = 2.890611442640554f, c2 = -0.4570457994644658f,
               c3 = 0.3731763325901154f, c4 = -0.4570457994644658f, c5 = 1.445305721320277f,
               c6 = -0.5900435899266435f;
-  float xx = x * x, yy = y * y, zz = z * z;
-#pragma unroll
-  for (int k = 0; k < 16; k++) dY[k][0] = dY[k][1] = dY[k][2] = 0.f;
-  dY[1][1] = -C1;
-  dY[2][2] = C1;
-  dY[3][0] = -C1;
-  dY[4][0] = a0 * y; dY[4][1] = a0 * x;
-  dY[5][1] = a1 * z; dY[5][2] = a1 * y;
-  dY[6][0] = -2.f * a2 * x; dY[6][1] = -2.f * a2 * y; dY[6][2] = 4.f * a2 * z;
-  dY[7][0] = a3 * z; dY[7][2] = a3 * x;
-  dY[8][0] = 2.f * a4 * x; dY[8][1] = -2.f * a4 * y;
-  dY[9][0] = c0 * 6.f * x * y; dY[9][1] = c0 * (3.f * xx - 3.f * yy);
-  dY[10][0] = c1 * y * z; dY[10][1] = c1 * x * z; dY[10][2] = c1 * x * y;
-  dY[11][0] = c2 * (-2.f * x * y); dY[11][1] = c2 * (4.f * zz - xx - 3.f * yy); dY[11][2] = c2 * 8.f * y * z;
-  dY[12][0] = c3 * (-6.f * x * z); dY[12][1] = c3 * (-6.f * y * z); dY[12][2] = c3 * (6.f * zz - 3.f * xx - 3.f * yy);
-  dY[13][0] = c4 * (4.f * zz - 3.f * xx - yy); dY[13][1] = c4 * (-2.f * x * y); dY[13][2] = c4 * 8.f * x * z;
-  dY[14][0] = c5 * 2.f * x * z; dY[14][1] = c5 * (-2.f * y * z); dY[14][2] = c5 * (xx - yy);
-  dY[15][0] = c6 * (3.f * xx - 3.f * yy); dY[15][1] = c6 * (-6.f * x * y);
+  const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, xz = x * z, yz = y * z;
+  gx = -C1 * c[3] + a0 * y * c[4] - 2.f * a2 * x * c[6] + a3 * z * c[7] + 2.f * a4 * x * c[8] +
+       6.f * c0 * xy * c[9] + c1 * yz * c[10] - 2.f * c2 * xy * c[11] - 6.f * c3 * xz * c[12] +
+       c4 * (4.f * zz - 3.f * xx - yy) * c[13] + 2.f * c5 * xz * c[14] + c6 * (3.f * xx - 3.f * yy) * c[15];
+  gy = -C1 * c[1] + a0 * x * c[4] + a1 * z * c[5] - 2.f * a2 * y * c[6] - 2.f * a4 * y * c[8] +
+       c0 * (3.f * xx - 3.f * yy) * c[9] + c1 * xz * c[10] + c2 * (4.f * zz - xx - 3.f * yy) * c[11] -
+       6.f * c3 * yz * c[12] - 2.f * c4 * xy * c[13] - 2.f * c5 * yz * c[14] - 6.f * c6 * xy * c[15];
+  gz = C1 * c[2] + a1 * y * c[5] + 4.f * a2 * z * c[6] + a3 * x * c[7] + c1 * xy * c[10] +
+       8.f * c2 * yz * c[11] + c3 * (6.f * zz - 3.f * xx - 3.f * yy) * c[12] + 8.f * c4 * xz * c[13] +
+       c5 * (xx - yy) * c[14];
 }
 
 // Chain rule O16 for one (Gaussian, view) given the summed record gradient g9 =
@@ -80,7 +75,7 @@ __device__ __forceinline__ void proj_bwd_view(const float g9[9], float4 X, const
                                               float qn, const float Rq[9], const float Sig[6],
                                               const float4* __restrict__ sh, int64_t n, int64_t i,
                                               const gs_dcam& cam, float gpos[3], float gls[3],
-                                              float gq[4], float& gop, float gsh[48]) {
+                                              float gq[4], float& gop, float* gsh) {
   const float* W = cam.R;
   // opacity: o = sigmoid(logit)
   const float o = 1.0f / (1.0f + expf(-X.w));
@@ -91,33 +86,35 @@ __device__ __forceinline__ void proj_bwd_view(const float g9[9], float4 X, const
   float dx = dvx * inv, dy = dvy * inv, dz = dvz * inv;
   float Y[16];
   sh_basis(dx, dy, dz, Y);
+  // pass 1 over the SH planes: the colour (for the clamp mask)
   float col[3] = {0.5f, 0.5f, 0.5f};
-  float shv[48];
 #pragma unroll
   for (int k = 0; k < 12; k++) {
-    float4 s4 = sh[(int64_t)k * n + i];
-    shv[4 * k] = s4.x; shv[4 * k + 1] = s4.y; shv[4 * k + 2] = s4.z; shv[4 * k + 3] = s4.w;
+    const float4 s4 = sh[(int64_t)k * n + i];
+    const float e[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+    for (int j = 0; j < 4; j++) col[(4 * k + j) % 3] = fmaf(Y[(4 * k + j) / 3], e[j], col[(4 * k + j) % 3]);
   }
-#pragma unroll
-  for (int k = 0; k < 16; k++)
-#pragma unroll
-    for (int ch = 0; ch < 3; ch++) col[ch] = fmaf(Y[k], shv[3 * k + ch], col[ch]);
   float gc[3];
 #pragma unroll
   for (int ch = 0; ch < 3; ch++) gc[ch] = col[ch] < 0.f ? 0.f : g9[6 + ch];
-  float dY[16][3];
-  sh_basis_grad(dx, dy, dz, dY);
-  float gd0 = 0.f, gd1 = 0.f, gd2 = 0.f;
+  // pass 2: dL/dsh = Y gc and the contraction c_k = sum_ch sh[k][ch] gc[ch] (L1-resident reload)
+  float ck[16];
 #pragma unroll
-  for (int k = 0; k < 16; k++)
+  for (int k = 0; k < 16; k++) ck[k] = 0.f;
 #pragma unroll
-    for (int ch = 0; ch < 3; ch++) {
-      gsh[3 * k + ch] = fmaf(Y[k], gc[ch], gsh[3 * k + ch]);
-      float sc = shv[3 * k + ch] * gc[ch];
-      gd0 = fmaf(sc, dY[k][0], gd0);
-      gd1 = fmaf(sc, dY[k][1], gd1);
-      gd2 = fmaf(sc, dY[k][2], gd2);
+  for (int k = 0; k < 12; k++) {
+    const float4 s4 = sh[(int64_t)k * n + i];
+    const float e[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int f = 4 * k + j, kk = f / 3, ch = f % 3;
+      ck[kk] = fmaf(e[j], gc[ch], ck[kk]);
+      gsh[f * kBlock] = fmaf(Y[kk], gc[ch], gsh[f * kBlock]);  // shared memory, column of this thread
     }
+  }
+  float gd0, gd1, gd2;
+  sh_poly_grad(dx, dy, dz, ck, gd0, gd1, gd2);
   float dd = dx * gd0 + dy * gd1 + dz * gd2;
   gpos[0] += (gd0 - dx * dd) * inv;
   gpos[1] += (gd1 - dy * dd) * inv;
@@ -212,8 +209,12 @@ __global__ void __launch_bounds__(kBlock) k_bwd_adam(planes P, planes Mo, planes
                                                      const int64_t* __restrict__ base, int64_t ncta,
                                                      const float* __restrict__ dL_dsend, adam_arg h) {
   __shared__ int s_cnt[kWarps * kMaxBuckets];
+  __shared__ float s_gsh[48 * kBlock];  // SH gradient accumulators, [coefficient][thread]
   const int b = cams.n;
   const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+  float* gsh = s_gsh + threadIdx.x;
+#pragma unroll
+  for (int f = 0; f < 48; f++) gsh[f * kBlock] = 0.f;
   uint32_t m[kMaxWords], u[kMaxWords];
   load_masks(maskw, n, i, NW, m);
   cta_rank_phase1(m, u, NW, nb, s_cnt);
@@ -249,9 +250,7 @@ __global__ void __launch_bounds__(kBlock) k_bwd_adam(planes P, planes Mo, planes
     Sig[4] = Mm[3] * Mm[6] + Mm[4] * Mm[7] + Mm[5] * Mm[8];
     Sig[5] = Mm[6] * Mm[6] + Mm[7] * Mm[7] + Mm[8] * Mm[8];
   }
-  float gpos[3] = {0, 0, 0}, gls[3] = {0, 0, 0}, gq[4] = {0, 0, 0, 0}, gop = 0.f, gsh[48];
-#pragma unroll
-  for (int k = 0; k < 48; k++) gsh[k] = 0.f;
+  float gpos[3] = {0, 0, 0}, gls[3] = {0, 0, 0}, gq[4] = {0, 0, 0, 0}, gop = 0.f;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   for (int v = 0; v < b; v++) {
@@ -285,16 +284,19 @@ __global__ void __launch_bounds__(kBlock) k_bwd_adam(planes P, planes Mo, planes
     Go.rot[i] = gq4;
 #pragma unroll
     for (int k = 0; k < 12; k++)
-      Go.sh[(int64_t)k * n + i] = make_float4(gsh[4 * k], gsh[4 * k + 1], gsh[4 * k + 2], gsh[4 * k + 3]);
+      Go.sh[(int64_t)k * n + i] = make_float4(gsh[(4 * k) * kBlock], gsh[(4 * k + 1) * kBlock],
+                                              gsh[(4 * k + 2) * kBlock], gsh[(4 * k + 3) * kBlock]);
   }
   if (kApply) {
     adam4(P.pos_op, Mo.pos_op, Vo.pos_op, i, gpo, 0, 0, 0, 3, h);
     adam4(P.ls, Mo.ls, Vo.ls, i, gl4, 4, 4, 4, -1, h);
     adam4(P.rot, Mo.rot, Vo.rot, i, gq4, 5, 5, 5, 5, h);
-    adam4(P.sh, Mo.sh, Vo.sh, i, make_float4(gsh[0], gsh[1], gsh[2], gsh[3]), 1, 1, 1, 2, h);
+    adam4(P.sh, Mo.sh, Vo.sh, i, make_float4(gsh[0], gsh[kBlock], gsh[2 * kBlock], gsh[3 * kBlock]), 1, 1, 1, 2, h);
 #pragma unroll
     for (int k = 1; k < 12; k++)
-      adam4(P.sh, Mo.sh, Vo.sh, (int64_t)k * n + i, make_float4(gsh[4 * k], gsh[4 * k + 1], gsh[4 * k + 2], gsh[4 * k + 3]),
+      adam4(P.sh, Mo.sh, Vo.sh, (int64_t)k * n + i,
+            make_float4(gsh[(4 * k) * kBlock], gsh[(4 * k + 1) * kBlock], gsh[(4 * k + 2) * kBlock],
+                        gsh[(4 * k + 3) * kBlock]),
             2, 2, 2, 2, h);
   }
 }

@@ -19,7 +19,7 @@ constexpr float kAlphaMin = 1.0f / 255.0f;
 constexpr float kTStop = 1e-4f;
 constexpr float kNear = 0.01f;
 constexpr float kDilate = 0.3f;
-constexpr int kBlock = 256;      // threads per CTA for Gaussian-wise kernels (project/adam)
+constexpr int kBlock = 128;      // threads per CTA for Gaussian-wise kernels (project/adam)
 
 struct gs_dcam {
   float R[9], t[3], fx, fy, cx, cy, campos[3];
@@ -92,11 +92,13 @@ __device__ __forceinline__ bool rect_of(float mx, float my, float r, int Wt, int
 struct gs_cov3 {
   bool ok;
   float S[6];  // S00, S01, S02, S11, S12, S22
+  float smax;  // largest scale (for the conservative early cull)
 };
 
 __device__ __forceinline__ gs_cov3 cov3_of(float4 ls, float4 q) {
   gs_cov3 o;
   float s0 = exp_rn(ls.x), s1 = exp_rn(ls.y), s2 = exp_rn(ls.z);
+  o.smax = fmaxf(s0, fmaxf(s1, s2));
   float n2 = add(add(add(mul(q.x, q.x), mul(q.y, q.y)), mul(q.z, q.z)), mul(q.w, q.w));
   o.ok = n2 > 0.0f;
   float qn = __fsqrt_rn(n2);
@@ -142,6 +144,19 @@ __device__ __forceinline__ gs_memb membership(const gs_cov3& cv, float X0, float
   o.mx = add(dvd(fxpx, p2), cam.cx);
   o.my = add(dvd(fypy, p2), cam.cy);
   o.depth = p2;
+  {
+    // Conservative early frustum cull (not part of the definition; it only skips Gaussians
+    // the exact chain below would also reject): lambda_max(Sigma') <= ||J||_F^2 smax^2 + 0.3
+    // (W orthonormal, Sigma = R diag(s^2) R^T), so the exact radius is <= r_ub and the exact
+    // rectangle is inside the r_ub rectangle.  1% + 2 px margins absorb fp32 rounding.
+    float iz = 1.0f / p2;
+    float jf2 = (cam.fx * cam.fx + cam.fy * cam.fy) * iz * iz +
+                (fxpx * fxpx + fypy * fypy) * (iz * iz) * (iz * iz);
+    float lam_ub = (jf2 * cv.smax * cv.smax + kDilate) * 1.01f;
+    float r_ub = ceilf(3.0f * sqrtf(lam_ub)) + 2.0f;
+    int a0, a1, a2, a3;
+    if (isfinite(r_ub) && !rect_of(o.mx, o.my, r_ub, Wt, Ht, a0, a1, a2, a3)) return o;
+  }
   float pz2 = mul(p2, p2);
   float j00 = dvd(cam.fx, p2), j02 = -dvd(fxpx, pz2);
   float j11 = dvd(cam.fy, p2), j12 = -dvd(fypy, pz2);

@@ -34,6 +34,7 @@ enum {
   SLOT_CT,            // rebalance prefix sums
   SLOT_MISC,          // small counters / dp
   SLOT_COUNT_GATHER,  // exchange count matrix
+  SLOT_RECTILES,      // bin_sort per-record tile counts -> pair starts
   SLOT_N
 };
 

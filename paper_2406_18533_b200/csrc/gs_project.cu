@@ -68,16 +68,10 @@ __global__ void __launch_bounds__(kBlock) k_project_write(
   cta_rank_phase1(m, u, NW, nb, s_cnt);
   // view-independent parameters
   float4 X = make_float4(0, 0, 0, 0), q = X, ls = X;
-  float shv[48];
   if (i < n) {
     X = pos_op[i];
     ls = log_scale[i];
     q = rot[i];
-#pragma unroll
-    for (int k = 0; k < 12; k++) {
-      float4 s4 = sh[(int64_t)k * n + i];
-      shv[4 * k] = s4.x; shv[4 * k + 1] = s4.y; shv[4 * k + 2] = s4.z; shv[4 * k + 3] = s4.w;
-    }
   }
   gs_cov3 cv = cov3_of(ls, q);
   const float opac = 1.0f / (1.0f + __expf(-X.w));
@@ -105,13 +99,16 @@ __global__ void __launch_bounds__(kBlock) k_project_write(
       float Y[16];
       sh_basis(dx * inv, dy * inv, dz * inv, Y);
       float col[3];
+      col[0] = col[1] = col[2] = 0.5f;
 #pragma unroll
-      for (int ch = 0; ch < 3; ch++) {
-        float s = 0.5f;
+      for (int k = 0; k < 12; k++) {  // SH planes read only for visible (i, v)
+        const float4 s4 = sh[(int64_t)k * n + i];
+        const float e[4] = {s4.x, s4.y, s4.z, s4.w};
 #pragma unroll
-        for (int k = 0; k < 16; k++) s = fmaf(Y[k], shv[3 * k + ch], s);
-        col[ch] = fmaxf(s, 0.0f);
+        for (int j = 0; j < 4; j++) col[(4 * k + j) % 3] = fmaf(Y[(4 * k + j) / 3], e[j], col[(4 * k + j) % 3]);
       }
+#pragma unroll
+      for (int ch = 0; ch < 3; ch++) col[ch] = fmaxf(col[ch], 0.0f);
       unsigned meta = (unsigned)((gid_base + i) * 32 + v);
       rec.a = make_float4(mb.mx, mb.my, mb.depth, mb.r);
       rec.b = make_float4(l11, l21, l22, opac);

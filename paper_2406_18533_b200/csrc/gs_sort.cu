@@ -24,14 +24,17 @@ constexpr int kSortThreads = 256;
 constexpr int kSmallCap = 4096;  // keys sorted in shared memory (32 KB)
 
 __global__ void k_rect_diff(const gs_rec* __restrict__ rec, int64_t n_recv, gs_geom geo, int v_lo,
-                            int v_hi, int* __restrict__ diff) {
+                            int v_hi, int* __restrict__ diff, int64_t* __restrict__ n_tiles) {
   int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n_recv) return;
+  if (j > n_recv) return;
+  if (j == n_recv) { n_tiles[j] = 0; return; }
+  n_tiles[j] = 0;
   float4 a = rec[j].a;
   int v = (int)(__float_as_uint(rec[j].c.w) & 31u);
   if (v < v_lo || v > v_hi) return;
   int tx0, tx1, ty0, ty1;
   if (!rect_of(a.x, a.y, a.w, geo.Wt, geo.Ht, tx0, tx1, ty0, ty1)) return;
+  n_tiles[j] = (int64_t)(tx1 - tx0 + 1) * (ty1 - ty0 + 1);
   const int ld = geo.Wt + 1;
   int* D = diff + (int64_t)(v - v_lo) * (geo.Ht + 1) * ld;
   atomicAdd(&D[ty0 * ld + tx0], 1);
@@ -74,43 +77,93 @@ __global__ void k_to_range(const int64_t* off, int64_t n_owned, int32_t* range, 
   if (lb < n_owned) cursor[lb] = (int32_t)off[lb];
 }
 
-__global__ void k_place(const gs_rec* __restrict__ rec, int64_t n_recv, gs_geom geo, int64_t B_lo,
-                        int64_t B_hi, int32_t* __restrict__ cursor, unsigned long long* __restrict__ keys) {
-  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n_recv) return;
-  float4 a = rec[j].a;
-  int v = (int)(__float_as_uint(rec[j].c.w) & 31u);
-  int tx0, tx1, ty0, ty1;
-  if (!rect_of(a.x, a.y, a.w, geo.Wt, geo.Ht, tx0, tx1, ty0, ty1)) return;
-  const unsigned long long hi = (unsigned long long)__float_as_uint(a.z) << 32;
-  const int64_t vb = (int64_t)v * geo.per_view;
-  // owned rows only
-  int ylo = ty0, yhi = ty1;
-  if (vb + (int64_t)ty0 * geo.Wt + tx1 < B_lo) ylo = (int)max((int64_t)ty0, (B_lo - vb - tx1 + geo.Wt - 1) / geo.Wt);
-  for (int ty = ylo; ty <= yhi; ty++) {
-    int64_t row = vb + (int64_t)ty * geo.Wt;
-    if (row + tx0 >= B_hi) break;
-    for (int tx = tx0; tx <= tx1; tx++) {
-      int64_t beta = row + tx;
-      if (beta < B_lo) continue;
-      if (beta >= B_hi) break;
-      int pos = atomicAdd(&cursor[beta - B_lo], 1);
-      keys[pos] = hi | (unsigned long long)j;
+// Pair-parallel placement: CTA c owns pairs [c*kPlacePairs, (c+1)*kPlacePairs) of the
+// (record, tile-of-its-rectangle) enumeration (pair_start = exclusive scan of tile counts);
+// every record has >= 1 tile, so at most kPlacePairs + 1 records overlap a CTA.  Their
+// rectangles are staged in shared memory, each thread binary-searches the record of each of
+// its pairs there and appends key = depth_bits << 32 | recv_idx to the block's list.
+constexpr int kPlaceThreads = 256;
+constexpr int kPlacePairs = 1024;
+
+__global__ void __launch_bounds__(kPlaceThreads) k_place(
+    const gs_rec* __restrict__ rec, int64_t n_recv, const int64_t* __restrict__ pair_start, int64_t n_full,
+    gs_geom geo, int64_t B_lo, int64_t B_hi, int32_t* __restrict__ cursor, unsigned long long* __restrict__ keys) {
+  __shared__ int64_t s_start[kPlacePairs + 2];
+  __shared__ int s_tx0[kPlacePairs + 1], s_ty0[kPlacePairs + 1], s_w[kPlacePairs + 1], s_v[kPlacePairs + 1];
+  __shared__ unsigned s_depth[kPlacePairs + 1];
+  __shared__ int64_t s_jlo;
+  __shared__ int s_nr;
+  const int64_t P0 = (int64_t)blockIdx.x * kPlacePairs;
+  const int64_t P1 = min(P0 + kPlacePairs, n_full);
+  if (threadIdx.x == 0) {
+    // first record whose range contains P0: last j with pair_start[j] <= P0
+    int64_t lo = 0, hi = n_recv;  // pair_start[n_recv] = n_full > P0
+    while (hi - lo > 1) {
+      int64_t mid = (lo + hi) >> 1;
+      if (pair_start[mid] <= P0) lo = mid; else hi = mid;
     }
+    int64_t lo2 = lo, hi2 = n_recv;  // last j with pair_start[j] <= P1 - 1
+    while (hi2 - lo2 > 1) {
+      int64_t mid = (lo2 + hi2) >> 1;
+      if (pair_start[mid] <= P1 - 1) lo2 = mid; else hi2 = mid;
+    }
+    s_jlo = lo;
+    s_nr = (int)(lo2 - lo + 1);
+  }
+  __syncthreads();
+  const int64_t jlo = s_jlo;
+  const int nr = s_nr;
+  for (int r = threadIdx.x; r < nr; r += kPlaceThreads) {
+    const int64_t j = jlo + r;
+    s_start[r] = pair_start[j];
+    const float4 a = rec[j].a;
+    int tx0, tx1, ty0, ty1;
+    rect_of(a.x, a.y, a.w, geo.Wt, geo.Ht, tx0, tx1, ty0, ty1);
+    s_tx0[r] = tx0;
+    s_ty0[r] = ty0;
+    s_w[r] = tx1 - tx0 + 1;
+    s_v[r] = (int)(__float_as_uint(rec[j].c.w) & 31u);
+    s_depth[r] = __float_as_uint(a.z);
+  }
+  if (threadIdx.x == 0) s_start[nr] = pair_start[jlo + nr];
+  __syncthreads();
+  for (int64_t pp = P0 + threadIdx.x; pp < P1; pp += kPlaceThreads) {
+    int lo = 0, hi = nr;  // last r with s_start[r] <= pp
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (s_start[mid] <= pp) lo = mid; else hi = mid;
+    }
+    const int t = (int)(pp - s_start[lo]), w = s_w[lo];
+    const int ty = s_ty0[lo] + t / w, tx = s_tx0[lo] + t % w;
+    const int64_t beta = (int64_t)s_v[lo] * geo.per_view + (int64_t)ty * geo.Wt + tx;
+    if (beta < B_lo || beta >= B_hi) continue;
+    const int pos = atomicAdd(&cursor[beta - B_lo], 1);
+    keys[pos] = ((unsigned long long)s_depth[lo] << 32) | (unsigned long long)(jlo + lo);
   }
 }
 
+// Bitonic network over P (power of two) keys in shared memory.  Compare-exchange t pairs
+// i = 2t - (t & (j-1)) with i + j; for j <= 32 a warp's 32 consecutive t touch only its own
+// 64 keys, so those stages synchronise with __syncwarp (when P/2 is a multiple of 32).
 __device__ __forceinline__ void bitonic_smem(unsigned long long* s, int P) {
+  const bool warp_local = (P / 2) % 32 == 0;
   for (int k = 2; k <= P; k <<= 1)
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int t = threadIdx.x; t < P / 2; t += kSortThreads) {
-        int i = (t / j) * 2 * j + (t % j), l = i + j;
-        bool up = (i & k) == 0;
-        unsigned long long x = s[i], y = s[l];
+        const int i = 2 * t - (t & (j - 1)), l = i + j;
+        const bool up = (i & k) == 0;
+        const unsigned long long x = s[i], y = s[l];
         if ((x > y) == up) { s[i] = y; s[l] = x; }
+      }
+      if (j <= 32 && warp_local && (j > 1 || k < P)) {
+        // next stage is warp-local too unless this was the last stage of a merge whose
+        // successor has j' = k (k >= 64 crosses warps)
+        const int jn = j > 1 ? j >> 1 : k;  // next stage's j
+        if (jn <= 32) { __syncwarp(); continue; }
       }
       __syncthreads();
     }
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(kSortThreads) k_sort_small(const int32_t* __restrict__ range,
@@ -217,13 +270,16 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
   int64_t* counts = (int64_t*)gs_slot_get(c, SLOT_COUNTS, (n_owned + 1) * sizeof(int64_t), st);
   int32_t* cursor = (int32_t*)gs_slot_get(c, SLOT_CURSOR, (n_owned + 1) * sizeof(int32_t), st);
   int32_t* large = (int32_t*)gs_slot_get(c, SLOT_LARGE, (n_owned + 8) * sizeof(int32_t), st);
-  if (!diff || !counts || !cursor || !large) return gs_fail(c, GS_ECUDA, "scratch");
+  int64_t* ntiles = (int64_t*)gs_slot_get(c, SLOT_RECTILES, (n_recv + 1) * sizeof(int64_t), st);
+  if (!diff || !counts || !cursor || !large || !ntiles) return gs_fail(c, GS_ECUDA, "scratch");
   GS_CUDA(c, cudaMemsetAsync(diff, 0, diff_n * sizeof(int), st));
   if (n_recv > 0) {
     GS_REQUIRE(c, recv_rec != nullptr, "null recv_rec");
     ++c->launches;
-    k_rect_diff<<<(unsigned)((n_recv + 255) / 256), 256, 0, st>>>((const gs_rec*)recv_rec, n_recv, geo,
-                                                                  v_lo, v_hi, diff);
+    k_rect_diff<<<(unsigned)((n_recv + 256) / 256), 256, 0, st>>>((const gs_rec*)recv_rec, n_recv, geo,
+                                                                  v_lo, v_hi, diff, ntiles);
+    s = gs_scan_i64(c, ntiles, ntiles, n_recv + 1, 0, st);  // pair_start
+    if (s != GS_OK) return s;
   }
   const int ld = geo.Wt + 1, rows = geo.Ht + 1;
   ++c->launches;
@@ -236,8 +292,10 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
   s = gs_scan_i64(c, counts, counts, n_owned + 1, 0, st);
   if (s != GS_OK) return s;
   GS_CUDA(c, cudaMemcpyAsync(c->pinned, counts + n_owned, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  if (n_recv > 0)
+    GS_CUDA(c, cudaMemcpyAsync(c->pinned + 1, ntiles + n_recv, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GS_CUDA(c, cudaStreamSynchronize(st));
-  const int64_t K = c->pinned[0];
+  const int64_t K = c->pinned[0], n_full = n_recv > 0 ? c->pinned[1] : 0;
   *n_pairs_h = K;
   if (K > pair_cap || K >= (1ll << 31))
     return gs_fail(c, GS_ECAPACITY, "pair capacity %lld < %lld", (long long)pair_cap, (long long)K);
@@ -249,8 +307,8 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
   unsigned long long* keys = (unsigned long long*)gs_slot_get(c, SLOT_KEYS, K * sizeof(unsigned long long), st);
   if (!keys) return gs_fail(c, GS_ECUDA, "key scratch (%lld pairs)", (long long)K);
   ++c->launches;
-  k_place<<<(unsigned)((n_recv + 255) / 256), 256, 0, st>>>((const gs_rec*)recv_rec, n_recv, geo, B_lo, B_hi,
-                                                            cursor, keys);
+  k_place<<<(unsigned)((n_full + kPlacePairs - 1) / kPlacePairs), kPlaceThreads, 0, st>>>(
+      (const gs_rec*)recv_rec, n_recv, ntiles, n_full, geo, B_lo, B_hi, cursor, keys);
   GS_CUDA(c, cudaMemsetAsync(large + n_owned, 0, 8 * sizeof(int32_t), st));
   int32_t* n_large = large + n_owned;
   ++c->launches;

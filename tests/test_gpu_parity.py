@@ -234,8 +234,10 @@ def test_adam_apply_matches_oracle():
         # fp32 state: error relative to the group's scale (m can cancel to ~0)
         np.testing.assert_allclose(got_m[:, k], mm, rtol=1e-5, atol=1e-6 * np.abs(mm).max())
         np.testing.assert_allclose(got_v[:, k], vv, rtol=1e-5, atol=1e-6 * np.abs(vv).max())
-        e_inf, e_2 = grad_metric(got_p[:, k] - theta0[:, k], th - theta0[:, k])
-        assert e_inf <= 1e-3 and e_2 <= 1e-3, (k, e_inf, e_2)
+        # parameters are stored in fp32: the update must agree with the fp64 Adam to 1e-3 of
+        # the step size plus the storage rounding of the parameter itself
+        tol = 1e-3 * np.abs(th - theta0[:, k]).max() + 2 * np.spacing(np.abs(th).astype(np.float32))
+        assert np.all(np.abs(got_p[:, k] - th) <= tol), (k, np.abs(got_p[:, k] - th).max())
 
 
 # ---------------------------------------------------------------- partition invariance + exchange sets

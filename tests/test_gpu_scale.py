@@ -1,0 +1,168 @@
+"""GPU parity at the paper's workload shapes (SURVEY §8(c) "Configs"): full-scene projection
+of Rubble-, garden- and MatrixCity-shaped scenes with one rank owning a 256-block window
+(a virtual rank of a 3-rank partition), compared with the oracle: exchange set and per-block
+lists bit-exact, pixels within 1e-4 on unflagged pixels, n_last exact, record gradients
+within the 1e-3 metric.  Plus sampled blocks of the full C2 bench configuration (16 views,
+4591x3436, 11.2M Gaussians) in the launch configuration bench.py times."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests.gsutil import block_major, decode_records, grad_metric
+
+L = pytest.importorskip("paper_2406_18533_b200._lib")
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def _params(sc):
+    return L.GaussianParams.from_arrays(sc.pos, sc.log_scale, sc.rot, sc.opac_logit, sc.sh, DEV, sc.gid_base)
+
+
+def _window_case(sc, cam, lo_frac=0.45, nblk=256, seed=0):
+    W, H = cam.width, cam.height
+    Wt, Ht = (W + 15) // 16, (H + 15) // 16
+    B = Wt * Ht
+    lo = int(B * lo_frac)
+    hi = min(B, lo + nblk)
+    dp = np.array([0, lo, hi, B], np.int64)
+    ctx = L.Context(0, 1, 3)  # virtual rank 1 of 3
+    p = _params(sc)
+    idx = torch.empty(L.project_index_bytes(ctx, p.n, 1), dtype=torch.uint8, device=DEV)
+    try:
+        cnt = L.project(ctx, p, [cam], dp, None, 0, idx)
+    except L.CapacityError as e:
+        cnt = e.counts
+    send = torch.empty((int(cnt.sum()) + 1, 48), dtype=torch.uint8, device=DEV)
+    cnt = L.project(ctx, p, [cam], dp, send, int(cnt.sum()), idx)
+    off = np.concatenate([[0], np.cumsum(cnt)])
+    recv = send[off[1]:off[2]].contiguous()
+    n_recv = int(cnt[1])
+    no = hi - lo
+    rng_t = torch.empty(no + 1, dtype=torch.int32, device=DEV)
+    try:
+        npairs = L.bin_sort(ctx, recv, n_recv, [cam], dp, None, 0, rng_t)
+    except L.CapacityError as e:
+        npairs = e.needed
+    srt = torch.empty(max(npairs, 1), dtype=torch.int32, device=DEV)
+    npairs = L.bin_sort(ctx, recv, n_recv, [cam], dp, srt, npairs, rng_t)
+    gt = synth.gt_image(seed, cam)
+    gt_t = torch.from_numpy(gt[None]).to(DEV)
+    T = torch.empty(no * 256, device=DEV)
+    nl = torch.empty(no * 256, dtype=torch.int32, device=DEV)
+    rgb = torch.empty(no * 768, device=DEV)
+    dpix = torch.empty(no * 768, device=DEV)
+    loss = torch.zeros(1, dtype=torch.float64, device=DEV)
+    L.render_fwd(ctx, recv, srt, rng_t, [cam], dp, (0, 0, 0), gt_t, 1, rgb, T, nl, dpix, loss, None, 0, None)
+    torch.cuda.synchronize()
+    # oracle over the same window
+    recs = oracle.make_records(sc, [cam], "parity")
+    o_off, o_ent = oracle.tile_lists(recs, lo, hi, Wt, Ht)
+    fwd = oracle.render_fwd(recs, o_off, o_ent, lo, hi, W, H, (0, 0, 0), gt[None], 1, 1e-5)
+    return dict(ctx=ctx, dp=dp, recv=recv, n_recv=n_recv, range=rng_t, sorted=srt, npairs=npairs, T=T, nl=nl,
+                rgb=rgb, dpix=dpix, recs=recs, off=o_off, ent=o_ent, fwd=fwd, no=no, lo=lo, hi=hi, W=W, H=H,
+                Wt=Wt, Ht=Ht, cam=cam, sc=sc, cnt=cnt)
+
+
+def _check_window(c):
+    # exchange set of rank 1 == oracle O10 (bit-exact, ascending gid)
+    mb = oracle.membership(c["sc"], c["cam"])
+    mask = oracle.exchange_sets(mb["vis"], mb["rect"], 0, c["Wt"], c["Ht"], c["dp"])
+    d = decode_records(c["recv"][: c["n_recv"]])
+    np.testing.assert_array_equal(d["gid"], np.nonzero(mask >> 1 & 1)[0])
+    for k in ("mx", "my", "depth"):
+        sel = d["gid"]
+        np.testing.assert_array_equal(d[k].view(np.uint32), mb[k][sel].view(np.uint32))
+    # per-block lists
+    rng = c["range"].cpu().numpy().astype(np.int64)
+    np.testing.assert_array_equal(rng, c["off"])
+    srt = c["sorted"][: c["npairs"]].cpu().numpy().view(np.uint32)
+    np.testing.assert_array_equal(d["gid"][srt], c["recs"].rec_i[c["ent"], 0])
+    # pixels
+    fwd, no = c["fwd"], c["no"]
+    unflag = (fwd["flags"] & 3) == 0
+    inside = np.zeros_like(unflag)
+    for k in range(no):
+        beta = c["lo"] + k
+        tx, ty = beta % c["Wt"], beta // c["Wt"]
+        px = tx * 16 + np.arange(256) % 16
+        py = ty * 16 + np.arange(256) // 16
+        inside[k] = (px < c["W"]) & (py < c["H"])
+    ok = unflag & inside
+    assert (inside & ~unflag).sum() <= max(2, 1e-3 * inside.sum()), (inside & ~unflag).sum()
+    np.testing.assert_array_equal(block_major(c["nl"], no)[ok], fwd["nlast"][ok])
+    assert np.abs(block_major(c["T"], no) - fwd["T"])[ok].max() <= 1e-4
+    assert np.abs(block_major(c["rgb"], no, 3) - fwd["c"])[ok].max() <= 1e-4
+    return ok
+
+
+def _check_bwd(c, ok):
+    ctx, dp, no = c["ctx"], c["dp"], c["no"]
+    up = synth.upstream_grad(21, (no, 256, 3)).astype(np.float64) * 1e-6
+    up[~ok] = 0
+    dpix = torch.from_numpy(np.ascontiguousarray(up.astype(np.float32).transpose(0, 2, 1)).reshape(-1)).to(DEV)
+    drec = torch.empty((max(c["n_recv"], 1), 9), device=DEV)
+    L.render_bwd(ctx, c["recv"], c["n_recv"], c["sorted"], c["range"], [c["cam"]], dp, (0, 0, 0), dpix, c["T"],
+                 c["nl"], drec, None, 0, None)
+    torch.cuda.synchronize()
+    g_or = oracle.render_bwd(c["recs"], c["off"], c["ent"], c["lo"], c["hi"], c["W"], c["H"],
+                             up.astype(np.float32).astype(np.float64))
+    d = decode_records(c["recv"][: c["n_recv"]])
+    pos = {int(g): j for j, g in enumerate(c["recs"].rec_i[:, 0])}
+    g_ref = g_or[[pos[int(g)] for g in d["gid"]]]
+    g_k = drec[: c["n_recv"]].cpu().numpy().astype(np.float64)
+    for name, sl in [("mean", slice(0, 2)), ("conic", slice(2, 5)), ("opacity", slice(5, 6)), ("rgb", slice(6, 9))]:
+        e_inf, e_2 = grad_metric(g_k[:, sl], g_ref[:, sl])
+        assert e_inf <= 1e-3 and e_2 <= 1e-3, (name, e_inf, e_2)
+
+
+@pytest.mark.parametrize("which", ["rubble", "garden", "city_street", "city_aerial"])
+def test_window_parity(which):
+    if which == "rubble":
+        sc, cam = synth.scene_rubble(11_200_000), synth.cameras_rubble(4)[1]
+    elif which == "garden":
+        sc, cam = synth.scene_garden(5_000_000), synth.cameras_garden(4)[2]
+    elif which == "city_street":
+        sc, cam = synth.scene_city(4_000_000), synth.cameras_city(128)[3]
+    else:
+        sc, cam = synth.scene_city(4_000_000), synth.cameras_city(128)[70]
+    c = _window_case(sc, cam, lo_frac=0.5 if which != "city_street" else 0.45)
+    assert c["n_recv"] > 0 and c["npairs"] > 0
+    ok = _check_window(c)
+    _check_bwd(c, ok)
+
+
+def test_full_c2_sampled_blocks():
+    """The bench configuration: 11.2M Gaussians, 16 views of 4591x3436, G=1, through the step
+    driver; sampled blocks of two views recomputed one by one by the oracle."""
+    from paper_2406_18533_b200.engine import GrendelTrainer
+    sc = synth.scene_rubble(11_200_000)
+    pool = synth.cameras_rubble(64)
+    cams = [pool[i] for i in synth.batch_schedule(64, 16, 1, 2)[0]]
+    W, H = cams[0].width, cams[0].height
+    gt = np.stack([synth.gt_image(2, c) for c in cams])
+    ctx = L.Context(0, 0, 1)
+    p = _params(sc)
+    tr = GrendelTrainer(ctx, p, W, H, 16, 64, cost_mode=L.COST_WORK, rebalance=False)
+    tr.step(cams, torch.from_numpy(gt).to(DEV), collect_stats=True)
+    torch.cuda.synchronize()
+    Wt, Ht = (W + 15) // 16, (H + 15) // 16
+    pv = Wt * Ht
+    rng = np.random.default_rng(3)
+    for v in (0, 9):
+        recs = oracle.make_records(sc, [cams[v]], "parity")
+        for blk in rng.integers(0, pv, 6):
+            off, ent = oracle.tile_lists(recs, int(blk), int(blk) + 1, Wt, Ht)
+            f = oracle.render_fwd(recs, off, ent, int(blk), int(blk) + 1, W, H, (0, 0, 0), gt[v][None], 16, 1e-5)
+            lb = v * pv + int(blk)
+            T = tr.T.t[lb].cpu().numpy()
+            nl = tr.nl.t[lb].cpu().numpy()
+            dpx = tr.dpix.t[lb].cpu().numpy().T
+            ok = (f["flags"][0] & 3) == 0
+            np.testing.assert_array_equal(nl[ok], f["nlast"][0][ok])
+            assert np.abs(T - f["T"][0])[ok].max() <= 1e-4
+            ok3 = ok & ((f["flags"][0] & 8) == 0)
+            np.testing.assert_allclose(dpx[ok3], f["dl_dc"][0][ok3], rtol=1e-6)
+            assert tr.range.t[lb + 1].item() - tr.range.t[lb].item() == len(ent)
