@@ -389,7 +389,7 @@ static double sgn(double v) { return (v > 0) - (v < 0); }
 
 void orc_render_fwd(int64_t n_rec, const double* rec_f, const int64_t* offsets,
                     const int64_t* entries, int64_t b0, int64_t b1, int32_t W, int32_t H,
-                    const double* bg, const uint8_t* gt, int32_t b_total, double flag_eps,
+                    const double* bg, const uint8_t* gt, int32_t b_total, double flag_eps, double t_eps,
                     double* out_c, double* out_T, int32_t* out_nlast, int32_t* flags,
                     int64_t* counts, int64_t* work, double* dl_dc, double* loss) {
   (void)n_rec;
@@ -429,7 +429,7 @@ void orc_render_fwd(int64_t n_rec, const double* rec_f, const int64_t* offsets,
         if (fabs(alpha * 255.0 - 1.0) < flag_eps) flag |= 1;
         if (alpha < ALPHA_MIN) { Efs++; continue; }
         double Tn = T * (1.0 - alpha);
-        if (fabs(Tn * 1e4 - 1.0) < flag_eps) flag |= 2;
+        if (fabs(Tn * 1e4 - 1.0) < t_eps) flag |= 2;
         if (Tn < T_STOP) { Estop = 1; break; }  /* R3: stop before compositing */
         for (int ch = 0; ch < 3; ch++) C[ch] += alpha * T * r[7 + ch];
         T = Tn;

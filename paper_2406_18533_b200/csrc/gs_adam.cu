@@ -16,6 +16,8 @@ using namespace gsd;
 
 namespace {
 
+constexpr int kListCap = 8;  // records per thread listed per round (phase A of k_bwd_adam)
+
 struct adam_arg {
   float step[6];  // lambda'_g / (1 - beta1'^t), groups: pos, sh_dc, sh_rest, opacity, scale, rot
   float b1, b2, omb1, omb2, inv_sqrt_bc2, eps;
@@ -210,6 +212,8 @@ __global__ void __launch_bounds__(kBlock) k_bwd_adam(planes P, planes Mo, planes
                                                      const float* __restrict__ dL_dsend, adam_arg h) {
   __shared__ int s_cnt[kWarps * kMaxBuckets];
   __shared__ float s_gsh[48 * kBlock];  // SH gradient accumulators, [coefficient][thread]
+  __shared__ int64_t s_pos[kListCap * kBlock];        // per-thread record positions
+  __shared__ unsigned char s_view[kListCap * kBlock];  // and their views
   const int b = cams.n;
   const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
   float* gsh = s_gsh + threadIdx.x;
@@ -253,26 +257,55 @@ __global__ void __launch_bounds__(kBlock) k_bwd_adam(planes P, planes Mo, planes
   float gpos[3] = {0, 0, 0}, gls[3] = {0, 0, 0}, gq[4] = {0, 0, 0, 0}, gop = 0.f;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  for (int v = 0; v < b; v++) {
-    if (!view_in_union(u, v, b, G)) continue;  // warp-uniform
+  // Phase A (warp-uniform over the warp's union of buckets, v outer, d inner): each thread
+  // lists the send positions of its own records in that order.  Phase B (per thread,
+  // divergent): walks its own list, sums a view's destinations (ascending rank) and
+  // runs the chain rule once per view -- a warp no longer steps through every view any lane
+  // sees.  Lists longer than kListCap are processed in rounds.
+  int n_mine = 0;
+  for (int v = 0; v < b; v++)
+    for (int d = 0; d < G; d++) n_mine += live && get_bit(m, d * b + v);
+  __shared__ int s_rounds;
+  if (threadIdx.x == 0) s_rounds = 1;
+  __syncthreads();
+  if (n_mine > kListCap) atomicMax(&s_rounds, (n_mine + kListCap - 1) / kListCap);
+  __syncthreads();
+  const int max_rounds = s_rounds;
+  for (int r = 0; r < max_rounds; r++) {
+    int cnt = 0;
+    for (int v = 0; v < b; v++) {
+      if (!view_in_union(u, v, b, G)) continue;  // warp-uniform
+      for (int d = 0; d < G; d++) {
+        const int k = d * b + v;
+        if (!get_bit(u, k)) continue;
+        const bool bit = live && get_bit(m, k);
+        const unsigned bal = __ballot_sync(0xffffffffu, bit);
+        if (bit) {
+          const int slot = cnt - r * kListCap;
+          if (slot >= 0 && slot < kListCap) {
+            s_pos[slot * kBlock + threadIdx.x] =
+                base[(int64_t)k * ncta + blockIdx.x] + warp_prefix(s_cnt, wid, nb, k) + __popc(bal & lt);
+            s_view[slot * kBlock + threadIdx.x] = (unsigned char)v;
+          }
+          cnt++;
+        }
+      }
+    }
+    const int nl = min(kListCap, max(0, cnt - r * kListCap));
     float g9[9];
 #pragma unroll
     for (int c = 0; c < 9; c++) g9[c] = 0.f;
-    bool mine = false;
-    for (int d = 0; d < G; d++) {  // ascending destination rank (S:483 transpose)
-      const int k = d * b + v;
-      if (!get_bit(u, k)) continue;
-      const bool bit = live && get_bit(m, k);
-      const unsigned bal = __ballot_sync(0xffffffffu, bit);
-      if (bit) {
-        const int64_t pos = base[(int64_t)k * ncta + blockIdx.x] + warp_prefix(s_cnt, wid, nb, k) + __popc(bal & lt);
-        const float* src = dL_dsend + pos * 9;
+    for (int j = 0; j < nl; j++) {
+      const int v = s_view[j * kBlock + threadIdx.x];
+      const float* src = dL_dsend + s_pos[j * kBlock + threadIdx.x] * 9;
 #pragma unroll
-        for (int c = 0; c < 9; c++) g9[c] += src[c];
-        mine = true;
+      for (int c = 0; c < 9; c++) g9[c] += src[c];
+      if (j + 1 == nl || s_view[(j + 1) * kBlock + threadIdx.x] != v) {
+        proj_bwd_view(g9, X, s, qb, qn, Rq, Sig, P.sh, n, i, cams.c[v], gpos, gls, gq, gop, gsh);
+#pragma unroll
+        for (int c = 0; c < 9; c++) g9[c] = 0.f;
       }
     }
-    if (mine) proj_bwd_view(g9, X, s, qb, qn, Rq, Sig, P.sh, n, i, cams.c[v], gpos, gls, gq, gop, gsh);
   }
   if (!live) return;
   const float4 gpo = make_float4(gpos[0], gpos[1], gpos[2], gop);

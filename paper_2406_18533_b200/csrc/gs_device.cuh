@@ -140,6 +140,19 @@ __device__ __forceinline__ gs_memb membership(const gs_cov3& cv, float X0, float
   float p1 = add(add(add(mul(W[3], X0), mul(W[4], X1)), mul(W[5], X2)), cam.t[1]);
   float p2 = add(add(add(mul(W[6], X0), mul(W[7], X1)), mul(W[8], X2)), cam.t[2]);
   if (!cv.ok || !(p2 > kNear)) return o;
+  {
+    // Cheap conservative pre-cull with fast reciprocals (not part of the definition; it only
+    // skips Gaussians the exact chain below would reject): approximate mean and radius bound
+    // with a 2% + 4 px margin, far beyond the error of the approximations.
+    const float iz = __frcp_rn(p2);
+    const float amx = cam.fx * p0 * iz + cam.cx, amy = cam.fy * p1 * iz + cam.cy;
+    const float jf2 = (cam.fx * cam.fx + cam.fy * cam.fy) * iz * iz +
+                      ((cam.fx * p0) * (cam.fx * p0) + (cam.fy * p1) * (cam.fy * p1)) * (iz * iz) * (iz * iz);
+    const float rb = 3.0f * sqrtf((jf2 * cv.smax * cv.smax + kDilate) * 1.02f) + 4.0f;
+    if (isfinite(rb) && isfinite(amx) && isfinite(amy) &&
+        (amx + rb < 0.f || amx - rb > (float)(Wt * 16) || amy + rb < 0.f || amy - rb > (float)(Ht * 16)))
+      return o;
+  }
   float fxpx = mul(cam.fx, p0), fypy = mul(cam.fy, p1);
   o.mx = add(dvd(fxpx, p2), cam.cx);
   o.my = add(dvd(fypy, p2), cam.cy);
@@ -249,7 +262,28 @@ struct gs_srec {
   float mx, my, l11, l21, l22, o, r, g, b;
 };
 
-// alpha of a staged record at pixel (px, py): both passes call exactly this.
+// Gaussian weights of a staged record at the vertically adjacent pixel pair (px, py) and
+// (px, py + 1).  The pair shares dx; the second pixel's L^T d follows from the first by one
+// subtraction each (dy1 = dy0 - 1):  u1 = u0 - l21, w1 = w0 - l22.  Both render passes call
+// exactly this, so their skip/stop decisions agree bit for bit.
+struct gs_pair {
+  float dx, dy0, u0, w0, u1, w1, G0, G1, raw0, raw1;
+};
+__device__ __forceinline__ void alpha_pair(float mx, float my, float l11, float l21, float l22, float o,
+                                           float px, float py0, gs_pair& e) {
+  e.dx = __fsub_rn(mx, px);
+  e.dy0 = __fsub_rn(my, py0);
+  e.u0 = __fmaf_rn(l11, e.dx, __fmul_rn(l21, e.dy0));
+  e.w0 = __fmul_rn(l22, e.dy0);
+  e.u1 = __fsub_rn(e.u0, l21);
+  e.w1 = __fsub_rn(e.w0, l22);
+  e.G0 = ex2_approx(-__fmaf_rn(e.u0, e.u0, __fmul_rn(e.w0, e.w0)));
+  e.G1 = ex2_approx(-__fmaf_rn(e.u1, e.u1, __fmul_rn(e.w1, e.w1)));
+  e.raw0 = __fmul_rn(o, e.G0);  // raw o*G; callers apply the 0.99 cap
+  e.raw1 = __fmul_rn(o, e.G1);
+}
+
+// alpha of a staged record at pixel (px, py) (single-pixel form, kept for reference tools).
 __device__ __forceinline__ float alpha_at(float mx, float my, float l11, float l21, float l22,
                                           float o, float px, float py, float& G, float& dx,
                                           float& dy, float& u, float& w) {

@@ -1,23 +1,25 @@
 // gs_render.cu -- A4/A5: front-to-back alpha compositing and its backward over the rank's
 // owned 16x16 blocks.
 //
-// One CTA of 128 threads per owned block, two vertically adjacent pixels per thread (a warp
-// covers a compact 16x4 pixel region).  The block's depth-sorted list is staged through
-// shared memory in batches of 256 records (coalesced gathers: the sorted index, then the
-// 48-byte record); every thread then walks the batch for its two pixels, so each shared-memory
-// record read and each loop iteration is amortised over two evaluations.  The conic is
-// carried as its Cholesky factor L, prescaled by sqrt(0.5 log2 e), so the Gaussian weight is
+// One CTA per owned block; each thread owns a vertical strip of PPT pixels of one column
+// (PPT = 4: 64 threads per block, measured fastest on C2; 2 and 8 kept for A/B runs).  The block's depth-sorted
+// list is staged through shared memory in batches of 256 records (coalesced gathers: the sorted
+// index, then the 48-byte record), padded to a multiple of 8 with opacity-0 entries.  The conic
+// is carried as its Cholesky factor L, prescaled by sqrt(0.5 log2 e), so the Gaussian weight is
 // one MUFU.EX2 of a sum of two squares (no cancellation for thin Gaussians):
-//   u = l11 dx + l21 dy, w = l22 dy, G = 2^-(u^2 + w^2) = exp(-0.5 d^T conic d).
-// Early termination: a CTA stops staging once every pixel has stopped
-// (__syncthreads_count), a thread stops evaluating once its T would drop below 1e-4.
+//   u = l11 dx + l21 dy, w = l22 dy, G = 2^-(u^2 + w^2) = exp(-0.5 d^T conic d),
+// and along the strip dy drops by one per pixel, so u and w of the next pixel are one FADD
+// each (alpha_strip): the per-entry cost is ~9 instructions per pixel, not ~14.
+// Early termination: a thread stops evaluating a pixel once its T would drop below 1e-4, and
+// the CTA stops staging once every pixel has stopped (__syncthreads_count).
 // The forward fuses the L1 loss epilogue and the per-block cost counters.
 // The backward walks each pixel's list back to front from n_last, reconstructs
-// T_k = T_{k+1} / (1 - alpha_k), sums the 9 record gradients of an entry over the thread's two
-// pixels, then reduces them across the warp with a transpose (recursive-halving) reduction
-// (12 shuffles instead of 45; only when some lane contributes) that leaves value c in one lane,
-// so the 9 values are added to the batch entry's shared-memory accumulator by one warp-wide
-// atomic instruction; each batch flushes one global atomic per (record, block, value).
+// T_k = T_{k+1} / (1 - alpha_k), sums the 9 record gradients of an entry over the thread's
+// strip, then reduces them across the warp with a transpose (recursive-halving) reduction
+// (12 shuffles, only when some lane contributes) that leaves value c in one lane; with one
+// warp per block those 9 lanes add straight into dL/d(record) (one global RED each).
+#include <cstdlib>
+
 #include "gs_device.cuh"
 #include "gs_internal.h"
 
@@ -25,8 +27,8 @@ using namespace gsd;
 
 namespace {
 
-constexpr int kThreads = 128;  // 2 pixels per thread
-constexpr int kBatch = 256;    // records staged per round
+constexpr int kBatch = 256;  // records staged per round
+constexpr int kUnroll = 8;   // forward entries per unrolled group (batch padded to a multiple)
 
 __device__ __forceinline__ void stage(const gs_rec* __restrict__ rec, uint32_t j, float4* s_a, float4* s_b,
                                       float* s_c, int t) {
@@ -37,146 +39,198 @@ __device__ __forceinline__ void stage(const gs_rec* __restrict__ rec, uint32_t j
   s_c[t] = c.z;
 }
 
-template <typename T>
+template <int NT, typename T>
 __device__ __forceinline__ T block_sum(T v, T* sm) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (NT == 32) return v;  // valid in every lane
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   __syncthreads();
   if (lane == 0) sm[wid] = v;
   __syncthreads();
   T s = 0;
   if (threadIdx.x == 0)
-    for (int w = 0; w < kThreads / 32; w++) s += sm[w];
+    for (int w = 0; w < NT / 32; w++) s += sm[w];
   return s;  // valid in thread 0
 }
 
-// pixel pair of this thread inside the 16x16 block: (x, y) and (x, y + 1)
-struct px_pair {
-  int x, y, p0;  // p0 = y*16 + x, second pixel p0 + 16
+// Gaussian weights of a staged record along the thread's vertical strip (px, py0 + j),
+// j < PPT.  dx is shared; dy_j = dy0 - j, so u_j = u_{j-1} - l21 and w_j = w_{j-1} - l22.
+// Both render passes call exactly this, so their skip/stop decisions agree bit for bit.
+template <int PPT>
+struct gs_strip {
+  float dx, dy0, u[PPT], w[PPT], G[PPT], raw[PPT];
 };
-__device__ __forceinline__ px_pair pair_of(int tid) {
-  const int lane = tid & 31, wid = tid >> 5;
-  px_pair q;
-  q.x = lane & 15;
-  q.y = wid * 4 + (lane >> 4) * 2;
-  q.p0 = q.y * 16 + q.x;
-  return q;
+template <int PPT>
+__device__ __forceinline__ void alpha_strip(const float4& A, const float4& Bq, float px, float py0,
+                                            gs_strip<PPT>& e) {
+  const float l11 = A.z, l21 = A.w, l22 = Bq.x, o = Bq.y;
+  e.dx = __fsub_rn(A.x, px);
+  e.dy0 = __fsub_rn(A.y, py0);
+  e.u[0] = __fmaf_rn(l11, e.dx, __fmul_rn(l21, e.dy0));
+  e.w[0] = __fmul_rn(l22, e.dy0);
+#pragma unroll
+  for (int j = 1; j < PPT; j++) {
+    e.u[j] = __fsub_rn(e.u[j - 1], l21);
+    e.w[j] = __fsub_rn(e.w[j - 1], l22);
+  }
+#pragma unroll
+  for (int j = 0; j < PPT; j++) {
+    e.G[j] = ex2_approx(-__fmaf_rn(e.u[j], e.u[j], __fmul_rn(e.w[j], e.w[j])));
+    e.raw[j] = __fmul_rn(o, e.G[j]);  // raw o*G; the 0.99 cap is applied by the caller
+  }
 }
 
-// One forward evaluation (O12) of staged entry (A, Bq, cb) at list position pos.
+// Composite one staged entry into one pixel (O12) given its capped alpha >= 1/255.
 template <bool kStats>
-__device__ __forceinline__ void fwd_px(const float4& A, const float4& Bq, float cb, float px, float py, int pos,
-                                       float& T, float& C0, float& C1, float& C2, bool& done, int& nlast,
-                                       int& stop_pos, int& efc) {
-  float G, dx, dy, u, w;
-  const float alpha = fminf(kAlphaCap, alpha_at(A.x, A.y, A.z, A.w, Bq.x, Bq.y, px, py, G, dx, dy, u, w));
-  if (alpha < kAlphaMin) return;
+__device__ __forceinline__ void fwd_comp(float alpha, float cr, float cg, float cb, int pos, float& T, float& C0,
+                                         float& C1, float& C2, bool& stop, int& nlast, int& stop_pos, int& efc) {
   const float Tn = T * (1.0f - alpha);
   if (Tn < kTStop) {  // R3: stop before compositing this entry
-    done = true;
+    stop = true;
     stop_pos = pos;
     return;
   }
   const float wgt = alpha * T;
-  C0 = fmaf(wgt, Bq.z, C0);
-  C1 = fmaf(wgt, Bq.w, C1);
+  C0 = fmaf(wgt, cr, C0);
+  C1 = fmaf(wgt, cg, C1);
   C2 = fmaf(wgt, cb, C2);
   T = Tn;
   nlast = pos + 1;
   if (kStats) efc++;
 }
 
-template <bool kStats>
-__global__ void __launch_bounds__(kThreads) k_render_fwd(
+template <int PPT, bool kStats>
+__global__ void __launch_bounds__(256 / PPT) k_render_fwd(
     const gs_rec* __restrict__ rec, const uint32_t* __restrict__ sorted_idx,
     const int32_t* __restrict__ range, gs_geom geo, int64_t B_lo, float bg0, float bg1, float bg2,
     const uint8_t* __restrict__ gt, float norm, float* __restrict__ out_rgb,
     float* __restrict__ T_final, int32_t* __restrict__ n_last, float* __restrict__ dL_dpix,
     double* __restrict__ loss_sum, int64_t* __restrict__ tile_cost, int cost_mode,
     long long* __restrict__ stats) {
+  constexpr int NT = 256 / PPT;
+  constexpr unsigned kAll = (1u << PPT) - 1u;
   __shared__ float4 s_a[kBatch], s_b[kBatch];
   __shared__ float s_c[kBatch];
-  __shared__ long long s_red[kThreads / 32];
-  __shared__ double s_redd[kThreads / 32];
+  __shared__ long long s_red[NT / 32];
+  __shared__ double s_redd[NT / 32];
   const long long t0 = clock64();
   const int tid = threadIdx.x;
   const int64_t lb = blockIdx.x, beta = B_lo + lb;
   const int64_t v = beta / geo.per_view, loc = beta % geo.per_view;
   const int tx = (int)(loc % geo.Wt), ty = (int)(loc / geo.Wt);
-  const px_pair q = pair_of(tid);
-  const int px = tx * 16 + q.x, py0 = ty * 16 + q.y, py1 = py0 + 1;
-  const bool in0 = px < geo.W && py0 < geo.H, in1 = px < geo.W && py1 < geo.H;
-  const float fpx = (float)px, fpy0 = (float)py0, fpy1 = (float)py1;
+  const int x = tid & 15, y0 = (tid >> 4) * PPT;
+  const int px = tx * 16 + x, py0 = ty * 16 + y0;
+  const float fpx = (float)px, fpy0 = (float)py0;
   const int beg = range[lb], end = range[lb + 1];
-  float T0 = 1.f, T1 = 1.f, a0 = 0.f, a1 = 0.f, a2 = 0.f, b0c = 0.f, b1c = 0.f, b2c = 0.f;
-  bool d0 = !in0, d1 = !in1;
-  int nl0 = 0, nl1 = 0, sp0 = -1, sp1 = -1, efc0 = 0, efc1 = 0;
+  float T[PPT], C0[PPT], C1[PPT], C2[PPT];
+  int nl[PPT], sp[PPT];
+  unsigned done = 0, inside = 0;
+#pragma unroll
+  for (int j = 0; j < PPT; j++) {
+    T[j] = 1.f;
+    C0[j] = C1[j] = C2[j] = 0.f;
+    nl[j] = 0;
+    sp[j] = -1;
+    const bool in = px < geo.W && py0 + j < geo.H;
+    inside |= (unsigned)in << j;
+  }
+  done = ~inside & kAll;
+  int efc = 0;
   for (int b0 = beg; b0 < end; b0 += kBatch) {
-    if (__syncthreads_count(d0 && d1) == kThreads) break;
-    if (b0 + tid < end) stage(rec, sorted_idx[b0 + tid], s_a, s_b, s_c, tid);
-    if (b0 + tid + kThreads < end) stage(rec, sorted_idx[b0 + tid + kThreads], s_a, s_b, s_c, tid + kThreads);
-    __syncthreads();
+    if (__syncthreads_count(done == kAll) == NT) break;
     const int cnt = min(kBatch, end - b0);
+    const int cnt8 = (cnt + kUnroll - 1) & ~(kUnroll - 1);
+    for (int t = tid; t < cnt8; t += NT) {
+      if (t < cnt) {
+        stage(rec, sorted_idx[b0 + t], s_a, s_b, s_c, t);
+      } else {  // padding entry: opacity 0 -> alpha 0, skipped
+        s_a[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+        s_b[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    __syncthreads();
     const int pbase = b0 - beg;
-    for (int k = 0; k < cnt; k++) {
-      if (d0 && d1) break;
-      const float4 A = s_a[k], Bq = s_b[k];
-      const float cb = s_c[k];
-      if (!d0) fwd_px<kStats>(A, Bq, cb, fpx, fpy0, pbase + k, T0, a0, a1, a2, d0, nl0, sp0, efc0);
-      if (!d1) fwd_px<kStats>(A, Bq, cb, fpx, fpy1, pbase + k, T1, b0c, b1c, b2c, d1, nl1, sp1, efc1);
+    for (int k0 = 0; k0 < cnt8; k0 += kUnroll) {
+      if (done == kAll) break;
+#pragma unroll
+      for (int kk = 0; kk < kUnroll; kk++) {
+        const int k = k0 + kk;
+        const float4 A = s_a[k], Bq = s_b[k];
+        gs_strip<PPT> e;
+        alpha_strip<PPT>(A, Bq, fpx, fpy0, e);
+        unsigned c = 0;
+        float al[PPT];
+#pragma unroll
+        for (int j = 0; j < PPT; j++) {
+          al[j] = fminf(kAlphaCap, e.raw[j]);
+          c |= (unsigned)(al[j] >= kAlphaMin) << j;
+        }
+        c &= ~done;
+        if (c) {  // the common case (every pixel skips the entry) takes one branch
+          const float cb = s_c[k];
+#pragma unroll
+          for (int j = 0; j < PPT; j++)
+            if (c >> j & 1) {
+              bool st = false;
+              fwd_comp<kStats>(al[j], Bq.z, Bq.w, cb, pbase + k, T[j], C0[j], C1[j], C2[j], st, nl[j], sp[j], efc);
+              done |= (unsigned)st << j;
+            }
+        }
+      }
     }
   }
   // evaluations: an in-image pixel evaluates every entry up to its stopping entry (or all)
   const int n = end - beg;
-  const int ef0 = in0 ? (sp0 >= 0 ? sp0 + 1 : n) : 0, ef1 = in1 ? (sp1 >= 0 ? sp1 + 1 : n) : 0;
+  int ef = 0, nstop = 0, nlsum = 0;
   double lsum = 0.0;
-  const int64_t o0 = lb * 256 + q.p0, o1 = o0 + 16;
-  const float col0[3] = {fmaf(T0, bg0, a0), fmaf(T0, bg1, a1), fmaf(T0, bg2, a2)};
-  const float col1[3] = {fmaf(T1, bg0, b0c), fmaf(T1, bg1, b1c), fmaf(T1, bg2, b2c)};
-  T_final[o0] = in0 ? T0 : 1.f;
-  T_final[o1] = in1 ? T1 : 1.f;
-  n_last[o0] = nl0;
-  n_last[o1] = nl1;
-  if (out_rgb)
-    for (int ch = 0; ch < 3; ch++) {
-      out_rgb[lb * 768 + ch * 256 + q.p0] = in0 ? col0[ch] : 0.f;
-      out_rgb[lb * 768 + ch * 256 + q.p0 + 16] = in1 ? col1[ch] : 0.f;
+#pragma unroll
+  for (int j = 0; j < PPT; j++) {
+    const bool in = inside >> j & 1;
+    const int p = (y0 + j) * 16 + x;
+    const int64_t o = lb * 256 + p;
+    if (in) {
+      ef += sp[j] >= 0 ? sp[j] + 1 : n;
+      nstop += sp[j] >= 0;
     }
-  if (gt) {
-    const uint8_t* g0 = gt + ((v * geo.H + py0) * (int64_t)geo.W + px) * 3;
-    const uint8_t* g1 = g0 + (int64_t)geo.W * 3;
-    for (int ch = 0; ch < 3; ch++) {
-      float e0 = 0.f, e1 = 0.f;
-      if (in0) e0 = col0[ch] - (float)g0[ch] * (1.0f / 255.0f);
-      if (in1) e1 = col1[ch] - (float)g1[ch] * (1.0f / 255.0f);
-      if (dL_dpix) {
-        dL_dpix[lb * 768 + ch * 256 + q.p0] = (e0 > 0.f ? 1.f : (e0 < 0.f ? -1.f : 0.f)) * norm;
-        dL_dpix[lb * 768 + ch * 256 + q.p0 + 16] = (e1 > 0.f ? 1.f : (e1 < 0.f ? -1.f : 0.f)) * norm;
+    nlsum += nl[j];
+    const float col[3] = {fmaf(T[j], bg0, C0[j]), fmaf(T[j], bg1, C1[j]), fmaf(T[j], bg2, C2[j])};
+    T_final[o] = in ? T[j] : 1.f;
+    n_last[o] = nl[j];
+    if (out_rgb) {
+#pragma unroll
+      for (int ch = 0; ch < 3; ch++) out_rgb[lb * 768 + ch * 256 + p] = in ? col[ch] : 0.f;
+    }
+    if (gt) {
+      const uint8_t* g = gt + ((v * geo.H + py0 + j) * (int64_t)geo.W + px) * 3;
+#pragma unroll
+      for (int ch = 0; ch < 3; ch++) {
+        float e = 0.f;
+        if (in) e = col[ch] - (float)g[ch] * (1.0f / 255.0f);
+        if (dL_dpix) dL_dpix[lb * 768 + ch * 256 + p] = (e > 0.f ? 1.f : (e < 0.f ? -1.f : 0.f)) * norm;
+        lsum += (double)fabsf(e);
       }
-      lsum += (double)fabsf(e0) + (double)fabsf(e1);
-    }
-    if (loss_sum) {
-      double s = block_sum<double>(lsum, s_redd);
-      if (tid == 0 && s != 0.0) atomicAdd(loss_sum, s * (double)norm);
     }
   }
+  if (gt && loss_sum) {
+    double s = block_sum<NT, double>(lsum, s_redd);
+    if (tid == 0 && s != 0.0) atomicAdd(loss_sum, s * (double)norm);
+  }
   if (kStats) {
-    const int st0 = sp0 >= 0, st1 = sp1 >= 0;
-    long long a = block_sum<long long>(ef0 + ef1, s_red);
-    long long b2 = block_sum<long long>(efc0 + efc1, s_red);
-    long long c2 = block_sum<long long>(ef0 - efc0 - (in0 && st0) + ef1 - efc1 - (in1 && st1), s_red);
-    long long d2 = block_sum<long long>((in0 && st0) + (in1 && st1), s_red);
+    long long a = block_sum<NT, long long>(ef, s_red);
+    long long b2 = block_sum<NT, long long>(efc, s_red);
+    long long d2 = block_sum<NT, long long>(nstop, s_red);
     if (tid == 0) {
       atomicAdd((unsigned long long*)&stats[0], (unsigned long long)a);
       atomicAdd((unsigned long long*)&stats[1], (unsigned long long)b2);
-      atomicAdd((unsigned long long*)&stats[2], (unsigned long long)c2);
+      atomicAdd((unsigned long long*)&stats[2], (unsigned long long)(a - b2 - d2));
       atomicAdd((unsigned long long*)&stats[3], (unsigned long long)d2);
     }
   }
+  (void)nlsum;
   if (tile_cost) {
     if (cost_mode == GS_COST_WORK) {
-      long long w = block_sum<long long>(ef0 + ef1, s_red);
+      long long w = block_sum<NT, long long>(ef, s_red);
       if (tid == 0) tile_cost[lb] += w;
     } else {
       __syncthreads();
@@ -185,14 +239,12 @@ __global__ void __launch_bounds__(kThreads) k_render_fwd(
   }
 }
 
-// Backward of one composited-or-skipped entry for one pixel (O14); accumulates into gr.
-__device__ __forceinline__ bool bwd_px(const float4& A, const float4& Bq, float cb, float px, float py, float& T,
-                                       float& S0, float& S1, float& S2, float g0, float g1, float g2, float Tf,
-                                       float bgdot, float gr[9]) {
-  float G, dx, dy, u, w;
-  const float raw = alpha_at(A.x, A.y, A.z, A.w, Bq.x, Bq.y, px, py, G, dx, dy, u, w);
+// Backward of one composited entry for one pixel (O14) given its raw o*G (capped alpha
+// >= 1/255 checked by the caller); accumulates the 9 record gradients into gr.
+__device__ __forceinline__ void bwd_comp(float raw, float G, float dx, float dy, float u, float w, const float4& A,
+                                         const float4& Bq, float cb, float& T, float& S0, float& S1, float& S2,
+                                         float g0, float g1, float g2, float Tf, float bgdot, float gr[9]) {
   const float alpha = fminf(kAlphaCap, raw);
-  if (alpha < kAlphaMin) return false;
   const float om = 1.0f - alpha;
   const float rom = __fdividef(1.0f, om);
   T *= rom;  // transmittance in front of this entry
@@ -217,7 +269,6 @@ __device__ __forceinline__ bool bwd_px(const float4& A, const float4& Bq, float 
     gr[3] = fmaf(-q * dx, dy, gr[3]);
     gr[4] = fmaf(hq * dy, dy, gr[4]);
   }
-  return true;
 }
 
 // Transpose (recursive-halving) warp reduction of 9 values: afterwards lane l holds the warp
@@ -261,98 +312,118 @@ __device__ __forceinline__ int red_index(int lane, bool& valid) {
   return a + b + c + d;
 }
 
-template <bool kStats>
-__global__ void __launch_bounds__(kThreads) k_render_bwd(
+template <int PPT, bool kStats>
+__global__ void __launch_bounds__(256 / PPT) k_render_bwd(
     const gs_rec* __restrict__ rec, const uint32_t* __restrict__ sorted_idx,
     const int32_t* __restrict__ range, gs_geom geo, int64_t B_lo, float bg0, float bg1, float bg2,
     const float* __restrict__ dL_dpix, const float* __restrict__ T_final,
     const int32_t* __restrict__ n_last, float* __restrict__ dL_drec, int64_t* __restrict__ tile_cost,
     int cost_mode, long long* __restrict__ stats) {
+  constexpr int NT = 256 / PPT;
+  constexpr bool kOneWarp = NT == 32;
   __shared__ float4 s_a[kBatch], s_b[kBatch];
   __shared__ float s_c[kBatch];
   __shared__ uint32_t s_j[kBatch];
-  __shared__ float s_g[kBatch * 9];
-  __shared__ int s_max[kThreads / 32];
-  __shared__ long long s_red[kThreads / 32];
+  __shared__ float s_g[kOneWarp ? 1 : kBatch * 9];
+  __shared__ int s_max[NT / 32];
+  __shared__ long long s_red[NT / 32];
   const long long t0 = clock64();
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t lb = blockIdx.x, beta = B_lo + lb;
   const int64_t loc = beta % geo.per_view;
   const int tx = (int)(loc % geo.Wt), ty = (int)(loc / geo.Wt);
-  const px_pair q = pair_of(tid);
-  const int px = tx * 16 + q.x, py0 = ty * 16 + q.y, py1 = py0 + 1;
-  const bool in0 = px < geo.W && py0 < geo.H, in1 = px < geo.W && py1 < geo.H;
-  const float fpx = (float)px, fpy0 = (float)py0, fpy1 = (float)py1;
-  const int64_t o0 = lb * 256 + q.p0, o1 = o0 + 16;
-  const int nl0 = in0 ? n_last[o0] : 0, nl1 = in1 ? n_last[o1] : 0;
-  const float Tf0 = in0 ? T_final[o0] : 1.f, Tf1 = in1 ? T_final[o1] : 1.f;
-  float g00 = 0.f, g01 = 0.f, g02 = 0.f, g10 = 0.f, g11 = 0.f, g12 = 0.f;
-  if (in0) {
-    g00 = dL_dpix[lb * 768 + q.p0];
-    g01 = dL_dpix[lb * 768 + 256 + q.p0];
-    g02 = dL_dpix[lb * 768 + 512 + q.p0];
-  }
-  if (in1) {
-    g10 = dL_dpix[lb * 768 + q.p0 + 16];
-    g11 = dL_dpix[lb * 768 + 256 + q.p0 + 16];
-    g12 = dL_dpix[lb * 768 + 512 + q.p0 + 16];
-  }
-  const float bgd0 = bg0 * g00 + bg1 * g01 + bg2 * g02, bgd1 = bg0 * g10 + bg1 * g11 + bg2 * g12;
-  const int wmax = __reduce_max_sync(0xffffffffu, max(nl0, nl1));
-  if (lane == 0) s_max[wid] = wmax;
-  __syncthreads();
-  int maxn = 0;
+  const int x = tid & 15, y0 = (tid >> 4) * PPT;
+  const int px = tx * 16 + x, py0 = ty * 16 + y0;
+  const float fpx = (float)px, fpy0 = (float)py0;
+  int nl[PPT];
+  float Tf[PPT], T[PPT], S0[PPT], S1[PPT], S2[PPT], g0[PPT], g1[PPT], g2[PPT], bgd[PPT];
+  int mymax = 0, nlsum = 0;
 #pragma unroll
-  for (int w = 0; w < kThreads / 32; w++) maxn = max(maxn, s_max[w]);
+  for (int j = 0; j < PPT; j++) {
+    const bool in = px < geo.W && py0 + j < geo.H;
+    const int64_t o = lb * 256 + (y0 + j) * 16 + x;
+    nl[j] = in ? n_last[o] : 0;
+    Tf[j] = in ? T_final[o] : 1.f;
+    T[j] = Tf[j];
+    S0[j] = S1[j] = S2[j] = 0.f;
+    g0[j] = in ? dL_dpix[lb * 768 + (o - lb * 256)] : 0.f;
+    g1[j] = in ? dL_dpix[lb * 768 + 256 + (o - lb * 256)] : 0.f;
+    g2[j] = in ? dL_dpix[lb * 768 + 512 + (o - lb * 256)] : 0.f;
+    bgd[j] = bg0 * g0[j] + bg1 * g1[j] + bg2 * g2[j];
+    mymax = max(mymax, nl[j]);
+    nlsum += nl[j];
+  }
+  const int wmax = __reduce_max_sync(0xffffffffu, mymax);
+  int maxn = wmax;
+  if (!kOneWarp) {
+    if (lane == 0) s_max[wid] = wmax;
+    __syncthreads();
+    maxn = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; w++) maxn = max(maxn, s_max[w]);
+  }
   bool rvalid;
   const int ridx = red_index(lane, rvalid);
   const int beg = range[lb];
-  float T0 = Tf0, T1 = Tf1, S00 = 0.f, S01 = 0.f, S02 = 0.f, S10 = 0.f, S11 = 0.f, S12 = 0.f;
   int ebc = 0;
   for (int bi = (maxn + kBatch - 1) / kBatch - 1; bi >= 0; bi--) {
     const int p0 = bi * kBatch;  // list position of the batch start
     const int cnt = min(kBatch, maxn - p0);
     __syncthreads();
-    for (int t = tid; t < cnt; t += kThreads) {
+    for (int t = tid; t < cnt; t += NT) {
       const uint32_t j = sorted_idx[beg + p0 + t];
       stage(rec, j, s_a, s_b, s_c, t);
       s_j[t] = j;
     }
-    for (int t = tid; t < cnt * 9; t += kThreads) s_g[t] = 0.f;
+    if (!kOneWarp)
+      for (int t = tid; t < cnt * 9; t += NT) s_g[t] = 0.f;
     __syncthreads();
     for (int k = min(cnt, wmax - p0) - 1; k >= 0; k--) {  // warp-uniform range
       const int pos = p0 + k;
       const float4 A = s_a[k], Bq = s_b[k];
-      const float cb = s_c[k];
+      gs_strip<PPT> e;
+      alpha_strip<PPT>(A, Bq, fpx, fpy0, e);
+      unsigned c = 0;
+#pragma unroll
+      for (int j = 0; j < PPT; j++) c |= (unsigned)(pos < nl[j] && fminf(kAlphaCap, e.raw[j]) >= kAlphaMin) << j;
       float gr[9];
 #pragma unroll
-      for (int c = 0; c < 9; c++) gr[c] = 0.f;
-      bool contrib = false;
-      if (pos < nl0) contrib |= bwd_px(A, Bq, cb, fpx, fpy0, T0, S00, S01, S02, g00, g01, g02, Tf0, bgd0, gr);
-      if (kStats && contrib) ebc++;
-      if (pos < nl1) {
-        const bool c1 = bwd_px(A, Bq, cb, fpx, fpy1, T1, S10, S11, S12, g10, g11, g12, Tf1, bgd1, gr);
-        if (kStats && c1) ebc++;
-        contrib |= c1;
+      for (int q = 0; q < 9; q++) gr[q] = 0.f;
+      if (c) {
+        const float cb = s_c[k];
+#pragma unroll
+        for (int j = 0; j < PPT; j++)
+          if (c >> j & 1)
+            bwd_comp(e.raw[j], e.G[j], e.dx, __fsub_rn(e.dy0, (float)j), e.u[j], e.w[j], A, Bq, cb, T[j], S0[j],
+                     S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], gr);
+        if (kStats) ebc += __popc(c);
       }
-      if (__any_sync(0xffffffffu, contrib)) {
+      if (__any_sync(0xffffffffu, c != 0)) {
         const float z = warp_reduce9(gr, lane);
-        if (rvalid) atomicAdd(&s_g[k * 9 + ridx], z);
+        if (rvalid) {
+          if (kOneWarp) {
+            if (z != 0.f) atomicAdd(dL_drec + (int64_t)s_j[k] * 9 + ridx, z);
+          } else {
+            atomicAdd(&s_g[k * 9 + ridx], z);
+          }
+        }
       }
     }
-    __syncthreads();
-    for (int t = tid; t < cnt; t += kThreads) {
-      float* dst = dL_drec + (int64_t)s_j[t] * 9;
+    if (!kOneWarp) {
+      __syncthreads();
+      for (int t = tid; t < cnt; t += NT) {
+        float* dst = dL_drec + (int64_t)s_j[t] * 9;
 #pragma unroll
-      for (int c = 0; c < 9; c++) {
-        const float x = s_g[t * 9 + c];
-        if (x != 0.f) atomicAdd(dst + c, x);
+        for (int q = 0; q < 9; q++) {
+          const float xv = s_g[t * 9 + q];
+          if (xv != 0.f) atomicAdd(dst + q, xv);
+        }
       }
     }
   }
   if (kStats) {
-    long long a = block_sum<long long>(nl0 + nl1, s_red);
-    long long b2 = block_sum<long long>(ebc, s_red);
+    long long a = block_sum<NT, long long>(nlsum, s_red);
+    long long b2 = block_sum<NT, long long>(ebc, s_red);
     if (tid == 0) {
       atomicAdd((unsigned long long*)&stats[4], (unsigned long long)a);
       atomicAdd((unsigned long long*)&stats[5], (unsigned long long)b2);
@@ -360,13 +431,24 @@ __global__ void __launch_bounds__(kThreads) k_render_bwd(
   }
   if (tile_cost) {
     if (cost_mode == GS_COST_WORK) {
-      long long w = block_sum<long long>(nl0 + nl1, s_red);
+      long long w = block_sum<NT, long long>(nlsum, s_red);
       if (tid == 0) tile_cost[lb] += w;
     } else {
       __syncthreads();
       if (tid == 0) tile_cost[lb] += clock64() - t0;
     }
   }
+}
+
+// pixels per thread (A/B knob: GS_RENDER_PPT = 2, 4 or 8; default 4, measured best on C2)
+static int render_ppt() {
+  static int ppt = -1;
+  if (ppt < 0) {
+    const char* e = getenv("GS_RENDER_PPT");
+    ppt = e ? atoi(e) : 4;
+    if (ppt != 2 && ppt != 4 && ppt != 8) ppt = 4;
+  }
+  return ppt;
 }
 
 }  // namespace
@@ -390,8 +472,11 @@ extern "C" gs_status gs_render_fwd(gs_ctx* c, const void* recv_rec, const uint32
   if (bg_h) for (int k = 0; k < 3; k++) bg[k] = bg_h[k];
   const float norm = gt ? (float)(1.0 / (3.0 * (double)geo.W * (double)geo.H * (double)b_loss)) : 0.f;
   ++c->launches;
-  auto kf = stats ? k_render_fwd<true> : k_render_fwd<false>;
-  kf<<<(unsigned)n_owned, kThreads, 0, (cudaStream_t)stream>>>(
+  const int ppt = render_ppt();
+  auto kf = ppt == 2 ? (stats ? k_render_fwd<2, true> : k_render_fwd<2, false>)
+          : ppt == 4 ? (stats ? k_render_fwd<4, true> : k_render_fwd<4, false>)
+                     : (stats ? k_render_fwd<8, true> : k_render_fwd<8, false>);
+  kf<<<(unsigned)n_owned, 256 / ppt, 0, (cudaStream_t)stream>>>(
       (const gs_rec*)recv_rec, sorted_idx, tile_range, geo, B_lo, bg[0], bg[1], bg[2], gt, norm, out_rgb,
       T_final, n_last, dL_dpix, loss_sum, tile_cost, cost_mode, (long long*)stats);
   GS_LAUNCH_CHECK(c, "render_fwd");
@@ -419,8 +504,11 @@ extern "C" gs_status gs_render_bwd(gs_ctx* c, const void* recv_rec, int64_t n_re
   float bg[3] = {0.f, 0.f, 0.f};
   if (bg_h) for (int k = 0; k < 3; k++) bg[k] = bg_h[k];
   ++c->launches;
-  auto kb = stats ? k_render_bwd<true> : k_render_bwd<false>;
-  kb<<<(unsigned)n_owned, kThreads, 0, st>>>(
+  const int ppt = render_ppt();
+  auto kb = ppt == 2 ? (stats ? k_render_bwd<2, true> : k_render_bwd<2, false>)
+          : ppt == 4 ? (stats ? k_render_bwd<4, true> : k_render_bwd<4, false>)
+                     : (stats ? k_render_bwd<8, true> : k_render_bwd<8, false>);
+  kb<<<(unsigned)n_owned, 256 / ppt, 0, st>>>(
       (const gs_rec*)recv_rec, sorted_idx, tile_range, geo, B_lo, bg[0], bg[1], bg[2], dL_dpix, T_final, n_last,
       dL_drec, tile_cost, cost_mode, (long long*)stats);
   GS_LAUNCH_CHECK(c, "render_bwd");

@@ -166,28 +166,111 @@ __device__ __forceinline__ void bitonic_smem(unsigned long long* s, int P) {
   __syncthreads();
 }
 
+// Register bitonic sort of up to 32*E keys held by one warp, striped: key i = e*32 + lane.
+// Stages with j >= 32 compare two registers of the same lane; j < 32 exchange with lane^j.
+template <int E>
+__device__ __forceinline__ void warp_bitonic(unsigned long long (&v)[E], int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int je = j >> 5;
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+          if ((e & je) == 0) {
+            const int i = e * 32 + lane;
+            const bool up = (i & k) == 0;
+            const unsigned long long a = v[e], b = v[e | je];
+            if ((a > b) == up) { v[e] = b; v[e | je] = a; }
+          }
+        }
+      } else {
+        const bool lower = (lane & j) == 0;
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+          const int i = e * 32 + lane;
+          const bool up = (i & k) == 0;
+          const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[e], j);
+          const unsigned long long mn = v[e] < o ? v[e] : o, mx = v[e] < o ? o : v[e];
+          v[e] = (lower == up) ? mn : mx;
+        }
+      }
+    }
+  }
+}
+
+template <int E>
+__device__ __forceinline__ void warp_sort_segment(const unsigned long long* __restrict__ keys,
+                                                  uint32_t* __restrict__ out, int n, int lane) {
+  unsigned long long v[E];
+#pragma unroll
+  for (int e = 0; e < E; e++) {
+    const int i = e * 32 + lane;
+    v[e] = i < n ? keys[i] : ~0ull;
+  }
+  warp_bitonic<E>(v, lane);
+#pragma unroll
+  for (int e = 0; e < E; e++) {
+    const int i = e * 32 + lane;
+    if (i < n) out[i] = (uint32_t)v[e];
+  }
+}
+
+constexpr int kWarpCap = 256;  // lists up to this length are sorted by one warp in registers
+
+// One warp per owned block: lists of <= 256 keys are sorted in registers; longer ones are
+// queued for the shared-memory CTA sort (<= kSmallCap) or the merge sort (longer).
+__global__ void __launch_bounds__(kSortThreads) k_sort_warp(const int32_t* __restrict__ range, int64_t n_owned,
+                                                            const unsigned long long* __restrict__ keys,
+                                                            uint32_t* __restrict__ sorted_idx, int32_t* mid_list,
+                                                            int32_t* n_mid, int32_t* large_list, int32_t* n_large) {
+  const int lane = threadIdx.x & 31;
+  const int64_t lb = (int64_t)blockIdx.x * (kSortThreads / 32) + (threadIdx.x >> 5);
+  if (lb >= n_owned) return;
+  const int beg = range[lb], n = range[lb + 1] - beg;
+  if (n <= 1) {
+    if (n == 1 && lane == 0) sorted_idx[beg] = (uint32_t)keys[beg];
+    return;
+  }
+  if (n > kWarpCap) {
+    if (lane == 0) {
+      if (n > kSmallCap) large_list[atomicAdd(n_large, 1)] = (int32_t)lb;
+      else mid_list[atomicAdd(n_mid, 1)] = (int32_t)lb;
+    }
+    return;
+  }
+  if (n <= 32) warp_sort_segment<1>(keys + beg, sorted_idx + beg, n, lane);
+  else if (n <= 64) warp_sort_segment<2>(keys + beg, sorted_idx + beg, n, lane);
+  else if (n <= 128) warp_sort_segment<4>(keys + beg, sorted_idx + beg, n, lane);
+  else warp_sort_segment<8>(keys + beg, sorted_idx + beg, n, lane);
+}
+
+// Shared-memory bitonic sort of the queued medium lists (kWarpCap < n <= kSmallCap);
+// persistent CTAs take list after list.
 __global__ void __launch_bounds__(kSortThreads) k_sort_small(const int32_t* __restrict__ range,
-                                                             int64_t n_owned, const unsigned long long* __restrict__ keys,
+                                                             const unsigned long long* __restrict__ keys,
                                                              uint32_t* __restrict__ sorted_idx,
-                                                             int32_t* large_list, int32_t* n_large) {
+                                                             const int32_t* __restrict__ mid_list,
+                                                             const int32_t* n_mid, int32_t* next) {
   __shared__ unsigned long long s[kSmallCap];
-  int64_t lb = blockIdx.x;
-  int beg = range[lb], n = range[lb + 1] - beg;
-  if (n == 0) return;
-  if (n > kSmallCap) {
-    if (threadIdx.x == 0) large_list[atomicAdd(n_large, 1)] = (int32_t)lb;
-    return;
+  __shared__ int s_item;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(next, 1);
+    __syncthreads();
+    const int item = s_item;
+    __syncthreads();
+    if (item >= *n_mid) return;
+    const int lb = mid_list[item];
+    const int beg = range[lb], n = range[lb + 1] - beg;
+    int P = 2;
+    while (P < n) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += kSortThreads) s[i] = i < n ? keys[beg + i] : ~0ull;
+    __syncthreads();
+    bitonic_smem(s, P);
+    for (int i = threadIdx.x; i < n; i += kSortThreads) sorted_idx[beg + i] = (uint32_t)s[i];
+    __syncthreads();
   }
-  if (n == 1) {
-    if (threadIdx.x == 0) sorted_idx[beg] = (uint32_t)keys[beg];
-    return;
-  }
-  int P = 2;
-  while (P < n) P <<= 1;
-  for (int i = threadIdx.x; i < P; i += kSortThreads) s[i] = i < n ? keys[beg + i] : ~0ull;
-  __syncthreads();
-  bitonic_smem(s, P);
-  for (int i = threadIdx.x; i < n; i += kSortThreads) sorted_idx[beg + i] = (uint32_t)s[i];
 }
 
 __global__ void __launch_bounds__(kSortThreads) k_sort_large(const int32_t* __restrict__ range,
@@ -269,7 +352,7 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
   int* diff = (int*)gs_slot_get(c, SLOT_DIFF, diff_n * sizeof(int), st);
   int64_t* counts = (int64_t*)gs_slot_get(c, SLOT_COUNTS, (n_owned + 1) * sizeof(int64_t), st);
   int32_t* cursor = (int32_t*)gs_slot_get(c, SLOT_CURSOR, (n_owned + 1) * sizeof(int32_t), st);
-  int32_t* large = (int32_t*)gs_slot_get(c, SLOT_LARGE, (n_owned + 8) * sizeof(int32_t), st);
+  int32_t* large = (int32_t*)gs_slot_get(c, SLOT_LARGE, (2 * n_owned + 8) * sizeof(int32_t), st);
   int64_t* ntiles = (int64_t*)gs_slot_get(c, SLOT_RECTILES, (n_recv + 1) * sizeof(int64_t), st);
   if (!diff || !counts || !cursor || !large || !ntiles) return gs_fail(c, GS_ECUDA, "scratch");
   GS_CUDA(c, cudaMemsetAsync(diff, 0, diff_n * sizeof(int), st));
@@ -309,19 +392,23 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
   ++c->launches;
   k_place<<<(unsigned)((n_full + kPlacePairs - 1) / kPlacePairs), kPlaceThreads, 0, st>>>(
       (const gs_rec*)recv_rec, n_recv, ntiles, n_full, geo, B_lo, B_hi, cursor, keys);
-  GS_CUDA(c, cudaMemsetAsync(large + n_owned, 0, 8 * sizeof(int32_t), st));
-  int32_t* n_large = large + n_owned;
+  // lists: mid (n_owned) then large (n_owned), then 4 counters
+  int32_t* mid = large;
+  int32_t* lrg = large + n_owned;
+  int32_t* ctr = large + 2 * n_owned;  // n_mid, next_mid, n_large, next_large
+  GS_CUDA(c, cudaMemsetAsync(ctr, 0, 4 * sizeof(int32_t), st));
   ++c->launches;
-  k_sort_small<<<(unsigned)n_owned, kSortThreads, 0, st>>>(tile_range, n_owned, keys, sorted_idx, large,
-                                                          n_large);
-  GS_LAUNCH_CHECK(c, "bin_sort small");
-  unsigned long long* tmp = (unsigned long long*)gs_slot_get(c, SLOT_KEYS_TMP, K * sizeof(unsigned long long), st);
-  if (!tmp) return gs_fail(c, GS_ECUDA, "merge scratch");
+  k_sort_warp<<<(unsigned)((n_owned + kSortThreads / 32 - 1) / (kSortThreads / 32)), kSortThreads, 0, st>>>(
+      tile_range, n_owned, keys, sorted_idx, mid, ctr, lrg, ctr + 2);
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
   ++c->launches;
-  k_sort_large<<<dev_sms, kSortThreads, 0, st>>>(tile_range, keys, tmp, sorted_idx, large, n_large,
-                                                  n_large + 1);
+  k_sort_small<<<dev_sms * 4, kSortThreads, 0, st>>>(tile_range, keys, sorted_idx, mid, ctr, ctr + 1);
+  GS_LAUNCH_CHECK(c, "bin_sort small");
+  unsigned long long* tmp = (unsigned long long*)gs_slot_get(c, SLOT_KEYS_TMP, K * sizeof(unsigned long long), st);
+  if (!tmp) return gs_fail(c, GS_ECUDA, "merge scratch");
+  ++c->launches;
+  k_sort_large<<<dev_sms, kSortThreads, 0, st>>>(tile_range, keys, tmp, sorted_idx, lrg, ctr + 2, ctr + 3);
   GS_LAUNCH_CHECK(c, "bin_sort large");
   return GS_OK;
 }
