@@ -9,6 +9,8 @@
 // colour -> SH and view direction, opacity -> logit), summed over the batch's views; then
 // Adam on all 59 parameters in registers (dense over the shard, R9).  The parameter gradient
 // never touches HBM unless GS_ADAM_WRITE_GRAD asks for it (parity mode).
+#include <cstdlib>
+
 #include "gs_device.cuh"
 #include "gs_index.cuh"
 
@@ -204,8 +206,8 @@ __device__ __forceinline__ void proj_bwd_view(const float g9[9], float4 X, const
   for (int k = 0; k < 4; k++) gq[k] += (gqb[k] - qb[k] * qd) * iqn;
 }
 
-template <bool kWriteGrad, bool kApply>
-__global__ void __launch_bounds__(kBlock) k_bwd_adam(planes P, planes Mo, planes Vo, planes Go, int64_t n,
+template <bool kWriteGrad, bool kApply, int kMinBlocks>
+__global__ void __launch_bounds__(kBlock, kMinBlocks) k_bwd_adam(planes P, planes Mo, planes Vo, planes Go, int64_t n,
                                                      gs_cams_arg cams, int G, int nb, int NW,
                                                      const uint32_t* __restrict__ maskw,
                                                      const int64_t* __restrict__ base, int64_t ncta,
@@ -214,6 +216,11 @@ __global__ void __launch_bounds__(kBlock) k_bwd_adam(planes P, planes Mo, planes
   __shared__ float s_gsh[48 * kBlock];  // SH gradient accumulators, [coefficient][thread]
   __shared__ int64_t s_pos[kListCap * kBlock];        // per-thread record positions
   __shared__ unsigned char s_view[kListCap * kBlock];  // and their views
+  // cameras in shared memory: lanes of a warp handle different views at the same time in
+  // phase B, and divergent indexing of the kernel-parameter bank would serialise
+  __shared__ gs_dcam s_cams[GS_MAX_VIEWS];
+  for (int t = threadIdx.x; t < cams.n * (int)(sizeof(gs_dcam) / 4); t += kBlock)
+    reinterpret_cast<float*>(s_cams)[t] = reinterpret_cast<const float*>(cams.c)[t];
   const int b = cams.n;
   const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
   float* gsh = s_gsh + threadIdx.x;
@@ -301,7 +308,7 @@ __global__ void __launch_bounds__(kBlock) k_bwd_adam(planes P, planes Mo, planes
 #pragma unroll
       for (int c = 0; c < 9; c++) g9[c] += src[c];
       if (j + 1 == nl || s_view[(j + 1) * kBlock + threadIdx.x] != v) {
-        proj_bwd_view(g9, X, s, qb, qn, Rq, Sig, P.sh, n, i, cams.c[v], gpos, gls, gq, gop, gsh);
+        proj_bwd_view(g9, X, s, qb, qn, Rq, Sig, P.sh, n, i, s_cams[v], gpos, gls, gq, gop, gsh);
 #pragma unroll
         for (int c = 0; c < 9; c++) g9[c] = 0.f;
       }
@@ -335,10 +342,12 @@ __global__ void __launch_bounds__(kBlock) k_bwd_adam(planes P, planes Mo, planes
 }
 
 // Adam from a stored gradient (GS_ADAM_APPLY without GS_ADAM_GRAD): elementwise over planes.
-__global__ void k_adam_apply(planes P, planes Mo, planes Vo, planes Go, int64_t n, adam_arg h) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= 15 * n) return;
-  const int64_t plane = t / n, i = t % n;
+__global__ void __launch_bounds__(256) k_adam_apply(planes P, planes Mo, planes Vo, planes Go, int64_t n,
+                                                    adam_arg h) {
+  // grid (ceil(n/256), 15): blockIdx.y = float4 plane (pos_op, log_scale, rot, sh 0..11)
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int plane = blockIdx.y;
   if (plane == 0) adam4(P.pos_op, Mo.pos_op, Vo.pos_op, i, Go.pos_op[i], 0, 0, 0, 3, h);
   else if (plane == 1) adam4(P.ls, Mo.ls, Vo.ls, i, Go.ls[i], 4, 4, 4, -1, h);
   else if (plane == 2) adam4(P.rot, Mo.rot, Vo.rot, i, Go.rot[i], 5, 5, 5, 5, h);
@@ -380,7 +389,7 @@ extern "C" gs_status gs_adam_step(gs_ctx* c, gs_params* p, gs_params* m, gs_para
   planes P = mk(p), Mo = m ? mk(m) : planes{}, Vo = v ? mk(v) : planes{}, Go = g ? mk(g) : planes{};
   if (!grad) {
     ++c->launches;
-    k_adam_apply<<<(unsigned)((15 * p->n + 255) / 256), 256, 0, st>>>(P, Mo, Vo, Go, p->n, h);
+    k_adam_apply<<<dim3((unsigned)((p->n + 255) / 256), 15), 256, 0, st>>>(P, Mo, Vo, Go, p->n, h);
     GS_LAUNCH_CHECK(c, "adam_apply");
     return GS_OK;
   }
@@ -395,13 +404,36 @@ extern "C" gs_status gs_adam_step(gs_ctx* c, gs_params* p, gs_params* m, gs_para
   gs_cams_arg cams = make_cams(cams_h, n_views);
   const unsigned grid = (unsigned)L.ncta;
   if (!wgrad && !apply) return gs_fail(c, GS_EINVAL, "GS_ADAM_GRAD alone computes nothing observable");
+  if (apply && g) {
+    // split path (default when a gradient buffer is given): the transformation backward writes
+    // the parameter gradient, then an elementwise Adam pass streams p, m, v, g at full
+    // occupancy; the fused kernel's register footprint caps its memory parallelism
+    ++c->launches;
+    k_bwd_adam<true, false, 1><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base, L.ncta,
+                                                        dL_dsend, h);
+    ++c->launches;
+    k_adam_apply<<<dim3((unsigned)((p->n + 255) / 256), 15), 256, 0, st>>>(P, Mo, Vo, Go, p->n, h);
+    GS_LAUNCH_CHECK(c, "bwd + adam_apply");
+    return GS_OK;
+  }
   ++c->launches;
   if (wgrad && apply)
-    k_bwd_adam<true, true><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base, L.ncta, dL_dsend, h);
+    k_bwd_adam<true, true, 1><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base, L.ncta, dL_dsend, h);
   else if (wgrad)
-    k_bwd_adam<true, false><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base, L.ncta, dL_dsend, h);
+    k_bwd_adam<true, false, 1><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base, L.ncta, dL_dsend, h);
   else
-    k_bwd_adam<false, true><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base, L.ncta, dL_dsend, h);
+  {
+    // A/B knob: GS_ADAM_MINB = minimum resident CTAs per SM requested from ptxas (1 or 4)
+    static int minb = -1;
+    if (minb < 0) {
+      const char* e = getenv("GS_ADAM_MINB");
+      minb = e ? atoi(e) : 1;
+    }
+    if (minb >= 4)
+      k_bwd_adam<false, true, 4><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base, L.ncta, dL_dsend, h);
+    else
+      k_bwd_adam<false, true, 1><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base, L.ncta, dL_dsend, h);
+  }
   GS_LAUNCH_CHECK(c, "bwd_adam");
   return GS_OK;
 }

@@ -41,7 +41,7 @@ class _Buf:
 class GrendelTrainer:
     def __init__(self, ctx: L.Context, params: L.GaussianParams, width: int, height: int, n_views: int,
                  n_images: int, lr=DEFAULT_LR, cost_mode=L.COST_MEASURED, bg=(0.0, 0.0, 0.0),
-                 rebalance=True, dp=None, device=None):
+                 rebalance=True, dp=None, device=None, split_adam=True):
         self.ctx, self.p = ctx, params
         self.device = device or params.pos_op.device
         self.W, self.H, self.b = width, height, n_views
@@ -50,6 +50,9 @@ class GrendelTrainer:
         self.G, self.rank = ctx.world, ctx.rank
         self.lr, self.cost_mode, self.bg, self.do_rebalance = tuple(lr), cost_mode, tuple(bg), rebalance
         self.m, self.v = params.zeros_like(), params.zeros_like()
+        # parameter-gradient buffer: gs_adam_step then runs backward and Adam as two passes
+        # (faster than the fused single kernel on B200)
+        self.g = params.zeros_like() if split_adam else None
         self.dp = uniform_dp(self.B, self.G) if dp is None else np.asarray(dp, np.int64)
         self.history = torch.full((n_images, self.Wt * self.Ht), -1, dtype=torch.int64, device=self.device)
         self.n_images = n_images
@@ -153,7 +156,7 @@ class GrendelTrainer:
         # A7 + A8 transformation backward + Adam
         rec("adam", 0)
         hp = L.adam_hparams(self.lr, self.b, self.step_count)
-        L.adam_step(ctx, self.p, self.m, self.v, None, cams, dp, dsend, self.bwd_index, hp,
+        L.adam_step(ctx, self.p, self.m, self.v, self.g, cams, dp, dsend, self.bwd_index, hp,
                     L.ADAM_GRAD | L.ADAM_APPLY, st)
         rec("adam", 1)
         # A9 rebalance for the next batch

@@ -1,0 +1,45 @@
+"""Debug helper (GPU box): find pixels where the kernel's n_last differs from the oracle's in
+the city_aerial window case and print the oracle's evaluation trace around the decision."""
+import sys
+import os
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle  # noqa
+import synth  # noqa
+from tests.gsutil import block_major  # noqa
+from tests.test_gpu_scale import _window_case  # noqa
+
+sc, cam = synth.scene_city(4_000_000), synth.cameras_city(128)[70]
+c = _window_case(sc, cam, lo_frac=0.5)
+no = c["no"]
+nl = block_major(c["nl"], no)
+T = block_major(c["T"], no)
+f = c["fwd"]
+bad = np.argwhere(nl != f["nlast"])
+print("mismatches", len(bad))
+for kb, p in bad[:4]:
+    print("block", kb, "pixel", p, "kernel nl", nl[kb, p], "oracle nl", f["nlast"][kb, p], "flags", f["flags"][kb, p],
+          "T k/o", T[kb, p], f["T"][kb, p])
+    beta = c["lo"] + kb
+    tx, ty = beta % c["Wt"], beta // c["Wt"]
+    px, py = tx * 16 + p % 16, ty * 16 + p // 16
+    ent = c["ent"][c["off"][kb]:c["off"][kb + 1]]
+    rec = c["recs"].rec_f[ent]
+    dx, dy = rec[:, 0] - px, rec[:, 1] - py
+    power = -0.5 * (rec[:, 3] * dx * dx + rec[:, 5] * dy * dy) - rec[:, 4] * dx * dy
+    alpha = np.minimum(0.99, rec[:, 6] * np.exp(power))
+    Tc = 1.0
+    lo_, hi_ = min(nl[kb, p], f["nlast"][kb, p]) - 3, max(nl[kb, p], f["nlast"][kb, p]) + 2
+    for k in range(len(ent)):
+        a = alpha[k]
+        if a < 1 / 255:
+            if lo_ <= k <= hi_:
+                print("  k=%d skip alpha*255=%.9f" % (k, a * 255))
+            continue
+        Tn = Tc * (1 - a)
+        if lo_ <= k <= hi_ or Tn < 1e-4:
+            print("  k=%d alpha=%.6g alpha*255=%.9f T'=%.9g" % (k, a, a * 255, Tn))
+        if Tn < 1e-4:
+            break
+        Tc = Tn
