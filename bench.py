@@ -223,6 +223,7 @@ def main():
     ap.add_argument("--cost-mode", default="measured", choices=["measured", "work", "paper_avg"])
     ap.add_argument("--no-rebalance", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-morton", action="store_true", help="keep the generator's (random) Gaussian order")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--breakdown-steps", type=int, default=2)
     ap.add_argument("--json-out", default=None)
@@ -254,6 +255,9 @@ def main():
     n = cfg["n"]
     lo, hi = n * rank // world, n * (rank + 1) // world
     scene = make_scene(cfg, lo, hi)
+    if not args.no_morton:
+        from paper_2406_18533_b200.layout import reorder_scene
+        scene = reorder_scene(scene)  # layout: Morton order within the rank's shard
     cams = make_cameras(cfg)
     W, H = cams[0].width, cams[0].height
     p = L.GaussianParams.from_arrays(scene.pos, scene.log_scale, scene.rot, scene.opac_logit, scene.sh, dev, lo)
@@ -285,6 +289,8 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # size all buffers for every batch this run will use (setup, not timed)
+    tr.reserve_for([batch_cams(k) for k in range(len(sched) - 1)])
     for _ in range(args.warmup):
         one_step()
     setup_s = time.perf_counter() - t_setup
@@ -423,7 +429,8 @@ def main():
                            "image": [W, H], "gaussians": n, "parallelism": "gaussian+pixel x%d (Grendel)" % world,
                            "l2_policy": "inputs larger than L2 (params+Adam state %.1f GB, GT %.2f GB/step)" % (
                                3 * 240 * n / 1e9, cfg["b"] * W * H * 3 / 1e9),
-                           "cost_mode": args.cost_mode, "rebalance": not args.no_rebalance},
+                           "cost_mode": args.cost_mode, "rebalance": not args.no_rebalance,
+                           "shard_layout": "random" if args.no_morton else "morton"},
                 "raster_ms_per_view": round(raster_ms_view, 3),
                 "calls_ms": {k: round(v, 3) for k, v in calls.items()},
                 "gpu_launches": int(launches),

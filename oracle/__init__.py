@@ -177,12 +177,16 @@ def tile_lists(recs: Records, b0, b1, Wt, Ht):
     return off, ent[: int(off[-1])]
 
 
-def render_fwd(recs, off, ent, b0, b1, W, H, bg=(0, 0, 0), gt=None, b_total=1, flag_eps=1e-5, t_eps=1e-3):
+def render_fwd(recs, off, ent, b0, b1, W, H, bg=(0, 0, 0), gt=None, b_total=1, flag_eps=1e-5, t_eps=1e-3,
+               cond_eps=1e-6):
     """O12/O13 over blocks [b0,b1).  gt: [n_views,H,W,3] uint8 or None.
     Flags mark pixels near a discontinuity: an evaluated alpha within
     flag_eps (relative) of 1/255, a T' within t_eps (relative) of 1e-4.  t_eps is wider because
     an fp32 renderer's T carries the relative error of (1 - alpha), which an alpha near the
-    0.99 cap amplifies ~alpha/(1 - alpha) = 99x (1e-6 -> 1e-4)."""
+    0.99 cap amplifies ~alpha/(1 - alpha) = 99x (1e-6 -> 1e-4).  The alpha test is on
+    |ln(255 alpha)| < flag_eps + cond_eps * S, S = |u| (|l11 dx| + |l21 dy|) + u^2 + w^2 the fp32
+    conditioning of the exponent -(u^2 + w^2)/2 through the conic's Cholesky factor (for thin
+    Gaussians u cancels large terms); cond_eps = 1e-6 ~ 16 eps_f32."""
     nb = b1 - b0
     o = dict(c=np.zeros((nb, 256, 3)), T=np.zeros((nb, 256)), nlast=np.zeros((nb, 256), np.int32),
              flags=np.zeros((nb, 256), np.int32), counts=np.zeros((nb, 256, 4), np.int64),
@@ -193,7 +197,8 @@ def render_fwd(recs, off, ent, b0, b1, W, H, bg=(0, 0, 0), gt=None, b_total=1, f
     ent = np.ascontiguousarray(ent, np.int64) if len(ent) else np.zeros(1, np.int64)
     lib().orc_render_fwd(C.c_int64(recs.n), _p(recs.rec_f), _p(off), _p(ent), C.c_int64(b0),
                          C.c_int64(b1), C.c_int32(W), C.c_int32(H), _p(bgv), _p(gtp),
-                         C.c_int32(b_total), C.c_double(flag_eps), C.c_double(t_eps), _p(o["c"]), _p(o["T"]),
+                         C.c_int32(b_total), C.c_double(flag_eps), C.c_double(t_eps), C.c_double(cond_eps),
+                         _p(o["c"]), _p(o["T"]),
                          _p(o["nlast"]), _p(o["flags"]), _p(o["counts"]), _p(o["work"]),
                          _p(o["dl_dc"]), C.byref(loss))
     o["loss"] = loss.value

@@ -390,6 +390,7 @@ static double sgn(double v) { return (v > 0) - (v < 0); }
 void orc_render_fwd(int64_t n_rec, const double* rec_f, const int64_t* offsets,
                     const int64_t* entries, int64_t b0, int64_t b1, int32_t W, int32_t H,
                     const double* bg, const uint8_t* gt, int32_t b_total, double flag_eps, double t_eps,
+                    double cond_eps,
                     double* out_c, double* out_T, int32_t* out_nlast, int32_t* flags,
                     int64_t* counts, int64_t* work, double* dl_dc, double* loss) {
   (void)n_rec;
@@ -418,23 +419,38 @@ void orc_render_fwd(int64_t n_rec, const double* rec_f, const int64_t* offsets,
         if (dl_dc) dl_dc[3 * o] = dl_dc[3 * o + 1] = dl_dc[3 * o + 2] = 0;
         continue;
       }
+      double terr = 0.0; /* bound on the fp32 renderer's relative error of T so far */
       for (int64_t k = 0; k < nL; k++) {
         const double* r = rec_f + 10 * L[k];
         double dx = r[0] - px, dy = r[1] - py;
         double power = -0.5 * (r[3] * dx * dx + r[5] * dy * dy) - r[4] * dx * dy;
+        double aeps = flag_eps;
         Ef++;
         if (power > 0) { flag |= 4; Efs++; continue; }
         double alpha = r[6] * exp(power);
         if (alpha > ALPHA_CAP) alpha = ALPHA_CAP;
-        if (fabs(alpha * 255.0 - 1.0) < flag_eps) flag |= 1;
+        {
+          /* conditioning of power in fp32: its absolute error is ~eps_f32 S (thin Gaussians:
+           * u cancels large terms), so the margin on |ln(255 alpha)| is
+           * flag_eps + cond_eps * S (discontinuities) */
+          /* S bounds |d power| / eps_f32 for an evaluation through the Cholesky factor of the
+           * conic (power = -(u^2 + w^2)/2, u = l11 dx + l21 dy, w = l22 dy) */
+          double l11 = sqrt(r[3]), l21 = r[4] / l11, l22 = sqrt(fmax(r[5] - l21 * l21, 0.0));
+          double u = l11 * dx + l21 * dy, w = l22 * dy;
+          double S = fabs(u) * (fabs(l11 * dx) + fabs(l21 * dy)) + u * u + w * w;
+          aeps = flag_eps + cond_eps * S;
+          if (alpha > 0 && fabs(log(alpha * 255.0)) < aeps) flag |= 1;
+        }
         if (alpha < ALPHA_MIN) { Efs++; continue; }
         double Tn = T * (1.0 - alpha);
-        if (fabs(Tn * 1e4 - 1.0) < t_eps) flag |= 2;
+        if (fabs(Tn * 1e4 - 1.0) < t_eps + terr) flag |= 2;
         if (Tn < T_STOP) { Estop = 1; break; }  /* R3: stop before compositing */
         for (int ch = 0; ch < 3; ch++) C[ch] += alpha * T * r[7 + ch];
         T = Tn;
         nlast = (int32_t)(k + 1);
         Efc++;
+        /* an alpha error aeps (relative) moves (1 - alpha) by aeps alpha / (1 - alpha) */
+        terr += aeps * alpha / (1.0 - alpha);
       }
       for (int ch = 0; ch < 3; ch++) C[ch] += T * bg[ch];
       for (int ch = 0; ch < 3; ch++) out_c[3 * o + ch] = C[ch];

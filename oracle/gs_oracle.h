@@ -61,7 +61,7 @@ void orc_tile_lists(int64_t n_rec, const double* rec_f, const int64_t* rec_i, in
 /* O12 (+ O13 when gt != NULL): forward compositing over blocks [b0,b1).
  * Block-major outputs, pixel p = ly*16+lx of the block:
  *   out_c[nb][256][3], out_T[nb][256], out_nlast[nb][256] (int32),
- *   flags[nb][256] (bit0: |255 alpha - 1| < flag_eps, bit1: |1e4 T' - 1| < t_eps, bit2: power>0 seen,
+ *   flags[nb][256] (bit0: |ln(255 alpha)| < flag_eps + cond_eps * S (S: fp32 conditioning of power, see .c), bit1: |1e4 T' - 1| < t_eps + (accumulated alpha-margin bound of T), bit2: power>0 seen,
  *                   bit3: |C-GT| < flag_eps (L1 sign ambiguous)),
  *   counts[nb][256][4] = (E_f, E_fc, E_fs, E_stop), work[nb] = sum_px (E_f + n_last),
  *   dl_dc[nb][256][3] = sign(C-GT)/(3 H W b_total) (only if gt), *loss += sum |C-GT|/(3HWb).
@@ -69,6 +69,7 @@ void orc_tile_lists(int64_t n_rec, const double* rec_f, const int64_t* rec_i, in
 void orc_render_fwd(int64_t n_rec, const double* rec_f, const int64_t* offsets,
                     const int64_t* entries, int64_t b0, int64_t b1, int32_t W, int32_t H,
                     const double* bg, const uint8_t* gt, int32_t b_total, double flag_eps, double t_eps,
+                    double cond_eps,
                     double* out_c, double* out_T, int32_t* out_nlast, int32_t* flags,
                     int64_t* counts, int64_t* work, double* dl_dc, double* loss);
 

@@ -442,6 +442,188 @@ __global__ void __launch_bounds__(256 / PPT) k_render_bwd(
   }
 }
 
+// Compacted backward: one warp per block.  The per-pixel backward state (T, S, dL/dC, T_final,
+// bg term) lives in shared memory.  For each entry the warp evaluates the skip test of all 256
+// pixels with the forward's exact strip decomposition (FP pixels per strip, q_strip<FP>),
+// compacts the contributing pixels into a shared list (pixel, u, w, q), and processes that
+// list 32 at a time -- lane L takes the L-th contributing pixel -- so the ~45-instruction
+// gradient body runs with all lanes busy instead of once per strip row with most lanes idle.
+// The 9 record gradients are then reduced across the warp once per entry (transpose
+// reduction) and added straight into dL/d(record).
+template <int FP, bool kStats>
+__global__ void __launch_bounds__(32) k_render_bwd_c(
+    const gs_rec* __restrict__ rec, const uint32_t* __restrict__ sorted_idx,
+    const int32_t* __restrict__ range, gs_geom geo, int64_t B_lo, float bg0, float bg1, float bg2,
+    const float* __restrict__ dL_dpix, const float* __restrict__ T_final,
+    const int32_t* __restrict__ n_last, float* __restrict__ dL_drec, int64_t* __restrict__ tile_cost,
+    int cost_mode, long long* __restrict__ stats) {
+  constexpr int kStrips = 8 / FP;   // forward strips handled by each lane
+  constexpr int kBB = 128;          // records staged per round
+  __shared__ float4 s_a[kBB], s_b[kBB];
+  __shared__ float2 s_c[kBB];
+  __shared__ uint32_t s_j[kBB];
+  __shared__ float s_T[256], s_S0[256], s_S1[256], s_S2[256], s_g0[256], s_g1[256], s_g2[256], s_Tf[256],
+      s_bgd[256];
+  __shared__ float4 s_list[256];  // contributing (pixel, u, w, q) of the current entry
+  const long long t0 = clock64();
+  const int lane = threadIdx.x;
+  const int64_t lb = blockIdx.x, beta = B_lo + lb;
+  const int64_t loc = beta % geo.per_view;
+  const int tx = (int)(loc % geo.Wt), ty = (int)(loc / geo.Wt);
+  // lane's forward strips: strip index st = lane + 32 i, column st & 15, first row FP*(st >> 4)
+  int nl[kStrips][FP];
+  float fpx[kStrips], fpy0[kStrips];
+  int mymax = 0, nlsum = 0;
+#pragma unroll
+  for (int i = 0; i < kStrips; i++) {
+    const int st = lane + 32 * i, x = st & 15, y0 = FP * (st >> 4);
+    const int px = tx * 16 + x, py0 = ty * 16 + y0;
+    fpx[i] = (float)px;
+    fpy0[i] = (float)py0;
+#pragma unroll
+    for (int j = 0; j < FP; j++) {
+      const int pp = (y0 + j) * 16 + x;
+      const bool in = px < geo.W && py0 + j < geo.H;
+      const int64_t o = lb * 256 + pp;
+      nl[i][j] = in ? n_last[o] : 0;
+      const float tf = in ? T_final[o] : 1.f;
+      const float g0 = in ? dL_dpix[lb * 768 + pp] : 0.f;
+      const float g1 = in ? dL_dpix[lb * 768 + 256 + pp] : 0.f;
+      const float g2 = in ? dL_dpix[lb * 768 + 512 + pp] : 0.f;
+      s_T[pp] = tf;
+      s_Tf[pp] = tf;
+      s_S0[pp] = s_S1[pp] = s_S2[pp] = 0.f;
+      s_g0[pp] = g0;
+      s_g1[pp] = g1;
+      s_g2[pp] = g2;
+      s_bgd[pp] = bg0 * g0 + bg1 * g1 + bg2 * g2;
+      mymax = max(mymax, nl[i][j]);
+      nlsum += nl[i][j];
+    }
+  }
+  const int maxn = __reduce_max_sync(0xffffffffu, mymax);
+  bool rvalid;
+  const int ridx = red_index(lane, rvalid);
+  const int beg = range[lb];
+  const float kQ = 1.3862943611198906f;  // 2 ln 2 = 1 / kLScale^2
+  int ebc = 0;
+  for (int bi = (maxn + kBB - 1) / kBB - 1; bi >= 0; bi--) {
+    const int p0 = bi * kBB;
+    const int cnt = min(kBB, maxn - p0);
+    __syncwarp();
+    for (int t = lane; t < cnt; t += 32) {
+      const uint32_t j = sorted_idx[beg + p0 + t];
+      stage(rec, j, s_a, s_b, s_c, t);
+      s_j[t] = j;
+    }
+    __syncwarp();
+    for (int k = cnt - 1; k >= 0; k--) {
+      const int pos = p0 + k;
+      const float4 A = s_a[k], Bq = s_b[k];
+      const float2 cq = s_c[k];
+      // 1. skip tests of the lane's pixels (bit-identical to the forward's decisions)
+      unsigned c[kStrips];
+      gs_strip<FP> e[kStrips];
+      int mine = 0;
+#pragma unroll
+      for (int i = 0; i < kStrips; i++) {
+        q_strip<FP>(A, Bq, fpx[i], fpy0[i], e[i]);
+        c[i] = 0;
+#pragma unroll
+        for (int j = 0; j < FP; j++) c[i] |= (unsigned)(pos < nl[i][j] && e[i].q[j] <= cq.y) << j;
+        mine += __popc(c[i]);
+      }
+      // 2. compaction offsets
+      int incl = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      if (total == 0) continue;
+      int w = incl - mine;
+#pragma unroll
+      for (int i = 0; i < kStrips; i++) {
+        const int st = lane + 32 * i, x = st & 15, y0 = FP * (st >> 4);
+        unsigned cc = c[i];
+        while (cc) {
+          const int j = __ffs(cc) - 1;
+          cc &= cc - 1;
+          float uj = 0.f, wj = 0.f, qj = 0.f;
+#pragma unroll
+          for (int jj = 0; jj < FP; jj++)
+            if (jj == j) { uj = e[i].u[jj]; wj = e[i].w[jj]; qj = e[i].q[jj]; }
+          s_list[w++] = make_float4(__int_as_float((y0 + j) * 16 + x), uj, wj, qj);
+        }
+      }
+      __syncwarp();
+      // 3. lane L processes contributions L, L + 32, ...
+      float gr[9];
+#pragma unroll
+      for (int q = 0; q < 9; q++) gr[q] = 0.f;
+      for (int idx = lane; idx < total; idx += 32) {
+        const float4 it = s_list[idx];
+        const int pp = __float_as_int(it.x);
+        const float u = it.y, wv = it.z, q = it.w;
+        const float px = (float)(tx * 16 + (pp & 15)), py = (float)(ty * 16 + (pp >> 4));
+        const float dx = __fsub_rn(A.x, px), dy = __fsub_rn(A.y, py);
+        const float G = ex2_approx(-q);
+        const float raw = __fmul_rn(Bq.y, G);
+        const float alpha = fminf(kAlphaCap, raw);
+        const float om = 1.0f - alpha;
+        const float rom = __fdividef(1.0f, om);
+        const float T = s_T[pp] * rom;  // transmittance in front of this entry
+        const float S0 = s_S0[pp], S1 = s_S1[pp], S2 = s_S2[pp];
+        const float g0 = s_g0[pp], g1 = s_g1[pp], g2 = s_g2[pp];
+        const float cr = Bq.z, cg = Bq.w, cb = cq.x;
+        const float wgt = alpha * T;
+        gr[6] = fmaf(wgt, g0, gr[6]);
+        gr[7] = fmaf(wgt, g1, gr[7]);
+        gr[8] = fmaf(wgt, g2, gr[8]);
+        const float dA = T * ((cr - S0) * g0 + (cg - S1) * g1 + (cb - S2) * g2) - s_Tf[pp] * rom * s_bgd[pp];
+        s_T[pp] = T;
+        s_S0[pp] = fmaf(alpha, cr - S0, S0);
+        s_S1[pp] = fmaf(alpha, cg - S1, S1);
+        s_S2[pp] = fmaf(alpha, cb - S2, S2);
+        if (raw <= kAlphaCap) {  // R6: zero gradient through the 0.99 cap
+          const float gG = G * dA;
+          const float qq = Bq.y * gG;  // dL/dpower
+          const float qs = qq * kQ;
+          gr[5] += gG;
+          gr[0] = fmaf(-qs, A.z * u, gr[0]);
+          gr[1] = fmaf(-qs, fmaf(A.w, u, Bq.x * wv), gr[1]);
+          const float hq = -0.5f * qq;
+          gr[2] = fmaf(hq * dx, dx, gr[2]);
+          gr[3] = fmaf(-qq * dx, dy, gr[3]);
+          gr[4] = fmaf(hq * dy, dy, gr[4]);
+        }
+      }
+      if (kStats) ebc += total;
+      // 4. one warp reduction per entry, straight into dL/d(record)
+      const float z = warp_reduce9(gr, lane);
+      if (rvalid && z != 0.f) atomicAdd(dL_drec + (int64_t)s_j[k] * 9 + ridx, z);
+      __syncwarp();
+    }
+  }
+  if (kStats) {
+    const long long a = __reduce_add_sync(0xffffffffu, (unsigned)nlsum);
+    if (lane == 0) {
+      atomicAdd((unsigned long long*)&stats[4], (unsigned long long)a);
+      atomicAdd((unsigned long long*)&stats[5], (unsigned long long)ebc);
+    }
+  }
+  if (tile_cost) {
+    if (cost_mode == GS_COST_WORK) {
+      const long long wsum = __reduce_add_sync(0xffffffffu, (unsigned)nlsum);
+      if (lane == 0) tile_cost[lb] += wsum;
+    } else {
+      __syncwarp();
+      if (lane == 0) tile_cost[lb] += clock64() - t0;
+    }
+  }
+}
+
 // pixels per thread (A/B knob: GS_RENDER_PPT = 2, 4 or 8; default 4, measured best on C2)
 static int render_ppt() {
   static int ppt = -1;
@@ -507,10 +689,22 @@ extern "C" gs_status gs_render_bwd(gs_ctx* c, const void* recv_rec, int64_t n_re
   if (bg_h) for (int k = 0; k < 3; k++) bg[k] = bg_h[k];
   ++c->launches;
   const int ppt = render_ppt();
+  static int compact = -1;
+  if (compact < 0) {
+    const char* e = getenv("GS_RENDER_BWD_COMPACT");
+    compact = e ? atoi(e) : 0;
+  }
   auto kb = ppt == 2 ? (stats ? k_render_bwd<2, true> : k_render_bwd<2, false>)
           : ppt == 4 ? (stats ? k_render_bwd<4, true> : k_render_bwd<4, false>)
                      : (stats ? k_render_bwd<8, true> : k_render_bwd<8, false>);
-  kb<<<(unsigned)n_owned, 256 / ppt, 0, st>>>(
+  int threads = 256 / ppt;
+  if (compact) {  // compacted one-warp backward, same strip decomposition as the forward
+    kb = ppt == 2 ? (stats ? k_render_bwd_c<2, true> : k_render_bwd_c<2, false>)
+       : ppt == 4 ? (stats ? k_render_bwd_c<4, true> : k_render_bwd_c<4, false>)
+                  : (stats ? k_render_bwd_c<8, true> : k_render_bwd_c<8, false>);
+    threads = 32;
+  }
+  kb<<<(unsigned)n_owned, threads, 0, st>>>(
       (const gs_rec*)recv_rec, sorted_idx, tile_range, geo, B_lo, bg[0], bg[1], bg[2], dL_dpix, T_final, n_last,
       dL_drec, tile_cost, cost_mode, (long long*)stats);
   GS_LAUNCH_CHECK(c, "render_bwd");

@@ -73,6 +73,36 @@ class GrendelTrainer:
         self.stats = torch.zeros(8, dtype=torch.int64, device=dev)
         self.last = {}
 
+    def reserve_for(self, batches):
+        """Size every growable buffer (and libgs's scratch) for the given camera batches by
+        running their projection and binning once (setup, outside any timed region)."""
+        saved = self.dp.copy()
+        for cams in batches:
+            cap = self.send.cap
+            while True:
+                try:
+                    cnt = L.project(self.ctx, self.p, cams, self.dp, self.send.t, cap, self.bwd_index)
+                    break
+                except L.CapacityError as e:
+                    self.send.ensure(int(e.counts.sum()))
+                    cap = self.send.cap
+            n = int(cnt.sum())
+            self.drec.ensure(n), self.dsend.ensure(n), self.recv.ensure(n if self.G > 1 else 0)
+            if self.G == 1:
+                no = self.n_owned
+                self.range.ensure(no + 1)
+                while True:
+                    try:
+                        L.bin_sort(self.ctx, self.send.t, n, cams, self.dp, self.sorted.t, self.sorted.cap,
+                                   self.range.t)
+                        break
+                    except L.CapacityError as e:
+                        self.sorted.ensure(e.needed)
+        no = self.B  # a rank may own up to every block after rebalancing
+        self.T.ensure(no), self.nl.ensure(no), self.dpix.ensure(no), self.cost.ensure(no), self.range.ensure(no + 1)
+        self.dp = saved
+        torch.cuda.synchronize()
+
     @property
     def n_owned(self):
         return int(self.dp[self.rank + 1] - self.dp[self.rank])

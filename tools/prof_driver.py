@@ -35,6 +35,8 @@ def main():
     b = a.views or cfg["b"]
     dev = torch.device("cuda", 0)
     sc = bench.make_scene(cfg, 0, cfg["n"])
+    from paper_2406_18533_b200.layout import reorder_scene
+    sc = reorder_scene(sc)
     cams = bench.make_cameras(cfg)
     sched = bench.batches(dict(cfg, b=b), a.warmup + a.steps + 1) if cfg["seed"] != 4 else \
         bench.batches(cfg, a.warmup + a.steps + 1)
