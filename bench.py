@@ -397,7 +397,8 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "dram_traffic.json")) as f:
-            traffic = json.load(f).get(args.config, {}).get(dom)
+            t = json.load(f).get(args.config, {}).get(dom)
+            traffic = None if t is None else {"bytes_per_launch": t["bytes"], "source": t["source"]}
     except Exception:
         pass
     rooflines = {}

@@ -178,7 +178,7 @@ def tile_lists(recs: Records, b0, b1, Wt, Ht):
 
 
 def render_fwd(recs, off, ent, b0, b1, W, H, bg=(0, 0, 0), gt=None, b_total=1, flag_eps=1e-5, t_eps=1e-3,
-               cond_eps=1e-6):
+               cond_eps=4e-7):
     """O12/O13 over blocks [b0,b1).  gt: [n_views,H,W,3] uint8 or None.
     Flags mark pixels near a discontinuity: an evaluated alpha within
     flag_eps (relative) of 1/255, a T' within t_eps (relative) of 1e-4.  t_eps is wider because
@@ -186,7 +186,7 @@ def render_fwd(recs, off, ent, b0, b1, W, H, bg=(0, 0, 0), gt=None, b_total=1, f
     0.99 cap amplifies ~alpha/(1 - alpha) = 99x (1e-6 -> 1e-4).  The alpha test is on
     |ln(255 alpha)| < flag_eps + cond_eps * S, S = |u| (|l11 dx| + |l21 dy|) + u^2 + w^2 the fp32
     conditioning of the exponent -(u^2 + w^2)/2 through the conic's Cholesky factor (for thin
-    Gaussians u cancels large terms); cond_eps = 1e-6 ~ 16 eps_f32."""
+    Gaussians u cancels large terms); cond_eps = 4e-7 ~ 7 eps_f32."""
     nb = b1 - b0
     o = dict(c=np.zeros((nb, 256, 3)), T=np.zeros((nb, 256)), nlast=np.zeros((nb, 256), np.int32),
              flags=np.zeros((nb, 256), np.int32), counts=np.zeros((nb, 256, 4), np.int64),

@@ -127,7 +127,8 @@ __global__ void __launch_bounds__(256 / PPT) k_render_fwd(
   const int beg = range[lb], end = range[lb + 1];
   float T[PPT], C0[PPT], C1[PPT], C2[PPT];
   int nl[PPT], sp[PPT];
-  unsigned done = 0, inside = 0;
+  bool dn[PPT];  // pixel done (stopped, or outside the image); kept as predicates
+  unsigned inside = 0;
 #pragma unroll
   for (int j = 0; j < PPT; j++) {
     T[j] = 1.f;
@@ -136,11 +137,17 @@ __global__ void __launch_bounds__(256 / PPT) k_render_fwd(
     sp[j] = -1;
     const bool in = px < geo.W && py0 + j < geo.H;
     inside |= (unsigned)in << j;
+    dn[j] = !in;
   }
-  done = ~inside & kAll;
   int efc = 0;
+  auto all_done = [&]() {
+    bool a = true;
+#pragma unroll
+    for (int j = 0; j < PPT; j++) a = a && dn[j];
+    return a;
+  };
   for (int b0 = beg; b0 < end; b0 += kBatch) {
-    if (__syncthreads_count(done == kAll) == NT) break;
+    if (__syncthreads_count(all_done()) == NT) break;
     const int cnt = min(kBatch, end - b0);
     const int cnt8 = (cnt + kUnroll - 1) & ~(kUnroll - 1);
     for (int t = tid; t < cnt8; t += NT) {
@@ -155,7 +162,7 @@ __global__ void __launch_bounds__(256 / PPT) k_render_fwd(
     __syncthreads();
     const int pbase = b0 - beg;
     for (int k0 = 0; k0 < cnt8; k0 += kUnroll) {
-      if (done == kAll) break;
+      if (all_done()) break;
 #pragma unroll
       for (int kk = 0; kk < kUnroll; kk++) {
         const int k = k0 + kk;
@@ -163,18 +170,20 @@ __global__ void __launch_bounds__(256 / PPT) k_render_fwd(
         const float2 cq = s_c[k];
         gs_strip<PPT> e;
         q_strip<PPT>(A, Bq, fpx, fpy0, e);
-        unsigned c = 0;
+        bool cj[PPT], any = false;
 #pragma unroll
-        for (int j = 0; j < PPT; j++) c |= (unsigned)(e.q[j] <= cq.y) << j;
-        c &= ~done;
-        if (c) {  // the common case (every pixel skips the entry) takes one branch
+        for (int j = 0; j < PPT; j++) {
+          cj[j] = !dn[j] && e.q[j] <= cq.y;
+          any = any || cj[j];
+        }
+        if (any) {  // the common case (every pixel skips the entry) takes one branch
 #pragma unroll
           for (int j = 0; j < PPT; j++)
-            if (c >> j & 1) {
+            if (cj[j]) {
               bool st = false;
               const float al = fminf(kAlphaCap, __fmul_rn(Bq.y, ex2_approx(-e.q[j])));
               fwd_comp<kStats>(al, Bq.z, Bq.w, cq.x, pbase + k, T[j], C0[j], C1[j], C2[j], st, nl[j], sp[j], efc);
-              done |= (unsigned)st << j;
+              dn[j] = st;
             }
         }
       }
@@ -321,10 +330,14 @@ __global__ void __launch_bounds__(256 / PPT) k_render_bwd(
     int cost_mode, long long* __restrict__ stats) {
   constexpr int NT = 256 / PPT;
   constexpr bool kOneWarp = NT == 32;
-  __shared__ float4 s_a[kBatch], s_b[kBatch];
-  __shared__ float2 s_c[kBatch];
-  __shared__ uint32_t s_j[kBatch];
-  __shared__ float s_g[kOneWarp ? 1 : kBatch * 9];
+  constexpr int kNW = NT / 32;   // warps per block
+  constexpr int kBB = 128;        // records staged per round
+  __shared__ float4 s_a[kBB], s_b[kBB];
+  __shared__ float2 s_c[kBB];
+  __shared__ uint32_t s_j[kBB];
+  // per-warp gradient slots: each (warp, entry, value) is written by exactly one lane, so no
+  // shared-memory atomics (a float atomicAdd on shared memory is a CAS loop on sm_100)
+  __shared__ float s_g[kOneWarp ? 1 : kNW * kBB * 9];
   __shared__ int s_max[NT / 32];
   __shared__ long long s_red[NT / 32];
   const long long t0 = clock64();
@@ -366,9 +379,9 @@ __global__ void __launch_bounds__(256 / PPT) k_render_bwd(
   const int ridx = red_index(lane, rvalid);
   const int beg = range[lb];
   int ebc = 0;
-  for (int bi = (maxn + kBatch - 1) / kBatch - 1; bi >= 0; bi--) {
-    const int p0 = bi * kBatch;  // list position of the batch start
-    const int cnt = min(kBatch, maxn - p0);
+  for (int bi = (maxn + kBB - 1) / kBB - 1; bi >= 0; bi--) {
+    const int p0 = bi * kBB;  // list position of the batch start
+    const int cnt = min(kBB, maxn - p0);
     __syncthreads();
     for (int t = tid; t < cnt; t += NT) {
       const uint32_t j = sorted_idx[beg + p0 + t];
@@ -376,7 +389,7 @@ __global__ void __launch_bounds__(256 / PPT) k_render_bwd(
       s_j[t] = j;
     }
     if (!kOneWarp)
-      for (int t = tid; t < cnt * 9; t += NT) s_g[t] = 0.f;
+      for (int t = tid; t < kNW * kBB * 9; t += NT) s_g[t] = 0.f;
     __syncthreads();
     for (int k = min(cnt, wmax - p0) - 1; k >= 0; k--) {  // warp-uniform range
       const int pos = p0 + k;
@@ -384,29 +397,35 @@ __global__ void __launch_bounds__(256 / PPT) k_render_bwd(
       const float2 cq = s_c[k];
       gs_strip<PPT> e;
       q_strip<PPT>(A, Bq, fpx, fpy0, e);
-      unsigned c = 0;
+      bool cj[PPT], any = false;
 #pragma unroll
-      for (int j = 0; j < PPT; j++) c |= (unsigned)(pos < nl[j] && e.q[j] <= cq.y) << j;
+      for (int j = 0; j < PPT; j++) {
+        cj[j] = pos < nl[j] && e.q[j] <= cq.y;
+        any = any || cj[j];
+      }
       float gr[9];
 #pragma unroll
       for (int q = 0; q < 9; q++) gr[q] = 0.f;
-      if (c) {
+      if (any) {
 #pragma unroll
         for (int j = 0; j < PPT; j++)
-          if (c >> j & 1) {
+          if (cj[j]) {
             const float G = ex2_approx(-e.q[j]);
             bwd_comp(__fmul_rn(Bq.y, G), G, e.dx, __fsub_rn(e.dy0, (float)j), e.u[j], e.w[j], A, Bq, cq.x, T[j],
                      S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], gr);
           }
-        if (kStats) ebc += __popc(c);
+        if (kStats) {
+#pragma unroll
+          for (int j = 0; j < PPT; j++) ebc += cj[j];
+        }
       }
-      if (__any_sync(0xffffffffu, c != 0)) {
+      if (__any_sync(0xffffffffu, any)) {
         const float z = warp_reduce9(gr, lane);
         if (rvalid) {
           if (kOneWarp) {
             if (z != 0.f) atomicAdd(dL_drec + (int64_t)s_j[k] * 9 + ridx, z);
           } else {
-            atomicAdd(&s_g[k * 9 + ridx], z);
+            s_g[(wid * kBB + k) * 9 + ridx] = z;
           }
         }
       }
@@ -417,7 +436,9 @@ __global__ void __launch_bounds__(256 / PPT) k_render_bwd(
         float* dst = dL_drec + (int64_t)s_j[t] * 9;
 #pragma unroll
         for (int q = 0; q < 9; q++) {
-          const float xv = s_g[t * 9 + q];
+          float xv = 0.f;
+#pragma unroll
+          for (int w = 0; w < kNW; w++) xv += s_g[(w * kBB + t) * 9 + q];
           if (xv != 0.f) atomicAdd(dst + q, xv);
         }
       }

@@ -97,5 +97,34 @@ def report(rep, out_md):
     print("\n".join(lines))
 
 
+def traffic(rep, config, out_json="profiles/dram_traffic.json"):
+    """Record dram__bytes_read.sum + dram__bytes_write.sum per launch of each kernel of a
+    --set full capture into profiles/dram_traffic.json[config][kernel-role]."""
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    hdr, units = rows[0], rows[1]
+    ki, ri, wi = hdr.index("Kernel Name"), hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    try:
+        d = json.load(open(out_json))
+    except Exception:
+        d = {}
+    roles = {"k_render_fwd": "render_fwd", "k_render_bwd": "render_bwd", "k_bwd_adam": "adam",
+             "k_project_write": "project", "k_place": "bin_sort"}
+    for r in rows[2:]:
+        name = _kname(r[ki])
+        role = next((v for k, v in roles.items() if name.startswith(k)), None)
+        if role is None:
+            continue
+        b = float(r[ri]) * scale.get(units[ri], 1) + float(r[wi]) * scale.get(units[wi], 1)
+        src = rep.replace("gpurun_out/prof_", "profiles/").replace(".ncu-rep", ".md")
+        d.setdefault(config, {})[role] = {"bytes": b, "source": src, "kernel": name}
+    json.dump(d, open(out_json, "w"), indent=1)
+    print(json.dumps(d, indent=1))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "report": report}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    if sys.argv[1] == "traffic":
+        traffic(sys.argv[2], sys.argv[3])
+    else:
+        {"launches": launches, "report": report}[sys.argv[1]](sys.argv[2], sys.argv[3])
