@@ -44,6 +44,71 @@ __device__ __forceinline__ void stage(const gs_rec* __restrict__ rec, uint32_t j
   s_c[t] = make_float2(c.z, b.w > 0.f ? __log2f(255.0f * b.w) : -1.0f);
 }
 
+// Could any pixel centre of the 16x16 block at (bx0, by0) see the staged record with
+// alpha >= 1/255?  Minimum of q(d) = |L'^T d|^2 over the continuous box of offsets
+// d = m - p (a convex quadratic: 0 if the box contains d = 0, else on one of its edges)
+// against qmax with a wide margin (5% of 1 + qmax in the exponent), so an entry is dropped only
+// when every pixel would skip it: a conservative, semantics-free cull (dropped entries are
+// no-ops for every pixel of the block).
+__device__ __forceinline__ bool block_may_hit(const float4& A, const float4& Bq, float qmax, float bx0, float by0) {
+  if (!(qmax >= 0.f)) return false;  // opacity < 1/255: never composited
+  const float l11 = A.z, l21 = A.w, l22 = Bq.x;
+  const float dxh = A.x - bx0, dxl = dxh - 15.f, dyh = A.y - by0, dyl = dyh - 15.f;
+  if (dxl <= 0.f && dxh >= 0.f && dyl <= 0.f && dyh >= 0.f) return true;
+  const float a = l11 * l11, b = l11 * l21, c = l21 * l21 + l22 * l22;
+  auto Q = [&](float dx, float dy) {
+    const float u = fmaf(l11, dx, l21 * dy), w = l22 * dy;
+    return fmaf(u, u, w * w);
+  };
+  float qmin = Q(dxl, fminf(fmaxf(-b * dxl / c, dyl), dyh));
+  qmin = fminf(qmin, Q(dxh, fminf(fmaxf(-b * dxh / c, dyl), dyh)));
+  qmin = fminf(qmin, Q(fminf(fmaxf(-b * dyl / a, dxl), dxh), dyl));
+  qmin = fminf(qmin, Q(fminf(fmaxf(-b * dyh / a, dxl), dxh), dyh));
+  return !(qmin > qmax + 0.05f * (1.0f + qmax));
+}
+
+// Stage the batch's records [0, cnt) into their slots and compact the indices of the records
+// that may be hit (block_may_hit) into s_idx, in list order, padded with kDummy up to a
+// multiple of `pad`.  Returns the number of kept entries (the caller syncs before reading).
+template <int NT, int BATCH>
+__device__ __forceinline__ int stage_compact(const gs_rec* __restrict__ rec, const uint32_t* __restrict__ sidx,
+                                             int cnt, float4* s_a, float4* s_b, float2* s_c, uint32_t* s_j,
+                                             unsigned char* s_idx, int* s_wc, float bx0, float by0, int pad,
+                                             int dummy) {
+  constexpr int kW = NT / 32, kI = BATCH / NT;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  unsigned bal[kI];
+#pragma unroll
+  for (int i = 0; i < kI; i++) {
+    const int t = tid + NT * i;
+    bool keep = false;
+    if (t < cnt) {
+      const uint32_t j = sidx[t];
+      stage(rec, j, s_a, s_b, s_c, t);
+      if (s_j) s_j[t] = j;
+      keep = block_may_hit(s_a[t], s_b[t], s_c[t].y, bx0, by0);
+    }
+    bal[i] = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) s_wc[i * kW + wid] = __popc(bal[i]);
+  }
+  __syncthreads();
+  int total = 0;
+#pragma unroll
+  for (int x = 0; x < kI * kW; x++) total += s_wc[x];
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int i = 0; i < kI; i++) {
+    if ((bal[i] >> lane) & 1u) {
+      int off = __popc(bal[i] & lt);
+      for (int x = 0; x < i * kW + wid; x++) off += s_wc[x];
+      s_idx[off] = (unsigned char)(tid + NT * i);
+    }
+  }
+  const int padded = (total + pad - 1) / pad * pad;
+  for (int t = total + tid; t < padded; t += NT) s_idx[t] = (unsigned char)dummy;
+  return total;
+}
+
 template <int NT, typename T>
 __device__ __forceinline__ T block_sum(T v, T* sm) {
 #pragma unroll
@@ -111,9 +176,15 @@ __global__ void __launch_bounds__(256 / PPT) k_render_fwd(
     double* __restrict__ loss_sum, int64_t* __restrict__ tile_cost, int cost_mode,
     long long* __restrict__ stats) {
   constexpr int NT = 256 / PPT;
-  constexpr unsigned kAll = (1u << PPT) - 1u;
-  __shared__ float4 s_a[kBatch], s_b[kBatch];
-  __shared__ float2 s_c[kBatch];
+  __shared__ float4 s_a[kBatch + 1], s_b[kBatch + 1];  // slot kBatch: the padding entry
+  __shared__ float2 s_c[kBatch + 1];
+  __shared__ unsigned char s_idx[kBatch + kUnroll];
+  __shared__ int s_wc[kBatch / 32];
+  if (threadIdx.x == 0) {  // padding entry: opacity 0, qmax < 0 <= q: never composited
+    s_a[kBatch] = make_float4(0.f, 0.f, 0.f, 0.f);
+    s_b[kBatch] = make_float4(0.f, 0.f, 0.f, 0.f);
+    s_c[kBatch] = make_float2(0.f, -1.0f);
+  }
   __shared__ long long s_red[NT / 32];
   __shared__ double s_redd[NT / 32];
   const long long t0 = clock64();
@@ -146,28 +217,22 @@ __global__ void __launch_bounds__(256 / PPT) k_render_fwd(
     for (int j = 0; j < PPT; j++) a = a && dn[j];
     return a;
   };
+  const float bx0 = (float)(tx * 16), by0 = (float)(ty * 16);
   for (int b0 = beg; b0 < end; b0 += kBatch) {
     if (__syncthreads_count(all_done()) == NT) break;
     const int cnt = min(kBatch, end - b0);
-    const int cnt8 = (cnt + kUnroll - 1) & ~(kUnroll - 1);
-    for (int t = tid; t < cnt8; t += NT) {
-      if (t < cnt) {
-        stage(rec, sorted_idx[b0 + t], s_a, s_b, s_c, t);
-      } else {  // padding entry: opacity 0 -> alpha 0, skipped
-        s_a[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-        s_b[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-        s_c[t] = make_float2(0.f, -1.0f);  // qmax < 0 <= q: never composited
-      }
-    }
+    const int kept = stage_compact<NT, kBatch>(rec, sorted_idx + b0, cnt, s_a, s_b, s_c, nullptr, s_idx, s_wc, bx0,
+                                               by0, kUnroll, kBatch);
     __syncthreads();
+    const int kept8 = (kept + kUnroll - 1) & ~(kUnroll - 1);
     const int pbase = b0 - beg;
-    for (int k0 = 0; k0 < cnt8; k0 += kUnroll) {
+    for (int k0 = 0; k0 < kept8; k0 += kUnroll) {
       if (all_done()) break;
 #pragma unroll
       for (int kk = 0; kk < kUnroll; kk++) {
-        const int k = k0 + kk;
-        const float4 A = s_a[k], Bq = s_b[k];
-        const float2 cq = s_c[k];
+        const int slot = s_idx[k0 + kk];
+        const float4 A = s_a[slot], Bq = s_b[slot];
+        const float2 cq = s_c[slot];
         gs_strip<PPT> e;
         q_strip<PPT>(A, Bq, fpx, fpy0, e);
         bool cj[PPT], any = false;
@@ -182,7 +247,8 @@ __global__ void __launch_bounds__(256 / PPT) k_render_fwd(
             if (cj[j]) {
               bool st = false;
               const float al = fminf(kAlphaCap, __fmul_rn(Bq.y, ex2_approx(-e.q[j])));
-              fwd_comp<kStats>(al, Bq.z, Bq.w, cq.x, pbase + k, T[j], C0[j], C1[j], C2[j], st, nl[j], sp[j], efc);
+              fwd_comp<kStats>(al, Bq.z, Bq.w, cq.x, pbase + slot, T[j], C0[j], C1[j], C2[j], st, nl[j], sp[j],
+                               efc);
               dn[j] = st;
             }
         }
@@ -335,6 +401,8 @@ __global__ void __launch_bounds__(256 / PPT) k_render_bwd(
   __shared__ float4 s_a[kBB], s_b[kBB];
   __shared__ float2 s_c[kBB];
   __shared__ uint32_t s_j[kBB];
+  __shared__ unsigned char s_idx[kBB];
+  __shared__ int s_wc[kBB / 32];
   // per-warp gradient slots: each (warp, entry, value) is written by exactly one lane, so no
   // shared-memory atomics (a float atomicAdd on shared memory is a CAS loop on sm_100)
   __shared__ float s_g[kOneWarp ? 1 : kNW * kBB * 9];
@@ -383,16 +451,15 @@ __global__ void __launch_bounds__(256 / PPT) k_render_bwd(
     const int p0 = bi * kBB;  // list position of the batch start
     const int cnt = min(kBB, maxn - p0);
     __syncthreads();
-    for (int t = tid; t < cnt; t += NT) {
-      const uint32_t j = sorted_idx[beg + p0 + t];
-      stage(rec, j, s_a, s_b, s_c, t);
-      s_j[t] = j;
-    }
+    const int kept = stage_compact<NT, kBB>(rec, sorted_idx + beg + p0, cnt, s_a, s_b, s_c, s_j, s_idx, s_wc,
+                                            (float)(tx * 16), (float)(ty * 16), 1, 0);
     if (!kOneWarp)
       for (int t = tid; t < kNW * kBB * 9; t += NT) s_g[t] = 0.f;
     __syncthreads();
-    for (int k = min(cnt, wmax - p0) - 1; k >= 0; k--) {  // warp-uniform range
+    for (int kc = kept - 1; kc >= 0; kc--) {
+      const int k = s_idx[kc];
       const int pos = p0 + k;
+      if (pos >= wmax) continue;  // warp-uniform
       const float4 A = s_a[k], Bq = s_b[k];
       const float2 cq = s_c[k];
       gs_strip<PPT> e;
@@ -432,7 +499,8 @@ __global__ void __launch_bounds__(256 / PPT) k_render_bwd(
     }
     if (!kOneWarp) {
       __syncthreads();
-      for (int t = tid; t < cnt; t += NT) {
+      for (int kc = tid; kc < kept; kc += NT) {
+        const int t = s_idx[kc];
         float* dst = dL_drec + (int64_t)s_j[t] * 9;
 #pragma unroll
         for (int q = 0; q < 9; q++) {

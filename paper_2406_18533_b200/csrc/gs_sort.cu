@@ -408,7 +408,7 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
   unsigned long long* tmp = (unsigned long long*)gs_slot_get(c, SLOT_KEYS_TMP, K * sizeof(unsigned long long), st);
   if (!tmp) return gs_fail(c, GS_ECUDA, "merge scratch");
   ++c->launches;
-  k_sort_large<<<dev_sms, kSortThreads, 0, st>>>(tile_range, keys, tmp, sorted_idx, lrg, ctr + 2, ctr + 3);
+  k_sort_large<<<dev_sms * 4, kSortThreads, 0, st>>>(tile_range, keys, tmp, sorted_idx, lrg, ctr + 2, ctr + 3);
   GS_LAUNCH_CHECK(c, "bin_sort large");
   return GS_OK;
 }
