@@ -35,6 +35,8 @@ enum {
   SLOT_MISC,          // small counters / dp
   SLOT_COUNT_GATHER,  // exchange count matrix
   SLOT_RECTILES,      // bin_sort per-record tile counts -> pair starts
+  SLOT_RADIX_HIST,    // bin_sort radix per-tile digit histograms -> offsets
+  SLOT_PSTART,        // bin_sort pair starts in depth order
   SLOT_N
 };
 

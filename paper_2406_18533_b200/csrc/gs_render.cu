@@ -73,7 +73,7 @@ __device__ __forceinline__ bool block_may_hit(const float4& A, const float4& Bq,
 template <int NT, int BATCH>
 __device__ __forceinline__ int stage_compact(const gs_rec* __restrict__ rec, const uint32_t* __restrict__ sidx,
                                              int cnt, float4* s_a, float4* s_b, float2* s_c, uint32_t* s_j,
-                                             unsigned char* s_idx, int* s_wc, float bx0, float by0, int pad,
+                                             unsigned short* s_idx, int* s_wc, float bx0, float by0, int pad,
                                              int dummy) {
   constexpr int kW = NT / 32, kI = BATCH / NT;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -101,11 +101,11 @@ __device__ __forceinline__ int stage_compact(const gs_rec* __restrict__ rec, con
     if ((bal[i] >> lane) & 1u) {
       int off = __popc(bal[i] & lt);
       for (int x = 0; x < i * kW + wid; x++) off += s_wc[x];
-      s_idx[off] = (unsigned char)(tid + NT * i);
+      s_idx[off] = (unsigned short)(tid + NT * i);
     }
   }
   const int padded = (total + pad - 1) / pad * pad;
-  for (int t = total + tid; t < padded; t += NT) s_idx[t] = (unsigned char)dummy;
+  for (int t = total + tid; t < padded; t += NT) s_idx[t] = (unsigned short)dummy;
   return total;
 }
 
@@ -174,11 +174,11 @@ __global__ void __launch_bounds__(256 / PPT) k_render_fwd(
     const uint8_t* __restrict__ gt, float norm, float* __restrict__ out_rgb,
     float* __restrict__ T_final, int32_t* __restrict__ n_last, float* __restrict__ dL_dpix,
     double* __restrict__ loss_sum, int64_t* __restrict__ tile_cost, int cost_mode,
-    long long* __restrict__ stats) {
+    long long* __restrict__ stats, int cull) {
   constexpr int NT = 256 / PPT;
   __shared__ float4 s_a[kBatch + 1], s_b[kBatch + 1];  // slot kBatch: the padding entry
   __shared__ float2 s_c[kBatch + 1];
-  __shared__ unsigned char s_idx[kBatch + kUnroll];
+  __shared__ unsigned short s_idx[kBatch + kUnroll];  // kBatch (the padding slot) needs 9 bits
   __shared__ int s_wc[kBatch / 32];
   if (threadIdx.x == 0) {  // padding entry: opacity 0, qmax < 0 <= q: never composited
     s_a[kBatch] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -221,8 +221,17 @@ __global__ void __launch_bounds__(256 / PPT) k_render_fwd(
   for (int b0 = beg; b0 < end; b0 += kBatch) {
     if (__syncthreads_count(all_done()) == NT) break;
     const int cnt = min(kBatch, end - b0);
-    const int kept = stage_compact<NT, kBatch>(rec, sorted_idx + b0, cnt, s_a, s_b, s_c, nullptr, s_idx, s_wc, bx0,
-                                               by0, kUnroll, kBatch);
+    int kept = cnt;
+    if (cull) {
+      kept = stage_compact<NT, kBatch>(rec, sorted_idx + b0, cnt, s_a, s_b, s_c, nullptr, s_idx, s_wc, bx0, by0,
+                                       kUnroll, kBatch);
+    } else {
+      for (int t = tid; t < cnt; t += NT) {
+        stage(rec, sorted_idx[b0 + t], s_a, s_b, s_c, t);
+        s_idx[t] = (unsigned short)t;
+      }
+      for (int t = cnt + tid; t < ((cnt + kUnroll - 1) & ~(kUnroll - 1)); t += NT) s_idx[t] = (unsigned short)kBatch;
+    }
     __syncthreads();
     const int kept8 = (kept + kUnroll - 1) & ~(kUnroll - 1);
     const int pbase = b0 - beg;
@@ -393,7 +402,7 @@ __global__ void __launch_bounds__(256 / PPT) k_render_bwd(
     const int32_t* __restrict__ range, gs_geom geo, int64_t B_lo, float bg0, float bg1, float bg2,
     const float* __restrict__ dL_dpix, const float* __restrict__ T_final,
     const int32_t* __restrict__ n_last, float* __restrict__ dL_drec, int64_t* __restrict__ tile_cost,
-    int cost_mode, long long* __restrict__ stats) {
+    int cost_mode, long long* __restrict__ stats, int cull) {
   constexpr int NT = 256 / PPT;
   constexpr bool kOneWarp = NT == 32;
   constexpr int kNW = NT / 32;   // warps per block
@@ -401,7 +410,7 @@ __global__ void __launch_bounds__(256 / PPT) k_render_bwd(
   __shared__ float4 s_a[kBB], s_b[kBB];
   __shared__ float2 s_c[kBB];
   __shared__ uint32_t s_j[kBB];
-  __shared__ unsigned char s_idx[kBB];
+  __shared__ unsigned short s_idx[kBB];
   __shared__ int s_wc[kBB / 32];
   // per-warp gradient slots: each (warp, entry, value) is written by exactly one lane, so no
   // shared-memory atomics (a float atomicAdd on shared memory is a CAS loop on sm_100)
@@ -451,8 +460,18 @@ __global__ void __launch_bounds__(256 / PPT) k_render_bwd(
     const int p0 = bi * kBB;  // list position of the batch start
     const int cnt = min(kBB, maxn - p0);
     __syncthreads();
-    const int kept = stage_compact<NT, kBB>(rec, sorted_idx + beg + p0, cnt, s_a, s_b, s_c, s_j, s_idx, s_wc,
-                                            (float)(tx * 16), (float)(ty * 16), 1, 0);
+    int kept = cnt;
+    if (cull) {
+      kept = stage_compact<NT, kBB>(rec, sorted_idx + beg + p0, cnt, s_a, s_b, s_c, s_j, s_idx, s_wc,
+                                    (float)(tx * 16), (float)(ty * 16), 1, 0);
+    } else {
+      for (int t = tid; t < cnt; t += NT) {
+        const uint32_t j = sorted_idx[beg + p0 + t];
+        stage(rec, j, s_a, s_b, s_c, t);
+        s_j[t] = j;
+        s_idx[t] = (unsigned short)t;
+      }
+    }
     if (!kOneWarp)
       for (int t = tid; t < kNW * kBB * 9; t += NT) s_g[t] = 0.f;
     __syncthreads();
@@ -713,6 +732,17 @@ __global__ void __launch_bounds__(32) k_render_bwd_c(
   }
 }
 
+// per-block ellipse cull of staged entries (A/B knob: GS_RENDER_CULL bit 0 forward, bit 1
+// backward; default both)
+static int render_cull() {
+  static int cull = -1;
+  if (cull < 0) {
+    const char* e = getenv("GS_RENDER_CULL");
+    cull = e ? atoi(e) & 3 : 3;
+  }
+  return cull;
+}
+
 // pixels per thread (A/B knob: GS_RENDER_PPT = 2, 4 or 8; default 4, measured best on C2)
 static int render_ppt() {
   static int ppt = -1;
@@ -751,7 +781,7 @@ extern "C" gs_status gs_render_fwd(gs_ctx* c, const void* recv_rec, const uint32
                      : (stats ? k_render_fwd<8, true> : k_render_fwd<8, false>);
   kf<<<(unsigned)n_owned, 256 / ppt, 0, (cudaStream_t)stream>>>(
       (const gs_rec*)recv_rec, sorted_idx, tile_range, geo, B_lo, bg[0], bg[1], bg[2], gt, norm, out_rgb,
-      T_final, n_last, dL_dpix, loss_sum, tile_cost, cost_mode, (long long*)stats);
+      T_final, n_last, dL_dpix, loss_sum, tile_cost, cost_mode, (long long*)stats, render_cull() & 1);
   GS_LAUNCH_CHECK(c, "render_fwd");
   return GS_OK;
 }
@@ -786,16 +816,20 @@ extern "C" gs_status gs_render_bwd(gs_ctx* c, const void* recv_rec, int64_t n_re
   auto kb = ppt == 2 ? (stats ? k_render_bwd<2, true> : k_render_bwd<2, false>)
           : ppt == 4 ? (stats ? k_render_bwd<4, true> : k_render_bwd<4, false>)
                      : (stats ? k_render_bwd<8, true> : k_render_bwd<8, false>);
-  int threads = 256 / ppt;
-  if (compact) {  // compacted one-warp backward, same strip decomposition as the forward
-    kb = ppt == 2 ? (stats ? k_render_bwd_c<2, true> : k_render_bwd_c<2, false>)
-       : ppt == 4 ? (stats ? k_render_bwd_c<4, true> : k_render_bwd_c<4, false>)
-                  : (stats ? k_render_bwd_c<8, true> : k_render_bwd_c<8, false>);
-    threads = 32;
+  const int threads = 256 / ppt;
+  // compacted one-warp backward, same strip decomposition as the forward
+  auto kc = ppt == 2 ? (stats ? k_render_bwd_c<2, true> : k_render_bwd_c<2, false>)
+          : ppt == 4 ? (stats ? k_render_bwd_c<4, true> : k_render_bwd_c<4, false>)
+                     : (stats ? k_render_bwd_c<8, true> : k_render_bwd_c<8, false>);
+  if (compact) {
+    kc<<<(unsigned)n_owned, 32, 0, st>>>(
+        (const gs_rec*)recv_rec, sorted_idx, tile_range, geo, B_lo, bg[0], bg[1], bg[2], dL_dpix, T_final, n_last,
+        dL_drec, tile_cost, cost_mode, (long long*)stats);
+  } else {
+    kb<<<(unsigned)n_owned, threads, 0, st>>>(
+        (const gs_rec*)recv_rec, sorted_idx, tile_range, geo, B_lo, bg[0], bg[1], bg[2], dL_dpix, T_final, n_last,
+        dL_drec, tile_cost, cost_mode, (long long*)stats, (render_cull() >> 1) & 1);
   }
-  kb<<<(unsigned)n_owned, threads, 0, st>>>(
-      (const gs_rec*)recv_rec, sorted_idx, tile_range, geo, B_lo, bg[0], bg[1], bg[2], dL_dpix, T_final, n_last,
-      dL_drec, tile_cost, cost_mode, (long long*)stats);
   GS_LAUNCH_CHECK(c, "render_bwd");
   return GS_OK;
 }

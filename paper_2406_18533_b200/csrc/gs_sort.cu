@@ -13,6 +13,9 @@
 // (depth, recv_idx) is unique within a block and recv_idx is ascending in gid within a
 // view (A1/A2 ordering), so the result is exactly the (depth, gid) order of O11 (R7)
 // whatever the placement order: no stable sort is needed.
+#include <algorithm>
+#include <cstdlib>
+
 #include "gs_device.cuh"
 #include "gs_internal.h"
 
@@ -328,7 +331,355 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_large(const int32_t* __re
   }
 }
 
+
+// ---------------------------------------------------------------- radix path (default)
+// Depth-presorted, stable block binning: sort the records by depth once (LSD radix over the
+// 32 depth bits, stable, so equal depths stay in recv_idx order), emit the (block, record)
+// pairs in that order -- each CTA writes a contiguous pair range, coalesced -- then stably
+// radix-sort the pairs by owned-block index only (ceil(log2(n_owned + 1)) bits, 2-3 passes).
+// Every block's list then comes out in (depth, recv_idx) order, whatever its length: no
+// per-block comparison sort, no long-list special case, and traffic linear in the pairs.
+// Pairs of non-owned blocks (G > 1, rectangles straddling the partition) get key n_owned and
+// sort past the end (they are never written out).
+constexpr int kRadixThreads = 256;
+constexpr int kRadixItems = 16;
+constexpr int kRadixTile = kRadixThreads * kRadixItems;  // 4096 elements per CTA
+constexpr int kRadixWarps = kRadixThreads / 32;
+constexpr int kRadixPerWarp = kRadixTile / kRadixWarps;   // 512 consecutive elements per warp
+
+// Per-record tile count of the rectangle (0 outside the rank's views); no binning atomics.
+__global__ void k_tile_counts(const gs_rec* __restrict__ rec, int64_t n_recv, gs_geom geo, int v_lo, int v_hi,
+                              int64_t* __restrict__ n_tiles) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j > n_recv) return;
+  int64_t t = 0;
+  if (j < n_recv) {
+    const float4 a = rec[j].a;
+    const int v = (int)(__float_as_uint(rec[j].c.w) & 31u);
+    int tx0, tx1, ty0, ty1;
+    if (v >= v_lo && v <= v_hi && rect_of(a.x, a.y, a.w, geo.Wt, geo.Ht, tx0, tx1, ty0, ty1))
+      t = (int64_t)(tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+  }
+  n_tiles[j] = t;
+}
+
+// tile_range from the block-sorted keys: range[b] = first position with key >= b, for
+// b in [0, n_owned] (position n_full stands for key n_owned; keys n_owned are other ranks').
+__global__ void k_key_ranges(const uint32_t* __restrict__ keys, int64_t n_full, uint32_t n_owned,
+                             int32_t* __restrict__ range) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > n_full) return;
+  const int64_t k = i < n_full ? (int64_t)keys[i] : (int64_t)n_owned;
+  const int64_t prev = i > 0 ? (int64_t)keys[i - 1] : -1;
+  for (int64_t b = prev + 1; b <= k && b <= (int64_t)n_owned; b++) range[b] = (int32_t)i;
+}
+
+// Per-tile digit histogram, digit-major: hist[d * ntiles + tile] (warp-aggregated smem adds).
+__global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const uint32_t* __restrict__ keys, int64_t n,
+                                                              int shift, int bits, int64_t ntiles,
+                                                              int64_t* __restrict__ hist) {
+  __shared__ int h[kRadixWarps][256];  // one copy per warp: fewer same-address conflicts
+  const int bins = 1 << bits;
+  const int w = threadIdx.x >> 5;
+  for (int i = threadIdx.x & 31; i < 256; i += 32) h[w][i] = 0;
+  __syncwarp();
+  const int64_t base = (int64_t)blockIdx.x * kRadixTile;
+  const uint32_t mask = (uint32_t)(bins - 1);
+#pragma unroll 4
+  for (int r = 0; r < kRadixItems; r++) {
+    const int64_t i = base + r * kRadixThreads + threadIdx.x;
+    if (i < n) atomicAdd(&h[w][(__ldg(keys + i) >> shift) & mask], 1);
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < bins; d += kRadixThreads) {
+    int t = 0;
+#pragma unroll
+    for (int ww = 0; ww < kRadixWarps; ww++) t += h[ww][d];
+    hist[(int64_t)d * ntiles + blockIdx.x] = t;
+  }
+}
+
+// Stable scatter of one digit pass.  Warp w ranks its 512 consecutive elements in 16 rounds
+// of 32 (match_any peers + a warp-private running count per digit), the CTA turns the
+// per-warp counts into tile-local offsets, the tile is reordered by digit in shared memory and
+// written out so that consecutive threads store consecutive positions of a digit's run.
+// off = exclusive scan of hist (global start of each (digit, tile)).  Only positions < n_write
+// are stored into vout (keys: all); kout == nullptr stores the values only.
+__global__ void __launch_bounds__(kRadixThreads, 3) k_radix_scatter(
+    const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
+    uint32_t* __restrict__ vout, int64_t n, int64_t n_write, int shift, int bits, int64_t ntiles,
+    const int64_t* __restrict__ off) {
+  const int bins = 1 << bits;
+  __shared__ int s_wh[kRadixWarps][257];
+  __shared__ int s_toff[256];
+  __shared__ int s_wsum[kRadixWarps];
+  __shared__ long long s_gbase[256];
+  __shared__ uint32_t s_k[kRadixTile], s_v[kRadixTile];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t mask = (uint32_t)(bins - 1);
+  const int64_t base = (int64_t)blockIdx.x * kRadixTile;
+  const int m = (int)min((int64_t)kRadixTile, n - base);
+  for (int d = lane; d < 257; d += 32) s_wh[w][d] = 0;
+  for (int d = tid; d < bins; d += kRadixThreads) s_gbase[d] = off[(int64_t)d * ntiles + blockIdx.x];
+  __syncwarp();
+  uint32_t kk[kRadixItems], vv[kRadixItems];
+  int rk[kRadixItems];
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int r = 0; r < kRadixItems; r++) {
+    const int li = w * kRadixPerWarp + r * 32 + lane;
+    const bool valid = li < m;
+    kk[r] = valid ? __ldg(kin + base + li) : 0u;
+    vv[r] = valid ? __ldg(vin + base + li) : 0u;
+    const int d = valid ? (int)((kk[r] >> shift) & mask) : 256;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const int cur = s_wh[w][d];
+    rk[r] = cur + __popc(peers & lt);
+    __syncwarp();
+    if ((peers & lt) == 0) s_wh[w][d] = cur + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: exclusive over warps, tile total
+  int tot = 0;
+  if (tid < bins) {
+#pragma unroll
+    for (int ww = 0; ww < kRadixWarps; ww++) {
+      const int t = s_wh[ww][tid];
+      s_wh[ww][tid] = tot;
+      tot += t;
+    }
+  }
+  // exclusive scan of the tile totals over digits (tid = digit)
+  int incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_wsum[w] = incl;
+  __syncthreads();
+  int wpre = 0;
+  for (int ww = 0; ww < w; ww++) wpre += s_wsum[ww];
+  s_toff[tid] = wpre + incl - tot;
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kRadixItems; r++) {
+    const int li = w * kRadixPerWarp + r * 32 + lane;
+    if (li < m) {
+      const int d = (int)((kk[r] >> shift) & mask);
+      const int pos = s_toff[d] + s_wh[w][d] + rk[r];
+      s_k[pos] = kk[r];
+      s_v[pos] = vv[r];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < m; i += kRadixThreads) {
+    const uint32_t k = s_k[i];
+    const int d = (int)((k >> shift) & mask);
+    const int64_t pos = s_gbase[d] + (i - s_toff[d]);
+    if (kout) kout[pos] = k;
+    if (pos < n_write) vout[pos] = s_v[i];
+  }
+}
+
+__global__ void k_depth_keys(const gs_rec* __restrict__ rec, int64_t n, uint32_t* __restrict__ keys,
+                             uint32_t* __restrict__ vals) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  keys[j] = __float_as_uint(rec[j].a.z);  // depth > 0: the bit pattern orders like the value
+  vals[j] = (uint32_t)j;
+}
+
+__global__ void k_gather_tiles(const uint32_t* __restrict__ order, const int64_t* __restrict__ ntiles, int64_t n,
+                               int64_t* __restrict__ ps) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > n) return;
+  ps[s] = s < n ? ntiles[order[s]] : 0;
+}
+
+// First record (in depth order) of every emission CTA: record s covers pairs
+// [ps[s], ps[s+1]); it is the first record of CTA c iff its range contains c * kPlacePairs.
+__global__ void k_cta_first(const int64_t* __restrict__ ps, int64_t n, int64_t* __restrict__ first) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int64_t a = ps[s], b = ps[s + 1];
+  for (int64_t c = (a + kPlacePairs - 1) / kPlacePairs; c * kPlacePairs < b; c++) first[c] = s;
+}
+
+// Emit the pairs of the depth-ordered records: CTA c writes pairs [c*kPlacePairs, ...) of
+// the enumeration pair_start (= scan of the tile counts in depth order); key = owned-block
+// index (n_owned for a block of another rank), value = recv_idx.  Every received record has
+// >= 1 tile (A1 emits a record only for a non-empty rectangle with an owned block), so at most
+// kPlacePairs + 1 records overlap a CTA.
+__global__ void __launch_bounds__(kPlaceThreads) k_emit(
+    const gs_rec* __restrict__ rec, const uint32_t* __restrict__ order, int64_t n_recv,
+    const int64_t* __restrict__ pair_start, const int64_t* __restrict__ first, int64_t n_full, gs_geom geo,
+    int64_t B_lo, int64_t B_hi, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  __shared__ int64_t s_start[kPlacePairs + 2];
+  __shared__ int s_tx0[kPlacePairs + 1], s_ty0[kPlacePairs + 1], s_w[kPlacePairs + 1], s_v[kPlacePairs + 1];
+  __shared__ uint32_t s_j[kPlacePairs + 1];
+  __shared__ int64_t s_slo;
+  __shared__ int s_nr;
+  const int64_t P0 = (int64_t)blockIdx.x * kPlacePairs;
+  const int64_t P1 = min(P0 + kPlacePairs, n_full);
+  if (threadIdx.x == 0) {
+    const int64_t lo = first[blockIdx.x];
+    int64_t hi = n_recv - 1;  // record holding pair P1 - 1
+    if (P1 < n_full) {
+      const int64_t t = first[blockIdx.x + 1];
+      hi = pair_start[t] == P1 ? t - 1 : t;
+    }
+    s_slo = lo;
+    s_nr = (int)(hi - lo + 1);
+  }
+  __syncthreads();
+  const int64_t slo = s_slo;
+  const int nr = s_nr;
+  for (int r = threadIdx.x; r < nr; r += kPlaceThreads) {
+    const int64_t sidx = slo + r;
+    s_start[r] = pair_start[sidx];
+    const uint32_t j = order[sidx];
+    const float4 a = rec[j].a;
+    int tx0, tx1, ty0, ty1;
+    rect_of(a.x, a.y, a.w, geo.Wt, geo.Ht, tx0, tx1, ty0, ty1);
+    s_tx0[r] = tx0;
+    s_ty0[r] = ty0;
+    s_w[r] = tx1 - tx0 + 1;
+    s_v[r] = (int)(__float_as_uint(rec[j].c.w) & 31u);
+    s_j[r] = j;
+  }
+  if (threadIdx.x == 0) s_start[nr] = pair_start[slo + nr];
+  __syncthreads();
+  const uint32_t n_owned = (uint32_t)(B_hi - B_lo);
+  for (int64_t pp = P0 + threadIdx.x; pp < P1; pp += kPlaceThreads) {
+    int lo = 0, hi = nr;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_start[mid] <= pp) lo = mid; else hi = mid;
+    }
+    const int t = (int)(pp - s_start[lo]), w = s_w[lo];
+    const int ty = s_ty0[lo] + t / w, tx = s_tx0[lo] + t % w;
+    const int64_t beta = (int64_t)s_v[lo] * geo.per_view + (int64_t)ty * geo.Wt + tx;
+    keys[pp] = (beta < B_lo || beta >= B_hi) ? n_owned : (uint32_t)(beta - B_lo);
+    vals[pp] = s_j[lo];
+  }
+}
+
 }  // namespace
+
+// Binning algorithm: radix (default) or the per-block comparison sorts (GS_BIN_SORT=bitonic).
+static bool bin_mode_radix() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("GS_BIN_SORT");
+    mode = (e && e[0] == 'b') ? 0 : 1;
+  }
+  return mode == 1;
+}
+
+// One stable LSD pass over n (key, value) elements (keys/values in kin/vin) on `bits` digit
+// bits at `shift`; kout may be null (values only).  Scratch: SLOT_RADIX_HIST.
+static gs_status radix_pass(gs_ctx* c, const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
+                            int64_t n, int64_t n_write, int shift, int bits, cudaStream_t st) {
+  if (n == 0) return GS_OK;
+  const int bins = 1 << bits;
+  const int64_t ntiles = (n + kRadixTile - 1) / kRadixTile;
+  int64_t* hist = (int64_t*)gs_slot_get(c, SLOT_RADIX_HIST, (size_t)bins * ntiles * sizeof(int64_t), st);
+  if (!hist) return gs_fail(c, GS_ECUDA, "radix histogram scratch");
+  ++c->launches;
+  k_radix_hist<<<(unsigned)ntiles, kRadixThreads, 0, st>>>(kin, n, shift, bits, ntiles, hist);
+  gs_status s = gs_scan_i64(c, hist, hist, (int64_t)bins * ntiles, 0, st);
+  if (s != GS_OK) return s;
+  ++c->launches;
+  k_radix_scatter<<<(unsigned)ntiles, kRadixThreads, 0, st>>>(kin, vin, kout, vout, n, n_write, shift, bits, ntiles,
+                                                              hist);
+  GS_LAUNCH_CHECK(c, "radix pass");
+  return GS_OK;
+}
+
+namespace {
+}  // namespace
+
+// Radix binning (see the comment above k_radix_hist).  Two host syncs: the pair total (scratch
+// sizing) and the owned pair count K (capacity, *n_pairs_h).
+static gs_status bin_sort_radix(gs_ctx* c, const gs_rec* rec, int64_t n_recv, gs_geom geo, int64_t B_lo,
+                                int64_t B_hi, uint32_t* sorted_idx, int64_t pair_cap, int32_t* tile_range,
+                                int64_t* n_pairs_h, cudaStream_t st) {
+  const int64_t n_owned = B_hi - B_lo;
+  const int v_lo = (int)(B_lo / geo.per_view), v_hi = (int)((B_hi - 1) / geo.per_view);
+  if (n_recv == 0) {
+    GS_CUDA(c, cudaMemsetAsync(tile_range, 0, (n_owned + 1) * sizeof(int32_t), st));
+    return GS_OK;
+  }
+  GS_REQUIRE(c, rec != nullptr, "null recv_rec");
+  int64_t* ntiles = (int64_t*)gs_slot_get(c, SLOT_RECTILES, (n_recv + 1) * sizeof(int64_t), st);
+  int64_t* ps = (int64_t*)gs_slot_get(c, SLOT_PSTART, (n_recv + 1) * sizeof(int64_t), st);
+  if (!ntiles || !ps) return gs_fail(c, GS_ECUDA, "scratch");
+  ++c->launches;
+  k_tile_counts<<<(unsigned)((n_recv + 256) / 256), 256, 0, st>>>(rec, n_recv, geo, v_lo, v_hi, ntiles);
+  gs_status s = gs_scan_i64(c, ntiles, ps, n_recv + 1, 0, st);  // only for the total
+  if (s != GS_OK) return s;
+  GS_CUDA(c, cudaMemcpyAsync(c->pinned, ps + n_recv, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(c, cudaStreamSynchronize(st));
+  const int64_t n_full = c->pinned[0];
+  // tile_range holds int32 positions: bound the pair total (a superset of the owned pairs)
+  if (n_full >= (1ll << 31))
+    return gs_fail(c, GS_ENOTSUP, "pair total %lld exceeds int32 positions", (long long)n_full);
+  const int64_t cap = max(n_full, n_recv);
+  uint32_t* A = (uint32_t*)gs_slot_get(c, SLOT_KEYS, 2 * cap * sizeof(uint32_t), st);
+  uint32_t* Bf = (uint32_t*)gs_slot_get(c, SLOT_KEYS_TMP, 2 * cap * sizeof(uint32_t), st);
+  if (!A || !Bf) return gs_fail(c, GS_ECUDA, "radix scratch (%lld pairs)", (long long)cap);
+  uint32_t *ka = A, *va = A + cap, *kb = Bf, *vb = Bf + cap;
+  // 1. records by depth (4 stable 8-bit passes: A -> B -> A -> B -> A)
+  ++c->launches;
+  k_depth_keys<<<(unsigned)((n_recv + 255) / 256), 256, 0, st>>>(rec, n_recv, ka, va);
+  for (int p = 0; p < 4; p++) {
+    s = (p & 1) ? radix_pass(c, kb, vb, ka, va, n_recv, n_recv, 8 * p, 8, st)
+                : radix_pass(c, ka, va, kb, vb, n_recv, n_recv, 8 * p, 8, st);
+    if (s != GS_OK) return s;
+  }
+  // 2. pair starts in depth order; 3. pairs (block, recv_idx) in depth order -> B
+  ++c->launches;
+  k_gather_tiles<<<(unsigned)((n_recv + 256) / 256), 256, 0, st>>>(va, ntiles, n_recv, ps);
+  s = gs_scan_i64(c, ps, ps, n_recv + 1, 0, st);
+  if (s != GS_OK) return s;
+  if (n_full > 0) {
+    const int64_t nct = (n_full + kPlacePairs - 1) / kPlacePairs;
+    int64_t* first = (int64_t*)gs_slot_get(c, SLOT_LARGE, (nct + 1) * sizeof(int64_t), st);
+    if (!first) return gs_fail(c, GS_ECUDA, "scratch");
+    ++c->launches;
+    k_cta_first<<<(unsigned)((n_recv + 255) / 256), 256, 0, st>>>(ps, n_recv, first);
+    ++c->launches;
+    k_emit<<<(unsigned)nct, kPlaceThreads, 0, st>>>(rec, va, n_recv, ps, first, n_full, geo, B_lo, B_hi, kb, vb);
+    GS_LAUNCH_CHECK(c, "bin_sort emit");
+  }
+  // 4. stable sort by owned-block index (other ranks' blocks: key n_owned, sorted last); the
+  //    last pass writes the values into sorted_idx (up to its capacity) and the keys into scratch
+  const int nbits = 32 - __builtin_clz((unsigned)n_owned);
+  const int passes = (nbits + 7) / 8, width = (nbits + passes - 1) / passes;
+  uint32_t *kin = kb, *vin = vb, *kout = ka, *vout = va;
+  for (int p = 0; p < passes; p++) {
+    const int shift = p * width, bits = min(width, nbits - shift);
+    const bool last = p == passes - 1;
+    s = radix_pass(c, kin, vin, kout, last ? sorted_idx : vout, n_full, last ? min(n_full, pair_cap) : n_full,
+                   shift, bits, st);
+    if (s != GS_OK) return s;
+    std::swap(kin, kout);
+    std::swap(vin, vout);
+  }
+  // 5. ranges from the sorted keys (now in kin)
+  ++c->launches;
+  k_key_ranges<<<(unsigned)((n_full + 256) / 256), 256, 0, st>>>(kin, n_full, (uint32_t)n_owned, tile_range);
+  GS_LAUNCH_CHECK(c, "bin_sort ranges");
+  int32_t* kp = (int32_t*)(c->pinned + 1);
+  GS_CUDA(c, cudaMemcpyAsync(kp, tile_range + n_owned, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(c, cudaStreamSynchronize(st));
+  const int64_t K = *kp;
+  *n_pairs_h = K;
+  if (K > pair_cap) return gs_fail(c, GS_ECAPACITY, "pair capacity %lld < %lld", (long long)pair_cap, (long long)K);
+  return GS_OK;
+}
 
 extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv, const gs_camera* cams_h,
                                  int n_views, const int64_t* dp_h, uint32_t* sorted_idx, int64_t pair_cap,
@@ -345,6 +696,11 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
   if (n_owned == 0) {
     GS_CUDA(c, cudaMemsetAsync(tile_range, 0, sizeof(int32_t), st));
     return GS_OK;
+  }
+  if (bin_mode_radix()) {
+    GS_REQUIRE(c, n_owned < (1ll << 31) - 1, "too many owned blocks");
+    return bin_sort_radix(c, (const gs_rec*)recv_rec, n_recv, geo, B_lo, B_hi, sorted_idx, pair_cap, tile_range,
+                          n_pairs_h, st);
   }
   const int v_lo = (int)(B_lo / geo.per_view), v_hi = (int)((B_hi - 1) / geo.per_view);
   const int nvl = v_hi - v_lo + 1;
@@ -376,7 +732,8 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
   if (s != GS_OK) return s;
   GS_CUDA(c, cudaMemcpyAsync(c->pinned, counts + n_owned, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   if (n_recv > 0)
-    GS_CUDA(c, cudaMemcpyAsync(c->pinned + 1, ntiles + n_recv, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GS_CUDA(c, cudaMemcpyAsync(c->pinned + 1, ntiles + n_recv, sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, st));
   GS_CUDA(c, cudaStreamSynchronize(st));
   const int64_t K = c->pinned[0], n_full = n_recv > 0 ? c->pinned[1] : 0;
   *n_pairs_h = K;
