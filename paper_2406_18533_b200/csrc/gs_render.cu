@@ -167,8 +167,8 @@ __device__ __forceinline__ void fwd_comp(float alpha, float cr, float cg, float 
   if (kStats) efc++;
 }
 
-template <int PPT, bool kStats>
-__global__ void __launch_bounds__(256 / PPT) k_render_fwd(
+template <int PPT, bool kStats, int MINB = 1>
+__global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
     const gs_rec* __restrict__ rec, const uint32_t* __restrict__ sorted_idx,
     const int32_t* __restrict__ range, gs_geom geo, int64_t B_lo, float bg0, float bg1, float bg2,
     const uint8_t* __restrict__ gt, float norm, float* __restrict__ out_rgb,
@@ -396,8 +396,8 @@ __device__ __forceinline__ int red_index(int lane, bool& valid) {
   return a + b + c + d;
 }
 
-template <int PPT, bool kStats>
-__global__ void __launch_bounds__(256 / PPT) k_render_bwd(
+template <int PPT, bool kStats, int MINB = 1>
+__global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
     const gs_rec* __restrict__ rec, const uint32_t* __restrict__ sorted_idx,
     const int32_t* __restrict__ range, gs_geom geo, int64_t B_lo, float bg0, float bg1, float bg2,
     const float* __restrict__ dL_dpix, const float* __restrict__ T_final,
@@ -743,6 +743,18 @@ static int render_cull() {
   return cull;
 }
 
+// resident-CTA floor of the PPT = 4 kernels, i.e. their register cap (A/B knobs:
+// GS_RENDER_FWD_MINB in {12, 16}, default 16 = 64 registers, 16 warps/SM;
+// GS_RENDER_BWD_MINB in {8, 10, 12}, default 12 = 80 registers; measured on C2)
+static int render_minb(int bwd) {
+  static int mb[2] = {-1, -1};
+  if (mb[bwd] < 0) {
+    const char* e = getenv(bwd ? "GS_RENDER_BWD_MINB" : "GS_RENDER_FWD_MINB");
+    mb[bwd] = e ? atoi(e) : (bwd ? 12 : 16);
+  }
+  return mb[bwd];
+}
+
 // pixels per thread (A/B knob: GS_RENDER_PPT = 2, 4 or 8; default 4, measured best on C2)
 static int render_ppt() {
   static int ppt = -1;
@@ -776,9 +788,11 @@ extern "C" gs_status gs_render_fwd(gs_ctx* c, const void* recv_rec, const uint32
   const float norm = gt ? (float)(1.0 / (3.0 * (double)geo.W * (double)geo.H * (double)b_loss)) : 0.f;
   ++c->launches;
   const int ppt = render_ppt();
+  const int mb = render_minb(0);
   auto kf = ppt == 2 ? (stats ? k_render_fwd<2, true> : k_render_fwd<2, false>)
-          : ppt == 4 ? (stats ? k_render_fwd<4, true> : k_render_fwd<4, false>)
-                     : (stats ? k_render_fwd<8, true> : k_render_fwd<8, false>);
+          : ppt == 8 ? (stats ? k_render_fwd<8, true> : k_render_fwd<8, false>)
+          : mb == 12 ? (stats ? k_render_fwd<4, true, 12> : k_render_fwd<4, false, 12>)
+                     : (stats ? k_render_fwd<4, true, 16> : k_render_fwd<4, false, 16>);
   kf<<<(unsigned)n_owned, 256 / ppt, 0, (cudaStream_t)stream>>>(
       (const gs_rec*)recv_rec, sorted_idx, tile_range, geo, B_lo, bg[0], bg[1], bg[2], gt, norm, out_rgb,
       T_final, n_last, dL_dpix, loss_sum, tile_cost, cost_mode, (long long*)stats, render_cull() & 1);
@@ -813,9 +827,12 @@ extern "C" gs_status gs_render_bwd(gs_ctx* c, const void* recv_rec, int64_t n_re
     const char* e = getenv("GS_RENDER_BWD_COMPACT");
     compact = e ? atoi(e) : 0;
   }
+  const int mb = render_minb(1);
   auto kb = ppt == 2 ? (stats ? k_render_bwd<2, true> : k_render_bwd<2, false>)
-          : ppt == 4 ? (stats ? k_render_bwd<4, true> : k_render_bwd<4, false>)
-                     : (stats ? k_render_bwd<8, true> : k_render_bwd<8, false>);
+          : ppt == 8 ? (stats ? k_render_bwd<8, true> : k_render_bwd<8, false>)
+          : mb == 8 ? (stats ? k_render_bwd<4, true, 8> : k_render_bwd<4, false, 8>)
+          : mb == 12 ? (stats ? k_render_bwd<4, true, 12> : k_render_bwd<4, false, 12>)
+                     : (stats ? k_render_bwd<4, true, 10> : k_render_bwd<4, false, 10>);
   const int threads = 256 / ppt;
   // compacted one-warp backward, same strip decomposition as the forward
   auto kc = ppt == 2 ? (stats ? k_render_bwd_c<2, true> : k_render_bwd_c<2, false>)
