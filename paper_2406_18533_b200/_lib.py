@@ -13,7 +13,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgs.so")
+# GS_LIB_VARIANT=<name> loads the in-tree A/B build libgs_<name>.so (tools/build_variant.sh)
+LIB_PATH = os.path.join(_HERE, "libgs_%s.so" % os.environ["GS_LIB_VARIANT"] if os.environ.get("GS_LIB_VARIANT")
+                        else "libgs.so")
 
 GS_OK, GS_EINVAL, GS_ECAPACITY, GS_ENONFINITE, GS_ECUDA, GS_ENCCL, GS_ENOTSUP = range(7)
 COST_MEASURED, COST_WORK, COST_PAPER_AVG = 0, 1, 2

@@ -46,13 +46,17 @@ def _nvcc():
     raise RuntimeError("nvcc not found")
 
 
-def build(force: bool = False, ptxas_v: bool = False, verbose: bool = False) -> str:
-    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    deps = srcs + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
+def build(force: bool = False, ptxas_v: bool = False, verbose: bool = False, csrc: str = CSRC,
+          out: str = OUT) -> str:
+    """Compile csrc/*.cu into out.  (csrc/out other than the defaults: A/B builds of another
+    revision, loaded by _lib when GS_LIB_VARIANT names them.)"""
+    srcs = sorted(glob.glob(os.path.join(csrc, "*.cu")))
+    deps = srcs + glob.glob(os.path.join(csrc, "*.cuh")) + glob.glob(os.path.join(csrc, "*.h")) + \
         [os.path.join(ROOT, "include", "gs.h"), __file__]
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(d) for d in deps):
-        return OUT
-    os.makedirs(BUILD, exist_ok=True)
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(d) for d in deps):
+        return out
+    build_dir = BUILD if out == OUT else BUILD + "_" + os.path.basename(out).replace(".", "_")
+    os.makedirs(build_dir, exist_ok=True)
     inc, lib = _nccl_dirs()
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
                     "-I" + os.path.join(ROOT, "include")]
@@ -63,7 +67,7 @@ def build(force: bool = False, ptxas_v: bool = False, verbose: bool = False) -> 
     nvcc = _nvcc()
 
     def comp(src):
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        obj = os.path.join(build_dir, os.path.basename(src) + ".o")
         cmd = [nvcc, "-c", src, "-o", obj] + flags
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -76,7 +80,7 @@ def build(force: bool = False, ptxas_v: bool = False, verbose: bool = False) -> 
         objs = list(ex.map(comp, srcs))
     # dynamic cudart: resolve to the same libcudart.so.12 torch loads (one runtime instance,
     # so torch streams are valid handles here)
-    link = [nvcc, "-shared", "--cudart", "shared", "-o", OUT + ".tmp"] + ARCH + objs
+    link = [nvcc, "-shared", "--cudart", "shared", "-o", out + ".tmp"] + ARCH + objs
     crt = _cudart_dir()
     if crt:
         link += ["-Xlinker", "-rpath=" + crt]
@@ -85,8 +89,8 @@ def build(force: bool = False, ptxas_v: bool = False, verbose: bool = False) -> 
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n%s\n%s" % (r.stdout, r.stderr))
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

@@ -355,6 +355,56 @@ __device__ __forceinline__ void bwd_comp(float raw, float G, float dx, float dy,
   }
 }
 
+// 1 / x for x in [0.01, 1] (1 - alpha): one MUFU.RCP, no range fix-up.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// Strip form of bwd_comp for pixel j of the thread's strip.  The six geometric gradients are
+// linear in q_j = o G_j dA_j with coefficients polynomial in j (u_j = u_0 - j l21,
+// w_j = w_0 - j l22, dy_j = dy_0 - j), so per pixel only the moments
+// acc = (sum gG, sum j gG, sum j^2 gG) are accumulated (gG = G dA, zero through the cap, R6);
+// strip_grads turns them into the 6 gradients once per entry.  Colour gradients as bwd_comp.
+template <int J>
+__device__ __forceinline__ void bwd_comp_strip(float raw, float G, const float4& Bq, float cb, float& T, float& S0,
+                                               float& S1, float& S2, float g0, float g1, float g2, float Tf,
+                                               float bgdot, float acc[3], float gc[3]) {
+  const float alpha = fminf(kAlphaCap, raw);
+  const float rom = rcp_approx(1.0f - alpha);
+  T *= rom;  // transmittance in front of this entry
+  const float wgt = alpha * T;
+  const float cr = Bq.z, cg = Bq.w;
+  gc[0] = fmaf(wgt, g0, gc[0]);
+  gc[1] = fmaf(wgt, g1, gc[1]);
+  gc[2] = fmaf(wgt, g2, gc[2]);
+  const float dA = T * ((cr - S0) * g0 + (cg - S1) * g1 + (cb - S2) * g2) - Tf * rom * bgdot;
+  S0 = fmaf(alpha, cr - S0, S0);
+  S1 = fmaf(alpha, cg - S1, S1);
+  S2 = fmaf(alpha, cb - S2, S2);
+  const float gG = raw <= kAlphaCap ? G * dA : 0.f;
+  acc[0] += gG;
+  if (J == 1) acc[1] += gG, acc[2] += gG;
+  if (J >= 2) acc[1] = fmaf((float)J, gG, acc[1]), acc[2] = fmaf((float)(J * J), gG, acc[2]);
+}
+
+// gr[0..5] of one entry from the strip moments (q = o gG; 2 ln 2 = 1 / kLScale^2):
+//   dL/dl11' = -2ln2 l11 sum q_j u_j,  dL/dl21' = -2ln2 sum q_j (l21 u_j + l22 w_j),
+//   dL/dconic-like (gr2..4) = -1/2 sum q dx^2, -sum q dx dy_j, -1/2 sum q dy_j^2, dL/do = sum gG.
+__device__ __forceinline__ void strip_grads(const float4& A, const float4& Bq, float dx, float dy0, float u0,
+                                            float w0, const float acc[3], float gr[9]) {
+  const float l11 = A.z, l21 = A.w, l22 = Bq.x, o = Bq.y;
+  const float Q0 = o * acc[0], Q1 = o * acc[1], Q2 = o * acc[2];
+  const float k = -1.3862943611198906f;
+  gr[5] = acc[0];
+  gr[0] = k * l11 * fmaf(u0, Q0, -l21 * Q1);
+  gr[1] = k * fmaf(fmaf(l21, u0, l22 * w0), Q0, -fmaf(l21, l21, l22 * l22) * Q1);
+  gr[2] = -0.5f * dx * dx * Q0;
+  gr[3] = -dx * fmaf(dy0, Q0, -Q1);
+  gr[4] = -0.5f * fmaf(dy0, fmaf(dy0, Q0, -2.0f * Q1), Q2);
+}
+
 // Transpose (recursive-halving) warp reduction of 9 values: afterwards lane l holds the warp
 // sum of value red_index(l) (valid lanes: 0,2,4,8,10,16,18,20,24).
 __device__ __forceinline__ float warp_reduce9(const float v[9], int lane) {
@@ -493,13 +543,25 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
 #pragma unroll
       for (int q = 0; q < 9; q++) gr[q] = 0.f;
       if (any) {
+        float acc[3] = {0.f, 0.f, 0.f};
 #pragma unroll
         for (int j = 0; j < PPT; j++)
           if (cj[j]) {
             const float G = ex2_approx(-e.q[j]);
-            bwd_comp(__fmul_rn(Bq.y, G), G, e.dx, __fsub_rn(e.dy0, (float)j), e.u[j], e.w[j], A, Bq, cq.x, T[j],
-                     S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], gr);
+            const float raw = __fmul_rn(Bq.y, G);
+            float* gc = gr + 6;
+            switch (j) {
+              case 0: bwd_comp_strip<0>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
+              case 1: bwd_comp_strip<1>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
+              case 2: bwd_comp_strip<2>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
+              case 3: bwd_comp_strip<3>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
+              case 4: bwd_comp_strip<4>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
+              case 5: bwd_comp_strip<5>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
+              case 6: bwd_comp_strip<6>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
+              default: bwd_comp_strip<7>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
+            }
           }
+        strip_grads(A, Bq, e.dx, e.dy0, e.u[0], e.w[0], acc, gr);
         if (kStats) {
 #pragma unroll
           for (int j = 0; j < PPT; j++) ebc += cj[j];
