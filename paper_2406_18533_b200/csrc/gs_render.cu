@@ -29,8 +29,8 @@ using namespace gsd;
 
 namespace {
 
-constexpr int kBatch = 256;  // records staged per round
-constexpr int kUnroll = 8;   // forward entries per unrolled group (batch padded to a multiple)
+constexpr int kFB = 128;    // forward: records staged per round
+constexpr int kUnroll = 8;  // forward entries per unrolled group (batch padded to a multiple)
 
 // Stage one record: (mx, my, l11', l21'), (l22', o, r, g), (b, qmax) with L' = L sqrt(0.5 log2 e)
 // and qmax = log2(255 o): alpha = o 2^-q >= 1/255  <=>  q <= qmax, so the skip test needs no
@@ -67,26 +67,38 @@ __device__ __forceinline__ bool block_may_hit(const float4& A, const float4& Bq,
   return !(qmin > qmax + 0.05f * (1.0f + qmax));
 }
 
-// Stage the batch's records [0, cnt) into their slots and compact the indices of the records
-// that may be hit (block_may_hit) into s_idx, in list order, padded with kDummy up to a
-// multiple of `pad`.  Returns the number of kept entries (the caller syncs before reading).
+// Stage the batch's records [0, cnt) *compacted*: the records that may be hit
+// (block_may_hit; all of them when !cull) are written, in list order, to slots [0, kept) as
+// (mx, my, l11', l21'), (l22', o, r, g), (b, qmax, list position, receive index), followed by
+// opacity-0 padding entries (qmax < 0 <= q: never composited) up to a multiple of `pad`.  The
+// render loops then read consecutive slots (no index indirection).  Returns kept; the caller
+// syncs before reading and must have synced before calling (slots are overwritten).
 template <int NT, int BATCH>
-__device__ __forceinline__ int stage_compact(const gs_rec* __restrict__ rec, const uint32_t* __restrict__ sidx,
-                                             int cnt, float4* s_a, float4* s_b, float2* s_c, uint32_t* s_j,
-                                             unsigned short* s_idx, int* s_wc, float bx0, float by0, int pad,
-                                             int dummy) {
+__device__ __forceinline__ int stage_records(const gs_rec* __restrict__ rec, const uint32_t* __restrict__ sidx,
+                                             int cnt, int pos0, float4* s_a, float4* s_b, float4* s_c, int* s_wc,
+                                             float bx0, float by0, bool cull, int pad) {
   constexpr int kW = NT / 32, kI = BATCH / NT;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  uint32_t jr[kI];
   unsigned bal[kI];
+  // pass 1: the cull test (only the index survives the barrier; pass 2 re-reads the record
+  // from L1, keeping the register footprint of the staging small)
 #pragma unroll
   for (int i = 0; i < kI; i++) {
     const int t = tid + NT * i;
     bool keep = false;
+    jr[i] = 0;
     if (t < cnt) {
-      const uint32_t j = sidx[t];
-      stage(rec, j, s_a, s_b, s_c, t);
-      if (s_j) s_j[t] = j;
-      keep = block_may_hit(s_a[t], s_b[t], s_c[t].y, bx0, by0);
+      jr[i] = sidx[t];
+      keep = true;
+      if (cull) {
+        const float4* p = reinterpret_cast<const float4*>(rec + jr[i]);
+        const float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+        (void)c;
+        keep = block_may_hit(make_float4(a.x, a.y, b.x * kLScale, b.y * kLScale),
+                             make_float4(b.z * kLScale, b.w, 0.f, 0.f),
+                             b.w > 0.f ? __log2f(255.0f * b.w) : -1.0f, bx0, by0);
+      }
     }
     bal[i] = __ballot_sync(0xffffffffu, keep);
     if (lane == 0) s_wc[i * kW + wid] = __popc(bal[i]);
@@ -101,11 +113,20 @@ __device__ __forceinline__ int stage_compact(const gs_rec* __restrict__ rec, con
     if ((bal[i] >> lane) & 1u) {
       int off = __popc(bal[i] & lt);
       for (int x = 0; x < i * kW + wid; x++) off += s_wc[x];
-      s_idx[off] = (unsigned short)(tid + NT * i);
+      const float4* p = reinterpret_cast<const float4*>(rec + jr[i]);
+      const float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+      s_a[off] = make_float4(a.x, a.y, b.x * kLScale, b.y * kLScale);
+      s_b[off] = make_float4(b.z * kLScale, b.w, c.x, c.y);
+      s_c[off] = make_float4(c.z, b.w > 0.f ? __log2f(255.0f * b.w) : -1.0f, __int_as_float(pos0 + tid + NT * i),
+                             __uint_as_float(jr[i]));
     }
   }
   const int padded = (total + pad - 1) / pad * pad;
-  for (int t = total + tid; t < padded; t += NT) s_idx[t] = (unsigned short)dummy;
+  for (int t = total + tid; t < padded; t += NT) {
+    s_a[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    s_b[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    s_c[t] = make_float4(0.f, -1.0f, 0.f, 0.f);
+  }
   return total;
 }
 
@@ -176,15 +197,8 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
     double* __restrict__ loss_sum, int64_t* __restrict__ tile_cost, int cost_mode,
     long long* __restrict__ stats, int cull) {
   constexpr int NT = 256 / PPT;
-  __shared__ float4 s_a[kBatch + 1], s_b[kBatch + 1];  // slot kBatch: the padding entry
-  __shared__ float2 s_c[kBatch + 1];
-  __shared__ unsigned short s_idx[kBatch + kUnroll];  // kBatch (the padding slot) needs 9 bits
-  __shared__ int s_wc[kBatch / 32];
-  if (threadIdx.x == 0) {  // padding entry: opacity 0, qmax < 0 <= q: never composited
-    s_a[kBatch] = make_float4(0.f, 0.f, 0.f, 0.f);
-    s_b[kBatch] = make_float4(0.f, 0.f, 0.f, 0.f);
-    s_c[kBatch] = make_float2(0.f, -1.0f);
-  }
+  __shared__ float4 s_a[kFB + kUnroll], s_b[kFB + kUnroll], s_c[kFB + kUnroll];
+  __shared__ int s_wc[kFB / 32];
   __shared__ long long s_red[NT / 32];
   __shared__ double s_redd[NT / 32];
   const long long t0 = clock64();
@@ -218,30 +232,18 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
     return a;
   };
   const float bx0 = (float)(tx * 16), by0 = (float)(ty * 16);
-  for (int b0 = beg; b0 < end; b0 += kBatch) {
+  for (int b0 = beg; b0 < end; b0 += kFB) {
     if (__syncthreads_count(all_done()) == NT) break;
-    const int cnt = min(kBatch, end - b0);
-    int kept = cnt;
-    if (cull) {
-      kept = stage_compact<NT, kBatch>(rec, sorted_idx + b0, cnt, s_a, s_b, s_c, nullptr, s_idx, s_wc, bx0, by0,
-                                       kUnroll, kBatch);
-    } else {
-      for (int t = tid; t < cnt; t += NT) {
-        stage(rec, sorted_idx[b0 + t], s_a, s_b, s_c, t);
-        s_idx[t] = (unsigned short)t;
-      }
-      for (int t = cnt + tid; t < ((cnt + kUnroll - 1) & ~(kUnroll - 1)); t += NT) s_idx[t] = (unsigned short)kBatch;
-    }
+    const int cnt = min(kFB, end - b0);
+    const int kept = stage_records<NT, kFB>(rec, sorted_idx + b0, cnt, b0 - beg, s_a, s_b, s_c, s_wc, bx0, by0,
+                                            cull != 0, kUnroll);
     __syncthreads();
     const int kept8 = (kept + kUnroll - 1) & ~(kUnroll - 1);
-    const int pbase = b0 - beg;
     for (int k0 = 0; k0 < kept8; k0 += kUnroll) {
       if (all_done()) break;
 #pragma unroll
       for (int kk = 0; kk < kUnroll; kk++) {
-        const int slot = s_idx[k0 + kk];
-        const float4 A = s_a[slot], Bq = s_b[slot];
-        const float2 cq = s_c[slot];
+        const float4 A = s_a[k0 + kk], Bq = s_b[k0 + kk], cq = s_c[k0 + kk];
         gs_strip<PPT> e;
         q_strip<PPT>(A, Bq, fpx, fpy0, e);
         bool cj[PPT], any = false;
@@ -256,8 +258,8 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
             if (cj[j]) {
               bool st = false;
               const float al = fminf(kAlphaCap, __fmul_rn(Bq.y, ex2_approx(-e.q[j])));
-              fwd_comp<kStats>(al, Bq.z, Bq.w, cq.x, pbase + slot, T[j], C0[j], C1[j], C2[j], st, nl[j], sp[j],
-                               efc);
+              fwd_comp<kStats>(al, Bq.z, Bq.w, cq.x, __float_as_int(cq.z), T[j], C0[j], C1[j], C2[j], st, nl[j],
+                               sp[j], efc);
               dn[j] = st;
             }
         }
@@ -457,10 +459,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   constexpr bool kOneWarp = NT == 32;
   constexpr int kNW = NT / 32;   // warps per block
   constexpr int kBB = 128;        // records staged per round
-  __shared__ float4 s_a[kBB], s_b[kBB];
-  __shared__ float2 s_c[kBB];
-  __shared__ uint32_t s_j[kBB];
-  __shared__ unsigned short s_idx[kBB];
+  __shared__ float4 s_a[kBB], s_b[kBB], s_c[kBB];
   __shared__ int s_wc[kBB / 32];
   // per-warp gradient slots: each (warp, entry, value) is written by exactly one lane, so no
   // shared-memory atomics (a float atomicAdd on shared memory is a CAS loop on sm_100)
@@ -510,27 +509,16 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
     const int p0 = bi * kBB;  // list position of the batch start
     const int cnt = min(kBB, maxn - p0);
     __syncthreads();
-    int kept = cnt;
-    if (cull) {
-      kept = stage_compact<NT, kBB>(rec, sorted_idx + beg + p0, cnt, s_a, s_b, s_c, s_j, s_idx, s_wc,
-                                    (float)(tx * 16), (float)(ty * 16), 1, 0);
-    } else {
-      for (int t = tid; t < cnt; t += NT) {
-        const uint32_t j = sorted_idx[beg + p0 + t];
-        stage(rec, j, s_a, s_b, s_c, t);
-        s_j[t] = j;
-        s_idx[t] = (unsigned short)t;
-      }
-    }
+    const int kept = stage_records<NT, kBB>(rec, sorted_idx + beg + p0, cnt, p0, s_a, s_b, s_c, s_wc,
+                                            (float)(tx * 16), (float)(ty * 16), cull != 0, 1);
     if (!kOneWarp)
       for (int t = tid; t < kNW * kBB * 9; t += NT) s_g[t] = 0.f;
     __syncthreads();
-    for (int kc = kept - 1; kc >= 0; kc--) {
-      const int k = s_idx[kc];
-      const int pos = p0 + k;
+    for (int k = kept - 1; k >= 0; k--) {
+      const float4 cq = s_c[k];
+      const int pos = __float_as_int(cq.z);
       if (pos >= wmax) continue;  // warp-uniform
       const float4 A = s_a[k], Bq = s_b[k];
-      const float2 cq = s_c[k];
       gs_strip<PPT> e;
       q_strip<PPT>(A, Bq, fpx, fpy0, e);
       bool cj[PPT], any = false;
@@ -571,7 +559,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
         const float z = warp_reduce9(gr, lane);
         if (rvalid) {
           if (kOneWarp) {
-            if (z != 0.f) atomicAdd(dL_drec + (int64_t)s_j[k] * 9 + ridx, z);
+            if (z != 0.f) atomicAdd(dL_drec + (int64_t)__float_as_uint(cq.w) * 9 + ridx, z);
           } else {
             s_g[(wid * kBB + k) * 9 + ridx] = z;
           }
@@ -580,9 +568,8 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
     }
     if (!kOneWarp) {
       __syncthreads();
-      for (int kc = tid; kc < kept; kc += NT) {
-        const int t = s_idx[kc];
-        float* dst = dL_drec + (int64_t)s_j[t] * 9;
+      for (int t = tid; t < kept; t += NT) {
+        float* dst = dL_drec + (int64_t)__float_as_uint(s_c[t].w) * 9;
 #pragma unroll
         for (int q = 0; q < 9; q++) {
           float xv = 0.f;
