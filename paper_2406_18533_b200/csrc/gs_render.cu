@@ -1,25 +1,26 @@
 // gs_render.cu -- A4/A5: front-to-back alpha compositing and its backward over the rank's
 // owned 16x16 blocks.
 //
-// One CTA per owned block; each thread owns a vertical strip of PPT pixels of one column
-// (PPT = 4: 64 threads per block, measured fastest on C2; 2 and 8 kept for A/B runs).  The block's depth-sorted
-// list is staged through shared memory in batches of 256 records (coalesced gathers: the sorted
-// index, then the 48-byte record), padded to a multiple of 8 with opacity-0 entries.  The conic
-// is carried as its Cholesky factor L, prescaled by sqrt(0.5 log2 e), so the Gaussian weight is
-// one MUFU.EX2 of a sum of two squares (no cancellation for thin Gaussians):
+// One CTA per owned block; each thread owns PPT pixels of one column, 16/PPT rows apart
+// (PPT = 4: 64 threads per block, measured fastest on C2; 2 and 8 kept for A/B runs), laid out
+// so that the 32 pixels of a warp sharing a j form an 8x4 patch (strip_layout).  The block's
+// depth-sorted list is staged through shared memory in batches (coalesced gathers: the sorted
+// index, then the 48-byte record); records that no pixel of the block can composite are culled
+// at staging (block_may_hit) and the rest are stored compacted, padded with opacity-0 entries.
+// The conic is carried as its Cholesky factor L, prescaled by sqrt(0.5 log2 e), so the
+// Gaussian weight is one MUFU.EX2 of a sum of two squares (no cancellation for thin Gaussians):
 //   u = l11 dx + l21 dy, w = l22 dy, G = 2^-(u^2 + w^2) = exp(-0.5 d^T conic d),
-// and along the strip dy drops by one per pixel, so u and w of the next pixel are one FADD
+// and between a thread's pixels dy drops by 16/PPT, so u and w of the next pixel are one FADD
 // each (q_strip).  A pixel skips an entry (alpha < 1/255) iff q > log2(255 o), precomputed per
-// staged record, so skipped evaluations (~3/4 of all) need no exponential: ~5 instructions
-// per pixel instead of ~14.
+// staged record, so skipped evaluations need no exponential.
 // Early termination: a thread stops evaluating a pixel once its T would drop below 1e-4, and
 // the CTA stops staging once every pixel has stopped (__syncthreads_count).
 // The forward fuses the L1 loss epilogue and the per-block cost counters.
 // The backward walks each pixel's list back to front from n_last, reconstructs
-// T_k = T_{k+1} / (1 - alpha_k), sums the 9 record gradients of an entry over the thread's
-// strip, then reduces them across the warp with a transpose (recursive-halving) reduction
-// (12 shuffles, only when some lane contributes) that leaves value c in one lane; with one
-// warp per block those 9 lanes add straight into dL/d(record) (one global RED each).
+// T_k = T_{k+1} / (1 - alpha_k), accumulates per entry three moments of the thread's pixels
+// from which the 6 geometric gradients follow in closed form (strip_grads) plus the 3 colour
+// gradients, then reduces the 9 values across the warp with a transpose (recursive-halving)
+// reduction (12 shuffles, only when some lane contributes) into per-warp shared-memory slots.
 #include <cstdlib>
 
 #include "gs_device.cuh"
@@ -31,18 +32,6 @@ namespace {
 
 constexpr int kFB = 128;    // forward: records staged per round
 constexpr int kUnroll = 8;  // forward entries per unrolled group (batch padded to a multiple)
-
-// Stage one record: (mx, my, l11', l21'), (l22', o, r, g), (b, qmax) with L' = L sqrt(0.5 log2 e)
-// and qmax = log2(255 o): alpha = o 2^-q >= 1/255  <=>  q <= qmax, so the skip test needs no
-// exponential (both passes decide skips with exactly this comparison).
-__device__ __forceinline__ void stage(const gs_rec* __restrict__ rec, uint32_t j, float4* s_a, float4* s_b,
-                                      float2* s_c, int t) {
-  const float4* p = reinterpret_cast<const float4*>(rec + j);
-  float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
-  s_a[t] = make_float4(a.x, a.y, b.x * kLScale, b.y * kLScale);
-  s_b[t] = make_float4(b.z * kLScale, b.w, c.x, c.y);
-  s_c[t] = make_float2(c.z, b.w > 0.f ? __log2f(255.0f * b.w) : -1.0f);
-}
 
 // Could any pixel centre of the 16x16 block at (bx0, by0) see the staged record with
 // alpha >= 1/255?  Minimum of q(d) = |L'^T d|^2 over the continuous box of offsets
@@ -69,7 +58,10 @@ __device__ __forceinline__ bool block_may_hit(const float4& A, const float4& Bq,
 
 // Stage the batch's records [0, cnt) *compacted*: the records that may be hit
 // (block_may_hit; all of them when !cull) are written, in list order, to slots [0, kept) as
-// (mx, my, l11', l21'), (l22', o, r, g), (b, qmax, list position, receive index), followed by
+// (mx, my, l11', l21'), (l22', o, r, g), (b, qmax, list position, receive index) with
+// L' = L sqrt(0.5 log2 e) and qmax = log2(255 o): alpha = o 2^-q >= 1/255 <=> q <= qmax, so the
+// skip test needs no exponential (both passes decide skips with exactly this comparison);
+// followed by
 // opacity-0 padding entries (qmax < 0 <= q: never composited) up to a multiple of `pad`.  The
 // render loops then read consecutive slots (no index indirection).  Returns kept; the caller
 // syncs before reading and must have synced before calling (slots are overwritten).
@@ -145,25 +137,47 @@ __device__ __forceinline__ T block_sum(T v, T* sm) {
   return s;  // valid in thread 0
 }
 
-// Exponents of a staged record along the thread's vertical strip (px, py0 + j), j < PPT:
-// q_j = u_j^2 + w_j^2 with G_j = 2^-q_j.  dx is shared; dy_j = dy0 - j, so u_j = u_{j-1} - l21
-// and w_j = w_{j-1} - l22.  Both render passes call exactly this, so their skip/stop
-// decisions agree bit for bit.
+// Pixel layout: thread t of a block's CTA owns PPT pixels of one column, RS = 16 / PPT rows
+// apart: (x, r + RS j), j < PPT.  A warp covers 8 columns x 4 values of r (RS >= 4), so the
+// 32 pixels sharing a j -- the lanes that take one compositing branch together -- form a
+// compact 8x4 patch (a small Gaussian's footprint fills more of it than of a 16x2 or strided
+// patch).
+template <int PPT>
+struct strip_layout {
+  static constexpr int RS = 16 / PPT;
+  __device__ static void of(int tid, int& x, int& r) {
+    const int w = tid >> 5, l = tid & 31;
+    if (RS >= 4) {
+      x = 8 * (w & 1) + (l & 7);
+      r = 4 * (w >> 1) + (l >> 3);
+    } else {
+      x = l & 15;
+      r = l >> 4;
+    }
+  }
+};
+
+// Exponents of a staged record at the thread's pixels (px, py0 + RS j), j < PPT:
+// q_j = u_j^2 + w_j^2 with G_j = 2^-q_j.  dx is shared; dy_j = dy0 - RS j, so
+// u_j = u_{j-1} - RS l21 and w_j = w_{j-1} - RS l22 (RS a power of two: exact products).
+// Both render passes call exactly this, so their skip/stop decisions agree bit for bit.
 template <int PPT>
 struct gs_strip {
   float dx, dy0, u[PPT], w[PPT], q[PPT];
 };
 template <int PPT>
 __device__ __forceinline__ void q_strip(const float4& A, const float4& Bq, float px, float py0, gs_strip<PPT>& e) {
+  constexpr float RS = (float)strip_layout<PPT>::RS;
   const float l11 = A.z, l21 = A.w, l22 = Bq.x;
+  const float sl21 = RS * l21, sl22 = RS * l22;
   e.dx = __fsub_rn(A.x, px);
   e.dy0 = __fsub_rn(A.y, py0);
   e.u[0] = __fmaf_rn(l11, e.dx, __fmul_rn(l21, e.dy0));
   e.w[0] = __fmul_rn(l22, e.dy0);
 #pragma unroll
   for (int j = 1; j < PPT; j++) {
-    e.u[j] = __fsub_rn(e.u[j - 1], l21);
-    e.w[j] = __fsub_rn(e.w[j - 1], l22);
+    e.u[j] = __fsub_rn(e.u[j - 1], sl21);
+    e.w[j] = __fsub_rn(e.w[j - 1], sl22);
   }
 #pragma unroll
   for (int j = 0; j < PPT; j++) e.q[j] = __fmaf_rn(e.u[j], e.u[j], __fmul_rn(e.w[j], e.w[j]));
@@ -206,7 +220,9 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
   const int64_t lb = blockIdx.x, beta = B_lo + lb;
   const int64_t v = beta / geo.per_view, loc = beta % geo.per_view;
   const int tx = (int)(loc % geo.Wt), ty = (int)(loc / geo.Wt);
-  const int x = tid & 15, y0 = (tid >> 4) * PPT;
+  constexpr int RS = strip_layout<PPT>::RS;
+  int x, y0;
+  strip_layout<PPT>::of(tid, x, y0);
   const int px = tx * 16 + x, py0 = ty * 16 + y0;
   const float fpx = (float)px, fpy0 = (float)py0;
   const int beg = range[lb], end = range[lb + 1];
@@ -220,7 +236,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
     C0[j] = C1[j] = C2[j] = 0.f;
     nl[j] = 0;
     sp[j] = -1;
-    const bool in = px < geo.W && py0 + j < geo.H;
+    const bool in = px < geo.W && py0 + RS * j < geo.H;
     inside |= (unsigned)in << j;
     dn[j] = !in;
   }
@@ -273,7 +289,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
 #pragma unroll
   for (int j = 0; j < PPT; j++) {
     const bool in = inside >> j & 1;
-    const int p = (y0 + j) * 16 + x;
+    const int p = (y0 + RS * j) * 16 + x;
     const int64_t o = lb * 256 + p;
     if (in) {
       ef += sp[j] >= 0 ? sp[j] + 1 : n;
@@ -288,7 +304,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
       for (int ch = 0; ch < 3; ch++) out_rgb[lb * 768 + ch * 256 + p] = in ? col[ch] : 0.f;
     }
     if (gt) {
-      const uint8_t* g = gt + ((v * geo.H + py0 + j) * (int64_t)geo.W + px) * 3;
+      const uint8_t* g = gt + ((v * geo.H + py0 + RS * j) * (int64_t)geo.W + px) * 3;
 #pragma unroll
       for (int ch = 0; ch < 3; ch++) {
         float e = 0.f;
@@ -325,38 +341,6 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
   }
 }
 
-// Backward of one composited entry for one pixel (O14) given its raw o*G (capped alpha
-// >= 1/255 checked by the caller); accumulates the 9 record gradients into gr.
-__device__ __forceinline__ void bwd_comp(float raw, float G, float dx, float dy, float u, float w, const float4& A,
-                                         const float4& Bq, float cb, float& T, float& S0, float& S1, float& S2,
-                                         float g0, float g1, float g2, float Tf, float bgdot, float gr[9]) {
-  const float alpha = fminf(kAlphaCap, raw);
-  const float om = 1.0f - alpha;
-  const float rom = __fdividef(1.0f, om);
-  T *= rom;  // transmittance in front of this entry
-  const float wgt = alpha * T;
-  const float cr = Bq.z, cg = Bq.w;
-  gr[6] = fmaf(wgt, g0, gr[6]);
-  gr[7] = fmaf(wgt, g1, gr[7]);
-  gr[8] = fmaf(wgt, g2, gr[8]);
-  const float dA = T * ((cr - S0) * g0 + (cg - S1) * g1 + (cb - S2) * g2) - Tf * rom * bgdot;
-  S0 = fmaf(alpha, cr - S0, S0);
-  S1 = fmaf(alpha, cg - S1, S1);
-  S2 = fmaf(alpha, cb - S2, S2);
-  if (raw <= kAlphaCap) {  // R6: zero gradient through the 0.99 cap
-    const float gG = G * dA;
-    const float q = Bq.y * gG;  // dL/dpower
-    const float qs = q * 1.3862943611198906f;  // 2 ln 2 = 1 / kLScale^2
-    gr[5] += gG;
-    gr[0] = fmaf(-qs, A.z * u, gr[0]);
-    gr[1] = fmaf(-qs, fmaf(A.w, u, Bq.x * w), gr[1]);
-    const float hq = -0.5f * q;
-    gr[2] = fmaf(hq * dx, dx, gr[2]);
-    gr[3] = fmaf(-q * dx, dy, gr[3]);
-    gr[4] = fmaf(hq * dy, dy, gr[4]);
-  }
-}
-
 // 1 / x for x in [0.01, 1] (1 - alpha): one MUFU.RCP, no range fix-up.
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
@@ -364,12 +348,12 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
-// Strip form of bwd_comp for pixel j of the thread's strip.  The six geometric gradients are
-// linear in q_j = o G_j dA_j with coefficients polynomial in j (u_j = u_0 - j l21,
-// w_j = w_0 - j l22, dy_j = dy_0 - j), so per pixel only the moments
-// acc = (sum gG, sum j gG, sum j^2 gG) are accumulated (gG = G dA, zero through the cap, R6);
-// strip_grads turns them into the 6 gradients once per entry.  Colour gradients as bwd_comp.
-template <int J>
+// Strip form of bwd_comp for the thread's pixel D rows below its first.  The six geometric
+// gradients are linear in q = o G dA with coefficients polynomial in D (u = u_0 - D l21,
+// w = w_0 - D l22, dy = dy_0 - D), so per pixel only the moments
+// acc = (sum gG, sum D gG, sum D^2 gG) are accumulated (gG = G dA, zero through the cap, R6);
+// strip_grads turns them into the 6 gradients once per entry.  (O14; R6: zero gradient through the 0.99 cap.)
+template <int D>
 __device__ __forceinline__ void bwd_comp_strip(float raw, float G, const float4& Bq, float cb, float& T, float& S0,
                                                float& S1, float& S2, float g0, float g1, float g2, float Tf,
                                                float bgdot, float acc[3], float gc[3]) {
@@ -387,8 +371,8 @@ __device__ __forceinline__ void bwd_comp_strip(float raw, float G, const float4&
   S2 = fmaf(alpha, cb - S2, S2);
   const float gG = raw <= kAlphaCap ? G * dA : 0.f;
   acc[0] += gG;
-  if (J == 1) acc[1] += gG, acc[2] += gG;
-  if (J >= 2) acc[1] = fmaf((float)J, gG, acc[1]), acc[2] = fmaf((float)(J * J), gG, acc[2]);
+  if (D == 1) acc[1] += gG, acc[2] += gG;
+  if (D >= 2) acc[1] = fmaf((float)D, gG, acc[1]), acc[2] = fmaf((float)(D * D), gG, acc[2]);
 }
 
 // gr[0..5] of one entry from the strip moments (q = o gG; 2 ln 2 = 1 / kLScale^2):
@@ -471,7 +455,9 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   const int64_t lb = blockIdx.x, beta = B_lo + lb;
   const int64_t loc = beta % geo.per_view;
   const int tx = (int)(loc % geo.Wt), ty = (int)(loc / geo.Wt);
-  const int x = tid & 15, y0 = (tid >> 4) * PPT;
+  constexpr int RS = strip_layout<PPT>::RS;
+  int x, y0;
+  strip_layout<PPT>::of(tid, x, y0);
   const int px = tx * 16 + x, py0 = ty * 16 + y0;
   const float fpx = (float)px, fpy0 = (float)py0;
   int nl[PPT];
@@ -479,8 +465,8 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   int mymax = 0, nlsum = 0;
 #pragma unroll
   for (int j = 0; j < PPT; j++) {
-    const bool in = px < geo.W && py0 + j < geo.H;
-    const int64_t o = lb * 256 + (y0 + j) * 16 + x;
+    const bool in = px < geo.W && py0 + RS * j < geo.H;
+    const int64_t o = lb * 256 + (y0 + RS * j) * 16 + x;
     nl[j] = in ? n_last[o] : 0;
     Tf[j] = in ? T_final[o] : 1.f;
     T[j] = Tf[j];
@@ -539,14 +525,14 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
             const float raw = __fmul_rn(Bq.y, G);
             float* gc = gr + 6;
             switch (j) {
-              case 0: bwd_comp_strip<0>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
-              case 1: bwd_comp_strip<1>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
-              case 2: bwd_comp_strip<2>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
-              case 3: bwd_comp_strip<3>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
-              case 4: bwd_comp_strip<4>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
-              case 5: bwd_comp_strip<5>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
-              case 6: bwd_comp_strip<6>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
-              default: bwd_comp_strip<7>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
+              case 0: bwd_comp_strip<0 * RS>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
+              case 1: bwd_comp_strip<1 * RS>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
+              case 2: bwd_comp_strip<2 * RS>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
+              case 3: bwd_comp_strip<3 * RS>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
+              case 4: bwd_comp_strip<4 * RS>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
+              case 5: bwd_comp_strip<5 * RS>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
+              case 6: bwd_comp_strip<6 * RS>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
+              default: bwd_comp_strip<7 * RS>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
             }
           }
         strip_grads(A, Bq, e.dx, e.dy0, e.u[0], e.w[0], acc, gr);
@@ -595,188 +581,6 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
     } else {
       __syncthreads();
       if (tid == 0) tile_cost[lb] += clock64() - t0;
-    }
-  }
-}
-
-// Compacted backward: one warp per block.  The per-pixel backward state (T, S, dL/dC, T_final,
-// bg term) lives in shared memory.  For each entry the warp evaluates the skip test of all 256
-// pixels with the forward's exact strip decomposition (FP pixels per strip, q_strip<FP>),
-// compacts the contributing pixels into a shared list (pixel, u, w, q), and processes that
-// list 32 at a time -- lane L takes the L-th contributing pixel -- so the ~45-instruction
-// gradient body runs with all lanes busy instead of once per strip row with most lanes idle.
-// The 9 record gradients are then reduced across the warp once per entry (transpose
-// reduction) and added straight into dL/d(record).
-template <int FP, bool kStats>
-__global__ void __launch_bounds__(32) k_render_bwd_c(
-    const gs_rec* __restrict__ rec, const uint32_t* __restrict__ sorted_idx,
-    const int32_t* __restrict__ range, gs_geom geo, int64_t B_lo, float bg0, float bg1, float bg2,
-    const float* __restrict__ dL_dpix, const float* __restrict__ T_final,
-    const int32_t* __restrict__ n_last, float* __restrict__ dL_drec, int64_t* __restrict__ tile_cost,
-    int cost_mode, long long* __restrict__ stats) {
-  constexpr int kStrips = 8 / FP;   // forward strips handled by each lane
-  constexpr int kBB = 128;          // records staged per round
-  __shared__ float4 s_a[kBB], s_b[kBB];
-  __shared__ float2 s_c[kBB];
-  __shared__ uint32_t s_j[kBB];
-  __shared__ float s_T[256], s_S0[256], s_S1[256], s_S2[256], s_g0[256], s_g1[256], s_g2[256], s_Tf[256],
-      s_bgd[256];
-  __shared__ float4 s_list[256];  // contributing (pixel, u, w, q) of the current entry
-  const long long t0 = clock64();
-  const int lane = threadIdx.x;
-  const int64_t lb = blockIdx.x, beta = B_lo + lb;
-  const int64_t loc = beta % geo.per_view;
-  const int tx = (int)(loc % geo.Wt), ty = (int)(loc / geo.Wt);
-  // lane's forward strips: strip index st = lane + 32 i, column st & 15, first row FP*(st >> 4)
-  int nl[kStrips][FP];
-  float fpx[kStrips], fpy0[kStrips];
-  int mymax = 0, nlsum = 0;
-#pragma unroll
-  for (int i = 0; i < kStrips; i++) {
-    const int st = lane + 32 * i, x = st & 15, y0 = FP * (st >> 4);
-    const int px = tx * 16 + x, py0 = ty * 16 + y0;
-    fpx[i] = (float)px;
-    fpy0[i] = (float)py0;
-#pragma unroll
-    for (int j = 0; j < FP; j++) {
-      const int pp = (y0 + j) * 16 + x;
-      const bool in = px < geo.W && py0 + j < geo.H;
-      const int64_t o = lb * 256 + pp;
-      nl[i][j] = in ? n_last[o] : 0;
-      const float tf = in ? T_final[o] : 1.f;
-      const float g0 = in ? dL_dpix[lb * 768 + pp] : 0.f;
-      const float g1 = in ? dL_dpix[lb * 768 + 256 + pp] : 0.f;
-      const float g2 = in ? dL_dpix[lb * 768 + 512 + pp] : 0.f;
-      s_T[pp] = tf;
-      s_Tf[pp] = tf;
-      s_S0[pp] = s_S1[pp] = s_S2[pp] = 0.f;
-      s_g0[pp] = g0;
-      s_g1[pp] = g1;
-      s_g2[pp] = g2;
-      s_bgd[pp] = bg0 * g0 + bg1 * g1 + bg2 * g2;
-      mymax = max(mymax, nl[i][j]);
-      nlsum += nl[i][j];
-    }
-  }
-  const int maxn = __reduce_max_sync(0xffffffffu, mymax);
-  bool rvalid;
-  const int ridx = red_index(lane, rvalid);
-  const int beg = range[lb];
-  const float kQ = 1.3862943611198906f;  // 2 ln 2 = 1 / kLScale^2
-  int ebc = 0;
-  for (int bi = (maxn + kBB - 1) / kBB - 1; bi >= 0; bi--) {
-    const int p0 = bi * kBB;
-    const int cnt = min(kBB, maxn - p0);
-    __syncwarp();
-    for (int t = lane; t < cnt; t += 32) {
-      const uint32_t j = sorted_idx[beg + p0 + t];
-      stage(rec, j, s_a, s_b, s_c, t);
-      s_j[t] = j;
-    }
-    __syncwarp();
-    for (int k = cnt - 1; k >= 0; k--) {
-      const int pos = p0 + k;
-      const float4 A = s_a[k], Bq = s_b[k];
-      const float2 cq = s_c[k];
-      // 1. skip tests of the lane's pixels (bit-identical to the forward's decisions)
-      unsigned c[kStrips];
-      gs_strip<FP> e[kStrips];
-      int mine = 0;
-#pragma unroll
-      for (int i = 0; i < kStrips; i++) {
-        q_strip<FP>(A, Bq, fpx[i], fpy0[i], e[i]);
-        c[i] = 0;
-#pragma unroll
-        for (int j = 0; j < FP; j++) c[i] |= (unsigned)(pos < nl[i][j] && e[i].q[j] <= cq.y) << j;
-        mine += __popc(c[i]);
-      }
-      // 2. compaction offsets
-      int incl = mine;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      if (total == 0) continue;
-      int w = incl - mine;
-#pragma unroll
-      for (int i = 0; i < kStrips; i++) {
-        const int st = lane + 32 * i, x = st & 15, y0 = FP * (st >> 4);
-        unsigned cc = c[i];
-        while (cc) {
-          const int j = __ffs(cc) - 1;
-          cc &= cc - 1;
-          float uj = 0.f, wj = 0.f, qj = 0.f;
-#pragma unroll
-          for (int jj = 0; jj < FP; jj++)
-            if (jj == j) { uj = e[i].u[jj]; wj = e[i].w[jj]; qj = e[i].q[jj]; }
-          s_list[w++] = make_float4(__int_as_float((y0 + j) * 16 + x), uj, wj, qj);
-        }
-      }
-      __syncwarp();
-      // 3. lane L processes contributions L, L + 32, ...
-      float gr[9];
-#pragma unroll
-      for (int q = 0; q < 9; q++) gr[q] = 0.f;
-      for (int idx = lane; idx < total; idx += 32) {
-        const float4 it = s_list[idx];
-        const int pp = __float_as_int(it.x);
-        const float u = it.y, wv = it.z, q = it.w;
-        const float px = (float)(tx * 16 + (pp & 15)), py = (float)(ty * 16 + (pp >> 4));
-        const float dx = __fsub_rn(A.x, px), dy = __fsub_rn(A.y, py);
-        const float G = ex2_approx(-q);
-        const float raw = __fmul_rn(Bq.y, G);
-        const float alpha = fminf(kAlphaCap, raw);
-        const float om = 1.0f - alpha;
-        const float rom = __fdividef(1.0f, om);
-        const float T = s_T[pp] * rom;  // transmittance in front of this entry
-        const float S0 = s_S0[pp], S1 = s_S1[pp], S2 = s_S2[pp];
-        const float g0 = s_g0[pp], g1 = s_g1[pp], g2 = s_g2[pp];
-        const float cr = Bq.z, cg = Bq.w, cb = cq.x;
-        const float wgt = alpha * T;
-        gr[6] = fmaf(wgt, g0, gr[6]);
-        gr[7] = fmaf(wgt, g1, gr[7]);
-        gr[8] = fmaf(wgt, g2, gr[8]);
-        const float dA = T * ((cr - S0) * g0 + (cg - S1) * g1 + (cb - S2) * g2) - s_Tf[pp] * rom * s_bgd[pp];
-        s_T[pp] = T;
-        s_S0[pp] = fmaf(alpha, cr - S0, S0);
-        s_S1[pp] = fmaf(alpha, cg - S1, S1);
-        s_S2[pp] = fmaf(alpha, cb - S2, S2);
-        if (raw <= kAlphaCap) {  // R6: zero gradient through the 0.99 cap
-          const float gG = G * dA;
-          const float qq = Bq.y * gG;  // dL/dpower
-          const float qs = qq * kQ;
-          gr[5] += gG;
-          gr[0] = fmaf(-qs, A.z * u, gr[0]);
-          gr[1] = fmaf(-qs, fmaf(A.w, u, Bq.x * wv), gr[1]);
-          const float hq = -0.5f * qq;
-          gr[2] = fmaf(hq * dx, dx, gr[2]);
-          gr[3] = fmaf(-qq * dx, dy, gr[3]);
-          gr[4] = fmaf(hq * dy, dy, gr[4]);
-        }
-      }
-      if (kStats) ebc += total;
-      // 4. one warp reduction per entry, straight into dL/d(record)
-      const float z = warp_reduce9(gr, lane);
-      if (rvalid && z != 0.f) atomicAdd(dL_drec + (int64_t)s_j[k] * 9 + ridx, z);
-      __syncwarp();
-    }
-  }
-  if (kStats) {
-    const long long a = __reduce_add_sync(0xffffffffu, (unsigned)nlsum);
-    if (lane == 0) {
-      atomicAdd((unsigned long long*)&stats[4], (unsigned long long)a);
-      atomicAdd((unsigned long long*)&stats[5], (unsigned long long)ebc);
-    }
-  }
-  if (tile_cost) {
-    if (cost_mode == GS_COST_WORK) {
-      const long long wsum = __reduce_add_sync(0xffffffffu, (unsigned)nlsum);
-      if (lane == 0) tile_cost[lb] += wsum;
-    } else {
-      __syncwarp();
-      if (lane == 0) tile_cost[lb] += clock64() - t0;
     }
   }
 }
@@ -871,11 +675,6 @@ extern "C" gs_status gs_render_bwd(gs_ctx* c, const void* recv_rec, int64_t n_re
   if (bg_h) for (int k = 0; k < 3; k++) bg[k] = bg_h[k];
   ++c->launches;
   const int ppt = render_ppt();
-  static int compact = -1;
-  if (compact < 0) {
-    const char* e = getenv("GS_RENDER_BWD_COMPACT");
-    compact = e ? atoi(e) : 0;
-  }
   const int mb = render_minb(1);
   auto kb = ppt == 2 ? (stats ? k_render_bwd<2, true> : k_render_bwd<2, false>)
           : ppt == 8 ? (stats ? k_render_bwd<8, true> : k_render_bwd<8, false>)
@@ -883,19 +682,10 @@ extern "C" gs_status gs_render_bwd(gs_ctx* c, const void* recv_rec, int64_t n_re
           : mb == 12 ? (stats ? k_render_bwd<4, true, 12> : k_render_bwd<4, false, 12>)
                      : (stats ? k_render_bwd<4, true, 10> : k_render_bwd<4, false, 10>);
   const int threads = 256 / ppt;
-  // compacted one-warp backward, same strip decomposition as the forward
-  auto kc = ppt == 2 ? (stats ? k_render_bwd_c<2, true> : k_render_bwd_c<2, false>)
-          : ppt == 4 ? (stats ? k_render_bwd_c<4, true> : k_render_bwd_c<4, false>)
-                     : (stats ? k_render_bwd_c<8, true> : k_render_bwd_c<8, false>);
-  if (compact) {
-    kc<<<(unsigned)n_owned, 32, 0, st>>>(
-        (const gs_rec*)recv_rec, sorted_idx, tile_range, geo, B_lo, bg[0], bg[1], bg[2], dL_dpix, T_final, n_last,
-        dL_drec, tile_cost, cost_mode, (long long*)stats);
-  } else {
-    kb<<<(unsigned)n_owned, threads, 0, st>>>(
-        (const gs_rec*)recv_rec, sorted_idx, tile_range, geo, B_lo, bg[0], bg[1], bg[2], dL_dpix, T_final, n_last,
-        dL_drec, tile_cost, cost_mode, (long long*)stats, (render_cull() >> 1) & 1);
-  }
+
+  kb<<<(unsigned)n_owned, threads, 0, st>>>(
+      (const gs_rec*)recv_rec, sorted_idx, tile_range, geo, B_lo, bg[0], bg[1], bg[2], dL_dpix, T_final, n_last,
+      dL_drec, tile_cost, cost_mode, (long long*)stats, (render_cull() >> 1) & 1);
   GS_LAUNCH_CHECK(c, "render_bwd");
   return GS_OK;
 }
