@@ -487,8 +487,18 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
 #pragma unroll
     for (int w = 0; w < NT / 32; w++) maxn = max(maxn, s_max[w]);
   }
-  bool rvalid;
-  const int ridx = red_index(lane, rvalid);
+  // this lane's gradient slot offset within an entry (value index, or -1), read back from
+  // shared memory when the register cap evicts it (cheaper than recomputing red_index)
+  __shared__ int s_ridx[NT];
+  {
+    bool v;
+    const int r = red_index(lane, v);
+    s_ridx[tid] = v ? r : -1;
+  }
+  __syncwarp();
+  const int ridx_s = s_ridx[tid];
+  const bool rvalid = ridx_s >= 0;
+  const int ridx = rvalid ? ridx_s : 0;
   const int beg = range[lb];
   int ebc = 0;
   for (int bi = (maxn + kBB - 1) / kBB - 1; bi >= 0; bi--) {
