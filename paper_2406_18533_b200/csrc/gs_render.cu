@@ -171,8 +171,12 @@ __device__ __forceinline__ void q_strip(const float4& A, const float4& Bq, float
   constexpr float RS = (float)strip_layout<PPT>::RS;
   const float l11 = A.z, l21 = A.w, l22 = Bq.x;
   const float sl21 = RS * l21, sl22 = RS * l22;
-  e.dx = __fsub_rn(A.x, px);
-  e.dy0 = __fsub_rn(A.y, py0);
+  // (dx, dy0) and the exponents of pixel pairs with packed fp32x2 operations (FADD2 / FFMA2 /
+  // FMUL2: one issue slot for two lanes' worth of work; per element identical to the scalar
+  // __fsub_rn / __fmaf_rn(u, u, w * w))
+  const float2 d = __fadd2_rn(make_float2(A.x, A.y), make_float2(-px, -py0));
+  e.dx = d.x;
+  e.dy0 = d.y;
   e.u[0] = __fmaf_rn(l11, e.dx, __fmul_rn(l21, e.dy0));
   e.w[0] = __fmul_rn(l22, e.dy0);
 #pragma unroll
@@ -181,7 +185,12 @@ __device__ __forceinline__ void q_strip(const float4& A, const float4& Bq, float
     e.w[j] = __fsub_rn(e.w[j - 1], sl22);
   }
 #pragma unroll
-  for (int j = 0; j < PPT; j++) e.q[j] = __fmaf_rn(e.u[j], e.u[j], __fmul_rn(e.w[j], e.w[j]));
+  for (int j = 0; j < PPT; j += 2) {
+    const float2 u = make_float2(e.u[j], e.u[j + 1]), w = make_float2(e.w[j], e.w[j + 1]);
+    const float2 q = __ffma2_rn(u, u, __fmul2_rn(w, w));
+    e.q[j] = q.x;
+    e.q[j + 1] = q.y;
+  }
 }
 
 // Composite one staged entry into one pixel (O12) given its capped alpha >= 1/255.
@@ -355,21 +364,20 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // acc = (sum gG, sum D gG, sum D^2 gG) are accumulated (gG = G dA, zero through the cap, R6);
 // strip_grads turns them into the 6 gradients once per entry.  (O14; R6: zero gradient through the 0.99 cap.)
 template <int D>
-__device__ __forceinline__ void bwd_comp_strip(float raw, float G, const float4& Bq, float cb, float& T, float& S0,
-                                               float& S1, float& S2, float g0, float g1, float g2, float Tf,
-                                               float bgdot, float acc[3], float gc[3]) {
+__device__ __forceinline__ void bwd_comp_strip(float raw, float G, const float4& Bq, float cb, float& T, float2& S01,
+                                               float& S2, float2 g01, float g2, float Tf, float bgdot, float acc[3],
+                                               float2& gc01, float& gc2) {
   const float alpha = fminf(kAlphaCap, raw);
   const float rom = rcp_approx(1.0f - alpha);
   T *= rom;  // transmittance in front of this entry
   const float wgt = alpha * T;
-  const float cr = Bq.z, cg = Bq.w;
-  gc[0] = fmaf(wgt, g0, gc[0]);
-  gc[1] = fmaf(wgt, g1, gc[1]);
-  gc[2] = fmaf(wgt, g2, gc[2]);
-  const float dA = T * ((cr - S0) * g0 + (cg - S1) * g1 + (cb - S2) * g2) - Tf * rom * bgdot;
-  S0 = fmaf(alpha, cr - S0, S0);
-  S1 = fmaf(alpha, cg - S1, S1);
-  S2 = fmaf(alpha, cb - S2, S2);
+  gc01 = __ffma2_rn(make_float2(wgt, wgt), g01, gc01);
+  gc2 = fmaf(wgt, g2, gc2);
+  const float2 d01 = __fadd2_rn(make_float2(Bq.z, Bq.w), make_float2(-S01.x, -S01.y));  // c - S (r, g)
+  const float d2 = cb - S2;
+  const float dA = T * fmaf(d2, g2, fmaf(d01.y, g01.y, d01.x * g01.x)) - Tf * rom * bgdot;
+  S01 = __ffma2_rn(make_float2(alpha, alpha), d01, S01);
+  S2 = fmaf(alpha, d2, S2);
   const float gG = raw <= kAlphaCap ? G * dA : 0.f;
   acc[0] += gG;
   if (D == 1) acc[1] += gG, acc[2] += gG;
@@ -462,7 +470,8 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   const int px = tx * 16 + x, py0 = ty * 16 + y0;
   const float fpx = (float)px, fpy0 = (float)py0;
   int nl[PPT];
-  float Tf[PPT], T[PPT], S0[PPT], S1[PPT], S2[PPT], g0[PPT], g1[PPT], g2[PPT], bgd[PPT];
+  float Tf[PPT], T[PPT], S2[PPT], g2[PPT], bgd[PPT];
+  float2 S01[PPT], g01[PPT];  // (r, g) pairs for packed fp32x2 updates
   int mymax = 0, nlsum = 0;
 #pragma unroll
   for (int j = 0; j < PPT; j++) {
@@ -471,11 +480,11 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
     nl[j] = in ? n_last[o] : 0;
     Tf[j] = in ? T_final[o] : 1.f;
     T[j] = Tf[j];
-    S0[j] = S1[j] = S2[j] = 0.f;
-    g0[j] = in ? dL_dpix[lb * 768 + (o - lb * 256)] : 0.f;
-    g1[j] = in ? dL_dpix[lb * 768 + 256 + (o - lb * 256)] : 0.f;
+    S01[j] = make_float2(0.f, 0.f);
+    S2[j] = 0.f;
+    g01[j] = make_float2(in ? dL_dpix[lb * 768 + (o - lb * 256)] : 0.f, in ? dL_dpix[lb * 768 + 256 + (o - lb * 256)] : 0.f);
     g2[j] = in ? dL_dpix[lb * 768 + 512 + (o - lb * 256)] : 0.f;
-    bgd[j] = bg0 * g0[j] + bg1 * g1[j] + bg2 * g2[j];
+    bgd[j] = bg0 * g01[j].x + bg1 * g01[j].y + bg2 * g2[j];
     mymax = max(mymax, nl[j]);
     nlsum += nl[j];
   }
@@ -529,24 +538,28 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
       for (int q = 0; q < 9; q++) gr[q] = 0.f;
       if (any) {
         float acc[3] = {0.f, 0.f, 0.f};
+        float2 gc01 = make_float2(0.f, 0.f);
+        float gc2 = 0.f;
 #pragma unroll
         for (int j = 0; j < PPT; j++)
           if (cj[j]) {
             const float G = ex2_approx(-e.q[j]);
             const float raw = __fmul_rn(Bq.y, G);
-            float* gc = gr + 6;
             switch (j) {
-              case 0: bwd_comp_strip<0 * RS>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
-              case 1: bwd_comp_strip<1 * RS>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
-              case 2: bwd_comp_strip<2 * RS>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
-              case 3: bwd_comp_strip<3 * RS>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
-              case 4: bwd_comp_strip<4 * RS>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
-              case 5: bwd_comp_strip<5 * RS>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
-              case 6: bwd_comp_strip<6 * RS>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
-              default: bwd_comp_strip<7 * RS>(raw, G, Bq, cq.x, T[j], S0[j], S1[j], S2[j], g0[j], g1[j], g2[j], Tf[j], bgd[j], acc, gc); break;
+              case 0: bwd_comp_strip<0 * RS>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 1: bwd_comp_strip<1 * RS>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 2: bwd_comp_strip<2 * RS>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 3: bwd_comp_strip<3 * RS>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 4: bwd_comp_strip<4 * RS>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 5: bwd_comp_strip<5 * RS>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 6: bwd_comp_strip<6 * RS>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              default: bwd_comp_strip<7 * RS>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
             }
           }
         strip_grads(A, Bq, e.dx, e.dy0, e.u[0], e.w[0], acc, gr);
+        gr[6] = gc01.x;
+        gr[7] = gc01.y;
+        gr[8] = gc2;
         if (kStats) {
 #pragma unroll
           for (int j = 0; j < PPT; j++) ebc += cj[j];
