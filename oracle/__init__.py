@@ -289,3 +289,33 @@ def block_to_image(arr, Wt, Ht, W, H, n_views):
     a = arr.reshape(n_views, Ht, Wt, 16, 16, *tail)
     a = np.moveaxis(a, 3, 2).reshape(n_views, Ht * 16, Wt * 16, *tail)
     return a[:, :H, :W]
+
+
+# ------------------------------------------------------------------ NEXT-1: L1 + D-SSIM
+
+SSIM_LAMBDA = 0.2  # S:301 (the 3DGS default; the paper names both losses but not the mix)
+
+
+def ssim_loss(img, gt, lam=SSIM_LAMBDA, want_grad=True):
+    """One image: (loss, ssim_mean, grad[H,W,3] or None) of (1-lam) L1 + lam (1 - SSIM);
+    img, gt float arrays [H,W,3] in [0,1] (gs_oracle.c orc_ssim_loss)."""
+    img = np.ascontiguousarray(img, np.float64)
+    gt = np.ascontiguousarray(gt, np.float64)
+    H, W = img.shape[:2]
+    loss, s = C.c_double(0), C.c_double(0)
+    grad = np.zeros_like(img) if want_grad else None
+    lib().orc_ssim_loss(C.c_int32(W), C.c_int32(H), _p(img), _p(gt), C.c_double(lam), C.byref(loss), C.byref(s),
+                        _p(grad))
+    return loss.value, s.value, grad
+
+
+def ssim_loss_batch(imgs, gts, lam=SSIM_LAMBDA):
+    """Batch of b images [b,H,W,3]: the step's loss = mean over images (as the L1 of O13
+    divided by b), gradient [b,H,W,3] of that mean."""
+    b = len(imgs)
+    tot, grads = 0.0, []
+    for i in range(b):
+        l, _, g = ssim_loss(imgs[i], gts[i], lam)
+        tot += l / b
+        grads.append(g / b)
+    return tot, np.stack(grads)

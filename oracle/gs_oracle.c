@@ -697,3 +697,91 @@ void orc_costs_to_et(int32_t mode, int64_t B, int32_t G, const int64_t* DP, cons
       et[i] = Ng > 0 ? (int64_t)((__int128)Cg * npix[i] / Ng) : 0;
   }
 }
+
+/* ------------------------------------------------------------------ NEXT-1: L1 + D-SSIM */
+/* P:114 "the 3DGS computes the L1 and SSIM loss by comparing the rendered image to the
+ * ground truth image ... the SSIM loss measures the similarity between pixel windows";
+ * S:278-282 (11x11 Gaussian window, sigma 1.5, C1 = 0.01^2, C2 = 0.03^2, mean over centres,
+ * analytic gradient), S:301 (lambda = 0.2).  Readings R12: the window is the
+ * normalised 1D Gaussian outer-multiplied with itself, values outside the image are zero
+ * (windows are not truncated or renormalised at the border), the mean runs over every pixel
+ * and channel of the image.
+ *
+ * For one channel and centre p, with window w and zero padding:
+ *   mx = sum w x, my = sum w y, Exx = sum w x^2, Eyy = sum w y^2, Exy = sum w x y,
+ *   A1 = 2 mx my + C1, A2 = 2 (Exy - mx my) + C2, B1 = mx^2 + my^2 + C1,
+ *   B2 = (Exx - mx^2) + (Eyy - my^2) + C2,  S(p) = A1 A2 / (B1 B2).
+ * Treating (mx, Exx, Exy) as the independent window statistics of x:
+ *   dS/dmx  = (2 my A2 - 2 my A1) / (B1 B2) - S (2 mx / B1 - 2 mx / B2)
+ *   dS/dExx = -S / B2,   dS/dExy = 2 A1 / (B1 B2),
+ * and dmx(p)/dx(q) = w(q - p), dExx(p)/dx(q) = 2 x(q) w(q - p), dExy(p)/dx(q) = y(q) w(q - p).
+ * Every window sum below is the direct 121-term double sum (no separable filtering). */
+static void orc_ssim_window(double w[11][11]) {
+  double g[11], s = 0.0;
+  for (int k = 0; k < 11; k++) {
+    const double d = (double)(k - 5);
+    g[k] = exp(-d * d / (2.0 * 1.5 * 1.5));
+    s += g[k];
+  }
+  for (int a = 0; a < 11; a++)
+    for (int b = 0; b < 11; b++) w[a][b] = (g[a] / s) * (g[b] / s);
+}
+
+void orc_ssim_loss(int32_t W, int32_t H, const double* img, const double* gt, double lambda, double* loss,
+                   double* ssim_mean, double* grad) {
+  const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+  const double N = 3.0 * (double)W * (double)H;
+  double w[11][11];
+  orc_ssim_window(w);
+  const int64_t np = (int64_t)W * H;
+  double* dmx = (double*)calloc((size_t)np, sizeof(double));
+  double* dxx = (double*)calloc((size_t)np, sizeof(double));
+  double* dxy = (double*)calloc((size_t)np, sizeof(double));
+  double l1 = 0.0, ssum = 0.0;
+  for (int c = 0; c < 3; c++) {
+    for (int py = 0; py < H; py++)
+      for (int px = 0; px < W; px++) {
+        double mx = 0, my = 0, exx = 0, eyy = 0, exy = 0;
+        for (int a = 0; a < 11; a++)
+          for (int b = 0; b < 11; b++) {
+            const int qy = py + a - 5, qx = px + b - 5;
+            if (qy < 0 || qy >= H || qx < 0 || qx >= W) continue; /* zero padding */
+            const double x = img[((int64_t)qy * W + qx) * 3 + c], y = gt[((int64_t)qy * W + qx) * 3 + c];
+            mx += w[a][b] * x;
+            my += w[a][b] * y;
+            exx += w[a][b] * x * x;
+            eyy += w[a][b] * y * y;
+            exy += w[a][b] * x * y;
+          }
+        const double A1 = 2.0 * mx * my + C1, A2 = 2.0 * (exy - mx * my) + C2;
+        const double B1 = mx * mx + my * my + C1, B2 = (exx - mx * mx) + (eyy - my * my) + C2;
+        const double S = A1 * A2 / (B1 * B2);
+        ssum += S;
+        const int64_t p = (int64_t)py * W + px;
+        dmx[p] = (2.0 * my * A2 - 2.0 * my * A1) / (B1 * B2) - S * (2.0 * mx / B1 - 2.0 * mx / B2);
+        dxx[p] = -S / B2;
+        dxy[p] = 2.0 * A1 / (B1 * B2);
+      }
+    for (int qy = 0; qy < H; qy++)
+      for (int qx = 0; qx < W; qx++) {
+        const int64_t q = (int64_t)qy * W + qx;
+        const double x = img[q * 3 + c], y = gt[q * 3 + c];
+        double gs = 0.0; /* d(sum_p S(p)) / dx(q) */
+        for (int a = 0; a < 11; a++)
+          for (int b = 0; b < 11; b++) {
+            const int py = qy - (a - 5), px = qx - (b - 5); /* q = p + (a-5, b-5) */
+            if (py < 0 || py >= H || px < 0 || px >= W) continue;
+            const int64_t p = (int64_t)py * W + px;
+            gs += w[a][b] * (dmx[p] + 2.0 * x * dxx[p] + y * dxy[p]);
+          }
+        const double e = x - y;
+        l1 += fabs(e);
+        if (grad) grad[q * 3 + c] = ((1.0 - lambda) * (e > 0 ? 1.0 : (e < 0 ? -1.0 : 0.0)) - lambda * gs) / N;
+      }
+  }
+  free(dmx);
+  free(dxx);
+  free(dxy);
+  if (ssim_mean) *ssim_mean = ssum / N;
+  if (loss) *loss = (1.0 - lambda) * l1 / N + lambda * (1.0 - ssum / N);
+}

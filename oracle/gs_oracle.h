@@ -99,6 +99,13 @@ int orc_division_points(const int64_t* ET, int64_t B, int32_t G, int64_t* DP);
 void orc_costs_to_et(int32_t mode, int64_t B, int32_t G, const int64_t* DP, const int64_t* cost,
                      const int64_t* npix, int64_t* et);
 
+/* NEXT-1 (reading R12): L = (1-lambda) L1 + lambda (1 - SSIM) of one
+ * image, img/gt [H][W][3] in [0,1]; SSIM = mean over pixels and channels of the 11x11
+ * Gaussian-window (sigma 1.5) SSIM map with zero padding; grad[H][W][3] = dL/dimg (may be
+ * NULL).  Direct window sums in fp64 (O(121 H W) per channel).                       */
+void orc_ssim_loss(int32_t W, int32_t H, const double* img, const double* gt, double lambda, double* loss,
+                   double* ssim_mean, double* grad);
+
 #ifdef __cplusplus
 }
 #endif
