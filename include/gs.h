@@ -243,6 +243,43 @@ gs_status gs_division_points(const int64_t* ET_h, int64_t B, int G, int64_t* DP_
 gs_status gs_exchange_plan(const int64_t* counts_h, int G, int rank, int64_t* send_off_h,
                            int64_t* recv_off_h);
 
+/* ------------------------------------------------------------------- NEXT-1 L1 + D-SSIM */
+/* The loss of P:114 ("computes the L1 and SSIM loss ... SSIM loss measures the similarity
+ * between pixel windows"), per view
+ *   L_v = (1 - lambda) mean|x - y| + lambda (1 - mean SSIM(x, y)),
+ * SSIM with an 11x11 Gaussian window (sigma 1.5, normalised 1D Gaussian squared), C1 = 0.01^2,
+ * C2 = 0.03^2, zero padding outside the image (R12), means over all pixels and
+ * channels; the batch loss is sum_v L_v / b_loss.  A pixel's gradient depends on the image
+ * within 10 pixels, so blocks next to another rank's range need that rank's rendered blocks
+ * (the halo: the not-owned 8-neighbours, same view, of owned blocks).                     */
+
+/* gs_halo_plan -- the rank's halo block ids (ascending) into halo_ids_h[cap]; *n_halo_h = count
+ * (GS_ECAPACITY if > cap, ids not written).  Empty at world 1.  Host only, no collective. */
+gs_status gs_halo_plan(gs_ctx* ctx, const gs_camera* cams_h, int n_views, const int64_t* dp_h,
+                       int64_t* halo_ids_h, int64_t cap, int64_t* n_halo_h);
+
+/* gs_halo_exchange -- COLLECTIVE (every rank, same order).  out_rgb: the rank's rendered
+ * owned blocks [n_owned][3][256] (gs_render_fwd out_rgb).  Writes halo[n_halo][3][256] and
+ * halo_ids[n_halo] (device, ascending, = gs_halo_plan) with the owners' blocks; grouped NCCL
+ * point-to-point over NVLink, counts derived from dp on every rank (no count exchange).
+ * halo_cap in blocks (GS_ECAPACITY if smaller, *n_halo_h = needed).  World 1: n_halo = 0.
+ * Virtual contexts (no communicator) fail with GS_EINVAL for world > 1.                  */
+gs_status gs_halo_exchange(gs_ctx* ctx, const float* out_rgb, const gs_camera* cams_h, int n_views,
+                           const int64_t* dp_h, float* halo, int64_t* halo_ids, int64_t halo_cap,
+                           int64_t* n_halo_h, void* stream);
+
+/* gs_loss_ssim -- fused loss forward + backward over the owned blocks (replaces the L1
+ * epilogue of gs_render_fwd: call gs_render_fwd with gt = NULL and out_rgb, then this).
+ * out_rgb [n_owned][3][256], halo/halo_ids/n_halo as gs_halo_exchange left them (device),
+ * gt uint8 [n_views][H][W][3] (value/255), lambda in [0,1].  Writes dL_dpix
+ * [n_owned][3][256] (zero outside the image) and adds the owned pixels' share of the batch
+ * loss to *loss_sum (device double, atomically).  A halo block missing from halo_ids traps
+ * the kernel (contract violation).                                                        */
+gs_status gs_loss_ssim(gs_ctx* ctx, const float* out_rgb, const float* halo, const int64_t* halo_ids,
+                       int64_t n_halo, const uint8_t* gt, const gs_camera* cams_h, int n_views,
+                       const int64_t* dp_h, float lambda, int b_loss, float* dL_dpix, double* loss_sum,
+                       void* stream);
+
 #ifdef __cplusplus
 }
 #endif

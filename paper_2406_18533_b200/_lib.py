@@ -80,6 +80,10 @@ _sig = {
                                C.POINTER(Camera), C.c_int, _P64, _vp]),
     "gs_division_points": (C.c_int, [_P64, _i64, C.c_int, _P64]),
     "gs_exchange_plan": (C.c_int, [_P64, C.c_int, C.c_int, _P64, _P64]),
+    "gs_halo_plan": (C.c_int, [_vp, C.POINTER(Camera), C.c_int, _P64, _P64, _i64, _P64]),
+    "gs_halo_exchange": (C.c_int, [_vp, _vp, C.POINTER(Camera), C.c_int, _P64, _vp, _vp, _i64, _P64, _vp]),
+    "gs_loss_ssim": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, C.POINTER(Camera), C.c_int, _P64, C.c_float,
+                               C.c_int, _vp, _vp, _vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -301,6 +305,47 @@ def render_bwd(ctx, recv_rec, n_recv, sorted_idx, tile_range, cams, dp, bg, dL_d
     st = _lib.gs_render_bwd(ctx.handle, _ptr(recv_rec), int(n_recv), _ptr(sorted_idx), _ptr(tile_range), ca,
                             len(cams), dpp, _bg(bg), _ptr(dL_dpix), _ptr(T_final), _ptr(n_last), _ptr(dL_drec),
                             _ptr(tile_cost), int(cost_mode), _ptr(stats), _stream(stream))
+    ctx.check(st)
+
+
+def halo_plan(ctx, cams, dp):
+    """NEXT-1: the rank's halo block ids (ascending numpy int64)."""
+    ca = cameras(cams)
+    _, dpp = _i64arr(dp)
+    n = C.c_int64(0)
+    st = _lib.gs_halo_plan(ctx.handle, ca, len(cams), dpp, None, 0, C.byref(n))
+    if st == GS_ECAPACITY or (st == GS_OK and n.value > 0):
+        ids = np.zeros(n.value, np.int64)
+        st = _lib.gs_halo_plan(ctx.handle, ca, len(cams), dpp, ids.ctypes.data_as(_P64), n.value, C.byref(n))
+        ctx.check(st)
+        return ids
+    ctx.check(st)
+    return np.zeros(0, np.int64)
+
+
+def halo_exchange(ctx, out_rgb, cams, dp, halo, halo_ids, stream=None):
+    """NEXT-1 (collective): fills halo [cap,3,256] f32 and halo_ids [cap] i64; returns n_halo."""
+    ca = cameras(cams)
+    _, dpp = _i64arr(dp)
+    n = C.c_int64(0)
+    cap = 0 if halo is None else min(halo.shape[0], halo_ids.shape[0])
+    st = _lib.gs_halo_exchange(ctx.handle, _ptr(out_rgb), ca, len(cams), dpp, _ptr(halo), _ptr(halo_ids), int(cap),
+                               C.byref(n), _stream(stream))
+    if st == GS_ECAPACITY:
+        e = CapacityError(st, ctx.last_error())
+        e.needed = int(n.value)
+        raise e
+    ctx.check(st)
+    return int(n.value)
+
+
+def loss_ssim(ctx, out_rgb, halo, halo_ids, n_halo, gt, cams, dp, lam, b_loss, dL_dpix, loss_sum, stream=None):
+    """NEXT-1: fused L1 + D-SSIM forward and backward over the owned blocks."""
+    ca = cameras(cams)
+    _, dpp = _i64arr(dp)
+    st = _lib.gs_loss_ssim(ctx.handle, _ptr(out_rgb), _ptr(halo), _ptr(halo_ids), int(n_halo), _ptr(gt), ca,
+                           len(cams), dpp, C.c_float(lam), int(b_loss), _ptr(dL_dpix), _ptr(loss_sum),
+                           _stream(stream))
     ctx.check(st)
 
 

@@ -261,3 +261,70 @@ extern "C" gs_status gs_rebalance(gs_ctx* c, const int64_t* owned_tile_cost, con
   for (int g = 0; g <= G; g++) dp_next_h[g] = c->pinned[g];
   return GS_OK;
 }
+
+// ------------------------------------------------------------------ NEXT-1 halo exchange
+namespace {
+__global__ void k_pack_blocks(const float* __restrict__ out_rgb, const int64_t* __restrict__ lbs, int64_t n,
+                              float* __restrict__ dst) {
+  const int64_t i = blockIdx.x;
+  if (i >= n) return;
+  const float* s = out_rgb + lbs[i] * 768;
+  float* d = dst + i * 768;
+  for (int t = threadIdx.x; t < 768; t += blockDim.x) d[t] = s[t];
+}
+}  // namespace
+
+// Every rank's halo (gs_halo_blocks of its range) is filled by the blocks' owners: the plan
+// of every peer is recomputed locally from dp (identical on every rank), so no counts are
+// exchanged; blocks travel whole (3 planes x 256 floats) in ascending id order per peer.
+extern "C" gs_status gs_halo_exchange(gs_ctx* c, const float* out_rgb, const gs_camera* cams_h, int n_views,
+                                      const int64_t* dp_h, float* halo, int64_t* halo_ids, int64_t halo_cap,
+                                      int64_t* n_halo_h, void* stream) {
+  if (!c) return GS_EINVAL;
+  gs_status s = gs_check_batch(c, cams_h, n_views, dp_h);
+  if (s != GS_OK) return s;
+  GS_REQUIRE(c, n_halo_h != nullptr, "null n_halo_h");
+  cudaStream_t st = (cudaStream_t)stream;
+  const gs_geom geo = gs_make_geom(&cams_h[0]);
+  const int G = c->world, r = c->rank;
+  const int64_t lo = dp_h[r], hi = dp_h[r + 1];
+  std::vector<int64_t> need;
+  gs_halo_blocks(geo, lo, hi, need);
+  *n_halo_h = (int64_t)need.size();
+  if ((int64_t)need.size() > halo_cap)
+    return gs_fail(c, GS_ECAPACITY, "halo capacity %lld < %lld", (long long)halo_cap, (long long)need.size());
+  if (G == 1) return GS_OK;  // a single rank owns every block: no halo
+  GS_REQUIRE(c, need.empty() || (halo && halo_ids), "null halo buffers");
+  // receive side: need is ascending, owners are ascending ranges -> contiguous per peer
+  std::vector<int64_t> rcnt(G, 0), roff(G, 0), scnt(G, 0), soff(G, 0), send_lb;
+  for (int64_t b : need) {
+    int g = 0;
+    while (!(b >= dp_h[g] && b < dp_h[g + 1])) g++;
+    rcnt[g]++;
+  }
+  for (int g = 1; g < G; g++) roff[g] = roff[g - 1] + rcnt[g - 1];
+  // send side: the owned blocks in each peer's halo
+  std::vector<int64_t> peer;
+  for (int g = 0; g < G; g++) {
+    soff[g] = (int64_t)send_lb.size();
+    if (g == r) continue;
+    gs_halo_blocks(geo, dp_h[g], dp_h[g + 1], peer);
+    for (int64_t b : peer)
+      if (b >= lo && b < hi) send_lb.push_back(b - lo);
+    scnt[g] = (int64_t)send_lb.size() - soff[g];
+  }
+  if (!need.empty())
+    GS_CUDA(c, cudaMemcpyAsync(halo_ids, need.data(), need.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  float* sbuf = nullptr;
+  if (!send_lb.empty()) {
+    int64_t* idx = (int64_t*)gs_slot_get(c, SLOT_HALO_IDX, send_lb.size() * sizeof(int64_t), st);
+    sbuf = (float*)gs_slot_get(c, SLOT_HALO_SEND, send_lb.size() * 768 * sizeof(float), st);
+    if (!idx || !sbuf) return gs_fail(c, GS_ECUDA, "halo scratch");
+    GS_CUDA(c, cudaMemcpyAsync(idx, send_lb.data(), send_lb.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    ++c->launches;
+    k_pack_blocks<<<(unsigned)send_lb.size(), 256, 0, st>>>(out_rgb, idx, (int64_t)send_lb.size(), sbuf);
+    GS_LAUNCH_CHECK(c, "halo pack");
+  }  // (pageable host sources: cudaMemcpyAsync has staged them before returning)
+  return p2p_exchange(c, (const char*)sbuf, soff.data(), scnt.data(), (char*)halo, roff.data(), rcnt.data(),
+                      768 * sizeof(float), st);
+}

@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "../../include/gs.h"
 
@@ -37,6 +38,8 @@ enum {
   SLOT_RECTILES,      // bin_sort per-record tile counts -> pair starts
   SLOT_RADIX_HIST,    // bin_sort radix per-tile digit histograms -> offsets
   SLOT_PSTART,        // bin_sort pair starts in depth order
+  SLOT_HALO_SEND,     // halo exchange: packed blocks to send
+  SLOT_HALO_IDX,      // halo exchange: owned-block indices to pack
   SLOT_N
 };
 
@@ -100,6 +103,10 @@ inline gs_geom gs_make_geom(const gs_camera* c) {
   g.per_view = (long long)g.Wt * g.Ht;
   return g;
 }
+
+// NEXT-1 halo of the owned block range [lo, hi): the not-owned 8-neighbours (same view,
+// inside the grid) of owned blocks, ascending (gs_loss.cu).
+void gs_halo_blocks(const gs_geom& geo, int64_t lo, int64_t hi, std::vector<int64_t>& out);
 inline gs_dp_arg gs_make_dp(const gs_ctx* c, const int64_t* dp_h) {
   gs_dp_arg d;
   d.G = c->world;

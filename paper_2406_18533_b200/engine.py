@@ -41,7 +41,7 @@ class _Buf:
 class GrendelTrainer:
     def __init__(self, ctx: L.Context, params: L.GaussianParams, width: int, height: int, n_views: int,
                  n_images: int, lr=DEFAULT_LR, cost_mode=L.COST_MEASURED, bg=(0.0, 0.0, 0.0),
-                 rebalance=True, dp=None, device=None, split_adam=True):
+                 rebalance=True, dp=None, device=None, split_adam=True, loss="l1", ssim_lambda=0.2):
         self.ctx, self.p = ctx, params
         self.device = device or params.pos_op.device
         self.W, self.H, self.b = width, height, n_views
@@ -49,6 +49,9 @@ class GrendelTrainer:
         self.B = n_views * self.Wt * self.Ht
         self.G, self.rank = ctx.world, ctx.rank
         self.lr, self.cost_mode, self.bg, self.do_rebalance = tuple(lr), cost_mode, tuple(bg), rebalance
+        if loss not in ("l1", "ssim"):
+            raise ValueError("loss must be 'l1' or 'ssim' (L1 + D-SSIM, NEXT-1)")
+        self.loss_kind, self.ssim_lambda = loss, float(ssim_lambda)
         self.m, self.v = params.zeros_like(), params.zeros_like()
         # parameter-gradient buffer: gs_adam_step then runs backward and Adam as two passes
         # (faster than the fused single kernel on B200)
@@ -66,6 +69,9 @@ class GrendelTrainer:
         self.T = _Buf(dev, torch.float32, (256,))
         self.nl = _Buf(dev, torch.int32, (256,))
         self.dpix = _Buf(dev, torch.float32, (3, 256))
+        self.rgb = _Buf(dev, torch.float32, (3, 256))      # rendered owned blocks (D-SSIM loss)
+        self.halo = _Buf(dev, torch.float32, (3, 256))     # other ranks' blocks within 10 px
+        self.halo_ids = _Buf(dev, torch.int64)
         self.cost = _Buf(dev, torch.int64)
         self.drec = _Buf(dev, torch.float32, (L.GRAD_FLOATS,))
         self.dsend = _Buf(dev, torch.float32, (L.GRAD_FLOATS,))
@@ -100,6 +106,8 @@ class GrendelTrainer:
                         self.sorted.ensure(e.needed)
         no = self.B  # a rank may own up to every block after rebalancing
         self.T.ensure(no), self.nl.ensure(no), self.dpix.ensure(no), self.cost.ensure(no), self.range.ensure(no + 1)
+        if self.loss_kind == "ssim":
+            self.rgb.ensure(no)
         self.dp = saved
         torch.cuda.synchronize()
 
@@ -167,9 +175,27 @@ class GrendelTrainer:
             self.stats.zero_()
             stats = self.stats
         rec("render_fwd", 0)
-        L.render_fwd(ctx, recv_t, self.sorted.t, self.range.t, cams, dp, self.bg, gt, self.b, None, self.T.t,
-                     self.nl.t, self.dpix.t, self.loss, self.cost.t, self.cost_mode, stats, st)
+        if self.loss_kind == "l1":  # L1 fused into the forward's epilogue (O13)
+            L.render_fwd(ctx, recv_t, self.sorted.t, self.range.t, cams, dp, self.bg, gt, self.b, None, self.T.t,
+                         self.nl.t, self.dpix.t, self.loss, self.cost.t, self.cost_mode, stats, st)
+        else:
+            self.rgb.ensure(no)
+            L.render_fwd(ctx, recv_t, self.sorted.t, self.range.t, cams, dp, self.bg, None, self.b, self.rgb.t,
+                         self.T.t, self.nl.t, None, None, self.cost.t, self.cost_mode, stats, st)
         rec("render_fwd", 1)
+        if self.loss_kind == "ssim":  # NEXT-1: halo exchange + fused L1 + D-SSIM
+            rec("loss", 0)
+            n_halo = 0
+            if self.G > 1:
+                while True:
+                    try:
+                        n_halo = L.halo_exchange(ctx, self.rgb.t, cams, dp, self.halo.t, self.halo_ids.t, st)
+                        break
+                    except L.CapacityError as e:
+                        self.halo.ensure(e.needed), self.halo_ids.ensure(e.needed)
+            L.loss_ssim(ctx, self.rgb.t, self.halo.t, self.halo_ids.t, n_halo, gt, cams, dp, self.ssim_lambda,
+                        self.b, self.dpix.t, self.loss, st)
+            rec("loss", 1)
         # A5 render backward
         rec("render_bwd", 0)
         L.render_bwd(ctx, recv_t, n_recv, self.sorted.t, self.range.t, cams, dp, self.bg, self.dpix.t, self.T.t,
@@ -200,13 +226,19 @@ class GrendelTrainer:
         return self.loss
 
 
-def make_events(names=("project", "exchange", "bin_sort", "render_fwd", "render_bwd", "exchange_grads", "adam",
-                       "rebalance")):
+def make_events(names=("project", "exchange", "bin_sort", "render_fwd", "loss", "render_bwd", "exchange_grads",
+                       "adam", "rebalance")):
     return {n: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for n in names}
 
 
 def event_ms(events):
-    return {n: s.elapsed_time(e) for n, (s, e) in events.items()}
+    out = {}
+    for n, (s, e) in events.items():
+        try:
+            out[n] = s.elapsed_time(e)
+        except RuntimeError:  # not recorded in this step (e.g. "loss" with the fused L1)
+            pass
+    return out
 
 
 def position_lr(step, lr_init=1.6e-4, lr_final=1.6e-6, max_steps=30000, extent=1.0):
