@@ -45,6 +45,10 @@ METRIC = "train views/sec at 1/2/4/8 B200 (Rubble-shaped 4K); fwd+bwd raster ms/
 
 # Roofline census (frozen): FP32-pipe lane-operations per evaluation.
 CENSUS = dict(fwd_comp=13, fwd_skip=8, fwd_stop=9, bwd_contrib=41, bwd_skip=8)
+# NEXT-1 D-SSIM census: lane-ops per pixel and channel of the separable
+# evaluation without halo recomputation -- window sums of 5 products 11 taps each way
+# (88 + 55), SSIM terms (30), 3 derivative maps filtered both ways (33 + 33), combination (10).
+SSIM_OPS_PER_PIXEL = 3 * (88 + 55 + 30 + 33 + 33 + 10)
 
 
 def make_scene(cfg, lo, hi):
@@ -227,6 +231,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--breakdown-steps", type=int, default=2)
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--loss", default="l1", choices=["l1", "ssim"],
+                    help="l1: the hot-path loss (R11); ssim: L1 + D-SSIM, lambda 0.2 (NEXT-1)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     args.warmup = max(args.warmup, 3)
@@ -269,7 +275,7 @@ def main():
     gt_batch = torch.empty((cfg["b"], H, W, 3), dtype=torch.uint8, device=dev)
     cost_mode = {"measured": L.COST_MEASURED, "work": L.COST_WORK, "paper_avg": L.COST_PAPER_AVG}[args.cost_mode]
     tr = GrendelTrainer(ctx, p, W, H, cfg["b"], len(cams), cost_mode=cost_mode, rebalance=not args.no_rebalance,
-                        device=dev)
+                        device=dev, loss=args.loss)
     stream = torch.cuda.current_stream()
     k_sched = [0]
 
@@ -319,7 +325,7 @@ def main():
     # ---------------- per-call breakdown + work counters (untimed pass)
     calls = {}
     stats = np.zeros(8, np.int64)
-    counts = dict(n_send=0, n_recv=0, n_pairs=0)
+    counts = dict(n_send=0, n_recv=0, n_pairs=0, n_owned=0)
     for _ in range(args.breakdown_steps):
         ev = make_events()
         one_step(events=ev, stats=True)
@@ -390,6 +396,7 @@ def main():
         "project": ("hbm", (236.0 * p.n + 48.0 * counts["n_send"]) / 1e9, "GB/s", float(pk.get("hbm_gbs", 6650.0))),
         "bin_sort": ("hbm", (28.0 * counts["n_pairs"] + 16.0 * counts["n_recv"]) / 1e9, "GB/s",
                      float(pk.get("hbm_gbs", 6650.0))),
+        "loss": ("alu", SSIM_OPS_PER_PIXEL * 256.0 * counts["n_owned"] / 1e12, "T FP32-lane-op/s", fp32_peak),
     }
     dom = max((k for k in work if k in calls), key=lambda k: calls[k])
     bound, amount, unit, peak = work[dom]
@@ -430,6 +437,7 @@ def main():
                            "image": [W, H], "gaussians": n, "parallelism": "gaussian+pixel x%d (Grendel)" % world,
                            "l2_policy": "inputs larger than L2 (params+Adam state %.1f GB, GT %.2f GB/step)" % (
                                3 * 240 * n / 1e9, cfg["b"] * W * H * 3 / 1e9),
+                           "loss": "l1" if args.loss == "l1" else "l1+dssim(0.2)",
                            "cost_mode": args.cost_mode, "rebalance": not args.no_rebalance,
                            "shard_layout": "random" if args.no_morton else "morton"},
                 "raster_ms_per_view": round(raster_ms_view, 3),

@@ -258,26 +258,34 @@ gs_status gs_exchange_plan(const int64_t* counts_h, int G, int rank, int64_t* se
 gs_status gs_halo_plan(gs_ctx* ctx, const gs_camera* cams_h, int n_views, const int64_t* dp_h,
                        int64_t* halo_ids_h, int64_t cap, int64_t* n_halo_h);
 
-/* gs_halo_exchange -- COLLECTIVE (every rank, same order).  out_rgb: the rank's rendered
- * owned blocks [n_owned][3][256] (gs_render_fwd out_rgb).  Writes halo[n_halo][3][256] and
- * halo_ids[n_halo] (device, ascending, = gs_halo_plan) with the owners' blocks; grouped NCCL
- * point-to-point over NVLink, counts derived from dp on every rank (no count exchange).
- * halo_cap in blocks (GS_ECAPACITY if smaller, *n_halo_h = needed).  World 1: n_halo = 0.
- * Virtual contexts (no communicator) fail with GS_EINVAL for world > 1.                  */
-gs_status gs_halo_exchange(gs_ctx* ctx, const float* out_rgb, const gs_camera* cams_h, int n_views,
+/* gs_halo_exchange -- COLLECTIVE (every rank, same order).  data: a per-owned-block array
+ * [n_owned][fpb] floats (the rendered blocks, fpb = 768, or the SSIM maps, fpb = 2304).
+ * Writes halo[n_halo][fpb] and halo_ids[n_halo] (device, ascending, = gs_halo_plan) with the
+ * owners' blocks; grouped NCCL point-to-point over NVLink, counts derived from dp on every
+ * rank (no count exchange).  halo_cap in blocks (GS_ECAPACITY if smaller, *n_halo_h =
+ * needed).  World 1: n_halo = 0.  Virtual contexts (no communicator) fail with GS_EINVAL
+ * for world > 1 (tests fill the halo themselves from gs_halo_plan).                     */
+gs_status gs_halo_exchange(gs_ctx* ctx, const float* data, int fpb, const gs_camera* cams_h, int n_views,
                            const int64_t* dp_h, float* halo, int64_t* halo_ids, int64_t halo_cap,
                            int64_t* n_halo_h, void* stream);
 
-/* gs_loss_ssim -- fused loss forward + backward over the owned blocks (replaces the L1
- * epilogue of gs_render_fwd: call gs_render_fwd with gt = NULL and out_rgb, then this).
- * out_rgb [n_owned][3][256], halo/halo_ids/n_halo as gs_halo_exchange left them (device),
- * gt uint8 [n_views][H][W][3] (value/255), lambda in [0,1].  Writes dL_dpix
- * [n_owned][3][256] (zero outside the image) and adds the owned pixels' share of the batch
- * loss to *loss_sum (device double, atomically).  A halo block missing from halo_ids traps
- * the kernel (contract violation).                                                        */
-gs_status gs_loss_ssim(gs_ctx* ctx, const float* out_rgb, const float* halo, const int64_t* halo_ids,
-                       int64_t n_halo, const uint8_t* gt, const gs_camera* cams_h, int n_views,
-                       const int64_t* dp_h, float lambda, int b_loss, float* dL_dpix, double* loss_sum,
+/* The loss replaces the L1 epilogue of gs_render_fwd (call it with gt = NULL and out_rgb):
+ *   gs_ssim_terms -> [gs_halo_exchange of maps, world > 1] -> gs_ssim_grad.
+ * gs_ssim_terms: out_rgb [n_owned][3][256] with its halo (halo_rgb [n_halo][3][256],
+ * halo_ids device ascending = gs_halo_plan), gt uint8 [n_views][H][W][3] (value/255),
+ * lambda in [0,1].  Writes maps[n_owned][3][3][256] (dS/dmu_x, dS/dE[x^2], dS/dE[xy] per
+ * channel at each pixel, zero outside the image) and adds the owned pixels' share of the
+ * batch loss sum_v L_v / b_loss to *loss_sum (device double, atomically).
+ * gs_ssim_grad: maps with their halo (halo_maps [n_halo][2304]), the same out_rgb and gt;
+ * writes dL_dpix[n_owned][3][256] (zero outside the image).  A halo block missing from
+ * halo_ids traps the kernel (contract violation).                                       */
+gs_status gs_ssim_terms(gs_ctx* ctx, const float* out_rgb, const float* halo_rgb, const int64_t* halo_ids,
+                        int64_t n_halo, const uint8_t* gt, const gs_camera* cams_h, int n_views,
+                        const int64_t* dp_h, float lambda, int b_loss, float* maps, double* loss_sum,
+                        void* stream);
+gs_status gs_ssim_grad(gs_ctx* ctx, const float* maps, const float* halo_maps, const int64_t* halo_ids,
+                       int64_t n_halo, const float* out_rgb, const uint8_t* gt, const gs_camera* cams_h,
+                       int n_views, const int64_t* dp_h, float lambda, int b_loss, float* dL_dpix,
                        void* stream);
 
 #ifdef __cplusplus

@@ -81,9 +81,12 @@ _sig = {
     "gs_division_points": (C.c_int, [_P64, _i64, C.c_int, _P64]),
     "gs_exchange_plan": (C.c_int, [_P64, C.c_int, C.c_int, _P64, _P64]),
     "gs_halo_plan": (C.c_int, [_vp, C.POINTER(Camera), C.c_int, _P64, _P64, _i64, _P64]),
-    "gs_halo_exchange": (C.c_int, [_vp, _vp, C.POINTER(Camera), C.c_int, _P64, _vp, _vp, _i64, _P64, _vp]),
-    "gs_loss_ssim": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, C.POINTER(Camera), C.c_int, _P64, C.c_float,
-                               C.c_int, _vp, _vp, _vp]),
+    "gs_halo_exchange": (C.c_int, [_vp, _vp, C.c_int, C.POINTER(Camera), C.c_int, _P64, _vp, _vp, _i64, _P64,
+                                   _vp]),
+    "gs_ssim_terms": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, C.POINTER(Camera), C.c_int, _P64, C.c_float,
+                                C.c_int, _vp, _vp, _vp]),
+    "gs_ssim_grad": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp, C.POINTER(Camera), C.c_int, _P64, C.c_float,
+                               C.c_int, _vp, _vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -323,14 +326,15 @@ def halo_plan(ctx, cams, dp):
     return np.zeros(0, np.int64)
 
 
-def halo_exchange(ctx, out_rgb, cams, dp, halo, halo_ids, stream=None):
-    """NEXT-1 (collective): fills halo [cap,3,256] f32 and halo_ids [cap] i64; returns n_halo."""
+def halo_exchange(ctx, data, cams, dp, halo, halo_ids, stream=None):
+    """NEXT-1 (collective): data [n_owned, fpb] f32 -> halo [cap, fpb], halo_ids [cap]; returns n_halo."""
     ca = cameras(cams)
     _, dpp = _i64arr(dp)
     n = C.c_int64(0)
+    fpb = int(data[0].numel()) if data is not None and data.shape[0] else int(np.prod(halo.shape[1:]))
     cap = 0 if halo is None else min(halo.shape[0], halo_ids.shape[0])
-    st = _lib.gs_halo_exchange(ctx.handle, _ptr(out_rgb), ca, len(cams), dpp, _ptr(halo), _ptr(halo_ids), int(cap),
-                               C.byref(n), _stream(stream))
+    st = _lib.gs_halo_exchange(ctx.handle, _ptr(data), fpb, ca, len(cams), dpp, _ptr(halo), _ptr(halo_ids),
+                               int(cap), C.byref(n), _stream(stream))
     if st == GS_ECAPACITY:
         e = CapacityError(st, ctx.last_error())
         e.needed = int(n.value)
@@ -339,13 +343,22 @@ def halo_exchange(ctx, out_rgb, cams, dp, halo, halo_ids, stream=None):
     return int(n.value)
 
 
-def loss_ssim(ctx, out_rgb, halo, halo_ids, n_halo, gt, cams, dp, lam, b_loss, dL_dpix, loss_sum, stream=None):
-    """NEXT-1: fused L1 + D-SSIM forward and backward over the owned blocks."""
+def ssim_terms(ctx, out_rgb, halo_rgb, halo_ids, n_halo, gt, cams, dp, lam, b_loss, maps, loss_sum, stream=None):
+    """NEXT-1 pass 1: SSIM statistics, loss share, derivative maps [n_owned, 3, 3, 256]."""
     ca = cameras(cams)
     _, dpp = _i64arr(dp)
-    st = _lib.gs_loss_ssim(ctx.handle, _ptr(out_rgb), _ptr(halo), _ptr(halo_ids), int(n_halo), _ptr(gt), ca,
-                           len(cams), dpp, C.c_float(lam), int(b_loss), _ptr(dL_dpix), _ptr(loss_sum),
-                           _stream(stream))
+    st = _lib.gs_ssim_terms(ctx.handle, _ptr(out_rgb), _ptr(halo_rgb), _ptr(halo_ids), int(n_halo), _ptr(gt), ca,
+                            len(cams), dpp, C.c_float(lam), int(b_loss), _ptr(maps), _ptr(loss_sum),
+                            _stream(stream))
+    ctx.check(st)
+
+
+def ssim_grad(ctx, maps, halo_maps, halo_ids, n_halo, out_rgb, gt, cams, dp, lam, b_loss, dL_dpix, stream=None):
+    """NEXT-1 pass 2: dL/dpix of L1 + D-SSIM over the owned blocks."""
+    ca = cameras(cams)
+    _, dpp = _i64arr(dp)
+    st = _lib.gs_ssim_grad(ctx.handle, _ptr(maps), _ptr(halo_maps), _ptr(halo_ids), int(n_halo), _ptr(out_rgb),
+                           _ptr(gt), ca, len(cams), dpp, C.c_float(lam), int(b_loss), _ptr(dL_dpix), _stream(stream))
     ctx.check(st)
 
 

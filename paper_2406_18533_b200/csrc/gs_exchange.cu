@@ -264,26 +264,27 @@ extern "C" gs_status gs_rebalance(gs_ctx* c, const int64_t* owned_tile_cost, con
 
 // ------------------------------------------------------------------ NEXT-1 halo exchange
 namespace {
-__global__ void k_pack_blocks(const float* __restrict__ out_rgb, const int64_t* __restrict__ lbs, int64_t n,
+__global__ void k_pack_blocks(const float* __restrict__ src, const int64_t* __restrict__ lbs, int64_t n, int fpb,
                               float* __restrict__ dst) {
   const int64_t i = blockIdx.x;
   if (i >= n) return;
-  const float* s = out_rgb + lbs[i] * 768;
-  float* d = dst + i * 768;
-  for (int t = threadIdx.x; t < 768; t += blockDim.x) d[t] = s[t];
+  const float* s = src + lbs[i] * fpb;
+  float* d = dst + i * fpb;
+  for (int t = threadIdx.x; t < fpb; t += blockDim.x) d[t] = s[t];
 }
 }  // namespace
 
 // Every rank's halo (gs_halo_blocks of its range) is filled by the blocks' owners: the plan
 // of every peer is recomputed locally from dp (identical on every rank), so no counts are
-// exchanged; blocks travel whole (3 planes x 256 floats) in ascending id order per peer.
-extern "C" gs_status gs_halo_exchange(gs_ctx* c, const float* out_rgb, const gs_camera* cams_h, int n_views,
+// exchanged; blocks travel whole (fpb floats each) in ascending id order per peer.
+extern "C" gs_status gs_halo_exchange(gs_ctx* c, const float* data, int fpb, const gs_camera* cams_h, int n_views,
                                       const int64_t* dp_h, float* halo, int64_t* halo_ids, int64_t halo_cap,
                                       int64_t* n_halo_h, void* stream) {
   if (!c) return GS_EINVAL;
   gs_status s = gs_check_batch(c, cams_h, n_views, dp_h);
   if (s != GS_OK) return s;
   GS_REQUIRE(c, n_halo_h != nullptr, "null n_halo_h");
+  GS_REQUIRE(c, fpb > 0, "floats per block must be > 0");
   cudaStream_t st = (cudaStream_t)stream;
   const gs_geom geo = gs_make_geom(&cams_h[0]);
   const int G = c->world, r = c->rank;
@@ -318,13 +319,13 @@ extern "C" gs_status gs_halo_exchange(gs_ctx* c, const float* out_rgb, const gs_
   float* sbuf = nullptr;
   if (!send_lb.empty()) {
     int64_t* idx = (int64_t*)gs_slot_get(c, SLOT_HALO_IDX, send_lb.size() * sizeof(int64_t), st);
-    sbuf = (float*)gs_slot_get(c, SLOT_HALO_SEND, send_lb.size() * 768 * sizeof(float), st);
+    sbuf = (float*)gs_slot_get(c, SLOT_HALO_SEND, send_lb.size() * fpb * sizeof(float), st);
     if (!idx || !sbuf) return gs_fail(c, GS_ECUDA, "halo scratch");
     GS_CUDA(c, cudaMemcpyAsync(idx, send_lb.data(), send_lb.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
     ++c->launches;
-    k_pack_blocks<<<(unsigned)send_lb.size(), 256, 0, st>>>(out_rgb, idx, (int64_t)send_lb.size(), sbuf);
+    k_pack_blocks<<<(unsigned)send_lb.size(), 256, 0, st>>>(data, idx, (int64_t)send_lb.size(), fpb, sbuf);
     GS_LAUNCH_CHECK(c, "halo pack");
   }  // (pageable host sources: cudaMemcpyAsync has staged them before returning)
   return p2p_exchange(c, (const char*)sbuf, soff.data(), scnt.data(), (char*)halo, roff.data(), rcnt.data(),
-                      768 * sizeof(float), st);
+                      (size_t)fpb * sizeof(float), st);
 }

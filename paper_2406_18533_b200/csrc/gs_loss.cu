@@ -6,19 +6,22 @@
 //   window (sigma 1.5), C1 = 0.01^2, C2 = 0.03^2, zero padding outside the image (R12),
 // means over every pixel and channel of the view, the batch loss divided by b (like O13).
 //
-// One CTA (256 threads) per owned block.  The gradient at a pixel needs the SSIM map's
-// derivatives at every centre within 5 pixels, and each of those needs the image within 5
-// pixels of it, so the CTA stages the 36x36 neighbourhood (10-pixel halo) of the block: from
-// the rank's own rendered blocks, from the halo buffer filled by gs_halo_exchange (blocks of
-// the same view owned by other ranks), or zero outside the image.  Per channel, in shared
-// memory:
-//   1. separable window sums of (x, y, x^2, y^2, xy) at the 26x26 centres around the block,
-//   2. S and its derivatives a = dS/dmu_x, b = dS/dE[x^2], c = dS/dE[xy] there (zero at
-//      centres outside the image),
-//   3. dSSIM_sum/dx = (w*a) + 2 x (w*b) + y (w*c) at the 16x16 pixels (separable again),
-// fused with the L1 sign term into dL/dpix, and the block's share of L into *loss_sum.
-// Every FP32 operation is on the CUDA cores: the window sums are 11-tap stencils over a few
-// thousand values per block (no contraction shape worth a tensor-core tile), and the
+// With mu_x, E[x^2], E[xy] the window statistics of x at a centre p, the SSIM map S(p) has
+// derivatives a = dS/dmu_x, b = dS/dE[x^2], c = dS/dE[xy], and
+//   d(sum_p S)/dx(q) = (w * a)(q) + 2 x(q) (w * b)(q) + y(q) (w * c)(q)        (w symmetric).
+// Two kernels, one CTA (256 threads) per owned block each:
+//   k_ssim_terms: stage x, y over the block + 5-pixel halo (26x26), separable window sums of
+//     (x, y, x^2, y^2, xy) at the block's 16x16 centres, S -> the block's loss share, and the
+//     9 maps (a, b, c per channel) -> HBM;
+//   k_ssim_grad: stage the maps over the block + 5-pixel halo, separable window sums of the
+//     maps, combine with x, y and the L1 sign into dL/dpix.
+// Between them a halo of maps is needed from neighbouring blocks (other ranks' ones through
+// gs_halo_exchange), so each statistic is computed once per pixel instead of once per pixel
+// per neighbouring block.  Both separable passes are register-blocked: a thread produces 4
+// consecutive outputs of a row (column) from 14 staged inputs held in registers, so shared
+// memory traffic is ~14 loads per 4 outputs instead of 11 per output; rows are padded to an
+// odd stride (no bank conflicts).  All arithmetic is FP32 on the CUDA cores: 11-tap stencils
+// over a few thousand values per block have no tensor-core-sized contraction, and the
 // variance E[x^2] - mu^2 needs fp32 mantissas.
 #include <algorithm>
 #include <cmath>
@@ -31,175 +34,171 @@ using namespace gsd;
 
 namespace {
 
-constexpr int kR = 36;   // staged region (block + 10-pixel halo)
-constexpr int kC = 26;   // centres whose SSIM terms the block's gradient needs (block + 5)
 constexpr int kThreads = 256;
+constexpr int kS = 26;        // staged side: block + 5-pixel halo each way
+constexpr int kLd = 27;       // odd row stride of staged tiles
+constexpr int kLdO = 17;      // odd row stride of 16-wide outputs
 
 struct ssim_arg {
   float g[11];  // normalised 1D Gaussian, sigma 1.5 (the 2D window is g x g)
   float lambda, norm;
 };
 
-// Dynamic shared memory layout (floats).
-constexpr int kXY = 3 * kR * kR;      // X or Y, 3 channels
-constexpr int kHS = 5 * kR * kC;      // horizontal sums of the 5 products, one channel
-constexpr int kM = 3 * kC * kC;       // a, b, c maps, one channel
-constexpr int kHB = 3 * kC * 16;      // horizontal sums of the maps, one channel
-constexpr size_t kSmem = (size_t)(2 * kXY + kHS + kM + kHB) * sizeof(float);
+// The 3x3 neighbourhood of blocks around block (tx, ty) of view v: planes of `fpb` floats
+// (the rank's own blocks, or halo slots found in the ascending halo id list), null outside
+// the grid.  Threads 0..8 fill s_src.
+__device__ __forceinline__ void neighbour_sources(const float* base, const float* halo, const int64_t* halo_ids,
+                                                  int64_t n_halo, const gs_geom& geo, int64_t B_lo, int64_t B_hi,
+                                                  int64_t v, int tx, int ty, int fpb, const float** s_src) {
+  const int t = threadIdx.x;
+  if (t >= 9) return;
+  const int bx = tx + t % 3 - 1, by = ty + t / 3 - 1;
+  const float* src = nullptr;
+  if (bx >= 0 && bx < geo.Wt && by >= 0 && by < geo.Ht) {
+    const int64_t nb = v * geo.per_view + (int64_t)by * geo.Wt + bx;
+    if (nb >= B_lo && nb < B_hi) {
+      src = base + (nb - B_lo) * fpb;
+    } else {
+      int64_t lo = 0, hi = n_halo;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (halo_ids[mid] < nb) lo = mid + 1; else hi = mid;
+      }
+      if (lo < n_halo && halo_ids[lo] == nb) src = halo + lo * fpb;
+      else __trap();  // halo not supplied: a contract violation, never a silent zero
+    }
+  }
+  s_src[t] = src;
+}
 
-__global__ void __launch_bounds__(kThreads) k_loss_ssim(
+// Which of the 3x3 neighbour blocks holds staged coordinate i (0..25, block starts at 5).
+__device__ __forceinline__ int nb_of(int i) { return i < 5 ? 0 : (i < 21 ? 1 : 2); }
+
+// Stage `np` planes (256 floats each, plane stride 256 within a block's record of fpb floats)
+// of the 26x26 neighbourhood into dst[plane][26][kLd] with 16-byte loads: the neighbourhood's
+// row r spans columns 11..36 of the three blocks side by side (48 columns = 12 float4), of
+// which float4s 2..9 overlap it.  Zero where there is no block (outside the grid).
+__device__ __forceinline__ void stage_planes(const float* const* s_src, int np, int plane0, float* dst) {
+  for (int it = threadIdx.x; it < np * kS * 8; it += kThreads) {
+    const int pl = it / (kS * 8), r = (it / 8) % kS, f = 2 + it % 8;
+    const int br = nb_of(r), bc = f >> 2, row = (r + 11) & 15;  // source block row/col, row in block
+    const float* src = s_src[br * 3 + bc];
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (src) q = __ldg(reinterpret_cast<const float4*>(src + (plane0 + pl) * 256 + row * 16 + (f & 3) * 4));
+    const float e[4] = {q.x, q.y, q.z, q.w};
+    float* d = dst + (pl * kS + r) * kLd;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int col = f * 4 + k - 11;
+      if (col >= 0 && col < kS) d[col] = e[k];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_ssim_terms(
     const float* __restrict__ out_rgb, const float* __restrict__ halo, const int64_t* __restrict__ halo_ids,
     int64_t n_halo, const uint8_t* __restrict__ gt, gs_geom geo, int64_t B_lo, int64_t B_hi, ssim_arg h,
-    float* __restrict__ dL_dpix, double* __restrict__ loss_sum) {
-  extern __shared__ float sm[];
-  float* X = sm;             // [3][36][36]
-  float* Y = X + kXY;        // [3][36][36]
-  float* HS = Y + kXY;       // [5][36][26]
-  float* M = HS + kHS;       // [3][26][26]
-  float* HB = M + kM;        // [3][26][16]
-  __shared__ const float* s_src[9];  // 3x3 neighbourhood of blocks: [3][256] planes or null
+    float* __restrict__ maps, double* __restrict__ loss_sum) {
+  __shared__ float X[3][kS][kLd], Y[3][kS][kLd];
+  __shared__ float HS[3][5][kS][kLdO];  // horizontal sums at the 16 own columns
+  __shared__ const float* s_src[9];
   __shared__ double s_red[kThreads / 32];
   const int tid = threadIdx.x;
   const int64_t lb = blockIdx.x, beta = B_lo + lb;
   const int64_t v = beta / geo.per_view, loc = beta % geo.per_view;
   const int tx = (int)(loc % geo.Wt), ty = (int)(loc / geo.Wt);
-  if (tid < 9) {
-    const int bx = tx + tid % 3 - 1, by = ty + tid / 3 - 1;
-    const float* src = nullptr;
-    if (bx >= 0 && bx < geo.Wt && by >= 0 && by < geo.Ht) {
-      const int64_t nb = v * geo.per_view + (int64_t)by * geo.Wt + bx;
-      if (nb >= B_lo && nb < B_hi) {
-        src = out_rgb + (nb - B_lo) * 768;
-      } else {  // another rank's block: its slot in the (ascending) halo id list
-        int64_t lo = 0, hi = n_halo;
-        while (lo < hi) {
-          const int64_t mid = (lo + hi) >> 1;
-          if (halo_ids[mid] < nb) lo = mid + 1; else hi = mid;
-        }
-        if (lo < n_halo && halo_ids[lo] == nb) src = halo + lo * 768;
-        else __trap();  // halo not supplied: a contract violation, never a silent zero
-      }
-    }
-    s_src[tid] = src;
-  }
+  neighbour_sources(out_rgb, halo, halo_ids, n_halo, geo, B_lo, B_hi, v, tx, ty, 768, s_src);
   __syncthreads();
-  // stage x (rendered) and y (ground truth) over the 36x36 region, zero outside the image
-  const int gx0 = tx * 16 - 10, gy0 = ty * 16 - 10;
-  for (int t = tid; t < kR * kR; t += kThreads) {
-    const int i = t / kR, j = t % kR;
-    const int gy = gy0 + i, gx = gx0 + j;
-    float x[3] = {0.f, 0.f, 0.f}, y[3] = {0.f, 0.f, 0.f};
+  // x: rendered planes (zero outside the grid; partial blocks hold zeros outside the image,
+  // see gs_render_fwd's out_rgb); y: ground truth, zero outside the image
+  stage_planes(s_src, 3, 0, &X[0][0][0]);
+  for (int t = tid; t < kS * kS; t += kThreads) {
+    const int i = t / kS, j = t % kS;
+    const int gy = ty * 16 - 5 + i, gx = tx * 16 - 5 + j;
+    float y[3] = {0.f, 0.f, 0.f};
     if (gx >= 0 && gx < geo.W && gy >= 0 && gy < geo.H) {
-      const int nbi = (i < 10 ? 0 : (i < 26 ? 1 : 2)) * 3 + (j < 10 ? 0 : (j < 26 ? 1 : 2));
-      const float* src = s_src[nbi];
-      const int p = (gy & 15) * 16 + (gx & 15);
       const uint8_t* g = gt + ((v * geo.H + gy) * (int64_t)geo.W + gx) * 3;
 #pragma unroll
-      for (int c = 0; c < 3; c++) {
-        x[c] = src[c * 256 + p];
-        y[c] = (float)g[c] * (1.0f / 255.0f);
+      for (int c = 0; c < 3; c++) y[c] = (float)g[c] * (1.0f / 255.0f);
+    }
+#pragma unroll
+    for (int c = 0; c < 3; c++) Y[c][i][j] = y[c];
+  }
+  __syncthreads();
+  // horizontal: item = (channel, row r, 4 output columns 4s..4s+3 <- staged cols 4s..4s+13)
+  for (int it = tid; it < 3 * kS * 4; it += kThreads) {
+    const int c = it / (kS * 4), r = (it / 4) % kS, s = it % 4;
+    float acc[4][5];
+#pragma unroll
+    for (int o = 0; o < 4; o++)
+#pragma unroll
+      for (int q = 0; q < 5; q++) acc[o][q] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 14; j++) {
+      const float x = X[c][r][4 * s + j], y = Y[c][r][4 * s + j];
+      const float p[5] = {x, y, x * x, y * y, x * y};
+#pragma unroll
+      for (int o = 0; o < 4; o++) {
+        const int k = j - o;
+        if (k >= 0 && k <= 10) {
+#pragma unroll
+          for (int q = 0; q < 5; q++) acc[o][q] = fmaf(h.g[k], p[q], acc[o][q]);
+        }
       }
     }
 #pragma unroll
-    for (int c = 0; c < 3; c++) {
-      X[c * kR * kR + t] = x[c];
-      Y[c * kR * kR + t] = y[c];
-    }
+    for (int o = 0; o < 4; o++)
+#pragma unroll
+      for (int q = 0; q < 5; q++) HS[c][q][r][4 * s + o] = acc[o][q];
   }
+  __syncthreads();
+  // vertical: item = (channel, column j, 4 output rows 4s..4s+3 <- rows 4s..4s+13) -> S, maps
   const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
   float lsum = 0.f;
-  for (int c = 0; c < 3; c++) {
-    const float* Xc = X + c * kR * kR;
-    const float* Yc = Y + c * kR * kR;
-    __syncthreads();
-    // 1a. horizontal window sums: HS[k][i][jj], centre column jj + 5 of the region
-    for (int t = tid; t < kR * kC; t += kThreads) {
-      const int i = t / kC, jj = t % kC;
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f, s4 = 0.f;
+  for (int it = tid; it < 3 * 16 * 4; it += kThreads) {
+    const int c = it / 64, s = (it / 16) % 4, j = it % 16;
+    float st[4][5];
 #pragma unroll
-      for (int k = 0; k < 11; k++) {
-        const float x = Xc[i * kR + jj + k], y = Yc[i * kR + jj + k], w = h.g[k];
-        s0 = fmaf(w, x, s0);
-        s1 = fmaf(w, y, s1);
-        s2 = fmaf(w * x, x, s2);
-        s3 = fmaf(w * y, y, s3);
-        s4 = fmaf(w * x, y, s4);
+    for (int o = 0; o < 4; o++)
+#pragma unroll
+      for (int q = 0; q < 5; q++) st[o][q] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 14; i++) {
+      float hv[5];
+#pragma unroll
+      for (int q = 0; q < 5; q++) hv[q] = HS[c][q][4 * s + i][j];
+#pragma unroll
+      for (int o = 0; o < 4; o++) {
+        const int k = i - o;
+        if (k >= 0 && k <= 10) {
+#pragma unroll
+          for (int q = 0; q < 5; q++) st[o][q] = fmaf(h.g[k], hv[q], st[o][q]);
+        }
       }
-      HS[0 * kR * kC + t] = s0;
-      HS[1 * kR * kC + t] = s1;
-      HS[2 * kR * kC + t] = s2;
-      HS[3 * kR * kC + t] = s3;
-      HS[4 * kR * kC + t] = s4;
     }
-    __syncthreads();
-    // 1b-2. vertical sums -> window statistics at centre (ii, jj) (region row ii + 5), SSIM
-    //       terms; centres outside the image contribute nothing
-    for (int t = tid; t < kC * kC; t += kThreads) {
-      const int ii = t / kC, jj = t % kC;
-      float st[5];
 #pragma unroll
-      for (int q = 0; q < 5; q++) {
-        float s = 0.f;
-#pragma unroll
-        for (int k = 0; k < 11; k++) s = fmaf(h.g[k], HS[q * kR * kC + (ii + k) * kC + jj], s);
-        st[q] = s;
-      }
-      const int gy = ty * 16 - 5 + ii, gx = tx * 16 - 5 + jj;
+    for (int o = 0; o < 4; o++) {
+      const int row = 4 * s + o, p = row * 16 + j;
+      const int gy = ty * 16 + row, gx = tx * 16 + j;
       float a = 0.f, b = 0.f, cc = 0.f;
-      if (gx >= 0 && gx < geo.W && gy >= 0 && gy < geo.H) {
-        const float mx = st[0], my = st[1];
-        const float A1 = 2.f * mx * my + C1, A2 = 2.f * (st[4] - mx * my) + C2;
-        const float B1 = mx * mx + my * my + C1, B2 = (st[2] - mx * mx) + (st[3] - my * my) + C2;
+      if (gx < geo.W && gy < geo.H) {
+        const float mx = st[o][0], my = st[o][1];
+        const float A1 = 2.f * mx * my + C1, A2 = 2.f * (st[o][4] - mx * my) + C2;
+        const float B1 = mx * mx + my * my + C1, B2 = (st[o][2] - mx * mx) + (st[o][3] - my * my) + C2;
         const float rB = 1.0f / (B1 * B2);
         const float S = A1 * A2 * rB;
         a = 2.f * my * (A2 - A1) * rB - 2.f * mx * S * (1.0f / B1 - 1.0f / B2);
         b = -S / B2;
         cc = 2.f * A1 * rB;
-        if (ii >= 5 && ii < 21 && jj >= 5 && jj < 21) {  // a centre of this block
-          const float x = Xc[(ii + 5) * kR + jj + 5], y = Yc[(ii + 5) * kR + jj + 5];
-          lsum += (1.f - h.lambda) * fabsf(x - y) + h.lambda * (1.f - S);
-        }
+        const float x = X[c][row + 5][j + 5], y = Y[c][row + 5][j + 5];
+        lsum += (1.f - h.lambda) * fabsf(x - y) + h.lambda * (1.f - S);
       }
-      M[0 * kC * kC + t] = a;
-      M[1 * kC * kC + t] = b;
-      M[2 * kC * kC + t] = cc;
-    }
-    __syncthreads();
-    // 3a. horizontal sums of the maps at the block's 16 columns
-    for (int t = tid; t < kC * 16; t += kThreads) {
-      const int ii = t / 16, j = t % 16;
-#pragma unroll
-      for (int q = 0; q < 3; q++) {
-        float s = 0.f;
-#pragma unroll
-        for (int k = 0; k < 11; k++) s = fmaf(h.g[k], M[q * kC * kC + ii * kC + j + k], s);
-        HB[q * kC * 16 + t] = s;
-      }
-    }
-    __syncthreads();
-    // 3b. vertical sums -> dSSIM_sum/dx at pixel (i, j) of the block; fused with the L1 term
-    {
-      const int i = tid / 16, j = tid % 16;
-      float s[3];
-#pragma unroll
-      for (int q = 0; q < 3; q++) {
-        float acc = 0.f;
-#pragma unroll
-        for (int k = 0; k < 11; k++) acc = fmaf(h.g[k], HB[q * kC * 16 + (i + k) * 16 + j], acc);
-        s[q] = acc;
-      }
-      const float x = Xc[(i + 10) * kR + j + 10], y = Yc[(i + 10) * kR + j + 10];
-      const int gy = ty * 16 + i, gx = tx * 16 + j;
-      float d = 0.f;
-      if (gx < geo.W && gy < geo.H) {
-        const float gs = s[0] + 2.f * x * s[1] + y * s[2];
-        const float e = x - y;
-        d = ((1.f - h.lambda) * (e > 0.f ? 1.f : (e < 0.f ? -1.f : 0.f)) - h.lambda * gs) * h.norm;
-      }
-      dL_dpix[lb * 768 + c * 256 + tid] = d;
+      float* m = maps + lb * 2304 + c * 256 + p;  // [lb][map 0..2][channel][256]
+      m[0] = a;
+      m[768] = b;
+      m[1536] = cc;
     }
   }
-  // block's share of the loss
   double v2 = (double)lsum * (double)h.norm;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v2 += __shfl_xor_sync(0xffffffffu, v2, o);
@@ -210,6 +209,94 @@ __global__ void __launch_bounds__(kThreads) k_loss_ssim(
     for (int w = 0; w < kThreads / 32; w++) s += s_red[w];
     if (s != 0.0) atomicAdd(loss_sum, s);
   }
+}
+
+__global__ void __launch_bounds__(kThreads) k_ssim_grad(
+    const float* __restrict__ maps, const float* __restrict__ halo, const int64_t* __restrict__ halo_ids,
+    int64_t n_halo, const float* __restrict__ out_rgb, const uint8_t* __restrict__ gt, gs_geom geo, int64_t B_lo,
+    int64_t B_hi, ssim_arg h, float* __restrict__ dL_dpix) {
+  __shared__ float M[9][kS][kLd];     // map m (a, b, c) of channel ch at index m * 3 + ch
+  __shared__ float HB[9][kS][kLdO];   // horizontal sums at the 16 own columns
+  __shared__ const float* s_src[9];
+  const int tid = threadIdx.x;
+  const int64_t lb = blockIdx.x, beta = B_lo + lb;
+  const int64_t v = beta / geo.per_view, loc = beta % geo.per_view;
+  const int tx = (int)(loc % geo.Wt), ty = (int)(loc / geo.Wt);
+  neighbour_sources(maps, halo, halo_ids, n_halo, geo, B_lo, B_hi, v, tx, ty, 2304, s_src);
+  __syncthreads();
+  stage_planes(s_src, 9, 0, &M[0][0][0]);  // maps are zero outside the image
+  __syncthreads();
+  // horizontal: item = (map, row r, 4 output columns)
+  for (int it = tid; it < 9 * kS * 4; it += kThreads) {
+    const int m = it / (kS * 4), r = (it / 4) % kS, s = it % 4;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < 14; j++) {
+      const float val = M[m][r][4 * s + j];
+#pragma unroll
+      for (int o = 0; o < 4; o++) {
+        const int k = j - o;
+        if (k >= 0 && k <= 10) acc[o] = fmaf(h.g[k], val, acc[o]);
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < 4; o++) HB[m][r][4 * s + o] = acc[o];
+  }
+  __syncthreads();
+  // vertical: item = (channel, column j, 4 output rows) -> dL/dpix
+  for (int it = tid; it < 3 * 16 * 4; it += kThreads) {
+    const int c = it / 64, s = (it / 16) % 4, j = it % 16;
+    float w3[4][3];
+#pragma unroll
+    for (int o = 0; o < 4; o++) w3[o][0] = w3[o][1] = w3[o][2] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 14; i++) {
+      float hv[3];
+#pragma unroll
+      for (int q = 0; q < 3; q++) hv[q] = HB[q * 3 + c][4 * s + i][j];
+#pragma unroll
+      for (int o = 0; o < 4; o++) {
+        const int k = i - o;
+        if (k >= 0 && k <= 10) {
+#pragma unroll
+          for (int q = 0; q < 3; q++) w3[o][q] = fmaf(h.g[k], hv[q], w3[o][q]);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < 4; o++) {
+      const int row = 4 * s + o, p = row * 16 + j;
+      const int gy = ty * 16 + row, gx = tx * 16 + j;
+      float d = 0.f;
+      if (gx < geo.W && gy < geo.H) {
+        const float x = out_rgb[lb * 768 + c * 256 + p];
+        const float y = (float)gt[((v * geo.H + gy) * (int64_t)geo.W + gx) * 3 + c] * (1.0f / 255.0f);
+        const float gs = w3[o][0] + 2.f * x * w3[o][1] + y * w3[o][2];
+        const float e = x - y;
+        d = ((1.f - h.lambda) * (e > 0.f ? 1.f : (e < 0.f ? -1.f : 0.f)) - h.lambda * gs) * h.norm;
+      }
+      dL_dpix[lb * 768 + c * 256 + p] = d;
+    }
+  }
+}
+
+gs_status ssim_args(gs_ctx* c, const gs_camera* cams_h, int n_views, const int64_t* dp_h, float lambda,
+                    int b_loss, int64_t n_halo, const float* halo, const int64_t* halo_ids, ssim_arg& h) {
+  gs_status s = gs_check_batch(c, cams_h, n_views, dp_h);
+  if (s != GS_OK) return s;
+  GS_REQUIRE(c, b_loss >= 1, "b_loss must be >= 1");
+  GS_REQUIRE(c, lambda >= 0.f && lambda <= 1.f, "lambda must be in [0, 1]");
+  GS_REQUIRE(c, n_halo >= 0 && (n_halo == 0 || (halo && halo_ids)), "halo arguments");
+  const gs_geom geo = gs_make_geom(&cams_h[0]);
+  double g[11], sum = 0.0;
+  for (int k = 0; k < 11; k++) {
+    g[k] = std::exp(-(double)((k - 5) * (k - 5)) / (2.0 * 1.5 * 1.5));
+    sum += g[k];
+  }
+  for (int k = 0; k < 11; k++) h.g[k] = (float)(g[k] / sum);
+  h.lambda = lambda;
+  h.norm = (float)(1.0 / (3.0 * (double)geo.W * (double)geo.H * (double)b_loss));
+  return GS_OK;
 }
 
 }  // namespace
@@ -257,39 +344,38 @@ extern "C" gs_status gs_halo_plan(gs_ctx* c, const gs_camera* cams_h, int n_view
   return GS_OK;
 }
 
-extern "C" gs_status gs_loss_ssim(gs_ctx* c, const float* out_rgb, const float* halo, const int64_t* halo_ids,
-                                  int64_t n_halo, const uint8_t* gt, const gs_camera* cams_h, int n_views,
-                                  const int64_t* dp_h, float lambda, int b_loss, float* dL_dpix, double* loss_sum,
-                                  void* stream) {
+extern "C" gs_status gs_ssim_terms(gs_ctx* c, const float* out_rgb, const float* halo_rgb, const int64_t* halo_ids,
+                                   int64_t n_halo, const uint8_t* gt, const gs_camera* cams_h, int n_views,
+                                   const int64_t* dp_h, float lambda, int b_loss, float* maps, double* loss_sum,
+                                   void* stream) {
   if (!c) return GS_EINVAL;
-  gs_status s = gs_check_batch(c, cams_h, n_views, dp_h);
+  ssim_arg h;
+  gs_status s = ssim_args(c, cams_h, n_views, dp_h, lambda, b_loss, n_halo, halo_rgb, halo_ids, h);
   if (s != GS_OK) return s;
-  GS_REQUIRE(c, b_loss >= 1, "b_loss must be >= 1");
-  GS_REQUIRE(c, lambda >= 0.f && lambda <= 1.f, "lambda must be in [0, 1]");
-  GS_REQUIRE(c, n_halo >= 0 && (n_halo == 0 || (halo && halo_ids)), "halo arguments");
   const int64_t B_lo = dp_h[c->rank], B_hi = dp_h[c->rank + 1], n_owned = B_hi - B_lo;
   if (n_owned == 0) return GS_OK;
-  GS_REQUIRE(c, out_rgb && gt && dL_dpix && loss_sum, "null argument");
-  gs_geom geo = gs_make_geom(&cams_h[0]);
-  ssim_arg h;
-  {
-    double g[11], sum = 0.0;
-    for (int k = 0; k < 11; k++) {
-      g[k] = std::exp(-(double)((k - 5) * (k - 5)) / (2.0 * 1.5 * 1.5));
-      sum += g[k];
-    }
-    for (int k = 0; k < 11; k++) h.g[k] = (float)(g[k] / sum);
-  }
-  h.lambda = lambda;
-  h.norm = (float)(1.0 / (3.0 * (double)geo.W * (double)geo.H * (double)b_loss));
-  static bool attr = false;
-  if (!attr) {
-    GS_CUDA(c, cudaFuncSetAttribute(k_loss_ssim, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
-    attr = true;
-  }
+  GS_REQUIRE(c, out_rgb && gt && maps && loss_sum, "null argument");
   ++c->launches;
-  k_loss_ssim<<<(unsigned)n_owned, kThreads, kSmem, (cudaStream_t)stream>>>(out_rgb, halo, halo_ids, n_halo, gt, geo,
-                                                                           B_lo, B_hi, h, dL_dpix, loss_sum);
-  GS_LAUNCH_CHECK(c, "loss_ssim");
+  k_ssim_terms<<<(unsigned)n_owned, kThreads, 0, (cudaStream_t)stream>>>(
+      out_rgb, halo_rgb, halo_ids, n_halo, gt, gs_make_geom(&cams_h[0]), B_lo, B_hi, h, maps, loss_sum);
+  GS_LAUNCH_CHECK(c, "ssim_terms");
+  return GS_OK;
+}
+
+extern "C" gs_status gs_ssim_grad(gs_ctx* c, const float* maps, const float* halo_maps, const int64_t* halo_ids,
+                                  int64_t n_halo, const float* out_rgb, const uint8_t* gt, const gs_camera* cams_h,
+                                  int n_views, const int64_t* dp_h, float lambda, int b_loss, float* dL_dpix,
+                                  void* stream) {
+  if (!c) return GS_EINVAL;
+  ssim_arg h;
+  gs_status s = ssim_args(c, cams_h, n_views, dp_h, lambda, b_loss, n_halo, halo_maps, halo_ids, h);
+  if (s != GS_OK) return s;
+  const int64_t B_lo = dp_h[c->rank], B_hi = dp_h[c->rank + 1], n_owned = B_hi - B_lo;
+  if (n_owned == 0) return GS_OK;
+  GS_REQUIRE(c, maps && out_rgb && gt && dL_dpix, "null argument");
+  ++c->launches;
+  k_ssim_grad<<<(unsigned)n_owned, kThreads, 0, (cudaStream_t)stream>>>(
+      maps, halo_maps, halo_ids, n_halo, out_rgb, gt, gs_make_geom(&cams_h[0]), B_lo, B_hi, h, dL_dpix);
+  GS_LAUNCH_CHECK(c, "ssim_grad");
   return GS_OK;
 }

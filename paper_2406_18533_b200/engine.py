@@ -72,6 +72,8 @@ class GrendelTrainer:
         self.rgb = _Buf(dev, torch.float32, (3, 256))      # rendered owned blocks (D-SSIM loss)
         self.halo = _Buf(dev, torch.float32, (3, 256))     # other ranks' blocks within 10 px
         self.halo_ids = _Buf(dev, torch.int64)
+        self.maps = _Buf(dev, torch.float32, (3, 3, 256))  # SSIM derivative maps of owned blocks
+        self.halo_maps = _Buf(dev, torch.float32, (3, 3, 256))
         self.cost = _Buf(dev, torch.int64)
         self.drec = _Buf(dev, torch.float32, (L.GRAD_FLOATS,))
         self.dsend = _Buf(dev, torch.float32, (L.GRAD_FLOATS,))
@@ -107,9 +109,19 @@ class GrendelTrainer:
         no = self.B  # a rank may own up to every block after rebalancing
         self.T.ensure(no), self.nl.ensure(no), self.dpix.ensure(no), self.cost.ensure(no), self.range.ensure(no + 1)
         if self.loss_kind == "ssim":
-            self.rgb.ensure(no)
+            self.rgb.ensure(no), self.maps.ensure(no)
         self.dp = saved
         torch.cuda.synchronize()
+
+    def _halo(self, data, buf, cams, dp, st):
+        """Other ranks' blocks within the D-SSIM window reach (world > 1; collective)."""
+        if self.G == 1:
+            return 0
+        while True:
+            try:
+                return L.halo_exchange(self.ctx, data, cams, dp, buf.t, self.halo_ids.t, st)
+            except L.CapacityError as e:
+                buf.ensure(e.needed), self.halo_ids.ensure(e.needed)
 
     @property
     def n_owned(self):
@@ -183,18 +195,15 @@ class GrendelTrainer:
             L.render_fwd(ctx, recv_t, self.sorted.t, self.range.t, cams, dp, self.bg, None, self.b, self.rgb.t,
                          self.T.t, self.nl.t, None, None, self.cost.t, self.cost_mode, stats, st)
         rec("render_fwd", 1)
-        if self.loss_kind == "ssim":  # NEXT-1: halo exchange + fused L1 + D-SSIM
+        if self.loss_kind == "ssim":  # NEXT-1: L1 + D-SSIM in two passes around halo exchanges
             rec("loss", 0)
-            n_halo = 0
-            if self.G > 1:
-                while True:
-                    try:
-                        n_halo = L.halo_exchange(ctx, self.rgb.t, cams, dp, self.halo.t, self.halo_ids.t, st)
-                        break
-                    except L.CapacityError as e:
-                        self.halo.ensure(e.needed), self.halo_ids.ensure(e.needed)
-            L.loss_ssim(ctx, self.rgb.t, self.halo.t, self.halo_ids.t, n_halo, gt, cams, dp, self.ssim_lambda,
-                        self.b, self.dpix.t, self.loss, st)
+            self.maps.ensure(no)
+            n_halo = self._halo(self.rgb.t, self.halo, cams, dp, st)
+            L.ssim_terms(ctx, self.rgb.t, self.halo.t, self.halo_ids.t, n_halo, gt, cams, dp, self.ssim_lambda,
+                         self.b, self.maps.t, self.loss, st)
+            n_halo = self._halo(self.maps.t, self.halo_maps, cams, dp, st)
+            L.ssim_grad(ctx, self.maps.t, self.halo_maps.t, self.halo_ids.t, n_halo, self.rgb.t, gt, cams, dp,
+                        self.ssim_lambda, self.b, self.dpix.t, st)
             rec("loss", 1)
         # A5 render backward
         rec("render_bwd", 0)

@@ -45,23 +45,46 @@ def _from_blocks(blk, Wt, Ht, W, H, b):
     return a[:, :H, :W]
 
 
-def _run(ctx, rgb_blocks, gt, cams, dp, lam, halo_src=None):
+def _terms(ctx, rgb_blocks, gt, cams, dp, lam):
+    """Pass 1 on rank ctx.rank: halo of rendered blocks taken from rgb_blocks (all blocks)."""
     L = _L()
     r = ctx.rank
     lo, hi = int(dp[r]), int(dp[r + 1])
     ids = L.halo_plan(ctx, cams, dp)
     own = torch.from_numpy(rgb_blocks[lo:hi]).to(DEV)
-    if len(ids):
-        halo = torch.from_numpy(np.ascontiguousarray(halo_src[ids])).to(DEV)
-        hid = torch.from_numpy(ids).to(DEV)
-    else:
-        halo, hid = None, None
-    gt_t = torch.from_numpy(gt).to(DEV)
-    dpix = torch.zeros((hi - lo, 3, 256), dtype=torch.float32, device=DEV)
+    halo = torch.from_numpy(np.ascontiguousarray(rgb_blocks[ids])).to(DEV) if len(ids) else None
+    hid = torch.from_numpy(ids).to(DEV) if len(ids) else None
+    maps = torch.zeros((hi - lo, 3, 3, 256), dtype=torch.float32, device=DEV)
     loss = torch.zeros(1, dtype=torch.float64, device=DEV)
-    L.loss_ssim(ctx, own, halo, hid, len(ids), gt_t, cams, dp, lam, len(cams), dpix, loss)
+    L.ssim_terms(ctx, own, halo, hid, len(ids), torch.from_numpy(gt).to(DEV), cams, dp, lam, len(cams), maps, loss)
     torch.cuda.synchronize()
-    return dpix.cpu().numpy(), float(loss.item()), ids
+    return maps.cpu().numpy(), float(loss.item())
+
+
+def _grad(ctx, all_maps, rgb_blocks, gt, cams, dp, lam):
+    """Pass 2 on rank ctx.rank: halo of maps taken from all_maps (every block's maps)."""
+    L = _L()
+    r = ctx.rank
+    lo, hi = int(dp[r]), int(dp[r + 1])
+    ids = L.halo_plan(ctx, cams, dp)
+    maps = torch.from_numpy(np.ascontiguousarray(all_maps[lo:hi])).to(DEV)
+    hm = torch.from_numpy(np.ascontiguousarray(all_maps[ids])).to(DEV) if len(ids) else None
+    hid = torch.from_numpy(ids).to(DEV) if len(ids) else None
+    own = torch.from_numpy(rgb_blocks[lo:hi]).to(DEV)
+    dpix = torch.zeros((hi - lo, 3, 256), dtype=torch.float32, device=DEV)
+    L.ssim_grad(ctx, maps, hm, hid, len(ids), own, torch.from_numpy(gt).to(DEV), cams, dp, lam, len(cams), dpix)
+    torch.cuda.synchronize()
+    return dpix.cpu().numpy()
+
+
+def _run_ranks(blocks, gt, cams, dp, lam):
+    L = _L()
+    G = len(dp) - 1
+    ctxs = [L.Context(0, r, G) for r in range(G)]
+    res = [_terms(ctxs[r], blocks, gt, cams, dp, lam) for r in range(G)]
+    all_maps = np.concatenate([m for m, _ in res])
+    dpix = np.concatenate([_grad(ctxs[r], all_maps, blocks, gt, cams, dp, lam) for r in range(G)])
+    return dpix, sum(l for _, l in res), all_maps
 
 
 @pytest.mark.parametrize("W,H,b,lam", [(64, 64, 1, 0.2), (75, 50, 2, 0.2), (150, 97, 1, 1.0), (41, 37, 2, 0.0)])
@@ -70,9 +93,8 @@ def test_loss_ssim_matches_oracle(W, H, b, lam):
     Wt, Ht = (W + 15) // 16, (H + 15) // 16
     img, gt = _images(W, H, b, seed=W + H)
     cams = _cams(W, H, b)
-    ctx = L.Context(0, 0, 1)
     dp = np.array([0, b * Wt * Ht], np.int64)
-    dpix, loss, _ = _run(ctx, _to_blocks(img, Wt, Ht), gt, cams, dp, lam)
+    dpix, loss, _ = _run_ranks(_to_blocks(img, Wt, Ht), gt, cams, dp, lam)
     lo, go = oracle.ssim_loss_batch(img.astype(np.float64), gt.astype(np.float64) / 255.0, lam)
     gk = _from_blocks(dpix, Wt, Ht, W, H, b)
     assert abs(loss - lo) <= 2e-6 * abs(lo) + 1e-9, (loss, lo)
@@ -122,15 +144,11 @@ def test_partition_equals_single_rank():
     img, gt = _images(W, H, b, seed=9)
     cams = _cams(W, H, b)
     blocks = _to_blocks(img, Wt, Ht)
-    d1, l1, _ = _run(L.Context(0, 0, 1), blocks, gt, cams, np.array([0, B], np.int64), lam)
+    d1, l1, m1 = _run_ranks(blocks, gt, cams, np.array([0, B], np.int64), lam)
     dp = np.array([0, 7, 23, 24, B], np.int64)  # uneven, a one-block rank, a seam inside a row
-    parts, tot = [], 0.0
-    for r in range(len(dp) - 1):
-        d, l, ids = _run(L.Context(0, r, len(dp) - 1), blocks, gt, cams, dp, lam, halo_src=blocks)
-        parts.append(d)
-        tot += l
-    assert np.array_equal(np.concatenate(parts), d1)  # same arithmetic per pixel: bitwise
-    assert abs(tot - l1) <= 1e-12 * abs(l1)
+    d4, l4, m4 = _run_ranks(blocks, gt, cams, dp, lam)
+    assert np.array_equal(m4, m1) and np.array_equal(d4, d1)  # same arithmetic per pixel: bitwise
+    assert abs(l4 - l1) <= 1e-12 * abs(l1)
 
 
 def test_trainer_step_with_ssim_loss():
@@ -146,7 +164,7 @@ def test_trainer_step_with_ssim_loss():
     loss = tr.step(cams, torch.from_numpy(gt).to(DEV), next_cams=cams)
     torch.cuda.synchronize()
     _, _, _, fwd = oracle.render_batch(sc, cams, "parity", (0, 0, 0), None, 1e-5)
-    img = oracle.block_to_image(fwd["C"], 4, 4, 64, 64, 1)
+    img = oracle.block_to_image(fwd["c"], 4, 4, 64, 64, 1)
     lo, _ = oracle.ssim_loss_batch(img, gt.astype(np.float64) / 255.0, 0.2)
     assert abs(loss.item() - lo) <= 1e-4 * lo, (loss.item(), lo)
     assert torch.count_nonzero(tr.drec.t[: tr.last["n_recv"]]) > 0
