@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_bwd_adam(planes P, plane
                                                      const float* __restrict__ dL_dsend, adam_arg h) {
   __shared__ int s_cnt[kWarps * kMaxBuckets];
   __shared__ float s_gsh[48 * kBlock];  // SH gradient accumulators, [coefficient][thread]
-  __shared__ int64_t s_pos[kListCap * kBlock];        // per-thread record positions
+  __shared__ int32_t s_pos[kListCap * kBlock];        // per-thread record positions (< 2^31)
   __shared__ unsigned char s_view[kListCap * kBlock];  // and their views
   // cameras in shared memory: lanes of a warp handle different views at the same time in
   // phase B, and divergent indexing of the kernel-parameter bank would serialise
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_bwd_adam(planes P, plane
           const int slot = cnt - r * kListCap;
           if (slot >= 0 && slot < kListCap) {
             s_pos[slot * kBlock + threadIdx.x] =
-                base[(int64_t)k * ncta + blockIdx.x] + warp_prefix(s_cnt, wid, nb, k) + __popc(bal & lt);
+                (int32_t)(base[(int64_t)k * ncta + blockIdx.x] + warp_prefix(s_cnt, wid, nb, k) + __popc(bal & lt));
             s_view[slot * kBlock + threadIdx.x] = (unsigned char)v;
           }
           cnt++;
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) k_bwd_adam(planes P, plane
     for (int c = 0; c < 9; c++) g9[c] = 0.f;
     for (int j = 0; j < nl; j++) {
       const int v = s_view[j * kBlock + threadIdx.x];
-      const float* src = dL_dsend + s_pos[j * kBlock + threadIdx.x] * 9;
+      const float* src = dL_dsend + (int64_t)s_pos[j * kBlock + threadIdx.x] * 9;
 #pragma unroll
       for (int c = 0; c < 9; c++) g9[c] += src[c];
       if (j + 1 == nl || s_view[(j + 1) * kBlock + threadIdx.x] != v) {
@@ -409,8 +409,30 @@ extern "C" gs_status gs_adam_step(gs_ctx* c, gs_params* p, gs_params* m, gs_para
     // the parameter gradient, then an elementwise Adam pass streams p, m, v, g at full
     // occupancy; the fused kernel's register footprint caps its memory parallelism
     ++c->launches;
-    k_bwd_adam<true, false, 1><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base, L.ncta,
-                                                        dL_dsend, h);
+    // A/B knob: GS_ADAM_SPLIT_MINB = minimum resident CTAs per SM of the gradient kernel
+    static int sminb = -1;
+    if (sminb < 0) {
+      const char* e = getenv("GS_ADAM_SPLIT_MINB");
+      sminb = e ? atoi(e) : 4;  // 4: 126 registers, C2 6.7 -> 5.0 ms (1: 188 registers, 8 warps/SM)
+    }
+    if (sminb >= 6)
+      k_bwd_adam<true, false, 6><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base,
+                                                          L.ncta, dL_dsend, h);
+    else if (sminb >= 5)
+      k_bwd_adam<true, false, 5><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base,
+                                                          L.ncta, dL_dsend, h);
+    else if (sminb >= 4)
+      k_bwd_adam<true, false, 4><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base,
+                                                          L.ncta, dL_dsend, h);
+    else if (sminb >= 3)
+      k_bwd_adam<true, false, 3><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base,
+                                                          L.ncta, dL_dsend, h);
+    else if (sminb >= 2)
+      k_bwd_adam<true, false, 2><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base,
+                                                          L.ncta, dL_dsend, h);
+    else
+      k_bwd_adam<true, false, 1><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base,
+                                                          L.ncta, dL_dsend, h);
     ++c->launches;
     k_adam_apply<<<dim3((unsigned)((p->n + 255) / 256), 15), 256, 0, st>>>(P, Mo, Vo, Go, p->n, h);
     GS_LAUNCH_CHECK(c, "bwd + adam_apply");

@@ -170,6 +170,8 @@ extern "C" gs_status gs_project(gs_ctx* c, const gs_params* p, const gs_camera* 
   GS_CUDA(c, cudaStreamSynchronize(st));
   for (int d = 0; d < G; d++) send_counts_h[d] = c->pinned[d + 1] - c->pinned[d];
   int64_t total = c->pinned[G];
+  // record positions are int32 in the backward (gs_adam_step) and the exchanges
+  if (total >= (1ll << 31)) return gs_fail(c, GS_ENOTSUP, "%lld records exceed int32 positions", (long long)total);
   if (total > send_cap)
     return gs_fail(c, GS_ECAPACITY, "send capacity %lld < %lld records", (long long)send_cap,
                    (long long)total);

@@ -245,7 +245,7 @@ def event_ms(events):
     for n, (s, e) in events.items():
         try:
             out[n] = s.elapsed_time(e)
-        except RuntimeError:  # not recorded in this step (e.g. "loss" with the fused L1)
+        except (RuntimeError, ValueError):  # not recorded this step (e.g. "loss" with the fused L1)
             pass
     return out
 
