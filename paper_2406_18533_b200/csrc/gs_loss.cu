@@ -34,7 +34,7 @@ using namespace gsd;
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 192;  // 6 warps: the vertical passes have exactly 192 items (3 x 16 x 4)
 constexpr int kS = 26;        // staged side: block + 5-pixel halo each way
 constexpr int kLd = 27;       // odd row stride of staged tiles
 constexpr int kLdO = 17;      // odd row stride of 16-wide outputs
@@ -69,6 +69,13 @@ __device__ __forceinline__ void neighbour_sources(const float* base, const float
     }
   }
   s_src[t] = src;
+}
+
+// 1/x by one MUFU.RCP (x >= 1e-4 here: no denormal range fix-up needed; ~1 ulp).
+__device__ __forceinline__ float rcp_fast(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
 }
 
 // Which of the 3x3 neighbour blocks holds staged coordinate i (0..25, block starts at 5).
@@ -185,10 +192,10 @@ __global__ void __launch_bounds__(kThreads) k_ssim_terms(
         const float mx = st[o][0], my = st[o][1];
         const float A1 = 2.f * mx * my + C1, A2 = 2.f * (st[o][4] - mx * my) + C2;
         const float B1 = mx * mx + my * my + C1, B2 = (st[o][2] - mx * mx) + (st[o][3] - my * my) + C2;
-        const float rB = 1.0f / (B1 * B2);
+        const float rB1 = rcp_fast(B1), rB2 = rcp_fast(B2), rB = rB1 * rB2;  // B1, B2 >= C1, C2 > 0
         const float S = A1 * A2 * rB;
-        a = 2.f * my * (A2 - A1) * rB - 2.f * mx * S * (1.0f / B1 - 1.0f / B2);
-        b = -S / B2;
+        a = 2.f * my * (A2 - A1) * rB - 2.f * mx * S * (rB1 - rB2);
+        b = -S * rB2;
         cc = 2.f * A1 * rB;
         const float x = X[c][row + 5][j + 5], y = Y[c][row + 5][j + 5];
         lsum += (1.f - h.lambda) * fabsf(x - y) + h.lambda * (1.f - S);
