@@ -15,11 +15,11 @@ ncu --set full --clock-control none --import-source on -k regex:'k_render_bwd|k_
     -s 6 -c 2 -o $OUT/prof_${TAG}_${CFG}_render $B > $OUT/prof_${TAG}_${CFG}_render.log 2>&1
 # 3. projection and binning kernels in the bench command
 ncu --set full --clock-control none --import-source on \
-    -k regex:'k_project_count|k_project_write|k_rect_diff|k_place|k_sort_warp|k_sort_small' \
-    -s 18 -c 6 -o $OUT/prof_${TAG}_${CFG}_bin $B > $OUT/prof_${TAG}_${CFG}_bin.log 2>&1
-# 4. the fused backward+Adam kernel writes all parameters and moments (8 GB at C2), which
-#    kernel replay must save/restore: capture it on a reduced copy (4 views, 2.8M Gaussians)
+    -k regex:'k_project_count|k_project_write|k_radix_scatter|k_radix_hist|k_emit|k_key_ranges' \
+    -s 150 -c 20 -o $OUT/prof_${TAG}_${CFG}_bin $B > $OUT/prof_${TAG}_${CFG}_bin.log 2>&1
+# 4. the Adam kernels write all parameters, moments and gradients (~11 GB at C2), which kernel
+#    replay must save/restore: capture them on a reduced copy (4 views, 2.8M Gaussians)
 D="python tools/prof_driver.py --config $CFG --views 4 --gaussians 2800000 --warmup 2 --steps 1"
-ncu --set full --clock-control none --import-source on -k regex:'k_bwd_adam' \
-    -s 2 -c 1 -o $OUT/prof_${TAG}_${CFG}_adam $D > $OUT/prof_${TAG}_${CFG}_adam.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:'k_bwd_adam|k_adam_apply' \
+    -s 4 -c 2 -o $OUT/prof_${TAG}_${CFG}_adam $D > $OUT/prof_${TAG}_${CFG}_adam.log 2>&1
 ls -la $OUT | tail -5
