@@ -168,3 +168,38 @@ def test_trainer_step_with_ssim_loss():
     lo, _ = oracle.ssim_loss_batch(img, gt.astype(np.float64) / 255.0, 0.2)
     assert abs(loss.item() - lo) <= 1e-4 * lo, (loss.item(), lo)
     assert torch.count_nonzero(tr.drec.t[: tr.last["n_recv"]]) > 0
+
+
+def test_full_size_c2_view_crops():
+    """The loss kernels at the bench's image size (one 4591x3436 C2 view, 61,705 blocks, the
+    launch configuration bench.py times), checked on crops the oracle can evaluate exactly:
+    dL/dpix at a pixel depends on the image within 10 pixels, so the oracle run on a crop
+    grown by 10 pixels (or clipped at a real image border, where both sides zero-pad) is exact
+    on the crop.  Crops: the four corners (partial blocks at the right/bottom edges) and
+    random interior windows."""
+    L = _L()
+    W, H, b, lam = 4591, 3436, 1, 0.2
+    Wt, Ht = (W + 15) // 16, (H + 15) // 16
+    rng = np.random.default_rng(11)
+    yy, xx = np.mgrid[0:H, 0:W]
+    img = np.clip(0.5 + 0.3 * np.sin(xx / 9.0)[..., None] * np.cos(yy / 13.0)[..., None]
+                  + 0.1 * rng.standard_normal((H, W, 3)), 0, 1).astype(np.float32)[None]
+    gt = np.clip(np.round((img + 0.15 * rng.standard_normal(img.shape)) * 255), 0, 255).astype(np.uint8)
+    cams = _cams(W, H, b)
+    dpix, loss, _ = _run_ranks(_to_blocks(img, Wt, Ht), gt, cams, np.array([0, Wt * Ht], np.int64), lam)
+    g = _from_blocks(dpix, Wt, Ht, W, H, b)[0]
+    crops = [(0, 0), (0, W - 40), (H - 40, 0), (H - 40, W - 40)]
+    crops += [(int(rng.integers(10, H - 60)), int(rng.integers(10, W - 60))) for _ in range(4)]
+    norm = 3.0 * W * H * b
+    for (r0, c0) in crops:
+        r1, c1 = r0 + 40, c0 + 40
+        R0, C0, R1, C1 = max(r0 - 10, 0), max(c0 - 10, 0), min(r1 + 10, H), min(c1 + 10, W)
+        x = img[0, R0:R1, C0:C1].astype(np.float64)
+        y = gt[0, R0:R1, C0:C1].astype(np.float64) / 255.0
+        _, _, go = oracle.ssim_loss(x, y, lam)
+        # the oracle normalises by the crop's pixel count: rescale to the view's
+        go = go * (3.0 * x.shape[0] * x.shape[1]) / norm
+        want = go[r0 - R0:r1 - R0, c0 - C0:c1 - C0]
+        got = g[r0:r1, c0:c1]
+        scale = np.abs(want).max()
+        assert np.abs(got - want).max() <= 2e-4 * scale, ((r0, c0), np.abs(got - want).max(), scale)
