@@ -288,6 +288,51 @@ gs_status gs_ssim_grad(gs_ctx* ctx, const float* maps, const float* halo_maps, c
                        int n_views, const int64_t* dp_h, float lambda, int b_loss, float* dL_dpix,
                        void* stream);
 
+/* ------------------------------------------------------------------- NEXT-2 densification */
+/* Adaptive density control on the Gaussians' owner (App. A.1, App. A.3
+ * "locally on the GPU that stores them"; readings R13-R14 in DESIGN.md).       */
+
+/* gs_densify_stats -- after gs_exchange_grads of a step (before or after gs_adam_step):
+ * for every (owned Gaussian i, view v) with a record, adds to grad_accum[i] the norm of the
+ * screen-space mean gradient of the per-image loss, || b (W/2 dL/dmx, H/2 dL/dmy) || (NDC
+ * units, the batch-mean loss scaled back by b = b_loss), adds 1 to denom[i], and raises
+ * max_radius[i] to the record's screen radius.  bwd_index, send_rec and dL_dsend are the
+ * step's gs_project / gs_exchange_grads buffers (same layouts); the three statistics arrays
+ * are device float[n], accumulated in place.                                             */
+gs_status gs_densify_stats(gs_ctx* ctx, const gs_camera* cams_h, int n_views, const int64_t* dp_h, int64_t n,
+                           const void* bwd_index, const void* send_rec, const float* dL_dsend, int b_loss,
+                           float* grad_accum, float* denom, float* max_radius, void* stream);
+
+typedef struct {
+  float grad_thresh;     /* average statistic selecting a Gaussian (0.0002, P's Table "(0.0002, 0.01)") */
+  float percent_dense;   /* max scale <= percent_dense * extent: clone, else split (0.01)          */
+  float scene_extent;    /* radius of the camera positions' bounding sphere               */
+  float min_opacity;     /* prune below (0.005)                                                    */
+  float max_screen_size; /* > 0: also prune max screen radius above it and max scale > 0.1 extent  */
+} gs_densify_cfg;
+
+/* gs_densify -- one densify-and-prune event on the rank's shard.  Selected = grad_accum/denom
+ * >= grad_thresh (0 where denom = 0).  A selected Gaussian whose largest log-scale is <=
+ * log(percent_dense * extent) is CLONED (an identical copy), otherwise SPLIT into two children
+ * x + R(q)(s . z_t), log-scale - log 1.6, opacity/rotation/SH copied, the parent removed;
+ * z_t = noise[i][t][0..2] (device float[n][2][3], N(0,1) draws supplied by the caller).
+ * Pruned: opacity < min_opacity (all), and with max_screen_size > 0 originals whose
+ * max_radius exceeds it or whose largest scale exceeds 0.1 extent (children: 1.6 * 0.1 extent
+ * on the parent's scale).  New Gaussians get zero Adam moments; survivors keep theirs.
+ * Output (caller-allocated planes laid out for the output count, out_cap Gaussians): kept
+ * originals, clones, first children, second children, each in parent order.  counts_h[4] =
+ * (kept originals, clones, children, total); GS_ECAPACITY if total > out_cap (host sync).
+ * The statistics should be zeroed by the caller afterwards (they index the old shard).    */
+gs_status gs_densify(gs_ctx* ctx, const gs_params* p, const gs_params* m, const gs_params* v,
+                     const float* grad_accum, const float* denom, const float* max_radius, const float* noise,
+                     const gs_densify_cfg* cfg, gs_params* p_out, gs_params* m_out, gs_params* v_out,
+                     int64_t out_cap, int64_t* counts_h, void* stream);
+
+/* gs_opacity_reset -- opacity logits clamped to logit(max_opacity) ("opacity reset"),
+ * the opacity lanes of the Adam moments m, v zeroed (may be NULL).                      */
+gs_status gs_opacity_reset(gs_ctx* ctx, gs_params* p, gs_params* m, gs_params* v, float max_opacity,
+                           void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,6 +45,11 @@ class Params(C.Structure):
                 ("sh", C.c_void_p), ("n", C.c_int64), ("gid_base", C.c_int64)]
 
 
+class DensifyCfg(C.Structure):
+    _fields_ = [("grad_thresh", C.c_float), ("percent_dense", C.c_float), ("scene_extent", C.c_float),
+                ("min_opacity", C.c_float), ("max_screen_size", C.c_float)]
+
+
 class AdamHparams(C.Structure):
     _fields_ = [("lr", C.c_float * 6), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
                 ("batch", C.c_int32), ("step", C.c_int64)]
@@ -87,6 +92,12 @@ _sig = {
                                 C.c_int, _vp, _vp, _vp]),
     "gs_ssim_grad": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp, C.POINTER(Camera), C.c_int, _P64, C.c_float,
                                C.c_int, _vp, _vp]),
+    "gs_densify_stats": (C.c_int, [_vp, C.POINTER(Camera), C.c_int, _P64, _i64, _vp, _vp, _vp, C.c_int, _vp, _vp,
+                                   _vp, _vp]),
+    "gs_densify": (C.c_int, [_vp, C.POINTER(Params), C.POINTER(Params), C.POINTER(Params), _vp, _vp, _vp, _vp,
+                             C.POINTER(DensifyCfg), C.POINTER(Params), C.POINTER(Params), C.POINTER(Params), _i64,
+                             _P64, _vp]),
+    "gs_opacity_reset": (C.c_int, [_vp, C.POINTER(Params), C.POINTER(Params), C.POINTER(Params), C.c_float, _vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -359,6 +370,54 @@ def ssim_grad(ctx, maps, halo_maps, halo_ids, n_halo, out_rgb, gt, cams, dp, lam
     _, dpp = _i64arr(dp)
     st = _lib.gs_ssim_grad(ctx.handle, _ptr(maps), _ptr(halo_maps), _ptr(halo_ids), int(n_halo), _ptr(out_rgb),
                            _ptr(gt), ca, len(cams), dpp, C.c_float(lam), int(b_loss), _ptr(dL_dpix), _stream(stream))
+    ctx.check(st)
+
+
+def densify_stats(ctx, cams, dp, n, bwd_index, send_rec, dL_dsend, b_loss, accum, denom, max_radius, stream=None):
+    """NEXT-2: accumulate the densification statistics of one step (in place)."""
+    ca = cameras(cams)
+    _, dpp = _i64arr(dp)
+    st = _lib.gs_densify_stats(ctx.handle, ca, len(cams), dpp, int(n), _ptr(bwd_index), _ptr(send_rec),
+                               _ptr(dL_dsend), int(b_loss), _ptr(accum), _ptr(denom), _ptr(max_radius),
+                               _stream(stream))
+    ctx.check(st)
+
+
+def densify_cfg(grad_thresh=0.0002, percent_dense=0.01, scene_extent=1.0, min_opacity=0.005, max_screen_size=0.0):
+    return DensifyCfg(grad_thresh, percent_dense, scene_extent, min_opacity, max_screen_size)
+
+
+def densify(ctx, p, m, v, accum, denom, max_radius, noise, cfg, stream=None):
+    """NEXT-2: one densify-and-prune event; returns (p2, m2, v2, counts[4]) as new buffers."""
+    ps, ms, vs = p.struct(), m.struct(), v.struct()
+    counts = np.zeros(4, np.int64)
+    e1, e2, e3 = (Params(None, None, None, None, 0, p.gid_base) for _ in range(3))
+    st = _lib.gs_densify(ctx.handle, C.byref(ps), C.byref(ms), C.byref(vs), _ptr(accum), _ptr(denom),
+                         _ptr(max_radius), _ptr(noise), C.byref(cfg), C.byref(e1), C.byref(e2), C.byref(e3), 0,
+                         counts.ctypes.data_as(_P64), _stream(stream))
+    if st not in (GS_OK, GS_ECAPACITY):
+        ctx.check(st)
+    n2 = int(counts[3])
+    p2 = GaussianParams.empty(n2, p.pos_op.device, p.gid_base, zero=False)
+    m2 = GaussianParams.empty(n2, p.pos_op.device, p.gid_base, zero=False)
+    v2 = GaussianParams.empty(n2, p.pos_op.device, p.gid_base, zero=False)
+    if n2 == 0:
+        return p2, m2, v2, counts
+    ps2, ms2, vs2 = p2.struct(), m2.struct(), v2.struct()
+    st = _lib.gs_densify(ctx.handle, C.byref(ps), C.byref(ms), C.byref(vs), _ptr(accum), _ptr(denom),
+                         _ptr(max_radius), _ptr(noise), C.byref(cfg), C.byref(ps2), C.byref(ms2), C.byref(vs2),
+                         n2, counts.ctypes.data_as(_P64), _stream(stream))
+    ctx.check(st)
+    return p2, m2, v2, counts
+
+
+def opacity_reset(ctx, p, m=None, v=None, max_opacity=0.01, stream=None):
+    """NEXT-2: clamp opacities to max_opacity and zero their Adam moments."""
+    ps = p.struct()
+    ms = m.struct() if m is not None else None
+    vs = v.struct() if v is not None else None
+    st = _lib.gs_opacity_reset(ctx.handle, C.byref(ps), C.byref(ms) if ms else None, C.byref(vs) if vs else None,
+                               C.c_float(max_opacity), _stream(stream))
     ctx.check(st)
 
 

@@ -40,6 +40,8 @@ enum {
   SLOT_PSTART,        // bin_sort pair starts in depth order
   SLOT_HALO_SEND,     // halo exchange: packed blocks to send
   SLOT_HALO_IDX,      // halo exchange: owned-block indices to pack
+  SLOT_DENSIFY,       // densify keep flags [4][n]
+  SLOT_DENSIFY_OFF,   // densify output positions
   SLOT_N
 };
 
