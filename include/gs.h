@@ -333,6 +333,37 @@ gs_status gs_densify(gs_ctx* ctx, const gs_params* p, const gs_params* m, const 
 gs_status gs_opacity_reset(gs_ctx* ctx, gs_params* p, gs_params* m, gs_params* v, float max_opacity,
                            void* stream);
 
+/* NEXT-2 random redistribution (App. B.2; reading R15): after
+ * densification the shard sizes differ; global index j = gid_base + local index moves to
+ * position pi(j) of a new global order in which rank d owns [floor(dN/G), floor((d+1)N/G)):
+ * sizes differ by at most one, the multiset of Gaussians (parameters + Adam m, v) unchanged.
+ * pi = 4-round Feistel bijection keyed by seed on the smallest even bit width covering N,
+ * cycle-walked into [0, N) (no table; identical on every rank).  Records of
+ * gs_redistribute_record_bytes() bytes: (new local index, p, m, v).                     */
+int64_t gs_redistribute_record_bytes(void);
+
+/* gs_redistribute_pack -- this rank's records grouped by destination rank (send_counts_h[G];
+ * any order within a group), n_total = N.  GS_ECAPACITY (counts valid) if cap (records) is
+ * smaller than the shard.  Host sync.                                                     */
+gs_status gs_redistribute_pack(gs_ctx* ctx, const gs_params* p, const gs_params* m, const gs_params* v,
+                               int64_t n_total, uint64_t seed, void* send_buf, int64_t cap,
+                               int64_t* send_counts_h, void* stream);
+
+/* gs_redistribute_unpack -- places n_recv received records at their new local indices of the
+ * output planes (p_out->n == n_recv == the rank's new size; traps on an index outside).     */
+gs_status gs_redistribute_unpack(gs_ctx* ctx, const void* recv_buf, int64_t n_recv, gs_params* p_out,
+                                 gs_params* m_out, gs_params* v_out, void* stream);
+
+/* gs_redistribute -- COLLECTIVE: all-gathers the shard sizes (p->gid_base must be the rank's
+ * offset), packs, exchanges by grouped NCCL point-to-point, unpacks; sets the outputs'
+ * gid_base.  Two calls: with recv_buf == NULL on every rank it only returns *n_total_h = N and
+ * *n_out_h = the rank's new size; then with send_buf (>= p->n records), recv_buf (>= n_out
+ * records) and output planes laid out for n_out.  A capacity below the queried size is a
+ * contract violation (GS_EINVAL on that rank only).  World 1: GS_ENOTSUP (the identity).   */
+gs_status gs_redistribute(gs_ctx* ctx, const gs_params* p, const gs_params* m, const gs_params* v, uint64_t seed,
+                          void* send_buf, int64_t send_cap, void* recv_buf, int64_t recv_cap, gs_params* p_out,
+                          gs_params* m_out, gs_params* v_out, int64_t* n_total_h, int64_t* n_out_h, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

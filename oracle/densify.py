@@ -127,3 +127,61 @@ def opacity_reset(shard, m, v, max_opacity=0.01):
     m2["opac_logit"] = np.zeros_like(m["opac_logit"])
     v2["opac_logit"] = np.zeros_like(v["opac_logit"])
     return s2, m2, v2
+
+
+# ------------------------------------------------------------------ random redistribution
+
+_M32 = 0xFFFFFFFF
+
+
+def _fmix32(h):
+    h ^= h >> 16
+    h = (h * 0x85EBCA6B) & _M32
+    h ^= h >> 13
+    h = (h * 0xC2B2AE35) & _M32
+    h ^= h >> 16
+    return h
+
+
+def feistel_half(N):
+    k = 2
+    while k < 64 and (1 << k) < N:
+        k += 1
+    return (k + (k & 1)) // 2
+
+
+def perm(j, N, seed):
+    """R15: the keyed bijection pi of [0, N) -- a 4-round Feistel network on the smallest even
+    bit width covering N (round function: murmur3's 32-bit finaliser of the seed, the round and
+    the right half), cycle-walked until the image falls in [0, N)."""
+    s = (seed ^ (seed >> 32)) & _M32
+    half = feistel_half(N)
+    mask = (1 << half) - 1
+    y = j
+    while True:
+        L, R = (y >> half) & mask, y & mask
+        for r in range(4):
+            f = _fmix32(s ^ ((r * 0x9E3779B9) & _M32) ^ _fmix32((R + 0x7F4A7C15 * (r + 1)) & _M32)) & mask
+            L, R = R, L ^ f
+        y = (L << half) | R
+        if y < N:
+            return y
+
+
+def redistribute(shards, states_m, states_v, seed):
+    """S:491-497 rebalance_gaussians: the concatenation of the rank shards (global index j) is
+    reordered by pi and cut into G ranges [floor(dN/G), floor((d+1)N/G)).  Returns the new
+    (shards, m, v) lists; Adam state travels with its Gaussian."""
+    G = len(shards)
+    cat = lambda ds: {k: np.concatenate([np.asarray(d[k]) for d in ds]) for k in FIELDS}
+    allp, allm, allv = cat(shards), cat(states_m), cat(states_v)
+    N = len(allp["pos"])
+    order = np.empty(N, np.int64)
+    for j in range(N):
+        order[perm(j, N, seed)] = j  # new position pi(j) holds old element j
+    out = []
+    for d in range(G):
+        lo, hi = d * N // G, (d + 1) * N // G
+        idx = order[lo:hi]
+        out.append(tuple({k: a[k][idx] for k in FIELDS} for a in (allp, allm, allv)))
+    return [o[0] for o in out], [o[1] for o in out], [o[2] for o in out]

@@ -98,6 +98,14 @@ _sig = {
                              C.POINTER(DensifyCfg), C.POINTER(Params), C.POINTER(Params), C.POINTER(Params), _i64,
                              _P64, _vp]),
     "gs_opacity_reset": (C.c_int, [_vp, C.POINTER(Params), C.POINTER(Params), C.POINTER(Params), C.c_float, _vp]),
+    "gs_redistribute_record_bytes": (C.c_int64, []),
+    "gs_redistribute_pack": (C.c_int, [_vp, C.POINTER(Params), C.POINTER(Params), C.POINTER(Params), _i64,
+                                       C.c_uint64, _vp, _i64, _P64, _vp]),
+    "gs_redistribute_unpack": (C.c_int, [_vp, _vp, _i64, C.POINTER(Params), C.POINTER(Params), C.POINTER(Params),
+                                         _vp]),
+    "gs_redistribute": (C.c_int, [_vp, C.POINTER(Params), C.POINTER(Params), C.POINTER(Params), C.c_uint64, _vp,
+                                  _i64, _vp, _i64, C.POINTER(Params), C.POINTER(Params), C.POINTER(Params), _P64,
+                                  _P64, _vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -419,6 +427,58 @@ def opacity_reset(ctx, p, m=None, v=None, max_opacity=0.01, stream=None):
     st = _lib.gs_opacity_reset(ctx.handle, C.byref(ps), C.byref(ms) if ms else None, C.byref(vs) if vs else None,
                                C.c_float(max_opacity), _stream(stream))
     ctx.check(st)
+
+
+def redistribute_record_bytes():
+    return int(_lib.gs_redistribute_record_bytes())
+
+
+def redistribute_pack(ctx, p, m, v, n_total, seed, stream=None):
+    """NEXT-2: this rank's (index, p, m, v) records grouped by destination; returns (buf, counts)."""
+    import torch
+    ps, ms, vs = p.struct(), m.struct(), v.struct()
+    counts = np.zeros(ctx.world, np.int64)
+    rb = redistribute_record_bytes()
+    buf = torch.empty((max(p.n, 1), rb), dtype=torch.uint8, device=p.pos_op.device)
+    st = _lib.gs_redistribute_pack(ctx.handle, C.byref(ps), C.byref(ms), C.byref(vs), int(n_total),
+                                   C.c_uint64(seed), _ptr(buf), p.n, counts.ctypes.data_as(_P64), _stream(stream))
+    ctx.check(st)
+    return buf, counts
+
+
+def redistribute_unpack(ctx, recv_buf, n_recv, gid_base, device, stream=None):
+    """NEXT-2: place received records; returns (p, m, v) of the new shard."""
+    p2, m2, v2 = (GaussianParams.empty(n_recv, device, gid_base, zero=False) for _ in range(3))
+    ps, ms, vs = p2.struct(), m2.struct(), v2.struct()
+    st = _lib.gs_redistribute_unpack(ctx.handle, _ptr(recv_buf), int(n_recv), C.byref(ps), C.byref(ms),
+                                     C.byref(vs), _stream(stream))
+    ctx.check(st)
+    return p2, m2, v2
+
+
+def redistribute(ctx, p, m, v, seed, stream=None):
+    """NEXT-2 (collective, world > 1): returns the new (p, m, v) shard (size query, then move)."""
+    import torch
+    rb = redistribute_record_bytes()
+    dev = p.pos_op.device
+    ps, ms, vs = p.struct(), m.struct(), v.struct()
+    nt, no = C.c_int64(0), C.c_int64(0)
+    q = [Params(None, None, None, None, 0, 0) for _ in range(3)]
+    st = _lib.gs_redistribute(ctx.handle, C.byref(ps), C.byref(ms), C.byref(vs), C.c_uint64(seed), None, 0, None, 0,
+                              *[C.byref(o) for o in q], C.byref(nt), C.byref(no), _stream(stream))
+    ctx.check(st)
+    n_out = int(no.value)
+    sbuf = torch.empty((max(p.n, 1), rb), dtype=torch.uint8, device=dev)
+    rbuf = torch.empty((max(n_out, 1), rb), dtype=torch.uint8, device=dev)
+    new = [GaussianParams.empty(n_out, dev, 0, zero=False) for _ in range(3)]
+    outs = [g.struct() for g in new]
+    st = _lib.gs_redistribute(ctx.handle, C.byref(ps), C.byref(ms), C.byref(vs), C.c_uint64(seed), _ptr(sbuf), p.n,
+                              _ptr(rbuf), n_out, *[C.byref(o) for o in outs], C.byref(nt), C.byref(no),
+                              _stream(stream))
+    ctx.check(st)
+    for g, o in zip(new, outs):
+        g.gid_base = int(o.gid_base)
+    return tuple(new)
 
 
 def exchange_grads(ctx, dL_drec, recv_counts, send_counts, dL_dsend, stream=None):

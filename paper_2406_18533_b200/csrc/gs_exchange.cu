@@ -329,3 +329,250 @@ extern "C" gs_status gs_halo_exchange(gs_ctx* c, const float* data, int fpb, con
   return p2p_exchange(c, (const char*)sbuf, soff.data(), scnt.data(), (char*)halo, roff.data(), rcnt.data(),
                       (size_t)fpb * sizeof(float), st);
 }
+
+// ------------------------------------------------------------------ NEXT-2 redistribution
+// Random redistribution of the Gaussians after densification ("redistribute the 3D
+// Gaussians after every few densification steps"; App. B.2 "random redistribution";
+// S:491-497): global index j (the rank's gid_base + local index) moves to position pi(j) of
+// the new global order, rank d owning [floor(d N / G), floor((d+1) N / G)) -- sizes differ by
+// at most one.  pi is a keyed bijection of [0, N) computed per element (4-round Feistel
+// network on the smallest even bit width covering N, cycle-walking into [0, N); reading R15),
+// so no permutation table exists anywhere and every rank agrees without communication.
+namespace {
+__host__ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  return h;
+}
+__device__ __forceinline__ uint64_t feistel_perm(uint64_t j, uint64_t N, uint32_t seed, int half) {
+  const uint32_t mask = (half >= 32) ? 0xffffffffu : ((1u << half) - 1u);
+  uint64_t y = j;
+  do {
+    uint32_t Lh = (uint32_t)(y >> half) & mask, Rh = (uint32_t)y & mask;
+    for (uint32_t r = 0; r < 4; r++) {
+      const uint32_t f = fmix32(seed ^ (r * 0x9e3779b9u) ^ fmix32(Rh + 0x7f4a7c15u * (r + 1))) & mask;
+      const uint32_t t = Lh ^ f;
+      Lh = Rh;
+      Rh = t;
+    }
+    y = ((uint64_t)Lh << half) | Rh;
+  } while (y >= N);
+  return y;
+}
+__host__ __device__ __forceinline__ int64_t range_lo(int d, int64_t N, int G) { return (int64_t)d * N / G; }
+
+constexpr int kRedistFloats = 184;  // [new index: 2 floats][pad 2][p 60][m 60][v 60]
+
+struct rplanes {
+  const float4 *pos_op, *ls, *rot, *sh;
+};
+struct wrplanes {
+  float4 *pos_op, *ls, *rot, *sh;
+};
+__device__ __forceinline__ void put60(float* d, const rplanes& p, int64_t n, int64_t i) {
+  float4* o = reinterpret_cast<float4*>(d);
+  o[0] = p.pos_op[i];
+  o[1] = p.ls[i];
+  o[2] = p.rot[i];
+#pragma unroll
+  for (int k = 0; k < 12; k++) o[3 + k] = p.sh[(int64_t)k * n + i];
+}
+__device__ __forceinline__ void get60(const float* s, const wrplanes& p, int64_t n, int64_t i) {
+  const float4* o = reinterpret_cast<const float4*>(s);
+  p.pos_op[i] = o[0];
+  p.ls[i] = o[1];
+  p.rot[i] = o[2];
+#pragma unroll
+  for (int k = 0; k < 12; k++) p.sh[(int64_t)k * n + i] = o[3 + k];
+}
+
+__global__ void k_redist_count(int64_t n, int64_t base, int64_t N, uint32_t seed, int half, int G,
+                               int64_t* __restrict__ counts) {
+  __shared__ int s_c[GS_MAX_WORLD];
+  if (threadIdx.x < GS_MAX_WORLD) s_c[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const uint64_t y = feistel_perm((uint64_t)(base + i), (uint64_t)N, seed, half);
+    int d = (int)((y * (uint64_t)G) / (uint64_t)N);
+    while (d + 1 < G && range_lo(d + 1, N, G) <= (int64_t)y) d++;
+    while (d > 0 && range_lo(d, N, G) > (int64_t)y) d--;
+    atomicAdd(&s_c[d], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < G && s_c[threadIdx.x]) atomicAdd((unsigned long long*)&counts[threadIdx.x], (unsigned long long)s_c[threadIdx.x]);
+}
+
+__global__ void k_redist_pack(rplanes P, rplanes M, rplanes V, int64_t n, int64_t base, int64_t N, uint32_t seed,
+                              int half, int G, int64_t* __restrict__ cursor, float* __restrict__ buf) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t y = feistel_perm((uint64_t)(base + i), (uint64_t)N, seed, half);
+  int d = (int)((y * (uint64_t)G) / (uint64_t)N);
+  while (d + 1 < G && range_lo(d + 1, N, G) <= (int64_t)y) d++;
+  while (d > 0 && range_lo(d, N, G) > (int64_t)y) d--;
+  const int64_t slot = (int64_t)atomicAdd((unsigned long long*)&cursor[d], 1ull);  // any order: placement is by index
+  float* rec = buf + slot * kRedistFloats;
+  const int64_t local = (int64_t)y - range_lo(d, N, G);
+  reinterpret_cast<int64_t*>(rec)[0] = local;
+  put60(rec + 4, P, n, i);
+  put60(rec + 64, M, n, i);
+  put60(rec + 124, V, n, i);
+}
+
+__global__ void k_redist_unpack(const float* __restrict__ buf, int64_t n_recv, wrplanes P, wrplanes M, wrplanes V,
+                                int64_t n_out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_recv) return;
+  const float* rec = buf + r * kRedistFloats;
+  const int64_t o = reinterpret_cast<const int64_t*>(rec)[0];
+  if (o < 0 || o >= n_out) __trap();  // corrupt transfer: never a silent misplacement
+  get60(rec + 4, P, n_out, o);
+  get60(rec + 64, M, n_out, o);
+  get60(rec + 124, V, n_out, o);
+}
+
+int feistel_half(int64_t N) {
+  int k = 2;
+  while (k < 64 && (1ll << k) < N) k++;
+  if (k & 1) k++;
+  return k / 2;
+}
+rplanes rp_of(const gs_params* q) {
+  return rplanes{(const float4*)q->pos_op, (const float4*)q->log_scale, (const float4*)q->rot, (const float4*)q->sh};
+}
+wrplanes wp_of(gs_params* q) {
+  return wrplanes{(float4*)q->pos_op, (float4*)q->log_scale, (float4*)q->rot, (float4*)q->sh};
+}
+}  // namespace
+
+extern "C" gs_status gs_redistribute_pack(gs_ctx* c, const gs_params* p, const gs_params* m, const gs_params* v,
+                                          int64_t n_total, uint64_t seed, void* send_buf, int64_t cap,
+                                          int64_t* send_counts_h, void* stream) {
+  if (!c) return GS_EINVAL;
+  GS_REQUIRE(c, p && m && v && send_counts_h, "null argument");
+  GS_REQUIRE(c, m->n == p->n && v->n == p->n, "m/v mis-sized");
+  GS_REQUIRE(c, n_total >= p->gid_base + p->n && n_total < (1ll << 32), "n_total out of range");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int G = c->world;
+  const int64_t n = p->n;
+  int64_t* cnt = (int64_t*)gs_slot_get(c, SLOT_MISC, 2 * GS_MAX_WORLD * sizeof(int64_t), st);
+  if (!cnt) return gs_fail(c, GS_ECUDA, "scratch");
+  GS_CUDA(c, cudaMemsetAsync(cnt, 0, 2 * GS_MAX_WORLD * sizeof(int64_t), st));
+  const int half = feistel_half(n_total);
+  const uint32_t sd = (uint32_t)(seed ^ (seed >> 32));
+  if (n > 0) {
+    ++c->launches;
+    k_redist_count<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, p->gid_base, n_total, sd, half, G, cnt);
+  }
+  GS_CUDA(c, cudaMemcpyAsync(c->pinned, cnt, G * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(c, cudaStreamSynchronize(st));
+  int64_t tot = 0;
+  for (int g = 0; g < G; g++) {
+    send_counts_h[g] = c->pinned[g];
+    c->pinned[GS_MAX_WORLD + g] = tot;  // cursors = exclusive prefix
+    tot += c->pinned[g];
+  }
+  if (tot > cap) return gs_fail(c, GS_ECAPACITY, "redistribution send capacity %lld < %lld", (long long)cap,
+                                (long long)tot);
+  if (n == 0) return GS_OK;
+  GS_REQUIRE(c, send_buf != nullptr, "null send_buf");
+  GS_CUDA(c, cudaMemcpyAsync(cnt + GS_MAX_WORLD, c->pinned + GS_MAX_WORLD, G * sizeof(int64_t),
+                             cudaMemcpyHostToDevice, st));
+  ++c->launches;
+  k_redist_pack<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rp_of(p), rp_of(m), rp_of(v), n, p->gid_base, n_total,
+                                                            sd, half, G, cnt + GS_MAX_WORLD, (float*)send_buf);
+  GS_LAUNCH_CHECK(c, "redistribute pack");
+  return GS_OK;
+}
+
+extern "C" gs_status gs_redistribute_unpack(gs_ctx* c, const void* recv_buf, int64_t n_recv, gs_params* p_out,
+                                            gs_params* m_out, gs_params* v_out, void* stream) {
+  if (!c) return GS_EINVAL;
+  GS_REQUIRE(c, p_out && m_out && v_out, "null argument");
+  GS_REQUIRE(c, n_recv == p_out->n && m_out->n == p_out->n && v_out->n == p_out->n,
+             "outputs must hold exactly the received Gaussians");
+  if (n_recv == 0) return GS_OK;
+  GS_REQUIRE(c, recv_buf != nullptr, "null recv_buf");
+  ++c->launches;
+  k_redist_unpack<<<(unsigned)((n_recv + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      (const float*)recv_buf, n_recv, wp_of(p_out), wp_of(m_out), wp_of(v_out), p_out->n);
+  GS_LAUNCH_CHECK(c, "redistribute unpack");
+  return GS_OK;
+}
+
+extern "C" int64_t gs_redistribute_record_bytes(void) { return kRedistFloats * sizeof(float); }
+
+extern "C" gs_status gs_redistribute(gs_ctx* c, const gs_params* p, const gs_params* m, const gs_params* v,
+                                     uint64_t seed, void* send_buf, int64_t send_cap, void* recv_buf,
+                                     int64_t recv_cap, gs_params* p_out, gs_params* m_out, gs_params* v_out,
+                                     int64_t* n_total_h, int64_t* n_out_h, void* stream) {
+  if (!c) return GS_EINVAL;
+  GS_REQUIRE(c, p && n_total_h && n_out_h, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int G = c->world, r = c->rank;
+  if (G == 1) {  // nothing to move: the single shard is already the new order's owner
+    *n_total_h = *n_out_h = p->n;
+    return gs_fail(c, GS_ENOTSUP, "world 1: redistribution is the identity, keep the shard");
+  }
+#ifdef GS_WITH_NCCL
+  if (!c->comm) return gs_fail(c, GS_EINVAL, "virtual context (no communicator): collectives unavailable");
+  // local argument checks first: a rank returning after a collective would desynchronise them
+  GS_REQUIRE(c, m && v && m->n == p->n && v->n == p->n, "m/v mis-sized");
+  GS_REQUIRE(c, recv_buf == nullptr || (send_buf != nullptr || p->n == 0) && send_cap >= p->n,
+             "send buffer must hold the shard");
+  // shard sizes -> N and this rank's global base (every rank's gid ranges are contiguous)
+  int64_t* dbuf = (int64_t*)gs_slot_get(c, SLOT_COUNT_GATHER, (G + G * G + 2) * sizeof(int64_t), st);
+  if (!dbuf) return gs_fail(c, GS_ECUDA, "scratch");
+  c->pinned[0] = p->n;
+  GS_CUDA(c, cudaMemcpyAsync(dbuf, c->pinned, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  GS_NCCL(c, ncclAllGather(dbuf, dbuf + 1, 1, ncclInt64, c->comm, st));
+  GS_CUDA(c, cudaMemcpyAsync(c->pinned + 64, dbuf + 1, G * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(c, cudaStreamSynchronize(st));
+  int64_t N = 0, base = 0;
+  for (int g = 0; g < G; g++) {
+    if (g == r) base = N;
+    N += c->pinned[64 + g];
+  }
+  *n_total_h = N;
+  GS_REQUIRE(c, p->gid_base == base, "gid_base must be the rank's offset in the global order");
+  const int64_t n_out = range_lo(r + 1, N, G) - range_lo(r, N, G);
+  *n_out_h = n_out;
+  if (recv_buf == nullptr) return GS_OK;  // size query (every rank passes NULL together)
+  // recv_cap below the queried size is a contract violation (the other ranks continue)
+  GS_REQUIRE(c, recv_cap >= n_out, "receive capacity %lld < %lld (query the size first)", (long long)recv_cap,
+             (long long)n_out);
+  GS_REQUIRE(c, p_out && m_out && v_out && p_out->n == n_out && m_out->n == n_out && v_out->n == n_out,
+             "output planes must be laid out for the queried size");
+  int64_t scnt[GS_MAX_WORLD];
+  gs_status s = gs_redistribute_pack(c, p, m, v, N, seed, send_buf, send_cap, scnt, stream);
+  if (s != GS_OK) return s;
+  // count matrix (all-gather of every rank's send counts)
+  for (int g = 0; g < G; g++) c->pinned[g] = scnt[g];
+  GS_CUDA(c, cudaMemcpyAsync(dbuf, c->pinned, G * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  GS_NCCL(c, ncclAllGather(dbuf, dbuf + G, G, ncclInt64, c->comm, st));
+  GS_CUDA(c, cudaMemcpyAsync(c->pinned + 64, dbuf + G, G * G * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(c, cudaStreamSynchronize(st));
+  int64_t soff[GS_MAX_WORLD], roff[GS_MAX_WORLD], rcnt[GS_MAX_WORLD];
+  int64_t so = 0, ro = 0;
+  for (int g = 0; g < G; g++) {
+    soff[g] = so;
+    so += scnt[g];
+    rcnt[g] = c->pinned[64 + g * G + r];
+    roff[g] = ro;
+    ro += rcnt[g];
+  }
+  if (ro != n_out) return gs_fail(c, GS_EINVAL, "redistribution counts inconsistent (%lld != %lld)", (long long)ro,
+                                  (long long)n_out);
+  s = p2p_exchange(c, (const char*)send_buf, soff, scnt, (char*)recv_buf, roff, rcnt, kRedistFloats * sizeof(float),
+                   st);
+  if (s != GS_OK) return s;
+  p_out->gid_base = m_out->gid_base = v_out->gid_base = range_lo(r, N, G);
+  return gs_redistribute_unpack(c, recv_buf, n_out, p_out, m_out, v_out, stream);
+#else
+  return gs_fail(c, GS_ENOTSUP, "built without NCCL");
+#endif
+}

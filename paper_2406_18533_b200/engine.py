@@ -41,7 +41,8 @@ class _Buf:
 class GrendelTrainer:
     def __init__(self, ctx: L.Context, params: L.GaussianParams, width: int, height: int, n_views: int,
                  n_images: int, lr=DEFAULT_LR, cost_mode=L.COST_MEASURED, bg=(0.0, 0.0, 0.0),
-                 rebalance=True, dp=None, device=None, split_adam=True, loss="l1", ssim_lambda=0.2):
+                 rebalance=True, dp=None, device=None, split_adam=True, loss="l1", ssim_lambda=0.2,
+                 densify_stats=False):
         self.ctx, self.p = ctx, params
         self.device = device or params.pos_op.device
         self.W, self.H, self.b = width, height, n_views
@@ -52,6 +53,9 @@ class GrendelTrainer:
         if loss not in ("l1", "ssim"):
             raise ValueError("loss must be 'l1' or 'ssim' (L1 + D-SSIM, NEXT-1)")
         self.loss_kind, self.ssim_lambda = loss, float(ssim_lambda)
+        # NEXT-2: densification statistics (accum, denom, max screen radius) per owned Gaussian
+        self.collect_densify = bool(densify_stats)
+        self.dstats = self._new_stats(params.n) if densify_stats else None
         self.m, self.v = params.zeros_like(), params.zeros_like()
         # parameter-gradient buffer: gs_adam_step then runs backward and Adam as two passes
         # (faster than the fused single kernel on B200)
@@ -112,6 +116,37 @@ class GrendelTrainer:
             self.rgb.ensure(no), self.maps.ensure(no)
         self.dp = saved
         torch.cuda.synchronize()
+
+    def _new_stats(self, n):
+        return tuple(torch.zeros(max(n, 1), dtype=torch.float32, device=self.device) for _ in range(3))
+
+    def densify(self, cfg=None, noise=None, generator=None):
+        """NEXT-2: one densify-and-prune event on this rank's shard (local).  noise:
+        N(0,1) draws [n, 2, 3] for split children (drawn here from `generator` if None).
+        Replaces the parameters, Adam state and index buffers; returns the counts
+        (kept, clones, children, total)."""
+        if self.dstats is None:
+            raise RuntimeError("construct the trainer with densify_stats=True")
+        cfg = cfg if cfg is not None else L.densify_cfg()
+        n = self.p.n
+        if noise is None:
+            noise = torch.randn((n, 2, 3), dtype=torch.float32, device=self.device, generator=generator)
+        p2, m2, v2, counts = L.densify(self.ctx, self.p, self.m, self.v, *self.dstats, noise, cfg)
+        self._replace_shard(p2, m2, v2)
+        return counts
+
+    def opacity_reset(self, max_opacity=0.01):
+        """NEXT-2: opacity reset."""
+        L.opacity_reset(self.ctx, self.p, self.m, self.v, max_opacity)
+
+    def _replace_shard(self, p, m, v):
+        self.p, self.m, self.v = p, m, v
+        if self.g is not None:
+            self.g = p.zeros_like()
+        self.bwd_index = torch.empty(L.project_index_bytes(self.ctx, p.n, self.b), dtype=torch.uint8,
+                                     device=self.device)
+        if self.dstats is not None:
+            self.dstats = self._new_stats(p.n)
 
     def _halo(self, data, buf, cams, dp, st):
         """Other ranks' blocks within the D-SSIM window reach (world > 1; collective)."""
@@ -218,6 +253,8 @@ class GrendelTrainer:
             L.exchange_grads(ctx, self.drec.t, recv_counts, send_counts, self.dsend.t, st)
             dsend = self.dsend.t
         rec("exchange_grads", 1)
+        if self.collect_densify:  # NEXT-2 statistics from this step's record gradients
+            L.densify_stats(ctx, cams, dp, self.p.n, self.bwd_index, self.send.t, dsend, self.b, *self.dstats, st)
         # A7 + A8 transformation backward + Adam
         rec("adam", 0)
         hp = L.adam_hparams(self.lr, self.b, self.step_count)

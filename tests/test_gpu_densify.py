@@ -102,3 +102,36 @@ def test_stats_match_oracle_backward():
     np.testing.assert_array_equal(mr.cpu().numpy(), orr.astype(np.float32))
     e_inf, e_2 = grad_metric(acc.cpu().numpy()[:, None], oa[:, None])
     assert e_inf <= 1e-3 and e_2 <= 1e-3, (e_inf, e_2)
+
+
+def test_redistribution_virtual_ranks_match_oracle():
+    """gs_redistribute_pack / _unpack on virtual ranks (the test moves the records between
+    them, as NCCL does in gs_redistribute): new shards bit-identical to the oracle's."""
+    rng = np.random.default_rng(9)
+    sizes = [1500, 200, 3100]
+    G, N = len(sizes), sum(sizes)
+    shards = [_shard(n, rng) for n in sizes]
+    ms = [_shard(n, rng) for n in sizes]
+    vs = [_shard(n, rng) for n in sizes]
+    seed = 424242
+    bases = np.concatenate([[0], np.cumsum(sizes)])
+    packed = []
+    for r in range(G):
+        ctx = L.Context(0, r, G)
+        p, m, v = _gp(shards[r]), _gp(ms[r]), _gp(vs[r])
+        for g in (p, m, v):
+            g.gid_base = int(bases[r])
+        buf, counts = L.redistribute_pack(ctx, p, m, v, N, seed)
+        torch.cuda.synchronize()
+        off = np.concatenate([[0], np.cumsum(counts)])
+        packed.append([buf[off[d]:off[d + 1]] for d in range(G)])
+    new_o, nm_o, nv_o = D.redistribute(shards, ms, vs, seed)
+    for d in range(G):
+        ctx = L.Context(0, d, G)
+        recv = torch.cat([packed[r][d] for r in range(G)])
+        lo = d * N // G
+        p2, m2, v2 = L.redistribute_unpack(ctx, recv, recv.shape[0], lo, DEV)
+        torch.cuda.synchronize()
+        assert p2.n == len(new_o[d]["pos"]) and p2.gid_base == lo
+        for got, want in ((p2, new_o[d]), (m2, nm_o[d]), (v2, nv_o[d])):
+            np.testing.assert_array_equal(got.to_flat(), _flat(want).astype(np.float32))

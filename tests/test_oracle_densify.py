@@ -95,3 +95,30 @@ def test_opacity_reset():
     assert abs(sig(float(s2["opac_logit"][0])) - 0.01) < 1e-7  # 0.9 -> 0.01
     assert s2["opac_logit"][1] == np.float32(logit[1])  # already below: unchanged
     assert not np.any(m2["opac_logit"]) and not np.any(v2["opac_logit"])
+
+
+def test_redistribution_permutation_is_a_bijection():
+    for N in (1, 2, 3, 7, 64, 100, 1000, 4097):
+        for seed in (0, 12345, 2 ** 40 + 7):
+            img = sorted(D.perm(j, N, seed) for j in range(N))
+            assert img == list(range(N))
+
+
+def test_redistribution_sizes_and_multiset():
+    # sizes {10, 2} -> {6, 6}; multiset of Gaussians (with their Adam state) unchanged
+    rng = np.random.default_rng(4)
+    sizes = [(10, 2), (5, 5, 5), (1, 0, 30, 2)]
+    for sz in sizes:
+        shards = [_shard(n, rng) for n in sz]
+        ms = [{k: a[k] * 2 for k in a} for a in shards]
+        vs = [{k: a[k] * 3 for k in a} for a in shards]
+        new, nm, nv = D.redistribute(shards, ms, vs, seed=99)
+        ns = [len(s["pos"]) for s in new]
+        assert sum(ns) == sum(sz) and max(ns) - min(ns) <= 1
+        key = lambda ds: sorted(map(tuple, np.concatenate([d["sh"] for d in ds]).round(12)))
+        assert key(new) == key(shards)
+        for s, m_, v_ in zip(new, nm, nv):  # state travels with its Gaussian
+            np.testing.assert_array_equal(m_["pos"], s["pos"] * 2)
+            np.testing.assert_array_equal(v_["sh"], s["sh"] * 3)
+    assert [len(s["pos"]) for s in D.redistribute([_shard(10, rng), _shard(2, rng)], [_shard(10, rng), _shard(2, rng)],
+                                                  [_shard(10, rng), _shard(2, rng)], 1)[0]] == [6, 6]
