@@ -59,6 +59,13 @@ def make_scene(cfg, lo, hi):
     return fn(n, seed, lo, hi)
 
 
+def scene_extent(cams):
+    """radius of the bounding sphere of the camera centres (c = -R^T t), x 1.1 as 3DGS."""
+    cs = np.array([-np.asarray(c.R, np.float64).reshape(3, 3).T @ np.asarray(c.t, np.float64) for c in cams])
+    centre = cs.mean(0)
+    return 1.1 * float(np.linalg.norm(cs - centre, axis=1).max())
+
+
 def make_cameras(cfg):
     seed = cfg["seed"]
     if seed == 0:
@@ -231,6 +238,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--breakdown-steps", type=int, default=2)
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--densify", action="store_true",
+                    help="NEXT-2: collect densification statistics every step and time one densify event at "
+                         "the end (extra 'densify' object in the JSON line)")
     ap.add_argument("--loss", default="l1", choices=["l1", "ssim"],
                     help="l1: the hot-path loss (R11); ssim: L1 + D-SSIM, lambda 0.2 (NEXT-1)")
     args = ap.parse_args()
@@ -275,7 +285,7 @@ def main():
     gt_batch = torch.empty((cfg["b"], H, W, 3), dtype=torch.uint8, device=dev)
     cost_mode = {"measured": L.COST_MEASURED, "work": L.COST_WORK, "paper_avg": L.COST_PAPER_AVG}[args.cost_mode]
     tr = GrendelTrainer(ctx, p, W, H, cfg["b"], len(cams), cost_mode=cost_mode, rebalance=not args.no_rebalance,
-                        device=dev, loss=args.loss)
+                        device=dev, loss=args.loss, densify_stats=args.densify)
     stream = torch.cuda.current_stream()
     k_sched = [0]
 
@@ -428,6 +438,36 @@ def main():
                          "of the Gaussians (scaled, shared by b views); %.1f s of CPU work" % s["cpu_s"],
                "parts_s_per_view": {k: round(v, 3) for k, v in s["parts"].items()}}
 
+    # ---------------- NEXT-2: one densify-and-prune event over the trained shard (after all
+    # other measurements: it changes the shard), plus the per-step statistics kernel
+    dens = None
+    if args.densify:
+        n_before = tr.p.n
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(cfg["seed"] + 300)
+        noise = torch.randn((n_before, 2, 3), dtype=torch.float32, device=dev, generator=gen)
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        w0.record()
+        kc = tr.densify(L.densify_cfg(scene_extent=float(scene_extent(cams))), noise=noise, events=(d0, d1))
+        w1.record()
+        torch.cuda.synchronize()
+        dms, wms = d0.elapsed_time(d1), w0.elapsed_time(w1)
+        # algorithmic bytes: read p, m, v (3 x 240 B) + 3 statistics (12 B) + noise (24 B) per
+        # Gaussian, write p, m, v of every output Gaussian (3 x 240 B)
+        dbytes = 756.0 * n_before + 720.0 * int(kc[3])
+        hbm = float(pk.get("hbm_gbs", 6650.0))
+        dens = {"event_ms": round(dms, 3), "event_with_alloc_ms": round(wms, 3), "n_before": int(n_before),
+                "counts": {
+                    "kept": int(kc[0]), "clones": int(kc[1]), "children": int(kc[2]), "total": int(kc[3])},
+                "stats_ms_per_step": round(calls.get("densify_stats", 0.0), 3),
+                "roofline": {"bound": "hbm", "achieved": round(dbytes / (dms / 1000.0) / 1e9, 1), "peak": hbm,
+                             "unit": "GB/s", "frac": round(dbytes / (dms / 1000.0) / 1e9 / hbm, 4)},
+                "note": "event_ms: device time of the placing gs_densify call (classify, scan, write); "
+                        "event_with_alloc_ms adds the size query and the new shard's allocation; statistics "
+                        "from the timed steps of this run"}
+
     if rank == 0:
         raster_ms_view = (calls.get("render_fwd", 0) + calls.get("render_bwd", 0)) / cfg["b"]
         line = {"metric": METRIC, "value": round(value, 3), "unit": "views/s", "n_gpus": world, "steps": args.steps,
@@ -451,6 +491,8 @@ def main():
                          "E_b": int(Eb), "E_bc": int(Ebc), "records": int(counts["n_recv"]),
                          "pairs": int(counts["n_pairs"])},
                 "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "setup_s": round(setup_s, 1)}
+        if dens is not None:
+            line["densify"] = dens
         s = json.dumps(line)
         print(s, flush=True)
         if args.json_out:

@@ -395,8 +395,10 @@ def densify_cfg(grad_thresh=0.0002, percent_dense=0.01, scene_extent=1.0, min_op
     return DensifyCfg(grad_thresh, percent_dense, scene_extent, min_opacity, max_screen_size)
 
 
-def densify(ctx, p, m, v, accum, denom, max_radius, noise, cfg, stream=None):
-    """NEXT-2: one densify-and-prune event; returns (p2, m2, v2, counts[4]) as new buffers."""
+def densify(ctx, p, m, v, accum, denom, max_radius, noise, cfg, stream=None, events=None):
+    """NEXT-2: one densify-and-prune event; returns (p2, m2, v2, counts[4]) as new buffers.
+    (A size query, the output allocation, then the placing call; `events` = (start, end)
+    CUDA events recorded around the placing call.)"""
     ps, ms, vs = p.struct(), m.struct(), v.struct()
     counts = np.zeros(4, np.int64)
     e1, e2, e3 = (Params(None, None, None, None, 0, p.gid_base) for _ in range(3))
@@ -412,9 +414,13 @@ def densify(ctx, p, m, v, accum, denom, max_radius, noise, cfg, stream=None):
     if n2 == 0:
         return p2, m2, v2, counts
     ps2, ms2, vs2 = p2.struct(), m2.struct(), v2.struct()
+    if events is not None:
+        events[0].record()
     st = _lib.gs_densify(ctx.handle, C.byref(ps), C.byref(ms), C.byref(vs), _ptr(accum), _ptr(denom),
                          _ptr(max_radius), _ptr(noise), C.byref(cfg), C.byref(ps2), C.byref(ms2), C.byref(vs2),
                          n2, counts.ctypes.data_as(_P64), _stream(stream))
+    if events is not None:
+        events[1].record()
     ctx.check(st)
     return p2, m2, v2, counts
 

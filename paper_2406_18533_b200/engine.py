@@ -120,7 +120,7 @@ class GrendelTrainer:
     def _new_stats(self, n):
         return tuple(torch.zeros(max(n, 1), dtype=torch.float32, device=self.device) for _ in range(3))
 
-    def densify(self, cfg=None, noise=None, generator=None):
+    def densify(self, cfg=None, noise=None, generator=None, events=None):
         """NEXT-2: one densify-and-prune event on this rank's shard (local).  noise:
         N(0,1) draws [n, 2, 3] for split children (drawn here from `generator` if None).
         Replaces the parameters, Adam state and index buffers; returns the counts
@@ -131,7 +131,7 @@ class GrendelTrainer:
         n = self.p.n
         if noise is None:
             noise = torch.randn((n, 2, 3), dtype=torch.float32, device=self.device, generator=generator)
-        p2, m2, v2, counts = L.densify(self.ctx, self.p, self.m, self.v, *self.dstats, noise, cfg)
+        p2, m2, v2, counts = L.densify(self.ctx, self.p, self.m, self.v, *self.dstats, noise, cfg, events=events)
         self._replace_shard(p2, m2, v2)
         return counts
 
@@ -254,7 +254,9 @@ class GrendelTrainer:
             dsend = self.dsend.t
         rec("exchange_grads", 1)
         if self.collect_densify:  # NEXT-2 statistics from this step's record gradients
+            rec("densify_stats", 0)
             L.densify_stats(ctx, cams, dp, self.p.n, self.bwd_index, self.send.t, dsend, self.b, *self.dstats, st)
+            rec("densify_stats", 1)
         # A7 + A8 transformation backward + Adam
         rec("adam", 0)
         hp = L.adam_hparams(self.lr, self.b, self.step_count)
@@ -273,7 +275,7 @@ class GrendelTrainer:
 
 
 def make_events(names=("project", "exchange", "bin_sort", "render_fwd", "loss", "render_bwd", "exchange_grads",
-                       "adam", "rebalance")):
+                       "densify_stats", "adam", "rebalance")):
     return {n: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for n in names}
 
 
