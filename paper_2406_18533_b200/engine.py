@@ -50,6 +50,7 @@ class GrendelTrainer:
         self.B = n_views * self.Wt * self.Ht
         self.G, self.rank = ctx.world, ctx.rank
         self.lr, self.cost_mode, self.bg, self.do_rebalance = tuple(lr), cost_mode, tuple(bg), rebalance
+        self.beta1, self.beta2 = 0.9, 0.999  # before the Eq. (2) scaling beta^b the kernel applies
         if loss not in ("l1", "ssim"):
             raise ValueError("loss must be 'l1' or 'ssim' (L1 + D-SSIM, NEXT-1)")
         self.loss_kind, self.ssim_lambda = loss, float(ssim_lambda)
@@ -259,7 +260,7 @@ class GrendelTrainer:
             rec("densify_stats", 1)
         # A7 + A8 transformation backward + Adam
         rec("adam", 0)
-        hp = L.adam_hparams(self.lr, self.b, self.step_count)
+        hp = L.adam_hparams(self.lr, self.b, self.step_count, self.beta1, self.beta2)
         L.adam_step(ctx, self.p, self.m, self.v, self.g, cams, dp, dsend, self.bwd_index, hp,
                     L.ADAM_GRAD | L.ADAM_APPLY, st)
         rec("adam", 1)
