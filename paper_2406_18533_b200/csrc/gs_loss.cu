@@ -86,18 +86,36 @@ __device__ __forceinline__ int nb_of(int i) { return i < 5 ? 0 : (i < 21 ? 1 : 2
 // row r spans columns 11..36 of the three blocks side by side (48 columns = 12 float4), of
 // which float4s 2..9 overlap it.  Zero where there is no block (outside the grid).
 __device__ __forceinline__ void stage_planes(const float* const* s_src, int np, int plane0, float* dst) {
-  for (int it = threadIdx.x; it < np * kS * 8; it += kThreads) {
-    const int pl = it / (kS * 8), r = (it / 8) % kS, f = 2 + it % 8;
-    const int br = nb_of(r), bc = f >> 2, row = (r + 11) & 15;  // source block row/col, row in block
-    const float* src = s_src[br * 3 + bc];
-    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (src) q = __ldg(reinterpret_cast<const float4*>(src + (plane0 + pl) * 256 + row * 16 + (f & 3) * 4));
-    const float e[4] = {q.x, q.y, q.z, q.w};
-    float* d = dst + (pl * kS + r) * kLd;
+  // loads of kU items are issued before their stores (memory-level parallelism: the staging
+  // is latency-bound, each CTA waits for it before any arithmetic)
+  constexpr int kU = 4;
+  const int total = np * kS * 8;
+  for (int base = threadIdx.x; base < total; base += kThreads * kU) {
+    float4 q[kU];
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
-      const int col = f * 4 + k - 11;
-      if (col >= 0 && col < kS) d[col] = e[k];
+    for (int u = 0; u < kU; u++) {
+      const int it = base + u * kThreads;
+      q[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (it < total) {
+        const int pl = it / (kS * 8), r = (it / 8) % kS, f = 2 + it % 8;
+        const float* src = s_src[nb_of(r) * 3 + (f >> 2)];
+        if (src) q[u] = __ldg(reinterpret_cast<const float4*>(src + (plane0 + pl) * 256 + ((r + 11) & 15) * 16 +
+                                                              (f & 3) * 4));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; u++) {
+      const int it = base + u * kThreads;
+      if (it < total) {
+        const int pl = it / (kS * 8), r = (it / 8) % kS, f = 2 + it % 8;
+        const float e[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+        float* d = dst + (pl * kS + r) * kLd;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const int col = f * 4 + k - 11;
+          if (col >= 0 && col < kS) d[col] = e[k];
+        }
+      }
     }
   }
 }
