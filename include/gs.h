@@ -143,7 +143,9 @@ gs_status gs_project(gs_ctx* ctx, const gs_params* p, const gs_camera* cams_h, i
  * P:529).  Exchanges the G x G count matrix (NCCL all-gather, host sync), then grouped
  * ncclSend/ncclRecv.  recv_rec receives the records ordered by ascending source rank,
  * so within each view they are in ascending gid.  recv_counts_h[G] = records from each
- * source; *n_recv_h = total.  GS_ECAPACITY if it exceeds recv_cap (nothing transferred).
+ * source; *n_recv_h = total.  The capacities travel with the counts: if ANY rank's total
+ * exceeds its recv_cap, EVERY rank returns GS_ECAPACITY (nothing transferred, each with its
+ * own counts), so a retry after growing the buffer stays collective.
  * world == 1: identity; recv_rec may alias send_rec (then nothing is copied).            */
 gs_status gs_exchange(gs_ctx* ctx, const void* send_rec, const int64_t* send_counts_h,
                       void* recv_rec, int64_t recv_cap, int64_t* recv_counts_h,

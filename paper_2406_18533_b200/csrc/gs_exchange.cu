@@ -51,23 +51,47 @@ extern "C" gs_status gs_exchange(gs_ctx* c, const void* send_rec, const int64_t*
   cudaStream_t st = (cudaStream_t)stream;
   const int G = c->world, r = c->rank;
   int64_t mat[GS_MAX_WORLD * GS_MAX_WORLD];
+  int64_t caps[GS_MAX_WORLD];
   if (G == 1) {
     mat[0] = send_counts_h[0];
+    caps[0] = recv_cap;
   } else {
 #ifdef GS_WITH_NCCL
     if (!c->comm) return gs_fail(c, GS_EINVAL, "virtual context (no communicator): collectives unavailable");
-    int64_t* dbuf = (int64_t*)gs_slot_get(c, SLOT_COUNT_GATHER, (G + G * G) * sizeof(int64_t), st);
+    // every rank's send counts AND receive capacity: a capacity shortfall on any rank makes
+    // every rank return GS_ECAPACITY together (a lone early return would leave its peers
+    // blocked in the point-to-point phase)
+    const int W1 = G + 1;
+    int64_t* dbuf = (int64_t*)gs_slot_get(c, SLOT_COUNT_GATHER, (W1 + G * W1) * sizeof(int64_t), st);
     if (!dbuf) return gs_fail(c, GS_ECUDA, "scratch");
     for (int g = 0; g < G; g++) c->pinned[g] = send_counts_h[g];
-    GS_CUDA(c, cudaMemcpyAsync(dbuf, c->pinned, G * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    GS_NCCL(c, ncclAllGather(dbuf, dbuf + G, G, ncclInt64, c->comm, st));
-    GS_CUDA(c, cudaMemcpyAsync(c->pinned + 64, dbuf + G, G * G * sizeof(int64_t),
-                               cudaMemcpyDeviceToHost, st));
+    c->pinned[G] = recv_cap;
+    GS_CUDA(c, cudaMemcpyAsync(dbuf, c->pinned, W1 * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    GS_NCCL(c, ncclAllGather(dbuf, dbuf + W1, W1, ncclInt64, c->comm, st));
+    GS_CUDA(c, cudaMemcpyAsync(c->pinned + 64, dbuf + W1, G * W1 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     GS_CUDA(c, cudaStreamSynchronize(st));
-    for (int k = 0; k < G * G; k++) mat[k] = c->pinned[64 + k];
+    for (int a = 0; a < G; a++) {
+      for (int b2 = 0; b2 < G; b2++) mat[a * G + b2] = c->pinned[64 + a * W1 + b2];
+      caps[a] = c->pinned[64 + a * W1 + G];
+    }
 #else
     return gs_fail(c, GS_ENOTSUP, "built without NCCL");
 #endif
+  }
+  {
+    bool short_any = false;
+    for (int d = 0; d < G; d++) {
+      int64_t need = 0;
+      for (int g = 0; g < G; g++) need += mat[g * G + d];
+      short_any |= need > caps[d];
+    }
+    if (short_any) {
+      int64_t mine = 0;
+      for (int g = 0; g < G; g++) mine += (recv_counts_h[g] = mat[g * G + r]);
+      *n_recv_h = mine;
+      return gs_fail(c, GS_ECAPACITY, "recv capacity short on some rank (this rank: %lld for %lld)",
+                     (long long)recv_cap, (long long)mine);
+    }
   }
   int64_t soff[GS_MAX_WORLD + 1], roff[GS_MAX_WORLD + 1], scnt[GS_MAX_WORLD], rcnt[GS_MAX_WORLD];
   if (gs_exchange_plan(mat, G, r, soff, roff) != GS_OK) return gs_fail(c, GS_EINVAL, "bad counts");
@@ -77,8 +101,6 @@ extern "C" gs_status gs_exchange(gs_ctx* c, const void* send_rec, const int64_t*
     recv_counts_h[g] = rcnt[g];
   }
   *n_recv_h = roff[G];
-  if (roff[G] > recv_cap)
-    return gs_fail(c, GS_ECAPACITY, "recv capacity %lld < %lld", (long long)recv_cap, (long long)roff[G]);
   if (roff[G] + soff[G] == 0) return GS_OK;
   GS_REQUIRE(c, send_rec && recv_rec, "null record buffer");
   return p2p_exchange(c, (const char*)send_rec, soff, scnt, (char*)recv_rec, roff, rcnt,

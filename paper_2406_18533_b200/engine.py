@@ -150,14 +150,14 @@ class GrendelTrainer:
             self.dstats = self._new_stats(p.n)
 
     def _halo(self, data, buf, cams, dp, st):
-        """Other ranks' blocks within the D-SSIM window reach (world > 1; collective)."""
+        """Other ranks' blocks within the D-SSIM window reach (world > 1; collective).  The
+        halo size is known locally (gs_halo_plan, host only), so the buffers are grown before
+        the collective call: no rank can fail it alone."""
         if self.G == 1:
             return 0
-        while True:
-            try:
-                return L.halo_exchange(self.ctx, data, cams, dp, buf.t, self.halo_ids.t, st)
-            except L.CapacityError as e:
-                buf.ensure(e.needed), self.halo_ids.ensure(e.needed)
+        need = len(L.halo_plan(self.ctx, cams, dp))
+        buf.ensure(need), self.halo_ids.ensure(need)
+        return L.halo_exchange(self.ctx, data, cams, dp, buf.t, self.halo_ids.t, st)
 
     @property
     def n_owned(self):
