@@ -93,7 +93,13 @@ class ClockSampler:
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
-        self.index, self.proc, self.lines = index, None, []
+        self.index, self.proc, self.lines, self.first = index, None, [], 0
+
+    def mark(self):
+        """Start of the timed region: only samples from here on count.  The sampler process is
+        started before the warm-up steps, so nvidia-smi's NVML start-up (which can hold the
+        driver for hundreds of ms on a fresh box) never lands inside the timed region."""
+        self.first = len(self.lines)
 
     def start(self):
         try:
@@ -102,6 +108,9 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 15.0:  # NVML up before anything is timed
+                time.sleep(0.05)
         except Exception:
             self.proc = None
 
@@ -117,7 +126,7 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
         rows = []
-        for ln in self.lines:
+        for ln in self.lines[self.first:]:
             f = [x.strip() for x in ln.split(",")]
             try:
                 rows.append((float(f[0]), float(f[1]), f[3:7]))
@@ -307,21 +316,27 @@ def main():
 
     # size all buffers for every batch this run will use (setup, not timed)
     tr.reserve_for([batch_cams(k) for k in range(len(sched) - 1)])
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         one_step()
     setup_s = time.perf_counter() - t_setup
 
     # ---------------- timed region (device-resident inputs)
     barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks.mark()
     l0 = ctx.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    step_ev = []
     for _ in range(args.steps):
         one_step()
+        step_ev.append(torch.cuda.Event(enable_timing=True))
+        step_ev[-1].record(stream)
     e1.record(stream)
     barrier()
+    step_ms = [e0.elapsed_time(step_ev[0])] + [a.elapsed_time(b) for a, b in zip(step_ev, step_ev[1:])]
+    print("timed steps (ms): " + " ".join("%.1f" % t for t in step_ms), file=sys.stderr, flush=True)
     clk = clocks.stop()
     launches = ctx.launch_count() - l0
     ms = e0.elapsed_time(e1)
