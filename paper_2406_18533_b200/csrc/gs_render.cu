@@ -31,6 +31,7 @@ using namespace gsd;
 namespace {
 
 constexpr int kFB = 128;    // forward: records staged per round
+constexpr int kFW = 64;     // warp-independent forward: records staged per warp round
 constexpr int kUnroll = 4;  // forward entries per unrolled group (batch padded to a multiple; 4 measured
                             // faster than 8 and 16 on C2)
 
@@ -40,21 +41,33 @@ constexpr int kUnroll = 4;  // forward entries per unrolled group (batch padded 
 // against qmax with a wide margin (5% of 1 + qmax in the exponent), so an entry is dropped only
 // when every pixel would skip it: a conservative, semantics-free cull (dropped entries are
 // no-ops for every pixel of the block).
-__device__ __forceinline__ bool block_may_hit(const float4& A, const float4& Bq, float qmax, float bx0, float by0) {
+// box_may_hit: the same test over the pixel centres [bx0, bx0 + ex] x [by0, by0 + ey] (the
+// warp-independent kernels test each warp's 8x16 half of the block).
+__device__ __forceinline__ bool box_may_hit(const float4& A, const float4& Bq, float qmax, float bx0, float by0,
+                                            float ex, float ey) {
   if (!(qmax >= 0.f)) return false;  // opacity < 1/255: never composited
   const float l11 = A.z, l21 = A.w, l22 = Bq.x;
-  const float dxh = A.x - bx0, dxl = dxh - 15.f, dyh = A.y - by0, dyl = dyh - 15.f;
+  const float dxh = A.x - bx0, dxl = dxh - ex, dyh = A.y - by0, dyl = dyh - ey;
   if (dxl <= 0.f && dxh >= 0.f && dyl <= 0.f && dyh >= 0.f) return true;
   const float a = l11 * l11, b = l11 * l21, c = l21 * l21 + l22 * l22;
   auto Q = [&](float dx, float dy) {
     const float u = fmaf(l11, dx, l21 * dy), w = l22 * dy;
     return fmaf(u, u, w * w);
   };
-  float qmin = Q(dxl, fminf(fmaxf(-b * dxl / c, dyl), dyh));
-  qmin = fminf(qmin, Q(dxh, fminf(fmaxf(-b * dxh / c, dyl), dyh)));
-  qmin = fminf(qmin, Q(fminf(fmaxf(-b * dyl / a, dxl), dxh), dyl));
-  qmin = fminf(qmin, Q(fminf(fmaxf(-b * dyh / a, dxl), dxh), dyh));
+  // edge minimisers -b dx / c and -b dy / a through one approximate reciprocal each (no IEEE
+  // division sequences): an error e in the minimiser raises q by O(e^2), far inside the margin
+  float rc, ra;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(c));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(a));
+  const float bc = -b * rc, ba = -b * ra;
+  float qmin = Q(dxl, fminf(fmaxf(bc * dxl, dyl), dyh));
+  qmin = fminf(qmin, Q(dxh, fminf(fmaxf(bc * dxh, dyl), dyh)));
+  qmin = fminf(qmin, Q(fminf(fmaxf(ba * dyl, dxl), dxh), dyl));
+  qmin = fminf(qmin, Q(fminf(fmaxf(ba * dyh, dxl), dxh), dyh));
   return !(qmin > qmax + 0.05f * (1.0f + qmax));
+}
+__device__ __forceinline__ bool block_may_hit(const float4& A, const float4& Bq, float qmax, float bx0, float by0) {
+  return box_may_hit(A, Bq, qmax, bx0, by0, 15.f, 15.f);
 }
 
 // Stage the batch's records [0, cnt) *compacted*: the records that may be hit
@@ -121,6 +134,62 @@ __device__ __forceinline__ int stage_records(const gs_rec* __restrict__ rec, con
     s_c[t] = make_float4(0.f, -1.0f, 0.f, 0.f);
   }
   return total;
+}
+
+// Warp-private form of stage_records for the warp-independent kernels (kWarp): the calling
+// warp stages records [0, cnt) of its own walk (KW / 32 per lane), culled against the pixel
+// centres of *its* 8x16 half of the block [hx0, hx0 + 7] x [hy0, hy0 + 15], compacted by
+// ballot into its private slots and padded to a multiple of `pad`.  No CTA barrier; the caller
+// must have __syncwarp'ed since its last read of the slots.
+template <int KW>
+__device__ __forceinline__ int stage_warp(const gs_rec* __restrict__ rec, const uint32_t* __restrict__ sidx, int cnt,
+                                          int pos0, float4* s_a, float4* s_b, float4* s_c, float hx0, float hy0,
+                                          bool cull, int pad) {
+  constexpr int kI = KW / 32;
+  const int lane = threadIdx.x & 31;
+  uint32_t jr[kI];
+  unsigned bal[kI];
+#pragma unroll
+  for (int i = 0; i < kI; i++) {
+    const int t = lane + 32 * i;
+    bool keep = false;
+    jr[i] = 0;
+    if (t < cnt) {
+      jr[i] = sidx[t];
+      keep = true;
+      if (cull) {
+        const float4* p = reinterpret_cast<const float4*>(rec + jr[i]);
+        const float4 a = __ldg(p), b = __ldg(p + 1);
+        keep = box_may_hit(make_float4(a.x, a.y, b.x * kLScale, b.y * kLScale),
+                           make_float4(b.z * kLScale, b.w, 0.f, 0.f),
+                           b.w > 0.f ? __log2f(255.0f * b.w) : -1.0f, hx0, hy0, 7.f, 15.f);
+      }
+    }
+    bal[i] = __ballot_sync(0xffffffffu, keep);
+  }
+  const unsigned lt = (1u << lane) - 1u;
+  int base = 0;
+#pragma unroll
+  for (int i = 0; i < kI; i++) {
+    if ((bal[i] >> lane) & 1u) {
+      const int off = base + __popc(bal[i] & lt);
+      const float4* p = reinterpret_cast<const float4*>(rec + jr[i]);
+      const float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+      s_a[off] = make_float4(a.x, a.y, b.x * kLScale, b.y * kLScale);
+      s_b[off] = make_float4(b.z * kLScale, b.w, c.x, c.y);
+      s_c[off] = make_float4(c.z, b.w > 0.f ? __log2f(255.0f * b.w) : -1.0f, __int_as_float(pos0 + lane + 32 * i),
+                             __uint_as_float(jr[i]));
+    }
+    base += __popc(bal[i]);
+  }
+  const int padded = (base + pad - 1) / pad * pad;
+  for (int t = base + lane; t < padded; t += 32) {
+    s_a[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    s_b[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    s_c[t] = make_float4(0.f, -1.0f, 0.f, 0.f);
+  }
+  __syncwarp();
+  return base;
 }
 
 template <int NT, typename T>
@@ -212,7 +281,9 @@ __device__ __forceinline__ void fwd_comp(float alpha, float cr, float cg, float 
   if (kStats) efc++;
 }
 
-template <int PPT, bool kStats, int MINB = 1>
+// kWarp (PPT = 4 only): the two warps walk the list independently, each over its own 8x16
+// half (stage_warp), with no CTA barrier until the epilogue.
+template <int PPT, bool kStats, int MINB = 1, bool kWarp = false>
 __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
     const gs_rec* __restrict__ rec, const uint32_t* __restrict__ sorted_idx,
     const int32_t* __restrict__ range, gs_geom geo, int64_t B_lo, float bg0, float bg1, float bg2,
@@ -221,7 +292,9 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
     double* __restrict__ loss_sum, int64_t* __restrict__ tile_cost, int cost_mode,
     long long* __restrict__ stats, int cull) {
   constexpr int NT = 256 / PPT;
-  __shared__ float4 s_a[kFB + kUnroll], s_b[kFB + kUnroll], s_c[kFB + kUnroll];
+  static_assert(!kWarp || PPT == 4, "warp-independent render needs PPT = 4 (one 8x16 half per warp)");
+  constexpr int kSlots = kWarp ? 2 * (kFW + kUnroll) : kFB + kUnroll;
+  __shared__ float4 s_a[kSlots], s_b[kSlots], s_c[kSlots];
   __shared__ int s_wc[kFB / 32];
   __shared__ long long s_red[NT / 32];
   __shared__ double s_redd[NT / 32];
@@ -258,18 +331,27 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
     return a;
   };
   const float bx0 = (float)(tx * 16), by0 = (float)(ty * 16);
-  for (int b0 = beg; b0 < end; b0 += kFB) {
-    if (__syncthreads_count(all_done()) == NT) break;
-    const int cnt = min(kFB, end - b0);
-    const int kept = stage_records<NT, kFB>(rec, sorted_idx + b0, cnt, b0 - beg, s_a, s_b, s_c, s_wc, bx0, by0,
-                                            cull != 0, kUnroll);
-    __syncthreads();
+  constexpr int kStep = kWarp ? kFW : kFB;
+  const int wofs = kWarp ? (tid >> 5) * (kFW + kUnroll) : 0;  // this warp's slots (kWarp)
+  for (int b0 = beg; b0 < end; b0 += kStep) {
+    const int cnt = min(kStep, end - b0);
+    int kept;
+    if constexpr (kWarp) {
+      if (__all_sync(0xffffffffu, all_done())) break;
+      kept = stage_warp<kFW>(rec, sorted_idx + b0, cnt, b0 - beg, s_a + wofs, s_b + wofs, s_c + wofs,
+                             bx0 + (float)(8 * (tid >> 5)), by0, cull != 0, kUnroll);
+    } else {
+      if (__syncthreads_count(all_done()) == NT) break;
+      kept = stage_records<NT, kFB>(rec, sorted_idx + b0, cnt, b0 - beg, s_a, s_b, s_c, s_wc, bx0, by0,
+                                    cull != 0, kUnroll);
+      __syncthreads();
+    }
     const int kept8 = (kept + kUnroll - 1) & ~(kUnroll - 1);
     for (int k0 = 0; k0 < kept8; k0 += kUnroll) {
       if (all_done()) break;
 #pragma unroll
       for (int kk = 0; kk < kUnroll; kk++) {
-        const float4 A = s_a[k0 + kk], Bq = s_b[k0 + kk], cq = s_c[k0 + kk];
+        const float4 A = s_a[wofs + k0 + kk], Bq = s_b[wofs + k0 + kk], cq = s_c[wofs + k0 + kk];
         gs_strip<PPT> e;
         q_strip<PPT>(A, Bq, fpx, fpy0, e);
         bool cj[PPT], any = false;
@@ -291,6 +373,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
         }
       }
     }
+    if constexpr (kWarp) __syncwarp();  // every lane is done with the slots before restaging
   }
   // evaluations: an in-image pixel evaluates every entry up to its stopping entry (or all)
   const int n = end - beg;
@@ -363,7 +446,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // w = w_0 - D l22, dy = dy_0 - D), so per pixel only the moments
 // acc = (sum gG, sum D gG, sum D^2 gG) are accumulated (gG = G dA, zero through the cap, R6);
 // strip_grads turns them into the 6 gradients once per entry.  (O14; R6: zero gradient through the 0.99 cap.)
-template <int D>
+template <int D, bool kBg = true>
 __device__ __forceinline__ void bwd_comp_strip(float raw, float G, const float4& Bq, float cb, float& T, float2& S01,
                                                float& S2, float2 g01, float g2, float Tf, float bgdot, float acc[3],
                                                float2& gc01, float& gc2) {
@@ -375,7 +458,10 @@ __device__ __forceinline__ void bwd_comp_strip(float raw, float G, const float4&
   gc2 = fmaf(wgt, g2, gc2);
   const float2 d01 = __fadd2_rn(make_float2(Bq.z, Bq.w), make_float2(-S01.x, -S01.y));  // c - S (r, g)
   const float d2 = cb - S2;
-  const float dA = T * fmaf(d2, g2, fmaf(d01.y, g01.y, d01.x * g01.x)) - Tf * rom * bgdot;
+  // kBg = false: black background (bg = 0), the T_final term vanishes (not left to the
+  // compiler: x * 0 does not fold in IEEE arithmetic)
+  const float dA = kBg ? T * fmaf(d2, g2, fmaf(d01.y, g01.y, d01.x * g01.x)) - Tf * rom * bgdot
+                       : T * fmaf(d2, g2, fmaf(d01.y, g01.y, d01.x * g01.x));
   S01 = __ffma2_rn(make_float2(alpha, alpha), d01, S01);
   S2 = fmaf(alpha, d2, S2);
   const float gG = raw <= kAlphaCap ? G * dA : 0.f;
@@ -441,7 +527,10 @@ __device__ __forceinline__ int red_index(int lane, bool& valid) {
   return a + b + c + d;
 }
 
-template <int PPT, bool kStats, int MINB = 1>
+// kWarp (PPT = 4 only): each warp walks its own 8x16 half back to front from its own
+// largest n_last (stage_warp), and adds its per-entry warp sums straight to dL/d(record)
+// (no per-warp slots, no CTA barrier).
+template <int PPT, bool kStats, int MINB = 1, bool kWarp = false, bool kBg = true>
 __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
     const gs_rec* __restrict__ rec, const uint32_t* __restrict__ sorted_idx,
     const int32_t* __restrict__ range, gs_geom geo, int64_t B_lo, float bg0, float bg1, float bg2,
@@ -452,11 +541,14 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   constexpr bool kOneWarp = NT == 32;
   constexpr int kNW = NT / 32;   // warps per block
   constexpr int kBB = 128;        // records staged per round
-  __shared__ float4 s_a[kBB], s_b[kBB], s_c[kBB];
+  constexpr int kBW = 64;         // kWarp: records staged per warp round
+  static_assert(!kWarp || PPT == 4, "warp-independent render needs PPT = 4 (one 8x16 half per warp)");
+  constexpr bool kDirect = kOneWarp || kWarp;  // warp sums go straight to global memory
+  __shared__ float4 s_a[kWarp ? 2 * kBW : kBB], s_b[kWarp ? 2 * kBW : kBB], s_c[kWarp ? 2 * kBW : kBB];
   __shared__ int s_wc[kBB / 32];
   // per-warp gradient slots: each (warp, entry, value) is written by exactly one lane, so no
   // shared-memory atomics (a float atomicAdd on shared memory is a CAS loop on sm_100)
-  __shared__ float s_g[kOneWarp ? 1 : kNW * kBB * 9];
+  __shared__ float s_g[kDirect ? 1 : kNW * kBB * 9];
   __shared__ int s_max[NT / 32];
   __shared__ long long s_red[NT / 32];
   const long long t0 = clock64();
@@ -490,7 +582,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   }
   const int wmax = __reduce_max_sync(0xffffffffu, mymax);
   int maxn = wmax;
-  if (!kOneWarp) {
+  if (!kOneWarp && !kWarp) {
     if (lane == 0) s_max[wid] = wmax;
     __syncthreads();
     maxn = 0;
@@ -511,20 +603,29 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   const int ridx = rvalid ? ridx_s : 0;
   const int beg = range[lb];
   int ebc = 0;
-  for (int bi = (maxn + kBB - 1) / kBB - 1; bi >= 0; bi--) {
-    const int p0 = bi * kBB;  // list position of the batch start
-    const int cnt = min(kBB, maxn - p0);
-    __syncthreads();
-    const int kept = stage_records<NT, kBB>(rec, sorted_idx + beg + p0, cnt, p0, s_a, s_b, s_c, s_wc,
-                                            (float)(tx * 16), (float)(ty * 16), cull != 0, 1);
-    if (!kOneWarp)
-      for (int t = tid; t < kNW * kBB * 9; t += NT) s_g[t] = 0.f;
-    __syncthreads();
+  constexpr int kStep = kWarp ? kBW : kBB;
+  const int wofs = kWarp ? wid * kBW : 0;  // this warp's slots (kWarp)
+  for (int bi = (maxn + kStep - 1) / kStep - 1; bi >= 0; bi--) {
+    const int p0 = bi * kStep;  // list position of the batch start
+    const int cnt = min(kStep, maxn - p0);
+    int kept;
+    if constexpr (kWarp) {
+      __syncwarp();
+      kept = stage_warp<kBW>(rec, sorted_idx + beg + p0, cnt, p0, s_a + wofs, s_b + wofs, s_c + wofs,
+                             (float)(tx * 16 + 8 * wid), (float)(ty * 16), cull != 0, 1);
+    } else {
+      __syncthreads();
+      kept = stage_records<NT, kBB>(rec, sorted_idx + beg + p0, cnt, p0, s_a, s_b, s_c, s_wc,
+                                    (float)(tx * 16), (float)(ty * 16), cull != 0, 1);
+      if (!kOneWarp)
+        for (int t = tid; t < kNW * kBB * 9; t += NT) s_g[t] = 0.f;
+      __syncthreads();
+    }
     for (int k = kept - 1; k >= 0; k--) {
-      const float4 cq = s_c[k];
+      const float4 cq = s_c[wofs + k];
       const int pos = __float_as_int(cq.z);
       if (pos >= wmax) continue;  // warp-uniform
-      const float4 A = s_a[k], Bq = s_b[k];
+      const float4 A = s_a[wofs + k], Bq = s_b[wofs + k];
       gs_strip<PPT> e;
       q_strip<PPT>(A, Bq, fpx, fpy0, e);
       bool cj[PPT], any = false;
@@ -533,42 +634,41 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
         cj[j] = pos < nl[j] && e.q[j] <= cq.y;
         any = any || cj[j];
       }
-      float gr[9];
-#pragma unroll
-      for (int q = 0; q < 9; q++) gr[q] = 0.f;
+      // lanes without a contributing pixel keep zero moments, so their strip_grads are zeros
+      float acc[3] = {0.f, 0.f, 0.f};
+      float2 gc01 = make_float2(0.f, 0.f);
+      float gc2 = 0.f;
       if (any) {
-        float acc[3] = {0.f, 0.f, 0.f};
-        float2 gc01 = make_float2(0.f, 0.f);
-        float gc2 = 0.f;
 #pragma unroll
         for (int j = 0; j < PPT; j++)
           if (cj[j]) {
             const float G = ex2_approx(-e.q[j]);
             const float raw = __fmul_rn(Bq.y, G);
             switch (j) {
-              case 0: bwd_comp_strip<0 * RS>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 1: bwd_comp_strip<1 * RS>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 2: bwd_comp_strip<2 * RS>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 3: bwd_comp_strip<3 * RS>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 4: bwd_comp_strip<4 * RS>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 5: bwd_comp_strip<5 * RS>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 6: bwd_comp_strip<6 * RS>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              default: bwd_comp_strip<7 * RS>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 0: bwd_comp_strip<0 * RS, kBg>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 1: bwd_comp_strip<1 * RS, kBg>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 2: bwd_comp_strip<2 * RS, kBg>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 3: bwd_comp_strip<3 * RS, kBg>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 4: bwd_comp_strip<4 * RS, kBg>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 5: bwd_comp_strip<5 * RS, kBg>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 6: bwd_comp_strip<6 * RS, kBg>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              default: bwd_comp_strip<7 * RS, kBg>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
             }
           }
-        strip_grads(A, Bq, e.dx, e.dy0, e.u[0], e.w[0], acc, gr);
-        gr[6] = gc01.x;
-        gr[7] = gc01.y;
-        gr[8] = gc2;
         if (kStats) {
 #pragma unroll
           for (int j = 0; j < PPT; j++) ebc += cj[j];
         }
       }
       if (__any_sync(0xffffffffu, any)) {
+        float gr[9];
+        strip_grads(A, Bq, e.dx, e.dy0, e.u[0], e.w[0], acc, gr);
+        gr[6] = gc01.x;
+        gr[7] = gc01.y;
+        gr[8] = gc2;
         const float z = warp_reduce9(gr, lane);
         if (rvalid) {
-          if (kOneWarp) {
+          if (kDirect) {
             if (z != 0.f) atomicAdd(dL_drec + (int64_t)__float_as_uint(cq.w) * 9 + ridx, z);
           } else {
             s_g[(wid * kBB + k) * 9 + ridx] = z;
@@ -576,7 +676,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
         }
       }
     }
-    if (!kOneWarp) {
+    if (!kDirect) {
       __syncthreads();
       for (int t = tid; t < kept; t += NT) {
         float* dst = dL_drec + (int64_t)__float_as_uint(s_c[t].w) * 9;
@@ -643,6 +743,17 @@ static int render_ppt() {
   return ppt;
 }
 
+// warp-independent 8x16 halves (A/B knob: GS_RENDER_WARP bit 0 forward, bit 1 backward;
+// PPT = 4 only; default both: C2 forward 22.65 -> 22.47 ms, backward 45.65 -> 44.27 ms)
+static int render_warp() {
+  static int w = -1;
+  if (w < 0) {
+    const char* e = getenv("GS_RENDER_WARP");
+    w = e ? atoi(e) & 3 : 3;
+  }
+  return w;
+}
+
 }  // namespace
 
 extern "C" gs_status gs_render_fwd(gs_ctx* c, const void* recv_rec, const uint32_t* sorted_idx,
@@ -668,6 +779,7 @@ extern "C" gs_status gs_render_fwd(gs_ctx* c, const void* recv_rec, const uint32
   const int mb = render_minb(0);
   auto kf = ppt == 2 ? (stats ? k_render_fwd<2, true> : k_render_fwd<2, false>)
           : ppt == 8 ? (stats ? k_render_fwd<8, true> : k_render_fwd<8, false>)
+          : (render_warp() & 1) ? (stats ? k_render_fwd<4, true, 16, true> : k_render_fwd<4, false, 16, true>)
           : mb == 12 ? (stats ? k_render_fwd<4, true, 12> : k_render_fwd<4, false, 12>)
                      : (stats ? k_render_fwd<4, true, 16> : k_render_fwd<4, false, 16>);
   kf<<<(unsigned)n_owned, 256 / ppt, 0, (cudaStream_t)stream>>>(
@@ -702,6 +814,9 @@ extern "C" gs_status gs_render_bwd(gs_ctx* c, const void* recv_rec, int64_t n_re
   const int mb = render_minb(1);
   auto kb = ppt == 2 ? (stats ? k_render_bwd<2, true> : k_render_bwd<2, false>)
           : ppt == 8 ? (stats ? k_render_bwd<8, true> : k_render_bwd<8, false>)
+          : (render_warp() & 2) ? (bg[0] == 0.f && bg[1] == 0.f && bg[2] == 0.f
+                                       ? (stats ? k_render_bwd<4, true, 12, true, false> : k_render_bwd<4, false, 12, true, false>)
+                                       : (stats ? k_render_bwd<4, true, 12, true> : k_render_bwd<4, false, 12, true>))
           : mb == 8 ? (stats ? k_render_bwd<4, true, 8> : k_render_bwd<4, false, 8>)
           : mb == 12 ? (stats ? k_render_bwd<4, true, 12> : k_render_bwd<4, false, 12>)
                      : (stats ? k_render_bwd<4, true, 10> : k_render_bwd<4, false, 10>);
