@@ -239,7 +239,7 @@ template <int PPT>
 __device__ __forceinline__ void q_strip(const float4& A, const float4& Bq, float px, float py0, gs_strip<PPT>& e) {
   constexpr float RS = (float)strip_layout<PPT>::RS;
   const float l11 = A.z, l21 = A.w, l22 = Bq.x;
-  const float sl21 = RS * l21, sl22 = RS * l22;
+
   // (dx, dy0) and the exponents of pixel pairs with packed fp32x2 operations (FADD2 / FFMA2 /
   // FMUL2: one issue slot for two lanes' worth of work; per element identical to the scalar
   // __fsub_rn / __fmaf_rn(u, u, w * w))
@@ -250,8 +250,10 @@ __device__ __forceinline__ void q_strip(const float4& A, const float4& Bq, float
   e.w[0] = __fmul_rn(l22, e.dy0);
 #pragma unroll
   for (int j = 1; j < PPT; j++) {
-    e.u[j] = __fsub_rn(e.u[j - 1], sl21);
-    e.w[j] = __fsub_rn(e.w[j - 1], sl22);
+    // u - RS l21 with RS a power of two: the product is exact, so the FMA equals the
+    // subtraction of the product (one instruction instead of two)
+    e.u[j] = __fmaf_rn(-RS, l21, e.u[j - 1]);
+    e.w[j] = __fmaf_rn(-RS, l22, e.w[j - 1]);
   }
 #pragma unroll
   for (int j = 0; j < PPT; j += 2) {
@@ -447,8 +449,8 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // acc = (sum gG, sum D gG, sum D^2 gG) are accumulated (gG = G dA, zero through the cap, R6);
 // strip_grads turns them into the 6 gradients once per entry.  (O14; R6: zero gradient through the 0.99 cap.)
 template <int D, bool kBg = true>
-__device__ __forceinline__ void bwd_comp_strip(float raw, float G, const float4& Bq, float cb, float& T, float2& S01,
-                                               float& S2, float2 g01, float g2, float Tf, float bgdot, float acc[3],
+__device__ __forceinline__ void bwd_comp_strip(float raw, float G, const float4& Bq, float cb, float& T, float& P,
+                                               float2 g01, float g2, float Tf, float bgdot, float acc[3],
                                                float2& gc01, float& gc2) {
   const float alpha = fminf(kAlphaCap, raw);
   const float rom = rcp_approx(1.0f - alpha);
@@ -456,14 +458,13 @@ __device__ __forceinline__ void bwd_comp_strip(float raw, float G, const float4&
   const float wgt = alpha * T;
   gc01 = __ffma2_rn(make_float2(wgt, wgt), g01, gc01);
   gc2 = fmaf(wgt, g2, gc2);
-  const float2 d01 = __fadd2_rn(make_float2(Bq.z, Bq.w), make_float2(-S01.x, -S01.y));  // c - S (r, g)
-  const float d2 = cb - S2;
+  // the behind-colour S enters only through (c - S) . dL/dC, so the pixel keeps P = S . dL/dC
+  // (S <- S + alpha (c - S)  =>  P <- P + alpha (c . dL/dC - P)): one scalar instead of S
+  const float dot = fmaf(cb, g2, fmaf(Bq.w, g01.y, Bq.z * g01.x)) - P;  // (c - S) . dL/dC
   // kBg = false: black background (bg = 0), the T_final term vanishes (not left to the
   // compiler: x * 0 does not fold in IEEE arithmetic)
-  const float dA = kBg ? T * fmaf(d2, g2, fmaf(d01.y, g01.y, d01.x * g01.x)) - Tf * rom * bgdot
-                       : T * fmaf(d2, g2, fmaf(d01.y, g01.y, d01.x * g01.x));
-  S01 = __ffma2_rn(make_float2(alpha, alpha), d01, S01);
-  S2 = fmaf(alpha, d2, S2);
+  const float dA = kBg ? T * dot - Tf * rom * bgdot : T * dot;
+  P = fmaf(alpha, dot, P);
   const float gG = raw <= kAlphaCap ? G * dA : 0.f;
   acc[0] += gG;
   if (D == 1) acc[1] += gG, acc[2] += gG;
@@ -530,6 +531,49 @@ __device__ __forceinline__ int red_index(int lane, bool& valid) {
 // kWarp (PPT = 4 only): each warp walks its own 8x16 half back to front from its own
 // largest n_last (stage_warp), and adds its per-entry warp sums straight to dL/d(record)
 // (no per-warp slots, no CTA barrier).
+// Buffered warp reduction (kWarp backward): the per-lane gradients of kF contributing
+// entries are stored as rows of 32 floats, row (slot, value) = the 32 lanes' values, then each
+// row is summed by one lane (8 float4 loads in lane-rotated chunk order: conflict-free; the
+// sum's order does not matter) and added to dL/d(record).  9 kF rows: lanes 0..31 take rows
+// 0..31, the 9 kF - 32 remaining rows are split over 32 / (9 kF - 32) lanes each and finished
+// by shuffles.  ~9 stores + 10 instructions per entry instead of the 12-shuffle transpose
+// reduction with its selects (~47).
+constexpr int kF = 4;  // entries per flush (36 rows: 32 + 4 x 8 lanes)
+__device__ __forceinline__ void flush_rows(const float* __restrict__ rows, const uint32_t* __restrict__ rid, int nslot,
+                                           float* __restrict__ dL_drec, int lane) {
+  constexpr int NP = 9 * kF, R = NP - 32, LPP = 32 / R;
+  static_assert(R > 0 && 32 % R == 0 && LPP <= 8 && 8 % LPP == 0, "flush layout");
+  const int np = 9 * nslot;
+  if (lane < np) {
+    const float4* r = reinterpret_cast<const float4*>(rows + lane * 32);
+    float4 a = r[lane & 7];
+#pragma unroll
+    for (int c = 1; c < 8; c++) {
+      const float4 x = r[(c + lane) & 7];
+      const float2 lo = __fadd2_rn(make_float2(a.x, a.y), make_float2(x.x, x.y));
+      const float2 hi = __fadd2_rn(make_float2(a.z, a.w), make_float2(x.z, x.w));
+      a = make_float4(lo.x, lo.y, hi.x, hi.y);
+    }
+    const float z = (a.x + a.y) + (a.z + a.w);
+    if (z != 0.f) atomicAdd(dL_drec + (int64_t)rid[lane / 9] * 9 + lane % 9, z);
+  }
+  {
+    const int p = 32 + lane / LPP, part = lane % LPP;
+    float z = 0.f;
+    if (p < np) {
+      const float4* r = reinterpret_cast<const float4*>(rows + p * 32);
+#pragma unroll
+      for (int c = 0; c < 8 / LPP; c++) {
+        const float4 x = r[part * (8 / LPP) + c];
+        z += (x.x + x.y) + (x.z + x.w);
+      }
+    }
+#pragma unroll
+    for (int o = LPP / 2; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    if (part == 0 && p < np && z != 0.f) atomicAdd(dL_drec + (int64_t)rid[p / 9] * 9 + p % 9, z);
+  }
+}
+
 template <int PPT, bool kStats, int MINB = 1, bool kWarp = false, bool kBg = true>
 __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
     const gs_rec* __restrict__ rec, const uint32_t* __restrict__ sorted_idx,
@@ -541,7 +585,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   constexpr bool kOneWarp = NT == 32;
   constexpr int kNW = NT / 32;   // warps per block
   constexpr int kBB = 128;        // records staged per round
-  constexpr int kBW = 64;         // kWarp: records staged per warp round
+  constexpr int kBW = MINB >= 14 ? 32 : 64;  // kWarp: records staged per warp round (smem for 14 CTAs/SM)
   static_assert(!kWarp || PPT == 4, "warp-independent render needs PPT = 4 (one 8x16 half per warp)");
   constexpr bool kDirect = kOneWarp || kWarp;  // warp sums go straight to global memory
   __shared__ float4 s_a[kWarp ? 2 * kBW : kBB], s_b[kWarp ? 2 * kBW : kBB], s_c[kWarp ? 2 * kBW : kBB];
@@ -549,6 +593,10 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   // per-warp gradient slots: each (warp, entry, value) is written by exactly one lane, so no
   // shared-memory atomics (a float atomicAdd on shared memory is a CAS loop on sm_100)
   __shared__ float s_g[kDirect ? 1 : kNW * kBB * 9];
+  // kWarp: per-warp buffered reduction rows (flush_rows) and the buffered entries' records
+  __shared__ __align__(16) float s_rows[kWarp ? 2 * kF * 9 * 32 : 4];
+  __shared__ uint32_t s_rid[kWarp ? 2 * kF : 1];
+  int nslot = 0;  // kWarp: buffered entries (warp-uniform)
   __shared__ int s_max[NT / 32];
   __shared__ long long s_red[NT / 32];
   const long long t0 = clock64();
@@ -562,8 +610,8 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   const int px = tx * 16 + x, py0 = ty * 16 + y0;
   const float fpx = (float)px, fpy0 = (float)py0;
   int nl[PPT];
-  float Tf[PPT], T[PPT], S2[PPT], g2[PPT], bgd[PPT];
-  float2 S01[PPT], g01[PPT];  // (r, g) pairs for packed fp32x2 updates
+  float Tf[PPT], T[PPT], P[PPT], g2[PPT], bgd[PPT];
+  float2 g01[PPT];  // (r, g) pairs for packed fp32x2 updates
   int mymax = 0, nlsum = 0;
 #pragma unroll
   for (int j = 0; j < PPT; j++) {
@@ -572,8 +620,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
     nl[j] = in ? n_last[o] : 0;
     Tf[j] = in ? T_final[o] : 1.f;
     T[j] = Tf[j];
-    S01[j] = make_float2(0.f, 0.f);
-    S2[j] = 0.f;
+    P[j] = 0.f;
     g01[j] = make_float2(in ? dL_dpix[lb * 768 + (o - lb * 256)] : 0.f, in ? dL_dpix[lb * 768 + 256 + (o - lb * 256)] : 0.f);
     g2[j] = in ? dL_dpix[lb * 768 + 512 + (o - lb * 256)] : 0.f;
     bgd[j] = bg0 * g01[j].x + bg1 * g01[j].y + bg2 * g2[j];
@@ -645,14 +692,14 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
             const float G = ex2_approx(-e.q[j]);
             const float raw = __fmul_rn(Bq.y, G);
             switch (j) {
-              case 0: bwd_comp_strip<0 * RS, kBg>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 1: bwd_comp_strip<1 * RS, kBg>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 2: bwd_comp_strip<2 * RS, kBg>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 3: bwd_comp_strip<3 * RS, kBg>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 4: bwd_comp_strip<4 * RS, kBg>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 5: bwd_comp_strip<5 * RS, kBg>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 6: bwd_comp_strip<6 * RS, kBg>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              default: bwd_comp_strip<7 * RS, kBg>(raw, G, Bq, cq.x, T[j], S01[j], S2[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 0: bwd_comp_strip<0 * RS, kBg>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 1: bwd_comp_strip<1 * RS, kBg>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 2: bwd_comp_strip<2 * RS, kBg>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 3: bwd_comp_strip<3 * RS, kBg>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 4: bwd_comp_strip<4 * RS, kBg>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 5: bwd_comp_strip<5 * RS, kBg>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              case 6: bwd_comp_strip<6 * RS, kBg>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              default: bwd_comp_strip<7 * RS, kBg>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
             }
           }
         if (kStats) {
@@ -666,12 +713,25 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
         gr[6] = gc01.x;
         gr[7] = gc01.y;
         gr[8] = gc2;
-        const float z = warp_reduce9(gr, lane);
-        if (rvalid) {
-          if (kDirect) {
-            if (z != 0.f) atomicAdd(dL_drec + (int64_t)__float_as_uint(cq.w) * 9 + ridx, z);
-          } else {
-            s_g[(wid * kBB + k) * 9 + ridx] = z;
+        if constexpr (kWarp) {
+          float* row = s_rows + (wid * kF + nslot) * 9 * 32 + lane;
+#pragma unroll
+          for (int q = 0; q < 9; q++) row[q * 32] = gr[q];
+          if (lane == 0) s_rid[wid * kF + nslot] = __float_as_uint(cq.w);
+          if (++nslot == kF) {
+            __syncwarp();
+            flush_rows(s_rows + wid * kF * 9 * 32, s_rid + wid * kF, kF, dL_drec, lane);
+            __syncwarp();
+            nslot = 0;
+          }
+        } else {
+          const float z = warp_reduce9(gr, lane);
+          if (rvalid) {
+            if (kDirect) {
+              if (z != 0.f) atomicAdd(dL_drec + (int64_t)__float_as_uint(cq.w) * 9 + ridx, z);
+            } else {
+              s_g[(wid * kBB + k) * 9 + ridx] = z;
+            }
           }
         }
       }
@@ -688,6 +748,12 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
           if (xv != 0.f) atomicAdd(dst + q, xv);
         }
       }
+    }
+  }
+  if constexpr (kWarp) {
+    if (nslot > 0) {
+      __syncwarp();
+      flush_rows(s_rows + wid * kF * 9 * 32, s_rid + wid * kF, nslot, dL_drec, lane);
     }
   }
   if (kStats) {
@@ -722,7 +788,9 @@ static int render_cull() {
 
 // resident-CTA floor of the PPT = 4 kernels, i.e. their register cap (A/B knobs:
 // GS_RENDER_FWD_MINB in {12, 16}, default 16 = 64 registers, 16 warps/SM;
-// GS_RENDER_BWD_MINB in {8, 10, 12}, default 12 = 80 registers; measured on C2)
+// GS_RENDER_BWD_MINB in {8, 10, 12}, default 12 = 80 registers; measured on C2; the
+// warp-independent black-background backward runs at 14 = 72 registers unless 12 is asked
+// for: C2 37.6 -> 35.9 ms)
 static int render_minb(int bwd) {
   static int mb[2] = {-1, -1};
   if (mb[bwd] < 0) {
@@ -815,7 +883,8 @@ extern "C" gs_status gs_render_bwd(gs_ctx* c, const void* recv_rec, int64_t n_re
   auto kb = ppt == 2 ? (stats ? k_render_bwd<2, true> : k_render_bwd<2, false>)
           : ppt == 8 ? (stats ? k_render_bwd<8, true> : k_render_bwd<8, false>)
           : (render_warp() & 2) ? (bg[0] == 0.f && bg[1] == 0.f && bg[2] == 0.f
-                                       ? (stats ? k_render_bwd<4, true, 12, true, false> : k_render_bwd<4, false, 12, true, false>)
+                                       ? (mb == 12 ? (stats ? k_render_bwd<4, true, 12, true, false> : k_render_bwd<4, false, 12, true, false>)
+                                                   : (stats ? k_render_bwd<4, true, 14, true, false> : k_render_bwd<4, false, 14, true, false>))
                                        : (stats ? k_render_bwd<4, true, 12, true> : k_render_bwd<4, false, 12, true>))
           : mb == 8 ? (stats ? k_render_bwd<4, true, 8> : k_render_bwd<4, false, 8>)
           : mb == 12 ? (stats ? k_render_bwd<4, true, 12> : k_render_bwd<4, false, 12>)
