@@ -788,14 +788,14 @@ static int render_cull() {
 
 // resident-CTA floor of the PPT = 4 kernels, i.e. their register cap (A/B knobs:
 // GS_RENDER_FWD_MINB in {12, 16}, default 16 = 64 registers, 16 warps/SM;
-// GS_RENDER_BWD_MINB in {8, 10, 12}, default 12 = 80 registers; measured on C2; the
-// warp-independent black-background backward runs at 14 = 72 registers unless 12 is asked
-// for: C2 37.6 -> 35.9 ms)
+// GS_RENDER_BWD_MINB in {8, 10, 12, 14}, default 14: the warp-independent black-background
+// backward at 72 registers (C2 37.6 -> 35.9 ms against 12 = 80 registers); the other backward
+// variants take 12 for anything but 8 and 10)
 static int render_minb(int bwd) {
   static int mb[2] = {-1, -1};
   if (mb[bwd] < 0) {
     const char* e = getenv(bwd ? "GS_RENDER_BWD_MINB" : "GS_RENDER_FWD_MINB");
-    mb[bwd] = e ? atoi(e) : (bwd ? 12 : 16);
+    mb[bwd] = e ? atoi(e) : (bwd ? 14 : 16);
   }
   return mb[bwd];
 }
@@ -887,8 +887,8 @@ extern "C" gs_status gs_render_bwd(gs_ctx* c, const void* recv_rec, int64_t n_re
                                                    : (stats ? k_render_bwd<4, true, 14, true, false> : k_render_bwd<4, false, 14, true, false>))
                                        : (stats ? k_render_bwd<4, true, 12, true> : k_render_bwd<4, false, 12, true>))
           : mb == 8 ? (stats ? k_render_bwd<4, true, 8> : k_render_bwd<4, false, 8>)
-          : mb == 12 ? (stats ? k_render_bwd<4, true, 12> : k_render_bwd<4, false, 12>)
-                     : (stats ? k_render_bwd<4, true, 10> : k_render_bwd<4, false, 10>);
+          : mb == 10 ? (stats ? k_render_bwd<4, true, 10> : k_render_bwd<4, false, 10>)
+                     : (stats ? k_render_bwd<4, true, 12> : k_render_bwd<4, false, 12>);
   const int threads = 256 / ppt;
 
   kb<<<(unsigned)n_owned, threads, 0, st>>>(
