@@ -235,8 +235,12 @@ template <int PPT>
 struct gs_strip {
   float dx, dy0, u[PPT], w[PPT], q[PPT];
 };
+// pen (forward): per-pixel penalty added inside the FMA that forms w^2 -- 0 for a live pixel
+// (w * w + 0 rounds exactly like w * w, so q is unchanged) and +inf for a finished one (q = inf
+// fails every skip test): the done flags cost no instruction per entry.  nullptr: no penalty.
 template <int PPT>
-__device__ __forceinline__ void q_strip(const float4& A, const float4& Bq, float px, float py0, gs_strip<PPT>& e) {
+__device__ __forceinline__ void q_strip(const float4& A, const float4& Bq, float px, float py0, gs_strip<PPT>& e,
+                                        const float2* pen = nullptr) {
   constexpr float RS = (float)strip_layout<PPT>::RS;
   const float l11 = A.z, l21 = A.w, l22 = Bq.x;
 
@@ -258,20 +262,24 @@ __device__ __forceinline__ void q_strip(const float4& A, const float4& Bq, float
 #pragma unroll
   for (int j = 0; j < PPT; j += 2) {
     const float2 u = make_float2(e.u[j], e.u[j + 1]), w = make_float2(e.w[j], e.w[j + 1]);
-    const float2 q = __ffma2_rn(u, u, __fmul2_rn(w, w));
+    const float2 q = __ffma2_rn(u, u, pen ? __ffma2_rn(w, w, pen[j / 2]) : __fmul2_rn(w, w));
     e.q[j] = q.x;
     e.q[j + 1] = q.y;
   }
 }
 
-// Composite one staged entry into one pixel (O12) given its capped alpha >= 1/255.
-template <bool kStats>
+// Composite one staged entry into one pixel (O12) given its capped alpha >= 1/255.  A pixel
+// that stops gets the +inf penalty (pen) and counts towards ndone; kTrack keeps its stop
+// position (evaluation counts: statistics and the WORK cost mode).
+template <bool kStats, bool kTrack>
 __device__ __forceinline__ void fwd_comp(float alpha, float cr, float cg, float cb, int pos, float& T, float& C0,
-                                         float& C1, float& C2, bool& stop, int& nlast, int& stop_pos, int& efc) {
+                                         float& C1, float& C2, float& pen, int& ndone, int& nlast, int& stop_pos,
+                                         int& efc) {
   const float Tn = T * (1.0f - alpha);
   if (Tn < kTStop) {  // R3: stop before compositing this entry
-    stop = true;
-    stop_pos = pos;
+    pen = __int_as_float(0x7f800000);
+    ndone++;
+    if (kTrack) stop_pos = pos;
     return;
   }
   const float wgt = alpha * T;
@@ -285,7 +293,7 @@ __device__ __forceinline__ void fwd_comp(float alpha, float cr, float cg, float 
 
 // kWarp (PPT = 4 only): the two warps walk the list independently, each over its own 8x16
 // half (stage_warp), with no CTA barrier until the epilogue.
-template <int PPT, bool kStats, int MINB = 1, bool kWarp = false>
+template <int PPT, bool kStats, int MINB = 1, bool kWarp = false, bool kTrack = true>
 __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
     const gs_rec* __restrict__ rec, const uint32_t* __restrict__ sorted_idx,
     const int32_t* __restrict__ range, gs_geom geo, int64_t B_lo, float bg0, float bg1, float bg2,
@@ -312,8 +320,10 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
   const float fpx = (float)px, fpy0 = (float)py0;
   const int beg = range[lb], end = range[lb + 1];
   float T[PPT], C0[PPT], C1[PPT], C2[PPT];
+  static_assert(kTrack || !kStats, "statistics need the stop positions");
   int nl[PPT], sp[PPT];
-  bool dn[PPT];  // pixel done (stopped, or outside the image); kept as predicates
+  float2 pen[PPT / 2];  // pixel pairs; 0: live pixel, +inf: stopped or outside the image (q_strip)
+  int ndone = 0;
   unsigned inside = 0;
 #pragma unroll
   for (int j = 0; j < PPT; j++) {
@@ -323,15 +333,11 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
     sp[j] = -1;
     const bool in = px < geo.W && py0 + RS * j < geo.H;
     inside |= (unsigned)in << j;
-    dn[j] = !in;
+    (j & 1 ? pen[j / 2].y : pen[j / 2].x) = in ? 0.f : __int_as_float(0x7f800000);
+    ndone += !in;
   }
   int efc = 0;
-  auto all_done = [&]() {
-    bool a = true;
-#pragma unroll
-    for (int j = 0; j < PPT; j++) a = a && dn[j];
-    return a;
-  };
+  auto all_done = [&]() { return ndone == PPT; };
   const float bx0 = (float)(tx * 16), by0 = (float)(ty * 16);
   constexpr int kStep = kWarp ? kFW : kFB;
   const int wofs = kWarp ? (tid >> 5) * (kFW + kUnroll) : 0;  // this warp's slots (kWarp)
@@ -355,22 +361,20 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
       for (int kk = 0; kk < kUnroll; kk++) {
         const float4 A = s_a[wofs + k0 + kk], Bq = s_b[wofs + k0 + kk], cq = s_c[wofs + k0 + kk];
         gs_strip<PPT> e;
-        q_strip<PPT>(A, Bq, fpx, fpy0, e);
+        q_strip<PPT>(A, Bq, fpx, fpy0, e, pen);
         bool cj[PPT], any = false;
 #pragma unroll
         for (int j = 0; j < PPT; j++) {
-          cj[j] = !dn[j] && e.q[j] <= cq.y;
+          cj[j] = e.q[j] <= cq.y;  // finished pixels have q = +inf
           any = any || cj[j];
         }
         if (any) {  // the common case (every pixel skips the entry) takes one branch
 #pragma unroll
           for (int j = 0; j < PPT; j++)
             if (cj[j]) {
-              bool st = false;
               const float al = fminf(kAlphaCap, __fmul_rn(Bq.y, ex2_approx(-e.q[j])));
-              fwd_comp<kStats>(al, Bq.z, Bq.w, cq.x, __float_as_int(cq.z), T[j], C0[j], C1[j], C2[j], st, nl[j],
-                               sp[j], efc);
-              dn[j] = st;
+              fwd_comp<kStats, kTrack>(al, Bq.z, Bq.w, cq.x, __float_as_int(cq.z), T[j], C0[j], C1[j], C2[j],
+                                       j & 1 ? pen[j / 2].y : pen[j / 2].x, ndone, nl[j], sp[j], efc);
             }
         }
       }
@@ -847,7 +851,9 @@ extern "C" gs_status gs_render_fwd(gs_ctx* c, const void* recv_rec, const uint32
   const int mb = render_minb(0);
   auto kf = ppt == 2 ? (stats ? k_render_fwd<2, true> : k_render_fwd<2, false>)
           : ppt == 8 ? (stats ? k_render_fwd<8, true> : k_render_fwd<8, false>)
-          : (render_warp() & 1) ? (stats ? k_render_fwd<4, true, 16, true> : k_render_fwd<4, false, 16, true>)
+          : (render_warp() & 1) ? (stats ? k_render_fwd<4, true, 16, true>
+                                   : cost_mode == GS_COST_WORK ? k_render_fwd<4, false, 16, true>
+                                                               : k_render_fwd<4, false, 16, true, false>)
           : mb == 12 ? (stats ? k_render_fwd<4, true, 12> : k_render_fwd<4, false, 12>)
                      : (stats ? k_render_fwd<4, true, 16> : k_render_fwd<4, false, 16>);
   kf<<<(unsigned)n_owned, 256 / ppt, 0, (cudaStream_t)stream>>>(
