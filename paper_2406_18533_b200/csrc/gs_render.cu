@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
     for (int k = kept - 1; k >= 0; k--) {
       const float4 cq = s_c[wofs + k];
       const int pos = __float_as_int(cq.z);
-      if (pos >= wmax) continue;  // warp-uniform
+      if (!kWarp && pos >= wmax) continue;  // warp-uniform (kWarp stages only positions < wmax)
       const float4 A = s_a[wofs + k], Bq = s_b[wofs + k];
       gs_strip<PPT> e;
       q_strip<PPT>(A, Bq, fpx, fpy0, e);
