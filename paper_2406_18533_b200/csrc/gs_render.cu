@@ -791,15 +791,16 @@ static int render_cull() {
 }
 
 // resident-CTA floor of the PPT = 4 kernels, i.e. their register cap (A/B knobs:
-// GS_RENDER_FWD_MINB in {12, 16}, default 16 = 64 registers, 16 warps/SM;
-// GS_RENDER_BWD_MINB in {8, 10, 12, 14}, default 14: the warp-independent black-background
-// backward at 72 registers (C2 37.6 -> 35.9 ms against 12 = 80 registers); the other backward
-// variants take 12 for anything but 8 and 10)
+// GS_RENDER_FWD_MINB: 12 or 16 for the block-staged forward, 16 / 18 / 20 for the
+// warp-independent one; default 18 = 56 registers (C2 18.6 -> 18.0 ms against 16);
+// GS_RENDER_BWD_MINB: 8 / 10 / 12 for the block-staged backward (else 12), 12 / 14 / 16 / 18
+// for the warp-independent black-background one; default 16 = 64 registers (C2 34.3 -> 33.8
+// ms against 14)).
 static int render_minb(int bwd) {
   static int mb[2] = {-1, -1};
   if (mb[bwd] < 0) {
     const char* e = getenv(bwd ? "GS_RENDER_BWD_MINB" : "GS_RENDER_FWD_MINB");
-    mb[bwd] = e ? atoi(e) : (bwd ? 14 : 16);
+    mb[bwd] = e ? atoi(e) : (bwd ? 16 : 18);
   }
   return mb[bwd];
 }
@@ -853,7 +854,9 @@ extern "C" gs_status gs_render_fwd(gs_ctx* c, const void* recv_rec, const uint32
           : ppt == 8 ? (stats ? k_render_fwd<8, true> : k_render_fwd<8, false>)
           : (render_warp() & 1) ? (stats ? k_render_fwd<4, true, 16, true>
                                    : cost_mode == GS_COST_WORK ? k_render_fwd<4, false, 16, true>
-                                                               : k_render_fwd<4, false, 16, true, false>)
+                                   : mb == 16 ? k_render_fwd<4, false, 16, true, false>
+                                   : mb == 20 ? k_render_fwd<4, false, 20, true, false>
+                                              : k_render_fwd<4, false, 18, true, false>)
           : mb == 12 ? (stats ? k_render_fwd<4, true, 12> : k_render_fwd<4, false, 12>)
                      : (stats ? k_render_fwd<4, true, 16> : k_render_fwd<4, false, 16>);
   kf<<<(unsigned)n_owned, 256 / ppt, 0, (cudaStream_t)stream>>>(
@@ -890,7 +893,9 @@ extern "C" gs_status gs_render_bwd(gs_ctx* c, const void* recv_rec, int64_t n_re
           : ppt == 8 ? (stats ? k_render_bwd<8, true> : k_render_bwd<8, false>)
           : (render_warp() & 2) ? (bg[0] == 0.f && bg[1] == 0.f && bg[2] == 0.f
                                        ? (mb == 12 ? (stats ? k_render_bwd<4, true, 12, true, false> : k_render_bwd<4, false, 12, true, false>)
-                                                   : (stats ? k_render_bwd<4, true, 14, true, false> : k_render_bwd<4, false, 14, true, false>))
+                                                   : mb == 14 ? (stats ? k_render_bwd<4, true, 14, true, false> : k_render_bwd<4, false, 14, true, false>)
+                                                   : mb == 18 ? (stats ? k_render_bwd<4, true, 18, true, false> : k_render_bwd<4, false, 18, true, false>)
+                                                   : (stats ? k_render_bwd<4, true, 16, true, false> : k_render_bwd<4, false, 16, true, false>))
                                        : (stats ? k_render_bwd<4, true, 12, true> : k_render_bwd<4, false, 12, true>))
           : mb == 8 ? (stats ? k_render_bwd<4, true, 8> : k_render_bwd<4, false, 8>)
           : mb == 10 ? (stats ? k_render_bwd<4, true, 10> : k_render_bwd<4, false, 10>)
