@@ -366,6 +366,89 @@ gs_status gs_redistribute(gs_ctx* ctx, const gs_params* p, const gs_params* m, c
                           void* send_buf, int64_t send_cap, void* recv_buf, int64_t recv_cap, gs_params* p_out,
                           gs_params* m_out, gs_params* v_out, int64_t* n_total_h, int64_t* n_out_h, void* stream);
 
+/* ------------------------------------------------------- NEXT-3 peer-memory (NVLink) exchange */
+/* NEXT-3 ("sparse all-to-all communication"): the two sparse
+ * all-to-alls done by the kernels that produce the data, over peer memory (NVLink stores and
+ * reductions on one NVSwitch box) instead of NCCL send/recv:
+ *   forward  -- gs_project_put writes every record straight into the DESTINATION rank's
+ *               receive buffer (no send buffer, no separate transfer);
+ *   backward -- gs_render_bwd_put adds each record's 9 gradient sums straight into the OWNER's
+ *               dL/d(sent record) buffer (no receive-side gradient buffer, no reverse transfer).
+ * One step with the plan P = the G x G count matrix (row s = records rank s sends to each d):
+ *   gs_project_count -> [all-gather counts: gs_exchange_counts or the caller] -> gs_p2p_plan ->
+ *   gs_project_put -> gs_p2p_barrier -> gs_bin_sort / gs_render_fwd (on the receive buffer) ->
+ *   gs_render_bwd_put -> gs_p2p_barrier -> gs_adam_step (on the own dL/dsend buffer).
+ * Receive order is the same as gs_exchange's (ascending source rank, then the source's send
+ * order), so every downstream result equals the NCCL path's (gradients up to the order of
+ * float additions).  Buffers: each rank allocates its three symmetric buffers with
+ * gs_sym_alloc (records, dL/dsend, barrier flags), exports their IPC handles, opens the
+ * peers' with gs_ipc_open and attaches all G pointers (gs_p2p_attach).  Ranks of one process
+ * (virtual ranks, tests) attach each other's pointers directly.                            */
+
+/* gs_p2p_offsets -- pure host arithmetic of the plan for `rank` (counts_h = G x G, row s =
+ * records source s sends to each destination d):
+ *   recv_seg_h[G+1]  receive-buffer offset of each source's records (prefix over s of C[s][rank]);
+ *   put_base_h[G]    where this rank's records for d start in d's receive buffer
+ *                    (sum over s < rank of C[s][d]);
+ *   send_off_h[G+1]  this rank's send order: destination buckets (prefix over d of C[rank][d]);
+ *   owner_off_h[G]   position, in source s's send order, of the records s sent to this rank
+ *                    (sum over d < rank of C[s][d]) -- where their gradients go.
+ * GS_EINVAL on a negative count or G outside [1, 32].                                     */
+gs_status gs_p2p_offsets(const int64_t* counts_h, int G, int rank, int64_t* recv_seg_h, int64_t* put_base_h,
+                         int64_t* send_off_h, int64_t* owner_off_h);
+
+/* gs_sym_alloc -- (re)allocates the context's symmetric buffer `which` (0: receive records,
+ * 1: dL/dsend floats, 2: barrier flags, zeroed) of at least `bytes`, returns its device
+ * pointer and its 64-byte CUDA IPC handle (for the peers' gs_ipc_open).  Owned by the
+ * context (freed by gs_destroy).  Growing invalidates the peers' mappings: re-exchange and
+ * re-attach.                                                                               */
+gs_status gs_sym_alloc(gs_ctx* ctx, int which, size_t bytes, void** dev_ptr_h, uint8_t handle_h[64]);
+/* gs_ipc_open -- maps a peer's IPC handle into this process (peer access over NVLink);
+ * closed by gs_destroy.                                                                    */
+gs_status gs_ipc_open(gs_ctx* ctx, const uint8_t handle_h[64], void** dev_ptr_h);
+/* gs_p2p_attach -- the G ranks' receive buffers (capacity in records), dL/dsend buffers
+ * (capacity in records of 9 floats) and flag arrays (G uint64 each), as device pointers valid
+ * in this process (entry `rank` = this rank's own).                                        */
+gs_status gs_p2p_attach(gs_ctx* ctx, void* const* recv_h, const int64_t* recv_cap_h, void* const* dsend_h,
+                        const int64_t* dsend_cap_h, void* const* flags_h);
+/* gs_p2p_plan -- sets the step's G x G count matrix (identical on every rank); *n_recv_h =
+ * records this rank receives.  GS_ECAPACITY on EVERY rank if any rank's receive or dL/dsend
+ * capacity is too small (all ranks see the same matrix and capacities).                    */
+gs_status gs_p2p_plan(gs_ctx* ctx, const int64_t* counts_h, int64_t* n_recv_h);
+/* gs_exchange_counts -- COLLECTIVE (NCCL all-gather): counts_all_h[G x G] from each rank's
+ * send_counts_h[G].  Host sync.                                                            */
+gs_status gs_exchange_counts(gs_ctx* ctx, const int64_t* send_counts_h, int64_t* counts_all_h, void* stream);
+/* gs_project_count -- the counting half of gs_project: writes bwd_index and send_counts_h
+ * (host sync); no records.                                                                  */
+gs_status gs_project_count(gs_ctx* ctx, const gs_params* p, const gs_camera* cams_h, int n_views,
+                           const int64_t* dp_h, int64_t* send_counts_h, void* bwd_index, void* stream);
+/* gs_project_put -- the writing half, fused with the forward exchange: after
+ * gs_project_count (same arguments, same bwd_index) and gs_p2p_plan, writes each record to
+ * destination d's receive buffer at put_base[d] + its index in the bucket, and zeroes this
+ * rank's dL/dsend rows [0, n_send) for the backward's reductions.  Peers may read only after
+ * gs_p2p_barrier.                                                                          */
+gs_status gs_project_put(gs_ctx* ctx, const gs_params* p, const gs_camera* cams_h, int n_views,
+                         const int64_t* dp_h, const void* bwd_index, void* stream);
+/* gs_render_bwd_put -- gs_render_bwd on this rank's receive buffer with the reverse exchange
+ * fused: record j from source s adds its gradient to s's dL/dsend row owner_off[s] +
+ * (j - recv_seg[s]) (float reductions over NVLink).  Same other arguments as gs_render_bwd
+ * (black background and the default warp-independent kernel only: GS_ENOTSUP otherwise).
+ * Owners may read dL/dsend only after gs_p2p_barrier.                                      */
+gs_status gs_render_bwd_put(gs_ctx* ctx, const void* recv_rec, int64_t n_recv, const uint32_t* sorted_idx,
+                            const int32_t* tile_range, const gs_camera* cams_h, int n_views, const int64_t* dp_h,
+                            const float* dL_dpix, const float* T_final, const int32_t* n_last, int64_t* tile_cost,
+                            int cost_mode, int64_t* stats, void* stream);
+/* gs_p2p_barrier -- device-side barrier over the attached flag arrays, asynchronous (no host
+ * sync): one kernel writes the next epoch into every rank's flag slot for this rank
+ * (system-scope release after the stream's earlier work) and waits until all ranks' slots
+ * reached it (acquire).  A wait longer than ~4 s ends the kernel and records a timeout that
+ * gs_p2p_status reports (no silent hang).  Virtual ranks of one process must issue it on
+ * different streams.                                                                       */
+gs_status gs_p2p_barrier(gs_ctx* ctx, void* stream);
+/* gs_p2p_status -- GS_ECUDA if a barrier of this context timed out since the last call (and
+ * clears it), else GS_OK.  Host sync on `stream`.                                         */
+gs_status gs_p2p_status(gs_ctx* ctx, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -106,6 +106,19 @@ _sig = {
     "gs_redistribute": (C.c_int, [_vp, C.POINTER(Params), C.POINTER(Params), C.POINTER(Params), C.c_uint64, _vp,
                                   _i64, _vp, _i64, C.POINTER(Params), C.POINTER(Params), C.POINTER(Params), _P64,
                                   _P64, _vp]),
+    # NEXT-3: peer-memory (NVLink) exchange
+    "gs_p2p_offsets": (C.c_int, [_P64, C.c_int, C.c_int, _P64, _P64, _P64, _P64]),
+    "gs_sym_alloc": (C.c_int, [_vp, C.c_int, _sz, C.POINTER(_vp), C.c_char_p]),
+    "gs_ipc_open": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp)]),
+    "gs_p2p_attach": (C.c_int, [_vp, C.POINTER(_vp), _P64, C.POINTER(_vp), _P64, C.POINTER(_vp)]),
+    "gs_p2p_plan": (C.c_int, [_vp, _P64, _P64]),
+    "gs_exchange_counts": (C.c_int, [_vp, _P64, _P64, _vp]),
+    "gs_project_count": (C.c_int, [_vp, C.POINTER(Params), C.POINTER(Camera), C.c_int, _P64, _P64, _vp, _vp]),
+    "gs_project_put": (C.c_int, [_vp, C.POINTER(Params), C.POINTER(Camera), C.c_int, _P64, _vp, _vp]),
+    "gs_render_bwd_put": (C.c_int, [_vp, _vp, _i64, _vp, _vp, C.POINTER(Camera), C.c_int, _P64, _vp, _vp, _vp,
+                                    _vp, C.c_int, _vp, _vp]),
+    "gs_p2p_barrier": (C.c_int, [_vp, _vp]),
+    "gs_p2p_status": (C.c_int, [_vp, _vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -118,7 +131,10 @@ def version() -> int:
 
 
 def _ptr(t):
-    return None if t is None else C.c_void_p(t.data_ptr())
+    """A torch tensor's device pointer, or a raw device pointer given as an int."""
+    if t is None:
+        return None
+    return C.c_void_p(t) if isinstance(t, int) else C.c_void_p(t.data_ptr())
 
 
 def _i64arr(vals):
@@ -542,3 +558,99 @@ def exchange_plan(counts, G, rank):
     if st != GS_OK:
         raise GSError(st, "gs_exchange_plan")
     return so, ro
+
+
+# ------------------------------------------------------------------ NEXT-3 peer-memory exchange
+SYM_RECV, SYM_DSEND, SYM_FLAGS = 0, 1, 2
+
+
+def p2p_offsets(counts, G, rank):
+    """Pure host plan arithmetic: (recv_seg[G+1], put_base[G], send_off[G+1], owner_off[G])."""
+    cm, cmp_ = _i64arr(np.asarray(counts, np.int64).reshape(-1))
+    out = [np.zeros(G + 1, np.int64), np.zeros(G, np.int64), np.zeros(G + 1, np.int64), np.zeros(G, np.int64)]
+    st = _lib.gs_p2p_offsets(cmp_, G, rank, *[o.ctypes.data_as(_P64) for o in out])
+    if st != GS_OK:
+        raise GSError(st, "gs_p2p_offsets")
+    return tuple(out)
+
+
+def sym_alloc(ctx, which, nbytes):
+    """Context-owned symmetric buffer: (device pointer int, 64-byte IPC handle)."""
+    ptr = C.c_void_p()
+    h = C.create_string_buffer(64)
+    ctx.check(_lib.gs_sym_alloc(ctx.handle, int(which), int(nbytes), C.byref(ptr), h))
+    return int(ptr.value), h.raw
+
+
+def ipc_open(ctx, handle: bytes):
+    ptr = C.c_void_p()
+    ctx.check(_lib.gs_ipc_open(ctx.handle, handle, C.byref(ptr)))
+    return int(ptr.value)
+
+
+def p2p_attach(ctx, recv_ptrs, recv_caps, dsend_ptrs, dsend_caps, flag_ptrs):
+    G = ctx.world
+    arr = lambda ps: (C.c_void_p * G)(*[C.c_void_p(int(q)) for q in ps])  # noqa: E731
+    _, rcp = rc = _i64arr(recv_caps)
+    _, dcp = dc = _i64arr(dsend_caps)
+    ctx.check(_lib.gs_p2p_attach(ctx.handle, arr(recv_ptrs), rcp, arr(dsend_ptrs), dcp, arr(flag_ptrs)))
+    del rc, dc
+
+
+def p2p_plan(ctx, counts):
+    """Sets the G x G count matrix; returns n_recv.  CapacityError on every rank together."""
+    cm, cmp_ = _i64arr(np.asarray(counts, np.int64).reshape(-1))
+    nr = C.c_int64(0)
+    st = _lib.gs_p2p_plan(ctx.handle, cmp_, C.byref(nr))
+    if st == GS_ECAPACITY:
+        e = CapacityError(st, ctx.last_error())
+        e.needed = int(nr.value)
+        raise e
+    ctx.check(st)
+    return int(nr.value)
+
+
+def exchange_counts(ctx, send_counts, stream=None):
+    """COLLECTIVE: the G x G count matrix (numpy int64 [G, G], row = source)."""
+    sc, scp = _i64arr(send_counts)
+    out = np.zeros(ctx.world * ctx.world, np.int64)
+    ctx.check(_lib.gs_exchange_counts(ctx.handle, scp, out.ctypes.data_as(_P64), _stream(stream)))
+    return out.reshape(ctx.world, ctx.world)
+
+
+def project_count(ctx, params, cams, dp, bwd_index, stream=None):
+    """Counting half of A1: send_counts (numpy int64[G])."""
+    ca = cameras(cams)
+    _, dpp = _i64arr(dp)
+    cnt, cntp = _i64arr(np.zeros(ctx.world))
+    ps = params.struct()
+    ctx.check(_lib.gs_project_count(ctx.handle, C.byref(ps), ca, len(cams), dpp, cntp, _ptr(bwd_index),
+                                    _stream(stream)))
+    return cnt
+
+
+def project_put(ctx, params, cams, dp, bwd_index, stream=None):
+    """Writing half of A1 fused with A2: records straight into the destinations' buffers."""
+    ca = cameras(cams)
+    _, dpp = _i64arr(dp)
+    ps = params.struct()
+    ctx.check(_lib.gs_project_put(ctx.handle, C.byref(ps), ca, len(cams), dpp, _ptr(bwd_index), _stream(stream)))
+
+
+def render_bwd_put(ctx, recv_rec, n_recv, sorted_idx, tile_range, cams, dp, dL_dpix, T_final, n_last, tile_cost,
+                   cost_mode, stats, stream=None, recv_ptr=None):
+    """A5 fused with A6: gradient sums straight into the owners' dL/dsend buffers."""
+    ca = cameras(cams)
+    _, dpp = _i64arr(dp)
+    rp = C.c_void_p(recv_ptr) if recv_ptr is not None else _ptr(recv_rec)
+    ctx.check(_lib.gs_render_bwd_put(ctx.handle, rp, int(n_recv), _ptr(sorted_idx), _ptr(tile_range), ca,
+                                     len(cams), dpp, _ptr(dL_dpix), _ptr(T_final), _ptr(n_last), _ptr(tile_cost),
+                                     int(cost_mode), _ptr(stats), _stream(stream)))
+
+
+def p2p_barrier(ctx, stream=None):
+    ctx.check(_lib.gs_p2p_barrier(ctx.handle, _stream(stream)))
+
+
+def p2p_status(ctx, stream=None):
+    ctx.check(_lib.gs_p2p_status(ctx.handle, _stream(stream)))

@@ -113,6 +113,10 @@ void gs_destroy(gs_ctx* c) {
   for (int s = 0; s < SLOT_N; s++)
     if (c->slot[s].ptr) cudaFree(c->slot[s].ptr);
   if (c->pinned) cudaFreeHost(c->pinned);
+  for (void* q : c->p2p.opened) cudaIpcCloseMemHandle(q);
+  if (c->p2p.err) cudaFree(c->p2p.err);
+  for (int k = 0; k < 3; k++)
+    if (c->p2p.sym[k]) cudaFree(c->p2p.sym[k]);
 #ifdef GS_WITH_NCCL
   if (c->comm) ncclCommDestroy(c->comm);
 #endif

@@ -45,8 +45,26 @@ enum {
   SLOT_N
 };
 
+// NEXT-3 peer-memory exchange state (gs_p2p.cu): symmetric buffers this context allocated,
+// peers' buffers opened from IPC handles, the attached per-rank pointers and the current plan.
+struct gs_p2p_state {
+  void* sym[3] = {nullptr, nullptr, nullptr};  // own symmetric buffers: records, dL/dsend, flags
+  size_t sym_bytes[3] = {0, 0, 0};
+  std::vector<void*> opened;                   // cudaIpcOpenMemHandle'd peer buffers
+  bool attached = false, planned = false;
+  void* recv[32] = {};                         // per rank: receive buffer (gs_rec)
+  int64_t recv_cap[32] = {};                   // records
+  float* dsend[32] = {};                       // per rank: dL/d(sent record) [n_send][9]
+  int64_t dsend_cap[32] = {};                  // records
+  unsigned long long* flags[32] = {};          // per rank: barrier flags [world]
+  unsigned long long epoch = 0;
+  int* err = nullptr;                          // device: barrier timed out
+  std::vector<int64_t> counts;                 // plan: G x G, row = source
+};
+
 struct gs_ctx {
   int device = 0, rank = 0, world = 1;
+  gs_p2p_state p2p;
   std::string err;
   gs_slot slot[SLOT_N];
   int64_t* pinned = nullptr;  // small pinned host mirror (>= 4096 int64)

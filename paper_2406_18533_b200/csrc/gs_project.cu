@@ -18,6 +18,13 @@ using namespace gsd;
 
 namespace {
 
+// Record destinations of k_project_write: the record at send-order position pos with
+// destination d goes to d_[d][pos] (all d_ = the send buffer for gs_project; for the fused
+// NEXT-3 path d_[d] = d's receive buffer + put_base[d] - send_off[d]).
+struct gs_outs {
+  gs_rec* d[GS_MAX_WORLD];
+};
+
 __global__ void __launch_bounds__(kBlock) k_project_count(
     const float4* __restrict__ pos_op, const float4* __restrict__ log_scale,
     const float4* __restrict__ rot, int64_t n, gs_cams_arg cams, gs_geom geo, gs_dp_arg dp,
@@ -59,7 +66,7 @@ __global__ void __launch_bounds__(kBlock) k_project_write(
     const float4* __restrict__ pos_op, const float4* __restrict__ log_scale,
     const float4* __restrict__ rot, const float4* __restrict__ sh, int64_t n, int64_t gid_base,
     gs_cams_arg cams, gs_geom geo, int G, int nb, int NW, const uint32_t* __restrict__ maskw,
-    const int64_t* __restrict__ base, int64_t ncta, gs_rec* __restrict__ out) {
+    const int64_t* __restrict__ base, int64_t ncta, gs_outs outs) {
   __shared__ int s_cnt[kWarps * kMaxBuckets];
   const int b = cams.n;
   int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
@@ -122,7 +129,7 @@ __global__ void __launch_bounds__(kBlock) k_project_write(
       if (bit) {
         int64_t pos = base[(int64_t)k * ncta + blockIdx.x] + warp_prefix(s_cnt, wid, nb, k) +
                       __popc(bal & lt);
-        out[pos] = rec;
+        outs.d[d][pos] = rec;  // own send buffer, or (NEXT-3) destination d's receive buffer
       }
     }
   }
@@ -135,17 +142,18 @@ extern "C" size_t gs_project_index_bytes(const gs_ctx* c, int64_t n, int n_views
   return index_layout(n, n_views, c->world).bytes;
 }
 
-extern "C" gs_status gs_project(gs_ctx* c, const gs_params* p, const gs_camera* cams_h,
-                                int n_views, const int64_t* dp_h, void* send_rec, int64_t send_cap,
-                                int64_t* send_counts_h, void* bwd_index, void* stream) {
-  if (!c) return GS_EINVAL;
+// Counting half (shared by gs_project and gs_project_count): bwd_index masks and per-CTA
+// bucket bases, per-destination counts to the host (one sync).
+static gs_status project_count_phase(gs_ctx* c, const gs_params* p, const gs_camera* cams_h, int n_views,
+                                     const int64_t* dp_h, int64_t* send_counts_h, void* bwd_index,
+                                     cudaStream_t st, int64_t* total_h) {
   gs_status s = gs_check_batch(c, cams_h, n_views, dp_h);
   if (s != GS_OK) return s;
   GS_REQUIRE(c, p && send_counts_h, "null argument");
   const int G = c->world, b = n_views, nb = b * G;
   GS_REQUIRE(c, nb <= kMaxBuckets, "n_views * world = %d exceeds %d", nb, kMaxBuckets);
-  cudaStream_t st = (cudaStream_t)stream;
   for (int d = 0; d < G; d++) send_counts_h[d] = 0;
+  *total_h = 0;
   if (p->n == 0) return GS_OK;
   GS_REQUIRE(c, bwd_index && p->pos_op && p->log_scale && p->rot && p->sh, "null buffer");
   gs_index_layout L = index_layout(p->n, b, G);
@@ -169,19 +177,79 @@ extern "C" gs_status gs_project(gs_ctx* c, const gs_params* p, const gs_camera* 
   GS_CUDA(c, cudaMemcpyAsync(c->pinned, tot, (G + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GS_CUDA(c, cudaStreamSynchronize(st));
   for (int d = 0; d < G; d++) send_counts_h[d] = c->pinned[d + 1] - c->pinned[d];
-  int64_t total = c->pinned[G];
-  // record positions are int32 in the backward (gs_adam_step) and the exchanges
-  if (total >= (1ll << 31)) return gs_fail(c, GS_ENOTSUP, "%lld records exceed int32 positions", (long long)total);
+  *total_h = c->pinned[G];
+  if (*total_h >= (1ll << 31))
+    return gs_fail(c, GS_ENOTSUP, "%lld records exceed int32 positions", (long long)*total_h);
+  return GS_OK;
+}
+
+// Writing half: records of the counted batch to outs (see gs_outs).
+static gs_status project_write_phase(gs_ctx* c, const gs_params* p, const gs_camera* cams_h, int n_views,
+                                     const void* bwd_index, const gs_outs& outs, cudaStream_t st) {
+  const int G = c->world, b = n_views, nb = b * G;
+  gs_index_layout L = index_layout(p->n, b, G);
+  const uint32_t* maskw = (const uint32_t*)bwd_index;
+  const int64_t* base = (const int64_t*)((const char*)bwd_index + L.base_off);
+  gs_cams_arg cams = make_cams(cams_h, n_views);
+  gs_geom geo = gs_make_geom(&cams_h[0]);
+  ++c->launches;
+  k_project_write<<<(unsigned)L.ncta, kBlock, 0, st>>>(
+      (const float4*)p->pos_op, (const float4*)p->log_scale, (const float4*)p->rot,
+      (const float4*)p->sh, p->n, p->gid_base, cams, geo, G, nb, L.NW, maskw, base, L.ncta, outs);
+  GS_LAUNCH_CHECK(c, "project_write");
+  return GS_OK;
+}
+
+extern "C" gs_status gs_project(gs_ctx* c, const gs_params* p, const gs_camera* cams_h,
+                                int n_views, const int64_t* dp_h, void* send_rec, int64_t send_cap,
+                                int64_t* send_counts_h, void* bwd_index, void* stream) {
+  if (!c) return GS_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t total = 0;
+  gs_status s = project_count_phase(c, p, cams_h, n_views, dp_h, send_counts_h, bwd_index, st, &total);
+  if (s != GS_OK) return s;
   if (total > send_cap)
     return gs_fail(c, GS_ECAPACITY, "send capacity %lld < %lld records", (long long)send_cap,
                    (long long)total);
   if (total == 0) return GS_OK;
   GS_REQUIRE(c, send_rec != nullptr, "null send_rec");
-  ++c->launches;
-  k_project_write<<<(unsigned)L.ncta, kBlock, 0, st>>>(
-      (const float4*)p->pos_op, (const float4*)p->log_scale, (const float4*)p->rot,
-      (const float4*)p->sh, p->n, p->gid_base, cams, geo, G, nb, L.NW, maskw, base, L.ncta,
-      (gs_rec*)send_rec);
-  GS_LAUNCH_CHECK(c, "project_write");
-  return GS_OK;
+  gs_outs outs;
+  for (int d = 0; d < GS_MAX_WORLD; d++) outs.d[d] = (gs_rec*)send_rec;
+  return project_write_phase(c, p, cams_h, n_views, bwd_index, outs, st);
+}
+
+extern "C" gs_status gs_project_count(gs_ctx* c, const gs_params* p, const gs_camera* cams_h, int n_views,
+                                      const int64_t* dp_h, int64_t* send_counts_h, void* bwd_index, void* stream) {
+  if (!c) return GS_EINVAL;
+  int64_t total = 0;
+  return project_count_phase(c, p, cams_h, n_views, dp_h, send_counts_h, bwd_index, (cudaStream_t)stream, &total);
+}
+
+extern "C" gs_status gs_project_put(gs_ctx* c, const gs_params* p, const gs_camera* cams_h, int n_views,
+                                    const int64_t* dp_h, const void* bwd_index, void* stream) {
+  if (!c) return GS_EINVAL;
+  gs_status s = gs_check_batch(c, cams_h, n_views, dp_h);
+  if (s != GS_OK) return s;
+  GS_REQUIRE(c, p, "null argument");
+  GS_REQUIRE(c, c->p2p.attached && c->p2p.planned, "gs_project_put needs gs_p2p_attach and gs_p2p_plan");
+  const int G = c->world, r = c->rank;
+  int64_t seg[GS_MAX_WORLD + 1], put[GS_MAX_WORLD], soff[GS_MAX_WORLD + 1], own[GS_MAX_WORLD];
+  s = gs_p2p_offsets(c->p2p.counts.data(), G, r, seg, put, soff, own);
+  if (s != GS_OK) return gs_fail(c, s, "bad plan");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n_send = soff[G];
+  if (n_send > 0) {  // zero the own gradient rows before any peer's backward adds into them
+    GS_REQUIRE(c, c->p2p.dsend[r] != nullptr, "null dL/dsend");
+    GS_CUDA(c, cudaMemsetAsync(c->p2p.dsend[r], 0, (size_t)n_send * 9 * sizeof(float), st));
+  }
+  if (p->n == 0 || n_send == 0) return GS_OK;
+  GS_REQUIRE(c, bwd_index && p->pos_op && p->log_scale && p->rot && p->sh, "null buffer");
+  gs_outs outs;
+  for (int d = 0; d < GS_MAX_WORLD; d++) outs.d[d] = nullptr;
+  for (int d = 0; d < G; d++)
+    if (soff[d + 1] > soff[d]) {
+      GS_REQUIRE(c, c->p2p.recv[d] != nullptr, "rank %d has no receive buffer", d);
+      outs.d[d] = (gs_rec*)c->p2p.recv[d] + (put[d] - soff[d]);
+    }
+  return project_write_phase(c, p, cams_h, n_views, bwd_index, outs, st);
 }

@@ -543,8 +543,23 @@ __device__ __forceinline__ int red_index(int lane, bool& valid) {
 // by shuffles.  ~9 stores + 10 instructions per entry instead of the 12-shuffle transpose
 // reduction with its selects (~47).
 constexpr int kF = 4;  // entries per flush (36 rows: 32 + 4 x 8 lanes)
+
+// Where the gradient of received record j goes: row base[s] + 9 j for the source s with
+// seg[s] <= j < seg[s+1].  Own buffer: nseg = 1, base[0] = dL/d(record).  NEXT-3
+// (gs_render_bwd_put): base[s] = source s's dL/dsend + 9 (owner_off[s] - seg[s]), so the
+// reduction lands in the owner's buffer over NVLink (the reverse exchange, fused).
+struct gs_gdst {
+  float* base[GS_MAX_WORLD];
+  long long seg[GS_MAX_WORLD + 1];
+  int nseg;
+};
+__device__ __forceinline__ float* gdst_row(const gs_gdst& g, uint32_t j) {
+  int s = 0;
+  while (s + 1 < g.nseg && (long long)j >= g.seg[s + 1]) s++;
+  return g.base[s] + (int64_t)j * 9;
+}
 __device__ __forceinline__ void flush_rows(const float* __restrict__ rows, const uint32_t* __restrict__ rid, int nslot,
-                                           float* __restrict__ dL_drec, int lane) {
+                                           const gs_gdst& dst, int lane) {
   constexpr int NP = 9 * kF, R = NP - 32, LPP = 32 / R;
   static_assert(R > 0 && 32 % R == 0 && LPP <= 8 && 8 % LPP == 0, "flush layout");
   const int np = 9 * nslot;
@@ -559,7 +574,7 @@ __device__ __forceinline__ void flush_rows(const float* __restrict__ rows, const
       a = make_float4(lo.x, lo.y, hi.x, hi.y);
     }
     const float z = (a.x + a.y) + (a.z + a.w);
-    if (z != 0.f) atomicAdd(dL_drec + (int64_t)rid[lane / 9] * 9 + lane % 9, z);
+    if (z != 0.f) atomicAdd(gdst_row(dst, rid[lane / 9]) + lane % 9, z);
   }
   {
     const int p = 32 + lane / LPP, part = lane % LPP;
@@ -574,7 +589,7 @@ __device__ __forceinline__ void flush_rows(const float* __restrict__ rows, const
     }
 #pragma unroll
     for (int o = LPP / 2; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-    if (part == 0 && p < np && z != 0.f) atomicAdd(dL_drec + (int64_t)rid[p / 9] * 9 + p % 9, z);
+    if (part == 0 && p < np && z != 0.f) atomicAdd(gdst_row(dst, rid[p / 9]) + p % 9, z);
   }
 }
 
@@ -584,7 +599,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
     const int32_t* __restrict__ range, gs_geom geo, int64_t B_lo, float bg0, float bg1, float bg2,
     const float* __restrict__ dL_dpix, const float* __restrict__ T_final,
     const int32_t* __restrict__ n_last, float* __restrict__ dL_drec, int64_t* __restrict__ tile_cost,
-    int cost_mode, long long* __restrict__ stats, int cull) {
+    int cost_mode, long long* __restrict__ stats, int cull, gs_gdst gdst) {
   constexpr int NT = 256 / PPT;
   constexpr bool kOneWarp = NT == 32;
   constexpr int kNW = NT / 32;   // warps per block
@@ -724,7 +739,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
           if (lane == 0) s_rid[wid * kF + nslot] = __float_as_uint(cq.w);
           if (++nslot == kF) {
             __syncwarp();
-            flush_rows(s_rows + wid * kF * 9 * 32, s_rid + wid * kF, kF, dL_drec, lane);
+            flush_rows(s_rows + wid * kF * 9 * 32, s_rid + wid * kF, kF, gdst, lane);
             __syncwarp();
             nslot = 0;
           }
@@ -757,7 +772,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   if constexpr (kWarp) {
     if (nslot > 0) {
       __syncwarp();
-      flush_rows(s_rows + wid * kF * 9 * 32, s_rid + wid * kF, nslot, dL_drec, lane);
+      flush_rows(s_rows + wid * kF * 9 * 32, s_rid + wid * kF, nslot, gdst, lane);
     }
   }
   if (kStats) {
@@ -866,6 +881,43 @@ extern "C" gs_status gs_render_fwd(gs_ctx* c, const void* recv_rec, const uint32
   return GS_OK;
 }
 
+// Shared launcher of gs_render_bwd and gs_render_bwd_put (gradient rows through gdst).
+static gs_status render_bwd_launch(gs_ctx* c, const void* recv_rec, const uint32_t* sorted_idx,
+                                   const int32_t* tile_range, const gs_camera* cams_h, const int64_t* dp_h,
+                                   const float* bg_h, const float* dL_dpix, const float* T_final,
+                                   const int32_t* n_last, float* dL_drec, const gs_gdst& gdst, bool put,
+                                   int64_t* tile_cost, int cost_mode, int64_t* stats, cudaStream_t st) {
+  const int64_t B_lo = dp_h[c->rank], n_owned = dp_h[c->rank + 1] - B_lo;
+  if (n_owned == 0) return GS_OK;
+  GS_REQUIRE(c, tile_range && T_final && n_last && dL_dpix, "null argument");
+  gs_geom geo = gs_make_geom(&cams_h[0]);
+  float bg[3] = {0.f, 0.f, 0.f};
+  if (bg_h) for (int k = 0; k < 3; k++) bg[k] = bg_h[k];
+  const int ppt = render_ppt();
+  const int mb = render_minb(1);
+  const bool black = bg[0] == 0.f && bg[1] == 0.f && bg[2] == 0.f;
+  if (put && !(ppt == 4 && (render_warp() & 2) && black))
+    return gs_fail(c, GS_ENOTSUP, "gs_render_bwd_put needs the warp-independent PPT=4 backward and bg = 0");
+  ++c->launches;
+  auto kb = ppt == 2 ? (stats ? k_render_bwd<2, true> : k_render_bwd<2, false>)
+          : ppt == 8 ? (stats ? k_render_bwd<8, true> : k_render_bwd<8, false>)
+          : (render_warp() & 2) ? (black
+                                       ? (mb == 12 ? (stats ? k_render_bwd<4, true, 12, true, false> : k_render_bwd<4, false, 12, true, false>)
+                                                   : mb == 14 ? (stats ? k_render_bwd<4, true, 14, true, false> : k_render_bwd<4, false, 14, true, false>)
+                                                   : mb == 18 ? (stats ? k_render_bwd<4, true, 18, true, false> : k_render_bwd<4, false, 18, true, false>)
+                                                   : (stats ? k_render_bwd<4, true, 16, true, false> : k_render_bwd<4, false, 16, true, false>))
+                                       : (stats ? k_render_bwd<4, true, 12, true> : k_render_bwd<4, false, 12, true>))
+          : mb == 8 ? (stats ? k_render_bwd<4, true, 8> : k_render_bwd<4, false, 8>)
+          : mb == 10 ? (stats ? k_render_bwd<4, true, 10> : k_render_bwd<4, false, 10>)
+                     : (stats ? k_render_bwd<4, true, 12> : k_render_bwd<4, false, 12>);
+  const int threads = 256 / ppt;
+  kb<<<(unsigned)n_owned, threads, 0, st>>>(
+      (const gs_rec*)recv_rec, sorted_idx, tile_range, geo, B_lo, bg[0], bg[1], bg[2], dL_dpix, T_final, n_last,
+      dL_drec, tile_cost, cost_mode, (long long*)stats, (render_cull() >> 1) & 1, gdst);
+  GS_LAUNCH_CHECK(c, "render_bwd");
+  return GS_OK;
+}
+
 extern "C" gs_status gs_render_bwd(gs_ctx* c, const void* recv_rec, int64_t n_recv,
                                    const uint32_t* sorted_idx, const int32_t* tile_range,
                                    const gs_camera* cams_h, int n_views, const int64_t* dp_h,
@@ -880,31 +932,40 @@ extern "C" gs_status gs_render_bwd(gs_ctx* c, const void* recv_rec, int64_t n_re
     GS_REQUIRE(c, dL_drec != nullptr, "null dL_drec");
     GS_CUDA(c, cudaMemsetAsync(dL_drec, 0, (size_t)n_recv * 9 * sizeof(float), st));
   }
-  const int64_t B_lo = dp_h[c->rank], n_owned = dp_h[c->rank + 1] - B_lo;
-  if (n_owned == 0) return GS_OK;
-  GS_REQUIRE(c, tile_range && T_final && n_last && dL_dpix, "null argument");
-  gs_geom geo = gs_make_geom(&cams_h[0]);
-  float bg[3] = {0.f, 0.f, 0.f};
-  if (bg_h) for (int k = 0; k < 3; k++) bg[k] = bg_h[k];
-  ++c->launches;
-  const int ppt = render_ppt();
-  const int mb = render_minb(1);
-  auto kb = ppt == 2 ? (stats ? k_render_bwd<2, true> : k_render_bwd<2, false>)
-          : ppt == 8 ? (stats ? k_render_bwd<8, true> : k_render_bwd<8, false>)
-          : (render_warp() & 2) ? (bg[0] == 0.f && bg[1] == 0.f && bg[2] == 0.f
-                                       ? (mb == 12 ? (stats ? k_render_bwd<4, true, 12, true, false> : k_render_bwd<4, false, 12, true, false>)
-                                                   : mb == 14 ? (stats ? k_render_bwd<4, true, 14, true, false> : k_render_bwd<4, false, 14, true, false>)
-                                                   : mb == 18 ? (stats ? k_render_bwd<4, true, 18, true, false> : k_render_bwd<4, false, 18, true, false>)
-                                                   : (stats ? k_render_bwd<4, true, 16, true, false> : k_render_bwd<4, false, 16, true, false>))
-                                       : (stats ? k_render_bwd<4, true, 12, true> : k_render_bwd<4, false, 12, true>))
-          : mb == 8 ? (stats ? k_render_bwd<4, true, 8> : k_render_bwd<4, false, 8>)
-          : mb == 10 ? (stats ? k_render_bwd<4, true, 10> : k_render_bwd<4, false, 10>)
-                     : (stats ? k_render_bwd<4, true, 12> : k_render_bwd<4, false, 12>);
-  const int threads = 256 / ppt;
+  gs_gdst g;
+  for (int k = 0; k < GS_MAX_WORLD; k++) g.base[k] = nullptr;
+  for (int k = 0; k <= GS_MAX_WORLD; k++) g.seg[k] = 0;
+  g.base[0] = dL_drec;
+  g.seg[1] = n_recv;
+  g.nseg = 1;
+  return render_bwd_launch(c, recv_rec, sorted_idx, tile_range, cams_h, dp_h, bg_h, dL_dpix, T_final, n_last,
+                           dL_drec, g, false, tile_cost, cost_mode, stats, st);
+}
 
-  kb<<<(unsigned)n_owned, threads, 0, st>>>(
-      (const gs_rec*)recv_rec, sorted_idx, tile_range, geo, B_lo, bg[0], bg[1], bg[2], dL_dpix, T_final, n_last,
-      dL_drec, tile_cost, cost_mode, (long long*)stats, (render_cull() >> 1) & 1);
-  GS_LAUNCH_CHECK(c, "render_bwd");
-  return GS_OK;
+extern "C" gs_status gs_render_bwd_put(gs_ctx* c, const void* recv_rec, int64_t n_recv, const uint32_t* sorted_idx,
+                                       const int32_t* tile_range, const gs_camera* cams_h, int n_views,
+                                       const int64_t* dp_h, const float* dL_dpix, const float* T_final,
+                                       const int32_t* n_last, int64_t* tile_cost, int cost_mode, int64_t* stats,
+                                       void* stream) {
+  if (!c) return GS_EINVAL;
+  gs_status s = gs_check_batch(c, cams_h, n_views, dp_h);
+  if (s != GS_OK) return s;
+  GS_REQUIRE(c, c->p2p.attached && c->p2p.planned, "gs_render_bwd_put needs gs_p2p_attach and gs_p2p_plan");
+  const int G = c->world;
+  int64_t seg[GS_MAX_WORLD + 1], put[GS_MAX_WORLD], soff[GS_MAX_WORLD + 1], own[GS_MAX_WORLD];
+  s = gs_p2p_offsets(c->p2p.counts.data(), G, c->rank, seg, put, soff, own);
+  if (s != GS_OK) return gs_fail(c, s, "bad plan");
+  GS_REQUIRE(c, n_recv == seg[G], "n_recv %lld does not match the plan (%lld)", (long long)n_recv,
+             (long long)seg[G]);
+  gs_gdst g;
+  for (int k = 0; k < GS_MAX_WORLD; k++) g.base[k] = nullptr;
+  for (int k = 0; k <= GS_MAX_WORLD; k++) g.seg[k] = k <= G ? seg[k] : seg[G];
+  for (int k = 0; k < G; k++)
+    if (seg[k + 1] > seg[k]) {
+      GS_REQUIRE(c, c->p2p.dsend[k] != nullptr, "rank %d has no dL/dsend buffer", k);
+      g.base[k] = c->p2p.dsend[k] + 9 * (own[k] - seg[k]);
+    }
+  g.nseg = G;
+  return render_bwd_launch(c, recv_rec, sorted_idx, tile_range, cams_h, dp_h, nullptr, dL_dpix, T_final, n_last,
+                           nullptr, g, true, tile_cost, cost_mode, stats, (cudaStream_t)stream);
 }

@@ -42,7 +42,7 @@ class GrendelTrainer:
     def __init__(self, ctx: L.Context, params: L.GaussianParams, width: int, height: int, n_views: int,
                  n_images: int, lr=DEFAULT_LR, cost_mode=L.COST_MEASURED, bg=(0.0, 0.0, 0.0),
                  rebalance=True, dp=None, device=None, split_adam=True, loss="l1", ssim_lambda=0.2,
-                 densify_stats=False):
+                 densify_stats=False, exchange="nccl", count_gather="nccl"):
         self.ctx, self.p = ctx, params
         self.device = device or params.pos_op.device
         self.W, self.H, self.b = width, height, n_views
@@ -54,6 +54,17 @@ class GrendelTrainer:
         if loss not in ("l1", "ssim"):
             raise ValueError("loss must be 'l1' or 'ssim' (L1 + D-SSIM, NEXT-1)")
         self.loss_kind, self.ssim_lambda = loss, float(ssim_lambda)
+        # NEXT-3: "p2p" = the exchanges fused into the producing kernels over peer memory
+        # (gs_project_put / gs_render_bwd_put, include/gs.h); "nccl" = grouped send/recv
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError("exchange must be 'nccl' or 'p2p'")
+        self.exchange_kind = exchange if ctx.world > 1 else "nccl"
+        if self.exchange_kind == "p2p" and (loss != "l1" or densify_stats or any(bg)):
+            raise ValueError("exchange='p2p' supports the L1 loss, black background, no densification statistics")
+        self.p2p = None  # (recv_ptr, dsend_ptr, recv_cap, dsend_cap) once attached
+        # which collective carries the G x G count matrix (G^2 int64): the context's NCCL
+        # communicator, or torch.distributed's process group (contexts without one)
+        self.count_gather = count_gather
         # NEXT-2: densification statistics (accum, denom, max screen radius) per owned Gaussian
         self.collect_densify = bool(densify_stats)
         self.dstats = self._new_stats(params.n) if densify_stats else None
@@ -159,6 +170,41 @@ class GrendelTrainer:
         buf.ensure(need), self.halo_ids.ensure(need)
         return L.halo_exchange(self.ctx, data, cams, dp, buf.t, self.halo_ids.t, st)
 
+    def _p2p_setup(self, recv_cap, dsend_cap):
+        """COLLECTIVE (every rank, same capacities): symmetric buffers, IPC handles exchanged
+        through torch.distributed, peers opened and attached (NEXT-3)."""
+        import torch.distributed as dist
+        ctx, G = self.ctx, self.G
+        rp, rh = L.sym_alloc(ctx, L.SYM_RECV, recv_cap * L.RECORD_BYTES)
+        dp_, dh = L.sym_alloc(ctx, L.SYM_DSEND, dsend_cap * L.GRAD_FLOATS * 4)
+        fp, fh = L.sym_alloc(ctx, L.SYM_FLAGS, G * 8)
+        allh = [None] * G
+        dist.all_gather_object(allh, (rh, dh, fh))
+        own = (rp, dp_, fp)
+        ptrs = [[own[k] if g == self.rank else L.ipc_open(ctx, allh[g][k]) for g in range(G)] for k in range(3)]
+        L.p2p_attach(ctx, ptrs[0], [recv_cap] * G, ptrs[1], [dsend_cap] * G, ptrs[2])
+        self.p2p = (rp, dp_, recv_cap, dsend_cap)
+
+    def _p2p_exchange(self, cams, dp, st):
+        """A1 + A2 fused: count, all-gather the count matrix, put the records into the
+        destinations' receive buffers, barrier.  Returns (send_counts, recv_counts, n_recv)."""
+        ctx = self.ctx
+        send_counts = L.project_count(ctx, self.p, cams, dp, self.bwd_index, st)
+        if self.count_gather == "nccl":
+            C = L.exchange_counts(ctx, send_counts, st)
+        else:
+            import torch.distributed as dist
+            rows = [None] * self.G
+            dist.all_gather_object(rows, [int(x) for x in send_counts])
+            C = np.array(rows, np.int64)
+        n_in, n_out = C.sum(0), C.sum(1)
+        if self.p2p is None or n_in.max() > self.p2p[2] or n_out.max() > self.p2p[3]:
+            self._p2p_setup(int(n_in.max() * 1.25) + 1024, int(n_out.max() * 1.25) + 1024)
+        n_recv = L.p2p_plan(ctx, C)
+        L.project_put(ctx, self.p, cams, dp, self.bwd_index, st)
+        L.p2p_barrier(ctx, st)
+        return send_counts, C[:, self.rank].copy(), n_recv
+
     @property
     def n_owned(self):
         return int(self.dp[self.rank + 1] - self.dp[self.rank])
@@ -175,10 +221,13 @@ class GrendelTrainer:
                 ev[name][k].record(torch.cuda.current_stream() if st is None else st)
 
         self.step_count += 1
+        p2p = self.exchange_kind == "p2p"
         # A1 project (retry on capacity)
         rec("project", 0)
         cap = self.send.cap
-        while True:
+        if p2p:  # NEXT-3: projection writes straight into the destinations (A1 + A2 fused)
+            send_counts, recv_counts, n_recv = self._p2p_exchange(cams, dp, st)
+        while not p2p:
             try:
                 send_counts = L.project(ctx, self.p, cams, dp, self.send.t, cap, self.bwd_index, st)
                 break
@@ -190,7 +239,9 @@ class GrendelTrainer:
         n_send = int(send_counts.sum())
         # A2 exchange
         rec("exchange", 0)
-        if self.G == 1:
+        if p2p:
+            recv_t = self.p2p[0]
+        elif self.G == 1:
             recv_t, recv_counts, n_recv = self.send.t, send_counts.copy(), n_send
         else:
             while True:
@@ -243,12 +294,19 @@ class GrendelTrainer:
             rec("loss", 1)
         # A5 render backward
         rec("render_bwd", 0)
-        L.render_bwd(ctx, recv_t, n_recv, self.sorted.t, self.range.t, cams, dp, self.bg, self.dpix.t, self.T.t,
-                     self.nl.t, self.drec.t, self.cost.t, self.cost_mode, stats, st)
+        if p2p:  # A5 + A6 fused: gradient sums reduced straight into the owners' buffers
+            L.render_bwd_put(ctx, recv_t, n_recv, self.sorted.t, self.range.t, cams, dp, self.dpix.t, self.T.t,
+                             self.nl.t, self.cost.t, self.cost_mode, stats, st)
+        else:
+            L.render_bwd(ctx, recv_t, n_recv, self.sorted.t, self.range.t, cams, dp, self.bg, self.dpix.t,
+                         self.T.t, self.nl.t, self.drec.t, self.cost.t, self.cost_mode, stats, st)
         rec("render_bwd", 1)
         # A6 reverse exchange
         rec("exchange_grads", 0)
-        if self.G == 1:
+        if p2p:
+            L.p2p_barrier(ctx, st)
+            dsend = self.p2p[1]
+        elif self.G == 1:
             dsend = self.drec.t
         else:
             L.exchange_grads(ctx, self.drec.t, recv_counts, send_counts, self.dsend.t, st)

@@ -7,6 +7,7 @@
 import csv
 import io
 import json
+import os
 import subprocess
 import sys
 from collections import OrderedDict, defaultdict
@@ -117,7 +118,7 @@ def traffic(rep, config, out_json="profiles/dram_traffic.json"):
         if role is None:
             continue
         b = float(r[ri]) * scale.get(units[ri], 1) + float(r[wi]) * scale.get(units[wi], 1)
-        src = rep.replace("gpurun_out/prof_", "profiles/").replace(".ncu-rep", ".md")
+        src = "profiles/" + os.path.basename(rep).replace("prof_", "").replace(".ncu-rep", ".md")
         d.setdefault(config, {})[role] = {"bytes": b, "source": src, "kernel": name}
     json.dump(d, open(out_json, "w"), indent=1)
     print(json.dumps(d, indent=1))
@@ -125,6 +126,6 @@ def traffic(rep, config, out_json="profiles/dram_traffic.json"):
 
 if __name__ == "__main__":
     if sys.argv[1] == "traffic":
-        traffic(sys.argv[2], sys.argv[3])
+        traffic(sys.argv[2], sys.argv[3], *sys.argv[4:5])
     else:
         {"launches": launches, "report": report}[sys.argv[1]](sys.argv[2], sys.argv[3])
