@@ -329,14 +329,26 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     step_ev = []
+    dbg = [] if os.environ.get("GS_BENCH_DEBUG") else None  # per-call events of every timed step
     for _ in range(args.steps):
-        one_step()
+        if dbg is not None:
+            dbg.append(make_events())
+            th0 = time.perf_counter()
+        one_step(events=None if dbg is None else dbg[-1])
+        if dbg is not None:
+            dbg[-1]["host_ms"] = 1000.0 * (time.perf_counter() - th0)
         step_ev.append(torch.cuda.Event(enable_timing=True))
         step_ev[-1].record(stream)
     e1.record(stream)
     barrier()
     step_ms = [e0.elapsed_time(step_ev[0])] + [a.elapsed_time(b) for a, b in zip(step_ev, step_ev[1:])]
     print("timed steps (ms): " + " ".join("%.1f" % t for t in step_ms), file=sys.stderr, flush=True)
+    if dbg is not None:
+        for k, ev in enumerate(dbg):
+            hm = ev.pop("host_ms")
+            print("step %d (batch %s) host %.1f ms: %s" % (k, sched[args.warmup + k], hm,
+                                                           {n: round(v, 2) for n, v in event_ms(ev).items()}),
+                  file=sys.stderr, flush=True)
     clk = clocks.stop()
     launches = ctx.launch_count() - l0
     ms = e0.elapsed_time(e1)
