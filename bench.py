@@ -16,6 +16,7 @@ Inputs (11.2M Gaussians x 3 states, 0.76 GB ground truth per batch) are far larg
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -317,12 +318,20 @@ def main():
     # size all buffers for every batch this run will use (setup, not timed)
     tr.reserve_for([batch_cams(k) for k in range(len(sched) - 1)])
     clocks = ClockSampler(local)
-    clocks.start()
+    if not os.environ.get("GS_NO_CLOCKS"):  # diagnostics: run without the nvidia-smi sampler
+        clocks.start()
     for _ in range(args.warmup):
         one_step()
     setup_s = time.perf_counter() - t_setup
 
     # ---------------- timed region (device-resident inputs)
+    # The step's host syncs (record and pair counts) leave the GPU idle while the host thread
+    # is paused, and a full Python garbage collection landing there cost one step 5-40 ms at a
+    # deterministic allocation count: collect and freeze the setup's objects, no automatic
+    # collections while timing (what a training loop does).
+    gc.collect()
+    gc.freeze()
+    gc.disable()
     barrier()
     clocks.mark()
     l0 = ctx.launch_count()
@@ -337,6 +346,7 @@ def main():
         one_step(events=None if dbg is None else dbg[-1])
         if dbg is not None:
             dbg[-1]["host_ms"] = 1000.0 * (time.perf_counter() - th0)
+            dbg[-1]["pairs"] = tr.last["n_pairs"]
         step_ev.append(torch.cuda.Event(enable_timing=True))
         step_ev[-1].record(stream)
     e1.record(stream)
@@ -345,8 +355,9 @@ def main():
     print("timed steps (ms): " + " ".join("%.1f" % t for t in step_ms), file=sys.stderr, flush=True)
     if dbg is not None:
         for k, ev in enumerate(dbg):
-            hm = ev.pop("host_ms")
-            print("step %d (batch %s) host %.1f ms: %s" % (k, sched[args.warmup + k], hm,
+            hm, npairs = ev.pop("host_ms"), ev.pop("pairs")
+            print("step %d (batch %s, %d pairs, cap %d) host %.1f ms: %s" % (k, sched[args.warmup + k], npairs,
+                                                                             tr.sorted.cap, hm,
                                                            {n: round(v, 2) for n, v in event_ms(ev).items()}),
                   file=sys.stderr, flush=True)
     clk = clocks.stop()
@@ -425,6 +436,8 @@ def main():
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         e2e = {"value": views / (float(ems.item()) / 1000.0), "unit": "views/s",
                "h2d_bytes_per_step": int(cfg["b"] * H * W * 3), "d2h_bytes_per_step": 8}
+
+    gc.enable()
 
     # ---------------- roofline of the dominant kernel
     pk, pk_src = peaks()

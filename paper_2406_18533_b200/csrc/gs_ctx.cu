@@ -29,13 +29,18 @@ void* gs_slot_get(gs_ctx* c, int slot, size_t bytes, cudaStream_t st) {
   gs_slot& s = c->slot[slot];
   if (bytes == 0) bytes = 16;
   if (s.bytes >= bytes) return s.ptr;
+  static const bool dbg = getenv("GS_DEBUG_SLOTS") != nullptr;
+  if (dbg) fprintf(stderr, "libgs: slot %d grows %zu -> %zu bytes\n", slot, s.bytes, bytes + bytes / 2);
   if (s.ptr) {
     cudaStreamSynchronize(st);
     cudaFree(s.ptr);
     s.ptr = nullptr;
     s.bytes = 0;
   }
-  size_t want = bytes + bytes / 8;  // headroom against regrowth
+  // headroom against regrowth: pair and record counts drift up as training grows the
+  // Gaussians (C2: +8 % pairs over 12 steps), and each regrowth of a GB-sized slot is a
+  // synchronising cudaFree + cudaMalloc (15-60 ms) inside a step
+  size_t want = bytes + bytes / 2;
   if (cudaMalloc(&s.ptr, want) != cudaSuccess) {
     cudaGetLastError();
     s.ptr = nullptr;

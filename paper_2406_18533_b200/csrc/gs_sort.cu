@@ -1,3 +1,5 @@
+#include <chrono>
+#include <cstdio>
 // gs_sort.cu -- A3: Z-buffer build ("iterates over intersecting Gaussians in
 // increasing depth"; App. A.2 "indices of intersecting gaussians for each pixel").
 //
@@ -620,8 +622,12 @@ static gs_status bin_sort_radix(gs_ctx* c, const gs_rec* rec, int64_t n_recv, gs
   k_tile_counts<<<(unsigned)((n_recv + 256) / 256), 256, 0, st>>>(rec, n_recv, geo, v_lo, v_hi, ntiles);
   gs_status s = gs_scan_i64(c, ntiles, ps, n_recv + 1, 0, st);  // only for the total
   if (s != GS_OK) return s;
+  static const bool dbg = getenv("GS_DEBUG_SORT") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto t0 = now();
   GS_CUDA(c, cudaMemcpyAsync(c->pinned, ps + n_recv, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GS_CUDA(c, cudaStreamSynchronize(st));
+  auto t1 = now();
   const int64_t n_full = c->pinned[0];
   // tile_range holds int32 positions: bound the pair total (a superset of the owned pairs)
   if (n_full >= (1ll << 31))
@@ -673,8 +679,15 @@ static gs_status bin_sort_radix(gs_ctx* c, const gs_rec* rec, int64_t n_recv, gs
   k_key_ranges<<<(unsigned)((n_full + 256) / 256), 256, 0, st>>>(kin, n_full, (uint32_t)n_owned, tile_range);
   GS_LAUNCH_CHECK(c, "bin_sort ranges");
   int32_t* kp = (int32_t*)(c->pinned + 1);
+  auto t2 = now();
   GS_CUDA(c, cudaMemcpyAsync(kp, tile_range + n_owned, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   GS_CUDA(c, cudaStreamSynchronize(st));
+  auto t3 = now();
+  if (dbg) {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    fprintf(stderr, "libgs bin_sort: n_full %lld  sync1 %.2f ms  enqueue %.2f ms  sync2 %.2f ms\n",
+            (long long)n_full, ms(t0, t1), ms(t1, t2), ms(t2, t3));
+  }
   const int64_t K = *kp;
   *n_pairs_h = K;
   if (K > pair_cap) return gs_fail(c, GS_ECAPACITY, "pair capacity %lld < %lld", (long long)pair_cap, (long long)K);

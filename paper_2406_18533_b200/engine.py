@@ -7,10 +7,14 @@ from __future__ import annotations
 
 import math
 
+import os
+
 import numpy as np
 import torch
 
 from . import _lib as L
+
+_DEBUG = bool(os.environ.get("GS_BENCH_DEBUG"))
 
 # 3DGS default learning rates ("default hyperparameters from the 3DGS repository";
 # values as S:349 lists them): pos, sh_dc, sh_rest, opacity, scale, rot
@@ -32,7 +36,7 @@ class _Buf:
 
     def ensure(self, n):
         if n > self.cap:
-            cap = max(int(n * 1.25) + 1024, 1024)
+            cap = max(int(n * 1.5) + 1024, 1024)  # counts drift up during training (see gs_slot_get)
             self.t = torch.empty((cap,) + self.row, dtype=self.dtype, device=self.device)
             self.cap = cap
         return self.t
@@ -262,6 +266,8 @@ class GrendelTrainer:
                                      self.range.t, st)
                 break
             except L.CapacityError as e:
+                if _DEBUG:
+                    print("engine: pair capacity %d < %d, growing" % (self.sorted.cap, e.needed), flush=True)
                 self.sorted.ensure(e.needed)
         rec("bin_sort", 1)
         # A4 render forward + fused L1
