@@ -251,6 +251,9 @@ def main():
     ap.add_argument("--densify", action="store_true",
                     help="NEXT-2: collect densification statistics every step and time one densify event at "
                          "the end (extra 'densify' object in the JSON line)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="N > 1: grouped NCCL send/recv, or NEXT-3's exchanges fused into the projection and "
+                         "render-backward kernels over peer memory (CUDA IPC / NVLink)")
     ap.add_argument("--loss", default="l1", choices=["l1", "ssim"],
                     help="l1: the hot-path loss (R11); ssim: L1 + D-SSIM, lambda 0.2 (NEXT-1)")
     args = ap.parse_args()
@@ -295,7 +298,7 @@ def main():
     gt_batch = torch.empty((cfg["b"], H, W, 3), dtype=torch.uint8, device=dev)
     cost_mode = {"measured": L.COST_MEASURED, "work": L.COST_WORK, "paper_avg": L.COST_PAPER_AVG}[args.cost_mode]
     tr = GrendelTrainer(ctx, p, W, H, cfg["b"], len(cams), cost_mode=cost_mode, rebalance=not args.no_rebalance,
-                        device=dev, loss=args.loss, densify_stats=args.densify)
+                        device=dev, loss=args.loss, densify_stats=args.densify, exchange=args.exchange)
     stream = torch.cuda.current_stream()
     k_sched = [0]
 
@@ -526,6 +529,7 @@ def main():
                                3 * 240 * n / 1e9, cfg["b"] * W * H * 3 / 1e9),
                            "loss": "l1" if args.loss == "l1" else "l1+dssim(0.2)",
                            "cost_mode": args.cost_mode, "rebalance": not args.no_rebalance,
+                           "exchange": args.exchange if world > 1 else "none (one rank)",
                            "shard_layout": "random" if args.no_morton else "morton"},
                 "raster_ms_per_view": round(raster_ms_view, 3),
                 "calls_ms": {k: round(v, 3) for k, v in calls.items()},
