@@ -136,18 +136,30 @@ __global__ void __launch_bounds__(kThreads) k_ssim_terms(
   __syncthreads();
   // x: rendered planes (zero outside the grid; partial blocks hold zeros outside the image,
   // see gs_render_fwd's out_rgb); y: ground truth, zero outside the image
-  stage_planes(s_src, 3, 0, &X[0][0][0]);
-  for (int t = tid; t < kS * kS; t += kThreads) {
+  // ground-truth bytes of the 26x26 window: every load of this thread (<= 4 pixels x 3 bytes)
+  // is issued before the first use, so their latencies overlap (the per-pixel load -> convert
+  // -> store chain was the kernel's top stall)
+  constexpr int kGI = (kS * kS + kThreads - 1) / kThreads;
+  uint8_t gb[kGI][3];
+#pragma unroll
+  for (int u = 0; u < kGI; u++) {
+    const int t = tid + u * kThreads;
     const int i = t / kS, j = t % kS;
     const int gy = ty * 16 - 5 + i, gx = tx * 16 - 5 + j;
-    float y[3] = {0.f, 0.f, 0.f};
-    if (gx >= 0 && gx < geo.W && gy >= 0 && gy < geo.H) {
-      const uint8_t* g = gt + ((v * geo.H + gy) * (int64_t)geo.W + gx) * 3;
+    const bool ok = t < kS * kS && gx >= 0 && gx < geo.W && gy >= 0 && gy < geo.H;
+    const uint8_t* g = gt + ((v * geo.H + gy) * (int64_t)geo.W + gx) * 3;
 #pragma unroll
-      for (int c = 0; c < 3; c++) y[c] = (float)g[c] * (1.0f / 255.0f);
+    for (int c = 0; c < 3; c++) gb[u][c] = ok ? __ldg(g + c) : (uint8_t)0;
+  }
+  stage_planes(s_src, 3, 0, &X[0][0][0]);
+#pragma unroll
+  for (int u = 0; u < kGI; u++) {
+    const int t = tid + u * kThreads;
+    if (t < kS * kS) {
+      const int i = t / kS, j = t % kS;
+#pragma unroll
+      for (int c = 0; c < 3; c++) Y[c][i][j] = (float)gb[u][c] * (1.0f / 255.0f);
     }
-#pragma unroll
-    for (int c = 0; c < 3; c++) Y[c][i][j] = y[c];
   }
   __syncthreads();
   // horizontal: item = (channel, row r, 4 output columns 4s..4s+3 <- staged cols 4s..4s+13)
@@ -261,6 +273,21 @@ __global__ void __launch_bounds__(kThreads) k_ssim_grad(
   const int64_t lb = blockIdx.x, beta = B_lo + lb;
   const int64_t v = beta / geo.per_view, loc = beta % geo.per_view;
   const int tx = (int)(loc % geo.Wt), ty = (int)(loc / geo.Wt);
+  // x and y of this thread's 4 output pixels of the vertical pass (item = tid: exactly 192
+  // items), loaded before the staging so their latency hides behind it
+  static_assert(3 * 16 * 4 == kThreads, "one vertical item per thread");
+  float xs[4], ys[4];
+  {
+    const int c = tid / 64, s4 = (tid / 16) % 4, j = tid % 16;
+#pragma unroll
+    for (int o = 0; o < 4; o++) {
+      const int row = 4 * s4 + o, p = row * 16 + j;
+      const int gy = ty * 16 + row, gx = tx * 16 + j;
+      const bool in = gx < geo.W && gy < geo.H;
+      xs[o] = in ? __ldg(out_rgb + lb * 768 + c * 256 + p) : 0.f;
+      ys[o] = in ? (float)__ldg(gt + ((v * geo.H + gy) * (int64_t)geo.W + gx) * 3 + c) * (1.0f / 255.0f) : 0.f;
+    }
+  }
   neighbour_sources(maps, halo, halo_ids, n_halo, geo, B_lo, B_hi, v, tx, ty, 2304, s_src);
   __syncthreads();
   stage_planes(s_src, 9, 0, &M[0][0][0]);  // maps are zero outside the image
@@ -311,8 +338,7 @@ __global__ void __launch_bounds__(kThreads) k_ssim_grad(
       const int gy = ty * 16 + row, gx = tx * 16 + j;
       float d = 0.f;
       if (gx < geo.W && gy < geo.H) {
-        const float x = out_rgb[lb * 768 + c * 256 + p];
-        const float y = (float)gt[((v * geo.H + gy) * (int64_t)geo.W + gx) * 3 + c] * (1.0f / 255.0f);
+        const float x = xs[o], y = ys[o];  // it == tid (one item per thread)
         const float gs = w3[o][0] + 2.f * x * w3[o][1] + y * w3[o][2];
         const float e = x - y;
         d = ((1.f - h.lambda) * (e > 0.f ? 1.f : (e < 0.f ? -1.f : 0.f)) - h.lambda * gs) * h.norm;
