@@ -141,7 +141,7 @@ __device__ __forceinline__ int stage_records(const gs_rec* __restrict__ rec, con
 // centres of *its* 8x16 half of the block [hx0, hx0 + 7] x [hy0, hy0 + 15], compacted by
 // ballot into its private slots and padded to a multiple of `pad`.  No CTA barrier; the caller
 // must have __syncwarp'ed since its last read of the slots.
-template <int KW>
+template <int KW, int ST = 1>
 __device__ __forceinline__ int stage_warp(const gs_rec* __restrict__ rec, const uint32_t* __restrict__ sidx, int cnt,
                                           int pos0, float4* s_a, float4* s_b, float4* s_c, float hx0, float hy0,
                                           bool cull, int pad) {
@@ -175,18 +175,18 @@ __device__ __forceinline__ int stage_warp(const gs_rec* __restrict__ rec, const 
       const int off = base + __popc(bal[i] & lt);
       const float4* p = reinterpret_cast<const float4*>(rec + jr[i]);
       const float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
-      s_a[off] = make_float4(a.x, a.y, b.x * kLScale, b.y * kLScale);
-      s_b[off] = make_float4(b.z * kLScale, b.w, c.x, c.y);
-      s_c[off] = make_float4(c.z, b.w > 0.f ? __log2f(255.0f * b.w) : -1.0f, __int_as_float(pos0 + lane + 32 * i),
+      s_a[ST * off] = make_float4(a.x, a.y, b.x * kLScale, b.y * kLScale);
+      s_b[ST * off] = make_float4(b.z * kLScale, b.w, c.x, c.y);
+      s_c[ST * off] = make_float4(c.z, b.w > 0.f ? __log2f(255.0f * b.w) : -1.0f, __int_as_float(pos0 + lane + 32 * i),
                              __uint_as_float(jr[i]));
     }
     base += __popc(bal[i]);
   }
   const int padded = (base + pad - 1) / pad * pad;
   for (int t = base + lane; t < padded; t += 32) {
-    s_a[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    s_b[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    s_c[t] = make_float4(0.f, -1.0f, 0.f, 0.f);
+    s_a[ST * t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    s_b[ST * t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    s_c[ST * t] = make_float4(0.f, -1.0f, 0.f, 0.f);
   }
   __syncwarp();
   return base;
@@ -464,7 +464,7 @@ __device__ __forceinline__ void bwd_comp_strip(float raw, float G, const float4&
   gc2 = fmaf(wgt, g2, gc2);
   // the behind-colour S enters only through (c - S) . dL/dC, so the pixel keeps P = S . dL/dC
   // (S <- S + alpha (c - S)  =>  P <- P + alpha (c . dL/dC - P)): one scalar instead of S
-  const float dot = fmaf(cb, g2, fmaf(Bq.w, g01.y, Bq.z * g01.x)) - P;  // (c - S) . dL/dC
+  const float dot = fmaf(cb, g2, fmaf(Bq.w, g01.y, fmaf(Bq.z, g01.x, -P)));  // (c - S) . dL/dC
   // kBg = false: black background (bg = 0), the T_final term vanishes (not left to the
   // compiler: x * 0 does not fold in IEEE arithmetic)
   const float dA = kBg ? T * dot - Tf * rom * bgdot : T * dot;
@@ -558,11 +558,13 @@ __device__ __forceinline__ float* gdst_row(const gs_gdst& g, uint32_t j) {
   while (s + 1 < g.nseg && (long long)j >= g.seg[s + 1]) s++;
   return g.base[s] + (int64_t)j * 9;
 }
-__device__ __forceinline__ void flush_rows(const float* __restrict__ rows, const uint32_t* __restrict__ rid, int nslot,
+__device__ __forceinline__ void flush_rows(const float* __restrict__ rows, uint32_t ridreg, int nslot,
                                            const gs_gdst& dst, int lane) {
+  // lane s of ridreg holds the record of buffered entry s
   constexpr int NP = 9 * kF, R = NP - 32, LPP = 32 / R;
   static_assert(R > 0 && 32 % R == 0 && LPP <= 8 && 8 % LPP == 0, "flush layout");
   const int np = 9 * nslot;
+  const uint32_t rid0 = __shfl_sync(0xffffffffu, ridreg, lane / 9);
   if (lane < np) {
     const float4* r = reinterpret_cast<const float4*>(rows + lane * 32);
     float4 a = r[lane & 7];
@@ -574,7 +576,7 @@ __device__ __forceinline__ void flush_rows(const float* __restrict__ rows, const
       a = make_float4(lo.x, lo.y, hi.x, hi.y);
     }
     const float z = (a.x + a.y) + (a.z + a.w);
-    if (z != 0.f) atomicAdd(gdst_row(dst, rid[lane / 9]) + lane % 9, z);
+    if (z != 0.f) atomicAdd(gdst_row(dst, rid0) + lane % 9, z);
   }
   {
     const int p = 32 + lane / LPP, part = lane % LPP;
@@ -589,7 +591,8 @@ __device__ __forceinline__ void flush_rows(const float* __restrict__ rows, const
     }
 #pragma unroll
     for (int o = LPP / 2; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-    if (part == 0 && p < np && z != 0.f) atomicAdd(gdst_row(dst, rid[p / 9]) + p % 9, z);
+    const uint32_t rid1 = __shfl_sync(0xffffffffu, ridreg, min(p, np - 1) / 9);
+    if (part == 0 && p < np && z != 0.f) atomicAdd(gdst_row(dst, rid1) + p % 9, z);
   }
 }
 
@@ -607,15 +610,19 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   constexpr int kBW = MINB >= 14 ? 32 : 64;  // kWarp: records staged per warp round (smem for 14 CTAs/SM)
   static_assert(!kWarp || PPT == 4, "warp-independent render needs PPT = 4 (one 8x16 half per warp)");
   constexpr bool kDirect = kOneWarp || kWarp;  // warp sums go straight to global memory
-  __shared__ float4 s_a[kWarp ? 2 * kBW : kBB], s_b[kWarp ? 2 * kBW : kBB], s_c[kWarp ? 2 * kBW : kBB];
+  __shared__ float4 s_a[kWarp ? 1 : kBB], s_b[kWarp ? 1 : kBB], s_c[kWarp ? 1 : kBB];
+  // kWarp: the staged entries as (A, Bq, cq) triples, so one pointer walks them (the three
+  // planes' base addresses were rematerialised per entry under the register cap)
+  __shared__ float4 s_e[kWarp ? 3 * 2 * kBW : 1];
   __shared__ int s_wc[kBB / 32];
   // per-warp gradient slots: each (warp, entry, value) is written by exactly one lane, so no
   // shared-memory atomics (a float atomicAdd on shared memory is a CAS loop on sm_100)
   __shared__ float s_g[kDirect ? 1 : kNW * kBB * 9];
   // kWarp: per-warp buffered reduction rows (flush_rows) and the buffered entries' records
   __shared__ __align__(16) float s_rows[kWarp ? 2 * kF * 9 * 32 : 4];
-  __shared__ uint32_t s_rid[kWarp ? 2 * kF : 1];
   int nslot = 0;  // kWarp: buffered entries (warp-uniform)
+  uint32_t ridreg = 0;  // kWarp: lane s holds the record of buffered entry s
+  float* rowp = s_rows + (threadIdx.x >> 5) * kF * 9 * 32 + (threadIdx.x & 31);  // kWarp: this lane's next row slot
   __shared__ int s_max[NT / 32];
   __shared__ long long s_red[NT / 32];
   const long long t0 = clock64();
@@ -669,6 +676,9 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   const int ridx = rvalid ? ridx_s : 0;
   const int beg = range[lb];
   int ebc = 0;
+  float acc[3] = {0.f, 0.f, 0.f};  // per-entry strip moments and colour gradients
+  float2 gc01 = make_float2(0.f, 0.f);
+  float gc2 = 0.f;
   constexpr int kStep = kWarp ? kBW : kBB;
   const int wofs = kWarp ? wid * kBW : 0;  // this warp's slots (kWarp)
   for (int bi = (maxn + kStep - 1) / kStep - 1; bi >= 0; bi--) {
@@ -677,8 +687,8 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
     int kept;
     if constexpr (kWarp) {
       __syncwarp();
-      kept = stage_warp<kBW>(rec, sorted_idx + beg + p0, cnt, p0, s_a + wofs, s_b + wofs, s_c + wofs,
-                             (float)(tx * 16 + 8 * wid), (float)(ty * 16), cull != 0, 1);
+      kept = stage_warp<kBW, 3>(rec, sorted_idx + beg + p0, cnt, p0, s_e + 3 * wofs, s_e + 3 * wofs + 1,
+                                s_e + 3 * wofs + 2, (float)(tx * 16 + 8 * wid), (float)(ty * 16), cull != 0, 1);
     } else {
       __syncthreads();
       kept = stage_records<NT, kBB>(rec, sorted_idx + beg + p0, cnt, p0, s_a, s_b, s_c, s_wc,
@@ -687,11 +697,12 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
         for (int t = tid; t < kNW * kBB * 9; t += NT) s_g[t] = 0.f;
       __syncthreads();
     }
-    for (int k = kept - 1; k >= 0; k--) {
-      const float4 cq = s_c[wofs + k];
+    const float4* ep = s_e + 3 * (wofs + kept - 1);  // kWarp: entry k's triple
+    for (int k = kept - 1; k >= 0; k--, ep -= 3) {
+      const float4 cq = kWarp ? ep[2] : s_c[k];
       const int pos = __float_as_int(cq.z);
       if (!kWarp && pos >= wmax) continue;  // warp-uniform (kWarp stages only positions < wmax)
-      const float4 A = s_a[wofs + k], Bq = s_b[wofs + k];
+      const float4 A = kWarp ? ep[0] : s_a[k], Bq = kWarp ? ep[1] : s_b[k];
       gs_strip<PPT> e;
       q_strip<PPT>(A, Bq, fpx, fpy0, e);
       bool cj[PPT], any = false;
@@ -701,9 +712,8 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
         any = any || cj[j];
       }
       // lanes without a contributing pixel keep zero moments, so their strip_grads are zeros
-      float acc[3] = {0.f, 0.f, 0.f};
-      float2 gc01 = make_float2(0.f, 0.f);
-      float gc2 = 0.f;
+      // (the accumulators live across entries and are re-zeroed after each warp sum: no
+      // per-entry zero moves)
       if (any) {
 #pragma unroll
         for (int j = 0; j < PPT; j++)
@@ -732,16 +742,20 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
         gr[6] = gc01.x;
         gr[7] = gc01.y;
         gr[8] = gc2;
+        acc[0] = acc[1] = acc[2] = 0.f;
+        gc01 = make_float2(0.f, 0.f);
+        gc2 = 0.f;
         if constexpr (kWarp) {
-          float* row = s_rows + (wid * kF + nslot) * 9 * 32 + lane;
 #pragma unroll
-          for (int q = 0; q < 9; q++) row[q * 32] = gr[q];
-          if (lane == 0) s_rid[wid * kF + nslot] = __float_as_uint(cq.w);
+          for (int q = 0; q < 9; q++) rowp[q * 32] = gr[q];
+          rowp += 9 * 32;
+          if (lane == nslot) ridreg = __float_as_uint(cq.w);
           if (++nslot == kF) {
             __syncwarp();
-            flush_rows(s_rows + wid * kF * 9 * 32, s_rid + wid * kF, kF, gdst, lane);
+            flush_rows(s_rows + wid * kF * 9 * 32, ridreg, kF, gdst, lane);
             __syncwarp();
             nslot = 0;
+            rowp -= kF * 9 * 32;
           }
         } else {
           const float z = warp_reduce9(gr, lane);
@@ -772,7 +786,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   if constexpr (kWarp) {
     if (nslot > 0) {
       __syncwarp();
-      flush_rows(s_rows + wid * kF * 9 * 32, s_rid + wid * kF, nslot, gdst, lane);
+      flush_rows(s_rows + wid * kF * 9 * 32, ridreg, nslot, gdst, lane);
     }
   }
   if (kStats) {
