@@ -47,7 +47,7 @@ def _nvcc():
 
 
 def build(force: bool = False, ptxas_v: bool = False, verbose: bool = False, csrc: str = CSRC,
-          out: str = OUT) -> str:
+          out: str = OUT, extra=()) -> str:
     """Compile csrc/*.cu into out.  (csrc/out other than the defaults: A/B builds of another
     revision, loaded by _lib when GS_LIB_VARIANT names them.)"""
     srcs = sorted(glob.glob(os.path.join(csrc, "*.cu")))
@@ -59,7 +59,7 @@ def build(force: bool = False, ptxas_v: bool = False, verbose: bool = False, csr
     os.makedirs(build_dir, exist_ok=True)
     inc, lib = _nccl_dirs()
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-                    "-I" + os.path.join(ROOT, "include")]
+                    "-I" + os.path.join(ROOT, "include")] + list(extra)  # extra: A/B defines
     if inc:
         flags += ["-DGS_WITH_NCCL", "-I" + inc]
     if ptxas_v:

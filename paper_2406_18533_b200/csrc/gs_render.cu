@@ -22,6 +22,7 @@
 // gradients, then reduces the 9 values across the warp with a transpose (recursive-halving)
 // reduction (12 shuffles, only when some lane contributes) into per-warp shared-memory slots.
 #include <cstdlib>
+#include <type_traits>
 
 #include "gs_device.cuh"
 #include "gs_internal.h"
@@ -268,6 +269,9 @@ __device__ __forceinline__ void q_strip(const float4& A, const float4& Bq, float
   }
 }
 
+// kCap = false: the entry's opacity is at most kCapFree, so raw = o G <= o (G <= 1) never
+// reaches the cap and the clamp and its zero-gradient select are skipped (identical results).
+constexpr float kCapFree = 0.98f;
 // Composite one staged entry into one pixel (O12) given its capped alpha >= 1/255.  A pixel
 // that stops gets the +inf penalty (pen) and counts towards ndone; kTrack keeps its stop
 // position (evaluation counts: statistics and the WORK cost mode).
@@ -452,11 +456,11 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // w = w_0 - D l22, dy = dy_0 - D), so per pixel only the moments
 // acc = (sum gG, sum D gG, sum D^2 gG) are accumulated (gG = G dA, zero through the cap, R6);
 // strip_grads turns them into the 6 gradients once per entry.  (O14; R6: zero gradient through the 0.99 cap.)
-template <int D, bool kBg = true>
+template <int D, bool kBg = true, bool kCap = true>
 __device__ __forceinline__ void bwd_comp_strip(float raw, float G, const float4& Bq, float cb, float& T, float& P,
                                                float2 g01, float g2, float Tf, float bgdot, float acc[3],
                                                float2& gc01, float& gc2) {
-  const float alpha = fminf(kAlphaCap, raw);
+  const float alpha = kCap ? fminf(kAlphaCap, raw) : raw;
   const float rom = rcp_approx(1.0f - alpha);
   T *= rom;  // transmittance in front of this entry
   const float wgt = alpha * T;
@@ -469,7 +473,7 @@ __device__ __forceinline__ void bwd_comp_strip(float raw, float G, const float4&
   // compiler: x * 0 does not fold in IEEE arithmetic)
   const float dA = kBg ? T * dot - Tf * rom * bgdot : T * dot;
   P = fmaf(alpha, dot, P);
-  const float gG = raw <= kAlphaCap ? G * dA : 0.f;
+  const float gG = (!kCap || raw <= kAlphaCap) ? G * dA : 0.f;
   acc[0] += gG;
   if (D == 1) acc[1] += gG, acc[2] += gG;
   if (D >= 2) acc[1] = fmaf((float)D, gG, acc[1]), acc[2] = fmaf((float)(D * D), gG, acc[2]);
@@ -542,7 +546,10 @@ __device__ __forceinline__ int red_index(int lane, bool& valid) {
 // 0..31, the 9 kF - 32 remaining rows are split over 32 / (9 kF - 32) lanes each and finished
 // by shuffles.  ~9 stores + 10 instructions per entry instead of the 12-shuffle transpose
 // reduction with its selects (~47).
-constexpr int kF = 4;  // entries per flush (36 rows: 32 + 4 x 8 lanes)
+#ifndef GS_BWD_KF
+#define GS_BWD_KF 4
+#endif
+constexpr int kF = GS_BWD_KF;  // entries per flush (4: 36 rows = 32 + 4 x 8 lanes; 3: 27 rows, one lane each)
 
 // Where the gradient of received record j goes: row base[s] + 9 j for the source s with
 // seg[s] <= j < seg[s+1].  Own buffer: nseg = 1, base[0] = dL/d(record).  NEXT-3
@@ -554,23 +561,31 @@ struct gs_gdst {
   int nseg;
 };
 __device__ __forceinline__ float* gdst_row(const gs_gdst& g, uint32_t j) {
+  if (g.nseg == 1) return g.base[0] + (int64_t)j * 9;  // own buffer (uniform branch)
   int s = 0;
   while (s + 1 < g.nseg && (long long)j >= g.seg[s + 1]) s++;
   return g.base[s] + (int64_t)j * 9;
 }
-__device__ __forceinline__ void flush_rows(const float* __restrict__ rows, uint32_t ridreg, int nslot,
+__device__ __forceinline__ void flush_rows(const float* __restrict__ rows_all, int wbytes, uint32_t ridreg, int nslot,
                                            const gs_gdst& dst, int lane) {
+  // rows_all: the CTA's row buffer (128-byte aligned); wbytes: this warp's byte offset (a
+  // multiple of 128, so it commutes with the chunk XOR below)
+  const float* rows = rows_all + wbytes / 4;
   // lane s of ridreg holds the record of buffered entry s
-  constexpr int NP = 9 * kF, R = NP - 32, LPP = 32 / R;
-  static_assert(R > 0 && 32 % R == 0 && LPP <= 8 && 8 % LPP == 0, "flush layout");
+  constexpr int NP = 9 * kF, R = NP > 32 ? NP - 32 : 1, LPP = 32 / R;
+  static_assert(NP <= 32 || (32 % R == 0 && LPP <= 8 && 8 % LPP == 0), "flush layout");
+  static_assert((kF * 9 * 32 * 4) % 128 == 0, "warp row buffers 128-byte aligned");
   const int np = 9 * nslot;
   const uint32_t rid0 = __shfl_sync(0xffffffffu, ridreg, lane / 9);
   if (lane < np) {
-    const float4* r = reinterpret_cast<const float4*>(rows + lane * 32);
-    float4 a = r[lane & 7];
+    // chunk c of row `lane` read at chunk (c ^ lane) & 7: the 8 lanes of a phase hit 8
+    // different bank groups (conflict-free), one LOP3 per chunk (rows 128-byte aligned)
+    const char* rb = reinterpret_cast<const char*>(rows_all);
+    const int ob = wbytes + (lane * 8 + (lane & 7)) * 16;
+    float4 a = *reinterpret_cast<const float4*>(rb + ob);
 #pragma unroll
     for (int c = 1; c < 8; c++) {
-      const float4 x = r[(c + lane) & 7];
+      const float4 x = *reinterpret_cast<const float4*>(rb + (ob ^ (c * 16)));
       const float2 lo = __fadd2_rn(make_float2(a.x, a.y), make_float2(x.x, x.y));
       const float2 hi = __fadd2_rn(make_float2(a.z, a.w), make_float2(x.z, x.w));
       a = make_float4(lo.x, lo.y, hi.x, hi.y);
@@ -578,7 +593,7 @@ __device__ __forceinline__ void flush_rows(const float* __restrict__ rows, uint3
     const float z = (a.x + a.y) + (a.z + a.w);
     if (z != 0.f) atomicAdd(gdst_row(dst, rid0) + lane % 9, z);
   }
-  {
+  if constexpr (NP > 32) {  // rows 32.. : LPP lanes per row
     const int p = 32 + lane / LPP, part = lane % LPP;
     float z = 0.f;
     if (p < np) {
@@ -619,7 +634,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   // shared-memory atomics (a float atomicAdd on shared memory is a CAS loop on sm_100)
   __shared__ float s_g[kDirect ? 1 : kNW * kBB * 9];
   // kWarp: per-warp buffered reduction rows (flush_rows) and the buffered entries' records
-  __shared__ __align__(16) float s_rows[kWarp ? 2 * kF * 9 * 32 : 4];
+  __shared__ __align__(128) float s_rows[kWarp ? 2 * kF * 9 * 32 : 4];
   int nslot = 0;  // kWarp: buffered entries (warp-uniform)
   uint32_t ridreg = 0;  // kWarp: lane s holds the record of buffered entry s
   float* rowp = s_rows + (threadIdx.x >> 5) * kF * 9 * 32 + (threadIdx.x & 31);  // kWarp: this lane's next row slot
@@ -715,22 +730,30 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
       // (the accumulators live across entries and are re-zeroed after each warp sum: no
       // per-entry zero moves)
       if (any) {
+        // warp-uniform: entries with o <= kCapFree skip the alpha clamp (bwd_comp_strip)
+        auto pixels = [&](auto capc) {
+          constexpr bool kCap = decltype(capc)::value;
 #pragma unroll
-        for (int j = 0; j < PPT; j++)
-          if (cj[j]) {
-            const float G = ex2_approx(-e.q[j]);
-            const float raw = __fmul_rn(Bq.y, G);
-            switch (j) {
-              case 0: bwd_comp_strip<0 * RS, kBg>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 1: bwd_comp_strip<1 * RS, kBg>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 2: bwd_comp_strip<2 * RS, kBg>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 3: bwd_comp_strip<3 * RS, kBg>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 4: bwd_comp_strip<4 * RS, kBg>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 5: bwd_comp_strip<5 * RS, kBg>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              case 6: bwd_comp_strip<6 * RS, kBg>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
-              default: bwd_comp_strip<7 * RS, kBg>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+          for (int j = 0; j < PPT; j++)
+            if (cj[j]) {
+              const float G = ex2_approx(-e.q[j]);
+              const float raw = __fmul_rn(Bq.y, G);
+              switch (j) {
+                case 0: bwd_comp_strip<0 * RS, kBg, kCap>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+                case 1: bwd_comp_strip<1 * RS, kBg, kCap>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+                case 2: bwd_comp_strip<2 * RS, kBg, kCap>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+                case 3: bwd_comp_strip<3 * RS, kBg, kCap>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+                case 4: bwd_comp_strip<4 * RS, kBg, kCap>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+                case 5: bwd_comp_strip<5 * RS, kBg, kCap>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+                case 6: bwd_comp_strip<6 * RS, kBg, kCap>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+                default: bwd_comp_strip<7 * RS, kBg, kCap>(raw, G, Bq, cq.x, T[j], P[j], g01[j], g2[j], Tf[j], bgd[j], acc, gc01, gc2); break;
+              }
             }
-          }
+        };
+        if (Bq.y > kCapFree)
+          pixels(std::true_type{});
+        else
+          pixels(std::false_type{});
         if (kStats) {
 #pragma unroll
           for (int j = 0; j < PPT; j++) ebc += cj[j];
@@ -752,7 +775,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
           if (lane == nslot) ridreg = __float_as_uint(cq.w);
           if (++nslot == kF) {
             __syncwarp();
-            flush_rows(s_rows + wid * kF * 9 * 32, ridreg, kF, gdst, lane);
+            flush_rows(s_rows, wid * kF * 9 * 32 * 4, ridreg, kF, gdst, lane);
             __syncwarp();
             nslot = 0;
             rowp -= kF * 9 * 32;
@@ -786,7 +809,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   if constexpr (kWarp) {
     if (nslot > 0) {
       __syncwarp();
-      flush_rows(s_rows + wid * kF * 9 * 32, ridreg, nslot, gdst, lane);
+      flush_rows(s_rows, wid * kF * 9 * 32 * 4, ridreg, nslot, gdst, lane);
     }
   }
   if (kStats) {
