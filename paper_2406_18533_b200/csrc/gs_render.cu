@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
   }
 }
 
-// 1 / x for x in [0.01, 1] (1 - alpha): one MUFU.RCP, no range fix-up.
+// 1 / x for x in [0.01, 1] (1 - alpha, an opacity): one MUFU.RCP, no range fix-up.
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -454,8 +454,9 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // Strip form of bwd_comp for the thread's pixel D rows below its first.  The six geometric
 // gradients are linear in q = o G dA with coefficients polynomial in D (u = u_0 - D l21,
 // w = w_0 - D l22, dy = dy_0 - D), so per pixel only the moments
-// acc = (sum gG, sum D gG, sum D^2 gG) are accumulated (gG = G dA, zero through the cap, R6);
-// strip_grads turns them into the 6 gradients once per entry.  (O14; R6: zero gradient through the 0.99 cap.)
+// acc = (sum q, sum D q, sum D^2 q) are accumulated (q = o G dA = alpha dA, zero through the
+// cap, R6; with a black background q = wgt . dot, one product); strip_grads turns them into
+// the 6 gradients once per entry.  (O14; R6: zero gradient through the 0.99 cap.)
 template <int D, bool kBg = true, bool kCap = true>
 __device__ __forceinline__ void bwd_comp_strip(float raw, float G, const float4& Bq, float cb, float& T, float& P,
                                                float2 g01, float g2, float Tf, float bgdot, float acc[3],
@@ -471,23 +472,26 @@ __device__ __forceinline__ void bwd_comp_strip(float raw, float G, const float4&
   const float dot = fmaf(cb, g2, fmaf(Bq.w, g01.y, fmaf(Bq.z, g01.x, -P)));  // (c - S) . dL/dC
   // kBg = false: black background (bg = 0), the T_final term vanishes (not left to the
   // compiler: x * 0 does not fold in IEEE arithmetic)
-  const float dA = kBg ? T * dot - Tf * rom * bgdot : T * dot;
+  // q = alpha dA, dA = T dot (- T_final rom bgdot): alpha T dot = wgt dot
+  const float qa = kBg ? alpha * (T * dot - Tf * rom * bgdot) : wgt * dot;
   P = fmaf(alpha, dot, P);
-  const float gG = (!kCap || raw <= kAlphaCap) ? G * dA : 0.f;
+  const float gG = (!kCap || raw <= kAlphaCap) ? qa : 0.f;
+  (void)G;
   acc[0] += gG;
   if (D == 1) acc[1] += gG, acc[2] += gG;
   if (D >= 2) acc[1] = fmaf((float)D, gG, acc[1]), acc[2] = fmaf((float)(D * D), gG, acc[2]);
 }
 
-// gr[0..5] of one entry from the strip moments (q = o gG; 2 ln 2 = 1 / kLScale^2):
+// gr[0..5] of one entry from the strip moments of q = o G dA (2 ln 2 = 1 / kLScale^2):
 //   dL/dl11' = -2ln2 l11 sum q_j u_j,  dL/dl21' = -2ln2 sum q_j (l21 u_j + l22 w_j),
-//   dL/dconic-like (gr2..4) = -1/2 sum q dx^2, -sum q dx dy_j, -1/2 sum q dy_j^2, dL/do = sum gG.
+//   dL/dconic-like (gr2..4) = -1/2 sum q dx^2, -sum q dx dy_j, -1/2 sum q dy_j^2,
+//   dL/do = sum G dA = sum q / o (o > 1/255 for any entry that composites).
 __device__ __forceinline__ void strip_grads(const float4& A, const float4& Bq, float dx, float dy0, float u0,
                                             float w0, const float acc[3], float gr[9]) {
   const float l11 = A.z, l21 = A.w, l22 = Bq.x, o = Bq.y;
-  const float Q0 = o * acc[0], Q1 = o * acc[1], Q2 = o * acc[2];
+  const float Q0 = acc[0], Q1 = acc[1], Q2 = acc[2];
   const float k = -1.3862943611198906f;
-  gr[5] = acc[0];
+  gr[5] = Q0 * rcp_approx(o);
   gr[0] = k * l11 * fmaf(u0, Q0, -l21 * Q1);
   gr[1] = k * fmaf(fmaf(l21, u0, l22 * w0), Q0, -fmaf(l21, l21, l22 * l22) * Q1);
   gr[2] = -0.5f * dx * dx * Q0;
@@ -547,7 +551,7 @@ __device__ __forceinline__ int red_index(int lane, bool& valid) {
 // by shuffles.  ~9 stores + 10 instructions per entry instead of the 12-shuffle transpose
 // reduction with its selects (~47).
 #ifndef GS_BWD_KF
-#define GS_BWD_KF 4
+#define GS_BWD_KF 3
 #endif
 constexpr int kF = GS_BWD_KF;  // entries per flush (4: 36 rows = 32 + 4 x 8 lanes; 3: 27 rows, one lane each)
 
