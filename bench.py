@@ -307,8 +307,10 @@ def main():
 
     def one_step(events=None, stats=False):
         k = k_sched[0]
-        idx = torch.tensor(sched[k], device=dev)
-        torch.index_select(gt_pool, 0, idx, out=gt_batch)
+        # the batch's ground truth: one contiguous device-to-device copy per view (cudaMemcpyAsync;
+        # torch.index_select's gather kernel took ~1.8 ms for the 0.76 GB of a C2 batch)
+        for i, j in enumerate(sched[k]):
+            gt_batch[i].copy_(gt_pool[j])
         loss = tr.step(batch_cams(k), gt_batch, next_cams=batch_cams(k + 1), events=events, collect_stats=stats)
         k_sched[0] += 1
         return loss
