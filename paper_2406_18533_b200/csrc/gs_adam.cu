@@ -413,7 +413,7 @@ extern "C" gs_status gs_adam_step(gs_ctx* c, gs_params* p, gs_params* m, gs_para
     static int sminb = -1;
     if (sminb < 0) {
       const char* e = getenv("GS_ADAM_SPLIT_MINB");
-      sminb = e ? atoi(e) : 4;  // 4: 126 registers, C2 6.7 -> 5.0 ms (1: 188 registers, 8 warps/SM)
+      sminb = e ? atoi(e) : 5;  // 5: C2 4.97 -> 4.83 ms vs 4 (126 registers; 1: 188 registers, 8 warps/SM: 6.7 ms)
     }
     if (sminb >= 6)
       k_bwd_adam<true, false, 6><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base,
