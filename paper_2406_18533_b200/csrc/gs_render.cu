@@ -269,9 +269,10 @@ __device__ __forceinline__ void q_strip(const float4& A, const float4& Bq, float
   }
 }
 
-// kCap = false: the entry's opacity is at most kCapFree, so raw = o G <= o (G <= 1) never
-// reaches the cap and the clamp and its zero-gradient select are skipped (identical results).
-constexpr float kCapFree = 0.98f;
+// kCap = false: the entry's opacity is at most kCapFree, so raw = o G <= o (G = ex2(-q) <= 1,
+// q >= 0) never reaches the cap and the clamp and its zero-gradient select are skipped
+// (identical results).  kCapFree sits 1e-4 below the cap: raw would need G > 1.0001.
+constexpr float kCapFree = 0.9899f;
 // Composite one staged entry into one pixel (O12) given its capped alpha >= 1/255.  A pixel
 // that stops gets the +inf penalty (pen) and counts towards ndone; kTrack keeps its stop
 // position (evaluation counts: statistics and the WORK cost mode).
