@@ -546,11 +546,11 @@ __device__ __forceinline__ int red_index(int lane, bool& valid) {
 // (no per-warp slots, no CTA barrier).
 // Buffered warp reduction (kWarp backward): the per-lane gradients of kF contributing
 // entries are stored as rows of 32 floats, row (slot, value) = the 32 lanes' values, then each
-// row is summed by one lane (8 float4 loads in lane-rotated chunk order: conflict-free; the
-// sum's order does not matter) and added to dL/d(record).  9 kF rows: lanes 0..31 take rows
-// 0..31, the 9 kF - 32 remaining rows are split over 32 / (9 kF - 32) lanes each and finished
-// by shuffles.  ~9 stores + 10 instructions per entry instead of the 12-shuffle transpose
-// reduction with its selects (~47).
+// row is summed by one lane (8 float4 loads at XOR-swizzled chunks: conflict-free; the sum's
+// order does not matter) and added to dL/d(record).  9 kF rows: with kF = 3 (default) lanes
+// 0..26 take one row each; with kF = 4 lanes 0..31 take rows 0..31 and the 4 remaining rows
+// are split over 8 lanes each and finished by shuffles.  ~9 stores + ~17 instructions per
+// entry instead of the 12-shuffle transpose reduction with its selects (~47).
 #ifndef GS_BWD_KF
 #define GS_BWD_KF 3
 #endif
