@@ -627,7 +627,11 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   constexpr bool kOneWarp = NT == 32;
   constexpr int kNW = NT / 32;   // warps per block
   constexpr int kBB = 128;        // records staged per round
-  constexpr int kBW = MINB >= 14 ? 32 : 64;  // kWarp: records staged per warp round (smem for 14 CTAs/SM)
+#ifndef GS_BWD_KBW16
+#define GS_BWD_KBW16 64
+#endif
+  // kWarp: records staged per warp round (64 fits 16 CTAs/SM with 3-entry flushes: 14.2 KB per CTA)
+  constexpr int kBW = MINB >= 18 ? 32 : (MINB >= 14 ? GS_BWD_KBW16 : 64);
   static_assert(!kWarp || PPT == 4, "warp-independent render needs PPT = 4 (one 8x16 half per warp)");
   constexpr bool kDirect = kOneWarp || kWarp;  // warp sums go straight to global memory
   __shared__ float4 s_a[kWarp ? 1 : kBB], s_b[kWarp ? 1 : kBB], s_c[kWarp ? 1 : kBB];
@@ -684,14 +688,16 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_bwd(
   }
   // this lane's gradient slot offset within an entry (value index, or -1), read back from
   // shared memory when the register cap evicts it (cheaper than recomputing red_index)
-  __shared__ int s_ridx[NT];
-  {
+  // (kWarp uses the buffered rows instead: no slot table, its shared memory goes to staging)
+  __shared__ int s_ridx[kWarp ? 1 : NT];
+  int ridx_s = -1;
+  if constexpr (!kWarp) {
     bool v;
     const int r = red_index(lane, v);
     s_ridx[tid] = v ? r : -1;
+    __syncwarp();
+    ridx_s = s_ridx[tid];
   }
-  __syncwarp();
-  const int ridx_s = s_ridx[tid];
   const bool rvalid = ridx_s >= 0;
   const int ridx = rvalid ? ridx_s : 0;
   const int beg = range[lb];
