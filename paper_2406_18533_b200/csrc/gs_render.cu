@@ -32,7 +32,10 @@ using namespace gsd;
 namespace {
 
 constexpr int kFB = 128;    // forward: records staged per round
-constexpr int kFW = 64;     // warp-independent forward: records staged per warp round
+#ifndef GS_FWD_KFW
+#define GS_FWD_KFW 64
+#endif
+constexpr int kFW = GS_FWD_KFW;  // warp-independent forward: records staged per warp round
 constexpr int kUnroll = 4;  // forward entries per unrolled group (batch padded to a multiple; 4 measured
                             // faster than 8 and 16 on C2)
 
