@@ -448,7 +448,8 @@ __global__ void __launch_bounds__(256 / PPT, MINB) k_render_fwd(
   }
 }
 
-// 1 / x for x in [0.01, 1] (1 - alpha, an opacity): one MUFU.RCP, no range fix-up.
+// 1 / x for x in [1/255, 1] (1 - alpha >= 0.01, or an opacity of a compositing entry): one
+// MUFU.RCP, no range fix-up (normal inputs only).
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
