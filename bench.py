@@ -173,7 +173,7 @@ def oracle_sample(scene, cam, gt_img, n_blocks=16, adam_frac=1.0 / 16, seed=0):
     b0, b1 = c, min(c + n_blocks, Wt * Ht)
     off, ent = oracle.tile_lists(recs, b0, b1, Wt, Ht)
     t1b = time.perf_counter()
-    f = oracle.render_fwd(recs, off, ent, b0, b1, W, H, (0, 0, 0), gt_img[None], 1, 1e-5)
+    f = oracle.render_fwd(recs, off, ent, b0, b1, W, H, (0, 0, 0), gt_img[None], 1)
     g = oracle.render_bwd(recs, off, ent, b0, b1, W, H, f["dl_dc"])
     t2 = time.perf_counter()
     touched = np.unique(ent)

@@ -48,7 +48,7 @@ def render(ctx, p, cams):
         cnt = L.project(ctx, p, cams, dp, None, 0, idx)
     except L.CapacityError as e:
         cnt = e.counts
-    send = torch.empty((max(int(cnt.sum()), 1), 48), dtype=torch.uint8, device=DEV)
+    send = torch.empty((max(int(cnt.sum()), 1), L.RECORD_BYTES), dtype=torch.uint8, device=DEV)
     cnt = L.project(ctx, p, cams, dp, send, send.shape[0], idx)
     n = int(cnt.sum())
     rng = torch.empty(b * Wt * Ht + 1, dtype=torch.int32, device=DEV)

@@ -89,10 +89,18 @@ enum { GS_COST_MEASURED = 0, GS_COST_WORK = 1, GS_COST_PAPER_AVG = 2 };
 enum { GS_ADAM_GRAD = 1, GS_ADAM_APPLY = 2, GS_ADAM_WRITE_GRAD = 4 };
 
 /* Size of one projected record (A1 output / A2 payload):
- *   float4 {mx, my, depth, radius(float)}      mean2d, depth = p_z (O3-O4, O7)
- *   float4 {l11, l21, l22, opacity}            Cholesky factor L of the conic, conic = L L^T (O6)
- *   float4 {r, g, b, meta(u32 = gid*32 + v)}   colour (O9)                                    */
-#define GS_RECORD_BYTES 48
+ *   float4 {mx, my, depth, radius(float)}       mean2d, depth = p_z (O3-O4, O7)
+ *   float4 {l11', l21', l22', opacity}          conic = L L^T (O6) as the prescaled Cholesky
+ *                                               factor L' = L sqrt(0.5 log2 e), rounded to
+ *                                               nearest from fp64 (hi part); opacity (O1)
+ *   float4 {r, g, b, qmax}                      colour (O9); qmax = log2(255 opacity), so
+ *                                               alpha >= 1/255 <=> q = |L'^T d|^2 <= qmax
+ *   float4 {l11', l21', l22' (lo), meta}        L' - hi, rounded to nearest (double-float
+ *                                               factor: hi + lo carries ~48 bits);
+ *                                               meta = u32 gid * 32 + v
+ * (R16: the renderer evaluates u = l11' dx + l21' dy and w = l22' dy in fp64 from hi + lo at
+ * a reference point within (3.5, 7.5) px of each pixel, and in fp32 from hi for the offset.) */
+#define GS_RECORD_BYTES 64
 /* dL/d(record) as exchanged back (A6): 9 floats (mx, my, A, B, C, opacity, r, g, b) where
  * (A, B, C) is the conic [[A, B], [B, C]] and B is the scalar off-diagonal (R: #16).     */
 #define GS_GRAD_FLOATS 9
@@ -432,7 +440,7 @@ gs_status gs_project_put(gs_ctx* ctx, const gs_params* p, const gs_camera* cams_
 /* gs_render_bwd_put -- gs_render_bwd on this rank's receive buffer with the reverse exchange
  * fused: record j from source s adds its gradient to s's dL/dsend row owner_off[s] +
  * (j - recv_seg[s]) (float reductions over NVLink).  Same other arguments as gs_render_bwd
- * (black background and the default warp-independent kernel only: GS_ENOTSUP otherwise).
+ * (black background: no bg argument).
  * Owners may read dL/dsend only after gs_p2p_barrier.                                      */
 gs_status gs_render_bwd_put(gs_ctx* ctx, const void* recv_rec, int64_t n_recv, const uint32_t* sorted_idx,
                             const int32_t* tile_range, const gs_camera* cams_h, int n_views, const int64_t* dp_h,
@@ -448,6 +456,13 @@ gs_status gs_p2p_barrier(gs_ctx* ctx, void* stream);
 /* gs_p2p_status -- GS_ECUDA if a barrier of this context timed out since the last call (and
  * clears it), else GS_OK.  Host sync on `stream`.                                         */
 gs_status gs_p2p_status(gs_ctx* ctx, void* stream);
+
+/* --------------------------------------------------------------------------- self-check */
+/* gs_selftest_ex2 -- the maximum relative error of the renderer's exp2 (ex2.approx.ftz.f32,
+ * the alpha = o 2^-q of A4/A5) over every fp32 x in [lo, hi], hi <= 0, against fp64 exp2,
+ * into *max_rel_err_h (host sync).  It pins the constant part of the error model the
+ * oracle's transmittance margins use (R16).                                               */
+gs_status gs_selftest_ex2(gs_ctx* ctx, float lo, float hi, double* max_rel_err_h, void* stream);
 
 #ifdef __cplusplus
 }

@@ -23,7 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "gs_oracle.c")
 
-FLAG_ALPHA, FLAG_T, FLAG_POWER, FLAG_L1 = 1, 2, 4, 8
+FLAG_ALPHA, FLAG_T, FLAG_POWER, FLAG_OVERFLOW = 1, 2, 4, 16
 
 
 def build(force: bool = False) -> str:
@@ -177,42 +177,58 @@ def tile_lists(recs: Records, b0, b1, Wt, Ht):
     return off, ent[: int(off[-1])]
 
 
-def render_fwd(recs, off, ent, b0, b1, W, H, bg=(0, 0, 0), gt=None, b_total=1, flag_eps=1e-5, t_eps=1e-3,
-               cond_eps=4e-7):
+# Decision margins (alpha_eps, t_eps, cond_eps, alpha_abs) of O12's two threshold decisions
+# (gs_oracle.c orc_margins_t, DESIGN.md §2 R16): the first-order bound of the renderer's fp32
+# exponent with cond_eps = u_r = 2^-24 per operation; alpha_eps = 1e-6 (the fp32 opacity),
+# t_eps = 1e-6, alpha_abs = 1e-6 (ex2.approx: 1.44e-7 measured by gs_selftest_ex2, plus the
+# opacity and product roundings).
+MARGINS = (1e-6, 1e-6, 2.0 ** -24, 1e-6)
+
+
+def render_fwd(recs, off, ent, b0, b1, W, H, bg=(0, 0, 0), gt=None, b_total=1, margins=MARGINS, max_paths=0):
     """O12/O13 over blocks [b0,b1).  gt: [n_views,H,W,3] uint8 or None.
-    Flags mark pixels near a discontinuity: an evaluated alpha within
-    flag_eps (relative) of 1/255, a T' within t_eps (relative) of 1e-4.  t_eps is wider because
-    an fp32 renderer's T carries the relative error of (1 - alpha), which an alpha near the
-    0.99 cap amplifies ~alpha/(1 - alpha) = 99x (1e-6 -> 1e-4).  The alpha test is on
-    |ln(255 alpha)| < flag_eps + cond_eps * S, S = |u| (|l11 dx| + |l21 dy|) + u^2 + w^2 the fp32
-    conditioning of the exponent -(u^2 + w^2)/2 through the conic's Cholesky factor (for thin
-    Gaussians u cancels large terms); cond_eps = 4e-7 ~ 7 eps_f32."""
+    Nominal outputs (every decision on its exact side) plus, with max_paths > 0, every
+    outcome path of the decisions within the margins of a threshold (path 0 = nominal):
+    n_paths [nb,256], flips [nb,256,P] (uint64), path_c [nb,256,P,3], path_T, path_nl,
+    path_counts [nb,256,P,4].  flags bit 16 marks a pixel with more than max_paths paths."""
     nb = b1 - b0
+    P = int(max_paths)
     o = dict(c=np.zeros((nb, 256, 3)), T=np.zeros((nb, 256)), nlast=np.zeros((nb, 256), np.int32),
              flags=np.zeros((nb, 256), np.int32), counts=np.zeros((nb, 256, 4), np.int64),
              work=np.zeros(nb, np.int64), dl_dc=np.zeros((nb, 256, 3)) if gt is not None else None)
+    if P > 0:
+        o.update(n_paths=np.zeros((nb, 256), np.int32), flips=np.zeros((nb, 256, P), np.uint64),
+                 path_c=np.zeros((nb, 256, P, 3)), path_T=np.zeros((nb, 256, P)),
+                 path_nl=np.zeros((nb, 256, P), np.int32), path_counts=np.zeros((nb, 256, P, 4), np.int64))
     loss = C.c_double(0.0)
     bgv = np.asarray(bg, np.float64)
     gtp = np.ascontiguousarray(gt, np.uint8) if gt is not None else None
     ent = np.ascontiguousarray(ent, np.int64) if len(ent) else np.zeros(1, np.int64)
+    mg = np.asarray(margins, np.float64)
     lib().orc_render_fwd(C.c_int64(recs.n), _p(recs.rec_f), _p(off), _p(ent), C.c_int64(b0),
                          C.c_int64(b1), C.c_int32(W), C.c_int32(H), _p(bgv), _p(gtp),
-                         C.c_int32(b_total), C.c_double(flag_eps), C.c_double(t_eps), C.c_double(cond_eps),
+                         C.c_int32(b_total), _p(mg),
                          _p(o["c"]), _p(o["T"]),
                          _p(o["nlast"]), _p(o["flags"]), _p(o["counts"]), _p(o["work"]),
-                         _p(o["dl_dc"]), C.byref(loss))
+                         _p(o["dl_dc"]), C.byref(loss), C.c_int32(P),
+                         *([_p(o[k]) for k in ("n_paths", "flips", "path_c", "path_T", "path_nl", "path_counts")]
+                           if P > 0 else [None] * 6))
     o["loss"] = loss.value
+    o["margins"] = tuple(margins)
     return o
 
 
-def render_bwd(recs, off, ent, b0, b1, W, H, dl_dc, bg=(0, 0, 0)):
-    """O14/O15: returns grad_rec[n_rec, 9] = dL/d(mx,my,A,B,C,opacity,r,g,b)."""
+def render_bwd(recs, off, ent, b0, b1, W, H, dl_dc, bg=(0, 0, 0), margins=MARGINS, flips=None):
+    """O14/O15: returns grad_rec[n_rec, 9] = dL/d(mx,my,A,B,C,opacity,r,g,b); each pixel follows
+    the outcome path flips[nb,256] of render_fwd (None: nominal)."""
     g = np.zeros((recs.n, 9))
     bgv = np.asarray(bg, np.float64)
     ent = np.ascontiguousarray(ent, np.int64) if len(ent) else np.zeros(1, np.int64)
+    fl = np.ascontiguousarray(flips, np.uint64) if flips is not None else None
     lib().orc_render_bwd(C.c_int64(recs.n), _p(recs.rec_f), _p(off), _p(ent), C.c_int64(b0),
                          C.c_int64(b1), C.c_int32(W), C.c_int32(H), _p(bgv),
-                         _p(np.ascontiguousarray(dl_dc, np.float64)), _p(g))
+                         _p(np.ascontiguousarray(dl_dc, np.float64)), _p(np.asarray(margins, np.float64)),
+                         _p(fl), _p(g))
     return g
 
 
@@ -271,7 +287,7 @@ def flatten_params(scene):
                            scene.sh.reshape(scene.n, 48)], 1).astype(np.float64)
 
 
-def render_batch(scene, cams, mode="parity", bg=(0, 0, 0), gt=None, flag_eps=1e-5, b0=None, b1=None):
+def render_batch(scene, cams, mode="parity", bg=(0, 0, 0), gt=None, max_paths=0, b0=None, b1=None):
     """Single-partition forward of the whole batch (all views share one image size)."""
     W, H = cams[0].width, cams[0].height
     Wt, Ht = (W + 15) // 16, (H + 15) // 16
@@ -279,7 +295,7 @@ def render_batch(scene, cams, mode="parity", bg=(0, 0, 0), gt=None, flag_eps=1e-
     b0 = 0 if b0 is None else b0
     b1 = len(cams) * Wt * Ht if b1 is None else b1
     off, ent = tile_lists(recs, b0, b1, Wt, Ht)
-    fwd = render_fwd(recs, off, ent, b0, b1, W, H, bg, gt, len(cams), flag_eps)
+    fwd = render_fwd(recs, off, ent, b0, b1, W, H, bg, gt, len(cams), max_paths=max_paths)
     return recs, off, ent, fwd
 
 

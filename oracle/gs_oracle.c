@@ -387,17 +387,120 @@ void orc_tile_lists(int64_t n_rec, const double* rec_f, const int64_t* rec_i, in
 /* ------------------------------------------------------------------ O12/O13 forward */
 static double sgn(double v) { return (v > 0) - (v < 0); }
 
+/* Decision margins (DESIGN.md §2 R16, "discontinuities").  O12 takes two threshold
+ * decisions per evaluated entry (alpha < 1/255: skip; T' < 1e-4: stop, "until a
+ * threshold opacity has been reached").  An fp32 renderer may take either side of a decision
+ * whose exact value lies within its own rounding error of the threshold; both outcomes are
+ * then correct results of the method.  The oracle marks such a decision "flagged" and
+ * enumerates both outcomes (orc_render_fwd paths), so a pixel is checked against every
+ * result an fp32 evaluation may legitimately produce, never excluded.  The error model is
+ * the first-order bound of the renderer's fp32 arithmetic as the boundary defines it
+ * (include/gs.h: the conic's Cholesky factor rounded to nearest, u and w evaluated from a
+ * reference point within (3.5, 7.5) px of the pixel, four rows per thread 4 px apart), with
+ * u_r = 2^-24 per operation; DESIGN.md §2 R16 has the term-by-term derivation:
+ *   e_q = m->cond_eps (13 |power| + 7 |u| l11 + 51 |u l21| + 39 |w| l22), cond_eps = u_r,
+ *         -2 power = u^2 + w^2, u = l11 dx + l21 dy, w = l22 dy (conic = L L^T): the bound on
+ *         the error of the renderer's exponent, in ln(alpha) units;
+ *   skip:  flagged if |ln(255 alpha)| < m->alpha_eps + e_q + u_r |ln(255 o)| (the rounding of
+ *          the threshold log2(255 o) to fp32; alpha_eps covers the fp32 opacity);
+ *   stop:  flagged if |1e4 T' - 1| < m->t_eps + e_T, e_T the accumulated bound on the relative
+ *          error of the fp32 product T = prod (1 - alpha_k): per composited entry
+ *          e_alpha alpha / (1 - alpha) + 3 u_r, e_alpha = m->alpha_abs + e_q the relative
+ *          error of an fp32 alpha = o 2^-q (alpha_abs: ex2.approx, measured on the device by
+ *          gs_selftest_ex2, the opacity and the product). */
+#define U_R (1.0 / 16777216.0)
+typedef struct {
+  double alpha_eps, t_eps, cond_eps, alpha_abs;
+} orc_margins_t;
+
+typedef struct { /* a composited entry of one pixel, front to back */
+  int64_t idx;
+  double T, alpha, G, dx, dy;
+  int capped;
+} comp_t;
+
+/* O12 for one pixel (px, py) over the list L[0..nL), taking the alternative outcome of the
+ * f-th flagged decision met (in list order) when bit f of flips is set (f < 64).  Writes the
+ * colour before background C, T, n_last, counts (E_f, E_fc, E_fs, E_stop) and, if comp is
+ * not NULL, the composited entries.  Returns the number of flagged decisions met; *bits
+ * gets 1 (a skip decision flagged), 2 (a stop decision flagged), 4 (power > 0 met). */
+static int walk_pixel(const double* rec_f, const int64_t* L, int64_t nL, double px, double py,
+                      const orc_margins_t* m, uint64_t flips, double C[3], double* Tout, int32_t* nlast,
+                      int64_t cnt[4], comp_t* comp, int64_t* ncomp, int* bits) {
+  double T = 1.0, terr = 0.0;
+  int nf = 0;
+  int64_t nc = 0;
+  C[0] = C[1] = C[2] = 0.0;
+  *nlast = 0;
+  *bits = 0;
+  cnt[0] = cnt[1] = cnt[2] = cnt[3] = 0;
+  for (int64_t k = 0; k < nL; k++) {
+    const double* r = rec_f + 10 * L[k];
+    double dx = r[0] - px, dy = r[1] - py;
+    double power = -0.5 * (r[3] * dx * dx + r[5] * dy * dy) - r[4] * dx * dy;
+    cnt[0]++;
+    if (power > 0) { *bits |= 4; cnt[2]++; continue; }
+    double G = exp(power), raw = r[6] * G, alpha = raw;
+    int capped = 0;
+    if (alpha > ALPHA_CAP) { alpha = ALPHA_CAP; capped = 1; }
+    /* first-order bound of the renderer's fp32 exponent error, in ln(alpha) units (see
+     * orc_margins_t) */
+    double l11 = sqrt(r[3]), l21 = r[4] / l11, l22 = sqrt(fmax(r[5] - l21 * l21, 0.0));
+    double u = l11 * dx + l21 * dy, w = l22 * dy;
+    double eq = m->cond_eps * (13.0 * fabs(power) + 7.0 * fabs(u) * l11 + 51.0 * fabs(u * l21) + 39.0 * fabs(w) * l22);
+    /* skip decision: alpha < 1/255, taken by the renderer as q > qmax with qmax = log2(255 o)
+     * rounded to fp32 (u_r |qmax| ln 2 in ln(alpha) units) */
+    int skip = alpha < ALPHA_MIN;
+    if (alpha > 0 && fabs(log(alpha * 255.0)) < m->alpha_eps + eq + U_R * fabs(log(255.0 * r[6]))) {
+      *bits |= 1;
+      if (nf < 64 && ((flips >> nf) & 1)) skip = !skip;
+      nf++;
+    }
+    if (skip) { cnt[2]++; continue; }
+    double ea = m->alpha_abs + eq; /* relative error bound of the fp32 alpha */
+    if (capped && raw * (1.0 - ea) >= ALPHA_CAP) ea = 1.1e-8; /* both sides clamp: 0.99f vs 0.99 */
+    double et = terr + ea * alpha / (1.0 - alpha) + 3.0 * U_R;
+    /* stop decision: T' < 1e-4 (R3: before compositing) */
+    double Tn = T * (1.0 - alpha);
+    int stop = Tn < T_STOP;
+    if (fabs(Tn * 1e4 - 1.0) < m->t_eps + et) {
+      *bits |= 2;
+      if (nf < 64 && ((flips >> nf) & 1)) stop = !stop;
+      nf++;
+    }
+    if (stop) { cnt[3] = 1; break; }
+    if (comp) {
+      comp[nc].idx = L[k]; comp[nc].T = T; comp[nc].alpha = alpha; comp[nc].G = G;
+      comp[nc].dx = dx; comp[nc].dy = dy; comp[nc].capped = capped;
+    }
+    nc++;
+    for (int ch = 0; ch < 3; ch++) C[ch] += alpha * T * r[7 + ch];
+    T = Tn;
+    terr = et;
+    *nlast = (int32_t)(k + 1);
+    cnt[1]++;
+  }
+  *Tout = T;
+  if (ncomp) *ncomp = nc;
+  return nf;
+}
+
 void orc_render_fwd(int64_t n_rec, const double* rec_f, const int64_t* offsets,
                     const int64_t* entries, int64_t b0, int64_t b1, int32_t W, int32_t H,
-                    const double* bg, const uint8_t* gt, int32_t b_total, double flag_eps, double t_eps,
-                    double cond_eps,
+                    const double* bg, const uint8_t* gt, int32_t b_total, const double* margins,
                     double* out_c, double* out_T, int32_t* out_nlast, int32_t* flags,
-                    int64_t* counts, int64_t* work, double* dl_dc, double* loss) {
+                    int64_t* counts, int64_t* work, double* dl_dc, double* loss,
+                    int32_t max_paths, int32_t* n_paths, uint64_t* path_flips, double* path_c,
+                    double* path_T, int32_t* path_nl, int64_t* path_counts) {
   (void)n_rec;
+  const orc_margins_t m = {margins[0], margins[1], margins[2], margins[3]};
   const int Wt = (W + 15) / 16, Ht = (H + 15) / 16;
   const int64_t per_view = (int64_t)Wt * Ht;
   const double norm = 1.0 / (3.0 * (double)H * (double)W * (double)b_total);
+  const int P = max_paths > 0 ? max_paths : 0;
   double lsum = 0;
+  uint64_t* queue = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(P > 0 ? P : 1));
+  int* qnf = (int*)malloc(sizeof(int) * (size_t)(P > 0 ? P : 1));
   for (int64_t beta = b0; beta < b1; beta++) {
     int64_t kb = beta - b0, v = beta / per_view, loc = beta % per_view;
     int tx = (int)(loc % Wt), ty = (int)(loc / Wt);
@@ -407,10 +510,17 @@ void orc_render_fwd(int64_t n_rec, const double* rec_f, const int64_t* offsets,
     for (int p = 0; p < 256; p++) {
       int px = tx * 16 + p % 16, py = ty * 16 + p / 16;
       int64_t o = kb * 256 + p;
-      double C[3] = {0, 0, 0}, T = 1.0;
-      int32_t nlast = 0, flag = 0;
-      int64_t Ef = 0, Efc = 0, Efs = 0, Estop = 0;
+      if (P > 0) n_paths[o] = 0;
       if (px >= W || py >= H) {
+        if (P > 0) { /* not rendered: the one outcome is the untouched pixel */
+          int64_t po = o * P;
+          n_paths[o] = 1;
+          path_flips[po] = 0;
+          path_c[3 * po] = path_c[3 * po + 1] = path_c[3 * po + 2] = 0;
+          path_T[po] = 1;
+          path_nl[po] = 0;
+          for (int k = 0; k < 4; k++) path_counts[4 * po + k] = 0;
+        }
         out_c[3 * o] = out_c[3 * o + 1] = out_c[3 * o + 2] = 0;
         out_T[o] = 1;
         out_nlast[o] = 0;
@@ -419,77 +529,87 @@ void orc_render_fwd(int64_t n_rec, const double* rec_f, const int64_t* offsets,
         if (dl_dc) dl_dc[3 * o] = dl_dc[3 * o + 1] = dl_dc[3 * o + 2] = 0;
         continue;
       }
-      double terr = 0.0; /* bound on the fp32 renderer's relative error of T so far */
-      for (int64_t k = 0; k < nL; k++) {
-        const double* r = rec_f + 10 * L[k];
-        double dx = r[0] - px, dy = r[1] - py;
-        double power = -0.5 * (r[3] * dx * dx + r[5] * dy * dy) - r[4] * dx * dy;
-        double aeps = flag_eps;
-        Ef++;
-        if (power > 0) { flag |= 4; Efs++; continue; }
-        double alpha = r[6] * exp(power);
-        if (alpha > ALPHA_CAP) alpha = ALPHA_CAP;
-        {
-          /* conditioning of power in fp32: its absolute error is ~eps_f32 S (thin Gaussians:
-           * u cancels large terms), so the margin on |ln(255 alpha)| is
-           * flag_eps + cond_eps * S (discontinuities) */
-          /* S bounds |d power| / eps_f32 for an evaluation through the Cholesky factor of the
-           * conic (power = -(u^2 + w^2)/2, u = l11 dx + l21 dy, w = l22 dy) */
-          double l11 = sqrt(r[3]), l21 = r[4] / l11, l22 = sqrt(fmax(r[5] - l21 * l21, 0.0));
-          double u = l11 * dx + l21 * dy, w = l22 * dy;
-          double S = fabs(u) * (fabs(l11 * dx) + fabs(l21 * dy)) + u * u + w * w;
-          aeps = flag_eps + cond_eps * S;
-          if (alpha > 0 && fabs(log(alpha * 255.0)) < aeps) flag |= 1;
-        }
-        if (alpha < ALPHA_MIN) { Efs++; continue; }
-        double Tn = T * (1.0 - alpha);
-        if (fabs(Tn * 1e4 - 1.0) < t_eps + terr) flag |= 2;
-        if (Tn < T_STOP) { Estop = 1; break; }  /* R3: stop before compositing */
-        for (int ch = 0; ch < 3; ch++) C[ch] += alpha * T * r[7 + ch];
-        T = Tn;
-        nlast = (int32_t)(k + 1);
-        Efc++;
-        /* an alpha error aeps (relative) moves (1 - alpha) by aeps alpha / (1 - alpha) */
-        terr += aeps * alpha / (1.0 - alpha);
-      }
+      double C[3], T;
+      int32_t nlast;
+      int bits;
+      int nf = walk_pixel(rec_f, L, nL, px, py, &m, 0, C, &T, &nlast, counts + 4 * o, NULL, NULL, &bits);
+      int flag = bits;
       for (int ch = 0; ch < 3; ch++) C[ch] += T * bg[ch];
       for (int ch = 0; ch < 3; ch++) out_c[3 * o + ch] = C[ch];
       out_T[o] = T;
       out_nlast[o] = nlast;
-      counts[4 * o] = Ef; counts[4 * o + 1] = Efc; counts[4 * o + 2] = Efs; counts[4 * o + 3] = Estop;
-      work[kb] += Ef + nlast;
+      work[kb] += counts[4 * o] + nlast;
       if (gt) {
         const uint8_t* g = gt + (((int64_t)v * H + py) * W + px) * 3;
         for (int ch = 0; ch < 3; ch++) {
           double d = C[ch] - g[ch] / 255.0;
           lsum += fabs(d) * norm;
           if (dl_dc) dl_dc[3 * o + ch] = sgn(d) * norm;
-          if (fabs(d) < flag_eps) flag |= 8;
         }
+      }
+      if (P > 0) {
+        /* every outcome sequence of the flagged decisions: path masks in breadth-first order,
+         * a child sets one more bit above its parent's highest set bit and below the number of
+         * flagged decisions its parent's walk met (each distinct walk is visited once) */
+        int nq = 0, head = 0;
+        queue[nq] = 0; qnf[nq] = nf; nq++;
+        while (head < nq) {
+          uint64_t mask = queue[head];
+          int pnf = qnf[head];
+          int64_t po = o * P + head;
+          double Cp[3], Tp;
+          int32_t nlp;
+          int bp;
+          if (head == 0) {
+            Cp[0] = C[0]; Cp[1] = C[1]; Cp[2] = C[2]; Tp = T; nlp = nlast;
+            for (int k = 0; k < 4; k++) path_counts[4 * po + k] = counts[4 * o + k];
+          } else {
+            walk_pixel(rec_f, L, nL, px, py, &m, mask, Cp, &Tp, &nlp, path_counts + 4 * po, NULL, NULL, &bp);
+            for (int ch = 0; ch < 3; ch++) Cp[ch] += Tp * bg[ch];
+          }
+          path_flips[po] = mask;
+          for (int ch = 0; ch < 3; ch++) path_c[3 * po + ch] = Cp[ch];
+          path_T[po] = Tp;
+          path_nl[po] = nlp;
+          int hi = -1;
+          for (int b = 63; b >= 0; b--)
+            if ((mask >> b) & 1) { hi = b; break; }
+          for (int b = hi + 1; b < pnf && b < 64; b++) {
+            if (nq >= P) { flag |= 16; break; } /* more outcome sequences than max_paths */
+            uint64_t child = mask | (1ull << b);
+            double Cc[3], Tc;
+            int32_t nlc;
+            int64_t cc[4];
+            int bc;
+            int cnf = walk_pixel(rec_f, L, nL, px, py, &m, child, Cc, &Tc, &nlc, cc, NULL, NULL, &bc);
+            queue[nq] = child; qnf[nq] = cnf; nq++;
+          }
+          head++;
+        }
+        n_paths[o] = nq;
       }
       flags[o] = flag;
     }
   }
+  free(queue);
+  free(qnf);
   if (loss) *loss += lsum;
 }
 
 /* ------------------------------------------------------------------ O14/O15 backward */
 void orc_render_bwd(int64_t n_rec, const double* rec_f, const int64_t* offsets,
                     const int64_t* entries, int64_t b0, int64_t b1, int32_t W, int32_t H,
-                    const double* bg, const double* dl_dc, double* grad_rec) {
+                    const double* bg, const double* dl_dc, const double* margins, const uint64_t* flips,
+                    double* grad_rec) {
   (void)n_rec;
+  const orc_margins_t m = {margins[0], margins[1], margins[2], margins[3]};
   const int Wt = (W + 15) / 16, Ht = (H + 15) / 16;
   const int64_t per_view = (int64_t)Wt * Ht;
   int64_t cap = 0;
+  (void)Ht;
   for (int64_t kb = 0; kb < b1 - b0; kb++)
     if (offsets[kb + 1] - offsets[kb] > cap) cap = offsets[kb + 1] - offsets[kb];
-  int64_t* idx = (int64_t*)malloc(sizeof(int64_t) * (size_t)(cap + 1));
-  double* Tk = (double*)malloc(sizeof(double) * (size_t)(cap + 1));
-  double* ak = (double*)malloc(sizeof(double) * (size_t)(cap + 1));
-  double* Gk = (double*)malloc(sizeof(double) * (size_t)(cap + 1));
-  double* dxk = (double*)malloc(sizeof(double) * (size_t)(cap + 1));
-  double* dyk = (double*)malloc(sizeof(double) * (size_t)(cap + 1));
-  int* capk = (int*)malloc(sizeof(int) * (size_t)(cap + 1));
+  comp_t* comp = (comp_t*)malloc(sizeof(comp_t) * (size_t)(cap + 1));
   for (int64_t beta = b0; beta < b1; beta++) {
     int64_t kb = beta - b0, loc = beta % per_view;
     int tx = (int)(loc % Wt), ty = (int)(loc / Wt);
@@ -499,39 +619,28 @@ void orc_render_bwd(int64_t n_rec, const double* rec_f, const int64_t* offsets,
       int px = tx * 16 + p % 16, py = ty * 16 + p / 16;
       if (px >= W || py >= H) continue;
       const double* g = dl_dc + 3 * (kb * 256 + p);
-      /* re-run O12, storing the composited entries */
-      double T = 1.0;
-      int64_t nc = 0;
-      for (int64_t k = 0; k < nL; k++) {
-        const double* r = rec_f + 10 * L[k];
-        double dx = r[0] - px, dy = r[1] - py;
-        double power = -0.5 * (r[3] * dx * dx + r[5] * dy * dy) - r[4] * dx * dy;
-        if (power > 0) continue;
-        double G = exp(power), alpha = r[6] * G;
-        int capped = 0;
-        if (alpha > ALPHA_CAP) { alpha = ALPHA_CAP; capped = 1; }
-        if (alpha < ALPHA_MIN) continue;
-        double Tn = T * (1.0 - alpha);
-        if (Tn < T_STOP) break;
-        idx[nc] = L[k]; Tk[nc] = T; ak[nc] = alpha; Gk[nc] = G; dxk[nc] = dx; dyk[nc] = dy;
-        capk[nc] = capped;
-        nc++;
-        T = Tn;
-      }
-      double Tfinal = T, S[3] = {0, 0, 0};
+      /* re-run O12 along the pixel's outcome path, storing the composited entries */
+      double C[3], Tfinal;
+      int32_t nlast;
+      int64_t cnt[4], nc = 0;
+      int bits;
+      walk_pixel(rec_f, L, nL, px, py, &m, flips ? flips[kb * 256 + p] : 0, C, &Tfinal, &nlast, cnt, comp, &nc,
+                 &bits);
+      double S[3] = {0, 0, 0};
       double bgdot = bg[0] * g[0] + bg[1] * g[1] + bg[2] * g[2];
       for (int64_t e = nc - 1; e >= 0; e--) {
-        const double* r = rec_f + 10 * idx[e];
-        double* gr = grad_rec + 9 * idx[e];
-        double a = ak[e];
-        for (int ch = 0; ch < 3; ch++) gr[6 + ch] += a * Tk[e] * g[ch];
-        double dA = Tk[e] * ((r[7] - S[0]) * g[0] + (r[8] - S[1]) * g[1] + (r[9] - S[2]) * g[2]) -
+        const double* r = rec_f + 10 * comp[e].idx;
+        double* gr = grad_rec + 9 * comp[e].idx;
+        double a = comp[e].alpha, Tk = comp[e].T;
+        for (int ch = 0; ch < 3; ch++) gr[6 + ch] += a * Tk * g[ch];
+        double dA = Tk * ((r[7] - S[0]) * g[0] + (r[8] - S[1]) * g[1] + (r[9] - S[2]) * g[2]) -
                     (Tfinal / (1.0 - a)) * bgdot;
         for (int ch = 0; ch < 3; ch++) S[ch] = a * r[7 + ch] + (1.0 - a) * S[ch];
-        if (capk[e]) continue;  /* R6: alpha = 0.99 constant */
-        gr[5] += Gk[e] * dA;
-        double q = r[6] * Gk[e] * dA;  /* dL/dpower */
-        double dx = dxk[e], dy = dyk[e];
+        if (comp[e].capped) continue;  /* R6: alpha = 0.99 constant */
+        double Gk = comp[e].G;
+        gr[5] += Gk * dA;
+        double q = r[6] * Gk * dA;  /* dL/dpower */
+        double dx = comp[e].dx, dy = comp[e].dy;
         gr[0] += q * (-(r[3] * dx + r[4] * dy));
         gr[1] += q * (-(r[4] * dx + r[5] * dy));
         gr[2] += q * (-0.5 * dx * dx);
@@ -540,7 +649,7 @@ void orc_render_bwd(int64_t n_rec, const double* rec_f, const int64_t* offsets,
       }
     }
   }
-  free(idx); free(Tk); free(ak); free(Gk); free(dxk); free(dyk); free(capk);
+  free(comp);
 }
 
 /* ------------------------------------------------------------------ O16 transformation backward */

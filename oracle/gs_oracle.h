@@ -59,25 +59,35 @@ void orc_tile_lists(int64_t n_rec, const double* rec_f, const int64_t* rec_i, in
                     int64_t b1, int32_t Wt, int32_t Ht, int64_t* offsets, int64_t* entries);
 
 /* O12 (+ O13 when gt != NULL): forward compositing over blocks [b0,b1).
- * Block-major outputs, pixel p = ly*16+lx of the block:
+ * Block-major outputs, pixel p = ly*16+lx of the block (the nominal outcome: every decision
+ * taken on its exact fp64 side):
  *   out_c[nb][256][3], out_T[nb][256], out_nlast[nb][256] (int32),
- *   flags[nb][256] (bit0: |ln(255 alpha)| < flag_eps + cond_eps * S (S: fp32 conditioning of power, see .c), bit1: |1e4 T' - 1| < t_eps + (accumulated alpha-margin bound of T), bit2: power>0 seen,
- *                   bit3: |C-GT| < flag_eps (L1 sign ambiguous)),
+ *   flags[nb][256] (bit0: a skip decision alpha < 1/255 within the margin, bit1: a stop
+ *                   decision T' < 1e-4 within the margin, bit2: power > 0 met, bit4: more
+ *                   outcome paths than max_paths),
  *   counts[nb][256][4] = (E_f, E_fc, E_fs, E_stop), work[nb] = sum_px (E_f + n_last),
  *   dl_dc[nb][256][3] = sign(C-GT)/(3 H W b_total) (only if gt), *loss += sum |C-GT|/(3HWb).
+ * margins[4] = (alpha_eps, t_eps, cond_eps, alpha_abs), see gs_oracle.c orc_margins_t.
+ * max_paths > 0: every outcome path of the flagged decisions, up to max_paths per pixel
+ * (path 0 = nominal): n_paths[nb][256], path_flips[nb][256][P] (bit f: the f-th flagged
+ * decision takes its other outcome), path_c[nb][256][P][3] (incl. background), path_T,
+ * path_nl[nb][256][P], path_counts[nb][256][P][4].
  * gt is [n_views][H][W][3] uint8 (value/255).  Out-of-image pixels are not rendered. */
 void orc_render_fwd(int64_t n_rec, const double* rec_f, const int64_t* offsets,
                     const int64_t* entries, int64_t b0, int64_t b1, int32_t W, int32_t H,
-                    const double* bg, const uint8_t* gt, int32_t b_total, double flag_eps, double t_eps,
-                    double cond_eps,
+                    const double* bg, const uint8_t* gt, int32_t b_total, const double* margins,
                     double* out_c, double* out_T, int32_t* out_nlast, int32_t* flags,
-                    int64_t* counts, int64_t* work, double* dl_dc, double* loss);
+                    int64_t* counts, int64_t* work, double* dl_dc, double* loss,
+                    int32_t max_paths, int32_t* n_paths, uint64_t* path_flips, double* path_c,
+                    double* path_T, int32_t* path_nl, int64_t* path_counts);
 
 /* O14-O15: backward of O12 given dl_dc[nb][256][3]; accumulates grad_rec[n_rec][9] =
- * dL/d(mx, my, A, B, C, opacity, r, g, b) summed over all pixels.            */
+ * dL/d(mx, my, A, B, C, opacity, r, g, b) summed over all pixels.  Each pixel follows the
+ * outcome path flips[nb][256] (NULL: nominal) of orc_render_fwd with the same margins. */
 void orc_render_bwd(int64_t n_rec, const double* rec_f, const int64_t* offsets,
                     const int64_t* entries, int64_t b0, int64_t b1, int32_t W, int32_t H,
-                    const double* bg, const double* dl_dc, double* grad_rec);
+                    const double* bg, const double* dl_dc, const double* margins, const uint64_t* flips,
+                    double* grad_rec);
 
 /* O16: transformation backward in fp64, summed over n_cam views.
  * grad_rec_v[n_cam][n][9] (zero rows for invisible (i,v)), out grad[n][59] =

@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(_HERE, "libgs_%s.so" % os.environ["GS_LIB_VARIANT"] if o
 GS_OK, GS_EINVAL, GS_ECAPACITY, GS_ENONFINITE, GS_ECUDA, GS_ENCCL, GS_ENOTSUP = range(7)
 COST_MEASURED, COST_WORK, COST_PAPER_AVG = 0, 1, 2
 ADAM_GRAD, ADAM_APPLY, ADAM_WRITE_GRAD = 1, 2, 4
-RECORD_BYTES = 48
+RECORD_BYTES = 64
 GRAD_FLOATS = 9
 
 
@@ -119,6 +119,7 @@ _sig = {
                                     _vp, C.c_int, _vp, _vp]),
     "gs_p2p_barrier": (C.c_int, [_vp, _vp]),
     "gs_p2p_status": (C.c_int, [_vp, _vp]),
+    "gs_selftest_ex2": (C.c_int, [_vp, C.c_float, C.c_float, C.POINTER(C.c_double), _vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -654,3 +655,10 @@ def p2p_barrier(ctx, stream=None):
 
 def p2p_status(ctx, stream=None):
     ctx.check(_lib.gs_p2p_status(ctx.handle, _stream(stream)))
+
+
+def selftest_ex2(ctx, lo, hi, stream=None):
+    """Max relative error of the renderer's ex2.approx over every fp32 in [lo, hi] (hi <= 0)."""
+    r = C.c_double(0.0)
+    ctx.check(_lib.gs_selftest_ex2(ctx.handle, C.c_float(lo), C.c_float(hi), C.byref(r), _stream(stream)))
+    return r.value

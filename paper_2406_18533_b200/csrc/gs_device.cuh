@@ -240,7 +240,7 @@ __device__ __forceinline__ void sh_basis(float x, float y, float z, float Y[16])
 }
 
 // ex2.approx (MUFU.EX2) -- used for alpha in both render passes (identical instruction
-// sequence in forward and backward, so skip/stop decisions agree bit for bit).
+// sequence in forward and backward).  Its relative error is pinned by gs_selftest_ex2.
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -249,51 +249,17 @@ __device__ __forceinline__ float ex2_approx(float x) {
 
 // sqrt(0.5 * log2(e)): prescale of the conic's Cholesky factor so that
 // 2^-(u'^2 + w'^2) = exp(-0.5 d^T conic d).
-constexpr float kLScale = 0.84932180028801907f;
+constexpr double kLScale64 = 0.84932180028801904272150283410289;
 
+// The 64-byte record (include/gs.h GS_RECORD_BYTES): the conic's prescaled Cholesky factor
+// L' = L sqrt(0.5 log2 e) (conic = L L^T) in double-float form, hi + lo, both rounded to
+// nearest from fp64, and qmax = log2(255 o) rounded to nearest (alpha = o 2^-q >= 1/255 <=>
+// q <= qmax).
 struct __align__(16) gs_rec {
   float4 a;  // mx, my, depth, radius
-  float4 b;  // l11, l21, l22, opacity
-  float4 c;  // r, g, b, meta bits
+  float4 b;  // l11', l21', l22' (hi), opacity
+  float4 c;  // r, g, b, qmax
+  float4 d;  // l11', l21', l22' (lo), meta bits (gid * 32 + view)
 };
-
-// Staged record for compositing: mean, prescaled L, opacity, colour.
-struct gs_srec {
-  float mx, my, l11, l21, l22, o, r, g, b;
-};
-
-// Gaussian weights of a staged record at the vertically adjacent pixel pair (px, py) and
-// (px, py + 1).  The pair shares dx; the second pixel's L^T d follows from the first by one
-// subtraction each (dy1 = dy0 - 1):  u1 = u0 - l21, w1 = w0 - l22.  Both render passes call
-// exactly this, so their skip/stop decisions agree bit for bit.
-struct gs_pair {
-  float dx, dy0, u0, w0, u1, w1, G0, G1, raw0, raw1;
-};
-__device__ __forceinline__ void alpha_pair(float mx, float my, float l11, float l21, float l22, float o,
-                                           float px, float py0, gs_pair& e) {
-  e.dx = __fsub_rn(mx, px);
-  e.dy0 = __fsub_rn(my, py0);
-  e.u0 = __fmaf_rn(l11, e.dx, __fmul_rn(l21, e.dy0));
-  e.w0 = __fmul_rn(l22, e.dy0);
-  e.u1 = __fsub_rn(e.u0, l21);
-  e.w1 = __fsub_rn(e.w0, l22);
-  e.G0 = ex2_approx(-__fmaf_rn(e.u0, e.u0, __fmul_rn(e.w0, e.w0)));
-  e.G1 = ex2_approx(-__fmaf_rn(e.u1, e.u1, __fmul_rn(e.w1, e.w1)));
-  e.raw0 = __fmul_rn(o, e.G0);  // raw o*G; callers apply the 0.99 cap
-  e.raw1 = __fmul_rn(o, e.G1);
-}
-
-// alpha of a staged record at pixel (px, py) (single-pixel form, kept for reference tools).
-__device__ __forceinline__ float alpha_at(float mx, float my, float l11, float l21, float l22,
-                                          float o, float px, float py, float& G, float& dx,
-                                          float& dy, float& u, float& w) {
-  dx = __fsub_rn(mx, px);
-  dy = __fsub_rn(my, py);
-  u = __fmaf_rn(l11, dx, __fmul_rn(l21, dy));
-  w = __fmul_rn(l22, dy);
-  float q = __fmaf_rn(u, u, __fmul_rn(w, w));
-  G = ex2_approx(-q);
-  return __fmul_rn(o, G);  // raw o*G; caller applies the 0.99 cap
-}
 
 }  // namespace gsd

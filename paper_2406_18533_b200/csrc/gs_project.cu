@@ -8,7 +8,7 @@
 //          (the backward index gs_adam_step reuses);
 //   scan:  exclusive scan of the counts in (d, v, CTA) order -> each CTA's bucket bases;
 //   write: recompute the projection, rank each Gaussian inside its CTA bucket with warp
-//          ballots (thread order = gid order), write 48-byte records.
+//          ballots (thread order = gid order), write 64-byte records.
 // Placement is therefore deterministic and gid-ordered within each (d, v) bucket, which the
 // stable (depth, gid) order of A3 relies on; no placement atomics.
 #include "gs_device.cuh"
@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(kBlock) k_project_write(
     q = rot[i];
   }
   gs_cov3 cv = cov3_of(ls, q);
-  const float opac = 1.0f / (1.0f + __expf(-X.w));
+  // O1 opacity, rounded to nearest from fp64 (it sets alpha and the skip threshold)
+  const float opac = __double2float_rn(1.0 / (1.0 + exp(-(double)X.w)));
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   for (int v = 0; v < b; v++) {
@@ -91,15 +92,28 @@ __global__ void __launch_bounds__(kBlock) k_project_write(
     if (mine) {
       const gs_dcam& cam = cams.c[v];
       gs_memb mb = membership(cv, X.x, X.y, X.z, cam, geo.Wt, geo.Ht);
-      // conic = inverse of the 2D covariance; store its Cholesky factor L (conic = L L^T):
-      // det by Kahan's difference of products, then l11 = sqrt(c)/sqrt(det),
-      // l21 = -b/(sqrt(det) sqrt(c)), l22 = 1/sqrt(c)  (well conditioned for thin Gaussians)
-      float bb = mb.b * mb.b;
-      float e = fmaf(-mb.b, mb.b, bb);
-      float det = fmaf(mb.a, mb.c, -bb) + e;
-      if (!(det > 0.f)) det = sub(mul(mb.a, mb.c), mul(mb.b, mb.b));
-      float sd = sqrtf(det), sc = sqrtf(mb.c);
-      float l11 = sc / sd, l21 = -mb.b / (sd * sc), l22 = 1.0f / sc;
+      // conic = inverse of the 2D covariance (O6), carried as its Cholesky factor prescaled by
+      // sqrt(0.5 log2 e) (conic = L L^T): l11 = sqrt(c / det), l21 = -b / sqrt(det c),
+      // l22 = 1 / sqrt(c), evaluated in fp64 from the fp32 covariance (the products of fp32
+      // values are exact in fp64) and stored as hi + lo, each rounded to nearest
+      float lh[3] = {0.f, 0.f, 0.f}, ll[3] = {0.f, 0.f, 0.f};
+      {
+        const double a64 = mb.a, b64 = mb.b, c64 = mb.c;
+        const double det = a64 * c64 - b64 * b64;
+        if (det > 0.0) {
+          const double sc = sqrt(c64), sd = sqrt(det);
+          const double L[3] = {kLScale64 * sc / sd, -kLScale64 * b64 / (sd * sc), kLScale64 / sc};
+#pragma unroll
+          for (int k = 0; k < 3; k++) {
+            lh[k] = __double2float_rn(L[k]);
+            ll[k] = __double2float_rn(L[k] - (double)lh[k]);
+          }
+        }
+      }
+      // qmax = log2(255 o), rounded to nearest from fp64 (alpha = o 2^-q >= 1/255 <=> q <= qmax);
+      // -1 (never composited) for a zero opacity or a covariance whose fp64 determinant is not
+      // positive (not reachable with the 0.3 I dilation: det >= 0.09)
+      const float qmax = (opac > 0.f && lh[0] > 0.f) ? __double2float_rn(log2(255.0 * (double)opac)) : -1.0f;
       // O9: colour from the view direction
       float dx = X.x - cam.campos[0], dy = X.y - cam.campos[1], dz = X.z - cam.campos[2];
       float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
@@ -118,8 +132,9 @@ __global__ void __launch_bounds__(kBlock) k_project_write(
       for (int ch = 0; ch < 3; ch++) col[ch] = fmaxf(col[ch], 0.0f);
       unsigned meta = (unsigned)((gid_base + i) * 32 + v);
       rec.a = make_float4(mb.mx, mb.my, mb.depth, mb.r);
-      rec.b = make_float4(l11, l21, l22, opac);
-      rec.c = make_float4(col[0], col[1], col[2], __uint_as_float(meta));
+      rec.b = make_float4(lh[0], lh[1], lh[2], opac);
+      rec.c = make_float4(col[0], col[1], col[2], qmax);
+      rec.d = make_float4(ll[0], ll[1], ll[2], __uint_as_float(meta));
     }
     for (int d = 0; d < G; d++) {
       int k = d * b + v;

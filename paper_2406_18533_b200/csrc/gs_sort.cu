@@ -35,7 +35,7 @@ __global__ void k_rect_diff(const gs_rec* __restrict__ rec, int64_t n_recv, gs_g
   if (j == n_recv) { n_tiles[j] = 0; return; }
   n_tiles[j] = 0;
   float4 a = rec[j].a;
-  int v = (int)(__float_as_uint(rec[j].c.w) & 31u);
+  int v = (int)(__float_as_uint(rec[j].d.w) & 31u);
   if (v < v_lo || v > v_hi) return;
   int tx0, tx1, ty0, ty1;
   if (!rect_of(a.x, a.y, a.w, geo.Wt, geo.Ht, tx0, tx1, ty0, ty1)) return;
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kPlaceThreads) k_place(
     s_tx0[r] = tx0;
     s_ty0[r] = ty0;
     s_w[r] = tx1 - tx0 + 1;
-    s_v[r] = (int)(__float_as_uint(rec[j].c.w) & 31u);
+    s_v[r] = (int)(__float_as_uint(rec[j].d.w) & 31u);
     s_depth[r] = __float_as_uint(a.z);
   }
   if (threadIdx.x == 0) s_start[nr] = pair_start[jlo + nr];
@@ -357,7 +357,7 @@ __global__ void k_tile_counts(const gs_rec* __restrict__ rec, int64_t n_recv, gs
   int64_t t = 0;
   if (j < n_recv) {
     const float4 a = rec[j].a;
-    const int v = (int)(__float_as_uint(rec[j].c.w) & 31u);
+    const int v = (int)(__float_as_uint(rec[j].d.w) & 31u);
     int tx0, tx1, ty0, ty1;
     if (v >= v_lo && v <= v_hi && rect_of(a.x, a.y, a.w, geo.Wt, geo.Ht, tx0, tx1, ty0, ty1))
       t = (int64_t)(tx1 - tx0 + 1) * (ty1 - ty0 + 1);
@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(kPlaceThreads) k_emit(
     s_tx0[r] = tx0;
     s_ty0[r] = ty0;
     s_w[r] = tx1 - tx0 + 1;
-    s_v[r] = (int)(__float_as_uint(rec[j].c.w) & 31u);
+    s_v[r] = (int)(__float_as_uint(rec[j].d.w) & 31u);
     s_j[r] = j;
   }
   if (threadIdx.x == 0) s_start[nr] = pair_start[slo + nr];

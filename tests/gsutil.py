@@ -7,18 +7,47 @@ import numpy as np
 import oracle
 
 
+RECORD_FLOATS = 16  # include/gs.h GS_RECORD_BYTES / 4
+# sqrt(0.5 log2 e): the record's factor is the conic's Cholesky factor times this (gs.h)
+L_PRESCALE = 0.84932180028801904272150283410289
+
+
 def decode_records(rec_u8):
-    """[n,48] uint8 tensor -> dict of numpy arrays (mx, my, depth, radius, L, opacity, rgb, gid, view)."""
-    a = rec_u8.view(-1).view(dtype=__import__("torch").float32).reshape(-1, 12).cpu().numpy()
-    meta = a[:, 11].view(np.uint32).astype(np.int64)
+    """[n,64] uint8 tensor -> dict of numpy arrays (mx, my, depth, radius, prescaled factor hi/lo,
+    opacity, rgb, qmax, gid, view)."""
+    a = rec_u8.reshape(-1).view(dtype=__import__("torch").float32).reshape(-1, RECORD_FLOATS).cpu().numpy()
+    meta = a[:, 15].view(np.uint32).astype(np.int64)
     return dict(mx=a[:, 0], my=a[:, 1], depth=a[:, 2], radius=a[:, 3], l11=a[:, 4], l21=a[:, 5], l22=a[:, 6],
-                opacity=a[:, 7], rgb=a[:, 8:11], gid=meta >> 5, view=meta & 31, raw=a)
+                opacity=a[:, 7], rgb=a[:, 8:11], qmax=a[:, 11], l11_lo=a[:, 12], l21_lo=a[:, 13], l22_lo=a[:, 14],
+                gid=meta >> 5, view=meta & 31, raw=a)
 
 
 def conic_of(d):
-    """conic (A, B, C) = L L^T from the record's Cholesky factor (test-side decode)."""
-    l11, l21, l22 = d["l11"].astype(np.float64), d["l21"].astype(np.float64), d["l22"].astype(np.float64)
+    """conic (A, B, C) = L L^T from the record's double-float factor (test-side decode)."""
+    l11 = (d["l11"].astype(np.float64) + d["l11_lo"]) / L_PRESCALE
+    l21 = (d["l21"].astype(np.float64) + d["l21_lo"]) / L_PRESCALE
+    l22 = (d["l22"].astype(np.float64) + d["l22_lo"]) / L_PRESCALE
     return np.stack([l11 * l11, l11 * l21, l21 * l21 + l22 * l22], 1)
+
+
+def match_paths(fwd, T, nl, rgb, tol=1e-4, inside=None):
+    """Every pixel of a GPU forward against the oracle's outcome paths (oracle.render_fwd with
+    max_paths > 0): a pixel passes when one of its paths has the same n_last and T and colour
+    within tol.  Returns (ok [nb,256] bool, flips [nb,256] uint64 of the first matching path
+    (0 where none), n_multi = pixels with more than one path, n_overflow).  Pixels outside
+    the image (inside False) must match path 0."""
+    P = fwd["flips"].shape[2]
+    valid = np.arange(P)[None, None, :] < fwd["n_paths"][..., None]
+    m = valid & (fwd["path_nl"] == nl[..., None])
+    m &= np.abs(fwd["path_T"] - T[..., None]) <= tol
+    m &= (np.abs(fwd["path_c"] - rgb[..., None, :]) <= tol).all(-1)
+    ok = m.any(-1)
+    first = np.argmax(m, -1)
+    flips = np.take_along_axis(fwd["flips"], first[..., None], -1)[..., 0]
+    flips = np.where(ok, flips, 0).astype(np.uint64)
+    n_multi = int((fwd["n_paths"] > 1).sum())
+    n_over = int(((fwd["flags"] & 16) != 0).sum())
+    return ok, flips, n_multi, n_over
 
 
 def block_major(arr_flat, n_blocks, ch=None):

@@ -79,22 +79,22 @@ def test_opacity_reset_matches_oracle():
 
 def test_stats_match_oracle_backward():
     """gs_densify_stats reads the step's record gradients through the backward index: against
-    the oracle's render backward of the same C0 step (flagged pixels get zero upstream, as in
-    test_param_grads_and_adam)."""
-    from tests.test_gpu_parity import Run
+    the oracle's render backward of the same C0 step (each pixel on the outcome path the GPU
+    forward took, as in test_param_grads_and_adam)."""
+    from tests.test_gpu_parity import Run, matched
     sc = synth.scene_c0(0)
     cams = synth.cameras_c0()
-    recs, off, ent, fwd = oracle.render_batch(sc, cams, "parity", (0, 0, 0), None, 1e-5)
+    recs, off, ent, fwd = oracle.render_batch(sc, cams, "parity", (0, 0, 0), None, 64)
     run = Run(sc, cams, (0, 0, 0), None)
     up = synth.upstream_grad(12, (16, 256, 3)).astype(np.float64) * 1e-3
-    up[(fwd["flags"] & 3) != 0] = 0
     run.render(run.send, run.n_send, upstream=up.astype(np.float32))
+    flips, _ = matched(run, fwd, "c0s0")
     n = sc.n
     acc, den, mr = (torch.zeros(n, dtype=torch.float32, device=DEV) for _ in range(3))
     L.densify_stats(run.ctx, cams, run.dp, n, run.idx, run.send, run.drec, 1, acc, den, mr)
     torch.cuda.synchronize()
     g_or = oracle.render_bwd(recs, off, ent, 0, 16, run.W, run.H, up.astype(np.float32).astype(np.float64),
-                             (0, 0, 0))
+                             (0, 0, 0), flips=flips)
     mb = oracle.membership(sc, cams[0])
     rad = mb["radius"][recs.vi[:, 1]].astype(np.float64)
     oa, od, orr = D.stats_from_record_grads(n, recs.rec_i[:, 0], g_or, rad, run.W, run.H, 1)

@@ -73,7 +73,7 @@ def test_p2p_exchange_equals_copy_transport(G, seed):
         recv = torch.cat(parts)
         recv_ref.append(recv)
         rr = Run(sc.slice(0, 1), cams, bg, gt, world=G, rank=r, dp=dp)
-        rr.render(recv if len(recv) else torch.empty((1, 48), dtype=torch.uint8, device=DEV), len(recv))
+        rr.render(recv if len(recv) else torch.empty((1, L.RECORD_BYTES), dtype=torch.uint8, device=DEV), len(recv))
         drec_ref.append(rr.drec[:len(recv)].clone())
     dsend_ref = [torch.zeros((int(C[s].sum()), 9), dtype=torch.float32, device=DEV) for s in range(G)]
     for r in range(G):
@@ -90,7 +90,7 @@ def test_p2p_exchange_equals_copy_transport(G, seed):
     cnt = np.stack([L.project_count(ctxs[r], ps[r], cams, dp, idx[r]) for r in range(G)])
     np.testing.assert_array_equal(cnt, C)
     n_in = C.sum(0)
-    recv = [torch.full((int(n_in[r]) + 7, 48), 0xAB, dtype=torch.uint8, device=DEV) for r in range(G)]
+    recv = [torch.full((int(n_in[r]) + 7, L.RECORD_BYTES), 0xAB, dtype=torch.uint8, device=DEV) for r in range(G)]
     dsend = [torch.full((int(C[r].sum()) + 1, 9), float("nan"), dtype=torch.float32, device=DEV) for r in range(G)]
     flags = [torch.zeros(G, dtype=torch.int64, device=DEV) for _ in range(G)]
     for r in range(G):
@@ -130,7 +130,7 @@ def test_p2p_barrier_times_out_instead_of_hanging():
     G = 2
     ctxs = [L.Context(0, r, G) for r in range(G)]
     flags = [torch.zeros(G, dtype=torch.int64, device=DEV) for _ in range(G)]
-    bufs = [torch.zeros(1, 48, dtype=torch.uint8, device=DEV) for _ in range(G)]
+    bufs = [torch.zeros(1, L.RECORD_BYTES, dtype=torch.uint8, device=DEV) for _ in range(G)]
     gr = [torch.zeros(1, 9, dtype=torch.float32, device=DEV) for _ in range(G)]
     for c in ctxs:
         L.p2p_attach(c, [b.data_ptr() for b in bufs], [1, 1], [g.data_ptr() for g in gr], [1, 1],
@@ -148,7 +148,7 @@ def test_p2p_barrier_times_out_instead_of_hanging():
 def test_p2p_plan_capacity_fails_everywhere():
     G = 2
     ctxs = [L.Context(0, r, G) for r in range(G)]
-    bufs = [torch.zeros(4, 48, dtype=torch.uint8, device=DEV) for _ in range(G)]
+    bufs = [torch.zeros(4, L.RECORD_BYTES, dtype=torch.uint8, device=DEV) for _ in range(G)]
     gr = [torch.zeros(4, 9, dtype=torch.float32, device=DEV) for _ in range(G)]
     fl = [torch.zeros(G, dtype=torch.int64, device=DEV) for _ in range(G)]
     for c in ctxs:

@@ -1,16 +1,19 @@
 """GPU parity at the paper's workload shapes (SURVEY §8(c) "Configs"): full-scene projection
 of Rubble-, garden- and MatrixCity-shaped scenes with one rank owning a 256-block window
 (a virtual rank of a 3-rank partition), compared with the oracle: exchange set and per-block
-lists bit-exact, pixels within 1e-4 on unflagged pixels, n_last exact, record gradients
-within the 1e-3 metric.  Plus sampled blocks of the full C2 bench configuration (16 views,
-4591x3436, 11.2M Gaussians) in the launch configuration bench.py times."""
+lists bit-exact; every pixel's n_last exact and colour / T within 1e-4 of one of the oracle's
+outcome paths (R16: both outcomes of a decision within the renderer's rounding of a
+threshold are valid); record gradients within the 1e-3 metric with the oracle following each
+pixel's path.  The fraction of pixels with more than one valid outcome is printed and bounded
+per scene shape (DESIGN.md §2 R16).  Plus sampled blocks of the full C2 bench configuration
+(16 views, 4591x3436, 11.2M Gaussians) in the launch configuration bench.py times."""
 import numpy as np
 import pytest
 import torch
 
 import oracle
 import synth
-from tests.gsutil import block_major, decode_records, grad_metric
+from tests.gsutil import block_major, decode_records, grad_metric, match_paths
 
 L = pytest.importorskip("paper_2406_18533_b200._lib")
 pytestmark = pytest.mark.gpu
@@ -35,7 +38,7 @@ def _window_case(sc, cam, lo_frac=0.45, nblk=256, seed=0):
         cnt = L.project(ctx, p, [cam], dp, None, 0, idx)
     except L.CapacityError as e:
         cnt = e.counts
-    send = torch.empty((int(cnt.sum()) + 1, 48), dtype=torch.uint8, device=DEV)
+    send = torch.empty((int(cnt.sum()) + 1, L.RECORD_BYTES), dtype=torch.uint8, device=DEV)
     cnt = L.project(ctx, p, [cam], dp, send, int(cnt.sum()), idx)
     off = np.concatenate([[0], np.cumsum(cnt)])
     recv = send[off[1]:off[2]].contiguous()
@@ -60,16 +63,13 @@ def _window_case(sc, cam, lo_frac=0.45, nblk=256, seed=0):
     # oracle over the same window
     recs = oracle.make_records(sc, [cam], "parity")
     o_off, o_ent = oracle.tile_lists(recs, lo, hi, Wt, Ht)
-    # flag margins for deep lists (hundreds to thousands of entries per pixel): 1e-4 relative
-    # on alpha (the kernel's exponent q = u^2 + w^2 carries ~1e-6..1e-5 relative error where
-    # u = l11 dx + l21 dy cancels), 1e-3 on T' (discontinuities)
-    fwd = oracle.render_fwd(recs, o_off, o_ent, lo, hi, W, H, (0, 0, 0), gt[None], 1, 1e-4, 1e-3)
+    fwd = oracle.render_fwd(recs, o_off, o_ent, lo, hi, W, H, (0, 0, 0), gt[None], 1, max_paths=64)
     return dict(ctx=ctx, dp=dp, recv=recv, n_recv=n_recv, range=rng_t, sorted=srt, npairs=npairs, T=T, nl=nl,
                 rgb=rgb, dpix=dpix, recs=recs, off=o_off, ent=o_ent, fwd=fwd, no=no, lo=lo, hi=hi, W=W, H=H,
                 Wt=Wt, Ht=Ht, cam=cam, sc=sc, cnt=cnt)
 
 
-def _check_window(c):
+def _check_window(c, max_multi):
     # exchange set of rank 1 == oracle O10 (bit-exact, ascending gid)
     mb = oracle.membership(c["sc"], c["cam"])
     mask = oracle.exchange_sets(mb["vis"], mb["rect"], 0, c["Wt"], c["Ht"], c["dp"])
@@ -83,41 +83,29 @@ def _check_window(c):
     np.testing.assert_array_equal(rng, c["off"])
     srt = c["sorted"][: c["npairs"]].cpu().numpy().view(np.uint32)
     np.testing.assert_array_equal(d["gid"][srt], c["recs"].rec_i[c["ent"], 0])
-    # pixels
+    # every pixel against the oracle's outcome paths
     fwd, no = c["fwd"], c["no"]
-    unflag = (fwd["flags"] & 3) == 0
-    inside = np.zeros_like(unflag)
-    for k in range(no):
-        beta = c["lo"] + k
-        tx, ty = beta % c["Wt"], beta // c["Wt"]
-        px = tx * 16 + np.arange(256) % 16
-        py = ty * 16 + np.arange(256) // 16
-        inside[k] = (px < c["W"]) & (py < c["H"])
-    ok = unflag & inside
-    # pixels within the flag margins of a threshold: a statistical fraction that grows with
-    # the evaluations per pixel and the thinness of the Gaussians (~1e-3 at hundreds of
-    # entries, 10-20 % in MatrixCity windows of thousands of large thin Gaussians); they are
-    # excluded, and a loose bound catches a renderer that drifts
-    nflag = int((inside & ~unflag).sum())
-    print("flagged pixels: %d of %d" % (nflag, int(inside.sum())))
-    assert nflag <= max(2, 0.25 * inside.sum()), nflag
-    np.testing.assert_array_equal(block_major(c["nl"], no)[ok], fwd["nlast"][ok])
-    assert np.abs(block_major(c["T"], no) - fwd["T"])[ok].max() <= 1e-4
-    assert np.abs(block_major(c["rgb"], no, 3) - fwd["c"])[ok].max() <= 1e-4
-    return ok
+    ok, flips, n_multi, n_over = match_paths(fwd, block_major(c["T"], no), block_major(c["nl"], no),
+                                             block_major(c["rgb"], no, 3))
+    npx = ok.size
+    print("pixels with more than one valid outcome: %d of %d (%.2e; bound %.0e), overflow %d" %
+          (n_multi, npx, n_multi / npx, max_multi, n_over))
+    assert n_over == 0
+    assert ok.all(), "pixels matching no outcome path: %d, e.g. %s" % ((~ok).sum(), np.argwhere(~ok)[:5].tolist())
+    assert n_multi <= max_multi * npx, n_multi
+    return flips
 
 
-def _check_bwd(c, ok):
+def _check_bwd(c, flips):
     ctx, dp, no = c["ctx"], c["dp"], c["no"]
     up = synth.upstream_grad(21, (no, 256, 3)).astype(np.float64) * 1e-6
-    up[~ok] = 0
     dpix = torch.from_numpy(np.ascontiguousarray(up.astype(np.float32).transpose(0, 2, 1)).reshape(-1)).to(DEV)
     drec = torch.empty((max(c["n_recv"], 1), 9), device=DEV)
     L.render_bwd(ctx, c["recv"], c["n_recv"], c["sorted"], c["range"], [c["cam"]], dp, (0, 0, 0), dpix, c["T"],
                  c["nl"], drec, None, 0, None)
     torch.cuda.synchronize()
     g_or = oracle.render_bwd(c["recs"], c["off"], c["ent"], c["lo"], c["hi"], c["W"], c["H"],
-                             up.astype(np.float32).astype(np.float64))
+                             up.astype(np.float32).astype(np.float64), flips=flips)
     d = decode_records(c["recv"][: c["n_recv"]])
     pos = {int(g): j for j, g in enumerate(c["recs"].rec_i[:, 0])}
     g_ref = g_or[[pos[int(g)] for g in d["gid"]]]
@@ -125,6 +113,11 @@ def _check_bwd(c, ok):
     for name, sl in [("mean", slice(0, 2)), ("conic", slice(2, 5)), ("opacity", slice(5, 6)), ("rgb", slice(6, 9))]:
         e_inf, e_2 = grad_metric(g_k[:, sl], g_ref[:, sl])
         assert e_inf <= 1e-3 and e_2 <= 1e-3, (name, e_inf, e_2)
+
+
+# bound on the fraction of pixels with more than one valid outcome, per scene shape (the
+# verdict's targets: Rubble / garden 1e-3, MatrixCity 1e-2)
+MAX_MULTI = {"rubble": 1e-3, "garden": 1e-3, "city_street": 1e-2, "city_aerial": 1e-2}
 
 
 @pytest.mark.parametrize("which", ["rubble", "garden", "city_street", "city_aerial"])
@@ -139,8 +132,8 @@ def test_window_parity(which):
         sc, cam = synth.scene_city(4_000_000), synth.cameras_city(128)[70]
     c = _window_case(sc, cam, lo_frac=0.5 if which != "city_street" else 0.45)
     assert c["n_recv"] > 0 and c["npairs"] > 0
-    ok = _check_window(c)
-    _check_bwd(c, ok)
+    flips = _check_window(c, MAX_MULTI[which])
+    _check_bwd(c, flips)
 
 
 def test_full_c2_sampled_blocks():
@@ -164,14 +157,28 @@ def test_full_c2_sampled_blocks():
         recs = oracle.make_records(sc, [cams[v]], "parity")
         for blk in rng.integers(0, pv, 6):
             off, ent = oracle.tile_lists(recs, int(blk), int(blk) + 1, Wt, Ht)
-            f = oracle.render_fwd(recs, off, ent, int(blk), int(blk) + 1, W, H, (0, 0, 0), gt[v][None], 16, 1e-5)
+            f = oracle.render_fwd(recs, off, ent, int(blk), int(blk) + 1, W, H, (0, 0, 0), gt[v][None], 16,
+                                  max_paths=64)
             lb = v * pv + int(blk)
-            T = tr.T.t[lb].cpu().numpy()
-            nl = tr.nl.t[lb].cpu().numpy()
+            T = tr.T.t[lb].cpu().numpy()[None]
+            nl = tr.nl.t[lb].cpu().numpy()[None]
+            # the trainer keeps no colour buffer: compare n_last and T on every pixel
+            P = f["flips"].shape[2]
+            valid = np.arange(P)[None, None, :] < f["n_paths"][..., None]
+            m = valid & (f["path_nl"] == nl[..., None]) & (np.abs(f["path_T"] - T[..., None]) <= 1e-4)
+            assert m.any(-1).all()
+            # dL/dpix: the sign of the nominal colour's residual wherever it is firm
             dpx = tr.dpix.t[lb].cpu().numpy().T
-            ok = (f["flags"][0] & 3) == 0
-            np.testing.assert_array_equal(nl[ok], f["nlast"][0][ok])
-            assert np.abs(T - f["T"][0])[ok].max() <= 1e-4
-            ok3 = ok & ((f["flags"][0] & 8) == 0)
-            np.testing.assert_allclose(dpx[ok3], f["dl_dc"][0][ok3], rtol=1e-6)
+            single = f["n_paths"][0] == 1
+            g = gt[v]
+            ty, tx = divmod(int(blk), Wt)
+            py = ty * 16 + np.arange(256) // 16
+            px = tx * 16 + np.arange(256) % 16
+            inside = (px < W) & (py < H)
+            gb = np.zeros((256, 3))
+            gb[inside] = g[py[inside], px[inside]] / 255.0
+            res = f["c"][0] - gb
+            firm = single[:, None] & inside[:, None] & (np.abs(res) > 1e-4)
+            np.testing.assert_allclose(dpx[firm], np.sign(res[firm]) / (3.0 * W * H * 16), rtol=1e-6)
+            assert np.all(np.isin(np.round(dpx * (3.0 * W * H * 16)), [-1, 0, 1]))  # every pixel: a valid sign
             assert tr.range.t[lb + 1].item() - tr.range.t[lb].item() == len(ent)
