@@ -40,6 +40,14 @@ constexpr int kNT = 64;     // threads per block CTA (two warps, one 8x16 half e
 constexpr int kFW = 64;     // forward: records staged per warp round
 constexpr int kBW = 64;     // backward: records staged per warp round
 constexpr int kUnroll = 4;  // forward entries per unrolled group (4 measured faster than 8 and 16 on C2)
+// resident-CTA floors (register caps) of the default kernels; compile-time so A/B builds can
+// vary them (python -m paper_2406_18533_b200.build extra defines), never selected at run time
+#ifndef GS_FWD_MINB
+#define GS_FWD_MINB 18
+#endif
+#ifndef GS_BWD_MINB
+#define GS_BWD_MINB 14
+#endif
 
 // Could any pixel centre of the box [bx0, bx0 + ex] x [by0, by0 + ey] see the record (mean
 // (mx, my), prescaled factor l11, l21, l22) with alpha >= 1/255?  Minimum of q(d) = |L'^T d|^2
@@ -231,7 +239,9 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_fwd(
   pixel_of(tid, x, y0);
   const int px = tx * 16 + x, py0 = ty * 16 + y0;
   const float hx0 = (float)(tx * 16 + 8 * wid), hy0 = (float)(ty * 16);
-  const float ex = 3.5f - (float)(lane & 7), ey0 = 7.5f - (float)y0;  // offsets from the half's centre
+  // offsets from the half's centre (exact); formed from px, py0 (which depend on the block index)
+  // so that the register allocator keeps them rather than recomputing them per entry
+  const float ex = (hx0 + 3.5f) - (float)px, ey0 = (hy0 + 7.5f) - (float)py0;
   const int beg = range[lb], end = range[lb + 1];
   float T[kPPT], C0[kPPT], C1[kPPT], C2[kPPT];
   int nl[kPPT], sp[kPPT];
@@ -471,7 +481,7 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_bwd(
   pixel_of(tid, x, y0);
   const int px = tx * 16 + x, py0 = ty * 16 + y0;
   const float hx0 = (float)(tx * 16 + 8 * wid), hy0 = (float)(ty * 16);
-  const float ex = 3.5f - (float)(lane & 7), ey0 = 7.5f - (float)y0;
+  const float ex = (hx0 + 3.5f) - (float)px, ey0 = (hy0 + 7.5f) - (float)py0;  // (see k_render_fwd)
   int nl[kPPT];
   float Tf[kPPT], T[kPPT], P[kPPT], g2[kPPT], bgd[kPPT];
   float2 g01[kPPT];  // (r, g) pairs for packed fp32x2 updates
@@ -628,7 +638,7 @@ extern "C" gs_status gs_render_fwd(gs_ctx* c, const void* recv_rec, const uint32
   // register caps (resident CTAs per SM): 16 with the stop positions tracked (statistics and
   // the WORK cost mode), 18 = 56 registers otherwise (C2 18.6 -> 18.0 ms against 16)
   auto kf = stats ? k_render_fwd<true, 16> : cost_mode == GS_COST_WORK ? k_render_fwd<false, 16>
-                                                                        : k_render_fwd<false, 18, false>;
+                                                                        : k_render_fwd<false, GS_FWD_MINB, false>;
   kf<<<(unsigned)n_owned, kNT, 0, (cudaStream_t)stream>>>(
       (const gs_rec*)recv_rec, sorted_idx, tile_range, geo, B_lo, bg[0], bg[1], bg[2], gt, norm, out_rgb,
       T_final, n_last, dL_dpix, loss_sum, tile_cost, cost_mode, (long long*)stats);
@@ -650,9 +660,10 @@ static gs_status render_bwd_launch(gs_ctx* c, const void* recv_rec, const uint32
   if (bg_h) for (int k = 0; k < 3; k++) bg[k] = bg_h[k];
   const bool black = bg[0] == 0.f && bg[1] == 0.f && bg[2] == 0.f;
   ++c->launches;
-  // register caps: 16 resident CTAs (64 registers) for the black-background kernel (C2 34.3 ->
-  // 33.8 ms against 14), 12 with the background term
-  auto kb = black ? (stats ? k_render_bwd<true, 16, false> : k_render_bwd<false, 16, false>)
+  // register caps: GS_BWD_MINB = 14 resident CTAs (72 registers) for the black-background kernel
+  // (C2 33.17 -> 32.55 ms against 16 with the fp64 reference staging; 12: 33.96 ms), 12 with the
+  // background term
+  auto kb = black ? (stats ? k_render_bwd<true, 16, false> : k_render_bwd<false, GS_BWD_MINB, false>)
                   : (stats ? k_render_bwd<true, 12, true> : k_render_bwd<false, 12, true>);
   kb<<<(unsigned)n_owned, kNT, 0, st>>>((const gs_rec*)recv_rec, sorted_idx, tile_range, geo, B_lo, bg[0], bg[1],
                                         bg[2], dL_dpix, T_final, n_last, tile_cost, cost_mode, (long long*)stats,
