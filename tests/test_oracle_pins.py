@@ -392,6 +392,107 @@ def test_p12_zero_upstream_and_occluded():
     assert np.all(g[2:] == 0) and np.any(g[:2] != 0)
 
 
+# ---------------------------------------------------------------- R6 the 0.99 cap (P12 cont.)
+def _cap_record(o, conic, mean=(8.0, 8.0), rgb=(0.3, 0.6, 0.9)):
+    rec_f = np.zeros((1, 10))
+    rec_f[0, 0:2] = mean
+    rec_f[0, 2] = 1.0
+    rec_f[0, 3:6] = conic
+    rec_f[0, 6] = o
+    rec_f[0, 7:10] = rgb
+    return oracle.Records(rec_f, np.zeros((1, 6), np.int64), None, None)
+
+
+@pytest.mark.parametrize("o", [0.9951, 0.999, 1.0])
+def test_r6_fully_capped_entry_has_zero_geometry_gradient(o):
+    """R6 (SURVEY #15): alpha = min(0.99, o G) is constant where o G > 0.99, so the true
+    derivative with respect to the mean, the conic and the opacity is exactly zero there.  A
+    wide Gaussian with o > 0.99 centred on the tile is capped at every pixel (o G >= 0.99 for
+    G >= 0.9951 / o): its mean / conic / opacity gradients must be exactly 0, its colour
+    gradient must not, and central differences of the image agree (they are 0 too)."""
+    recs = _cap_record(o, (2e-5, 0.0, 2e-5), mean=(7.5, 7.5))
+    off, ent = oracle.tile_lists(recs, 0, 1, 1, 1)
+    dx = np.arange(256) % 16 - 7.5
+    dy = np.arange(256) // 16 - 7.5
+    assert np.all(o * np.exp(-0.5 * 2e-5 * (dx * dx + dy * dy)) > 0.99 + 1e-6)  # every pixel capped
+    w = synth.upstream_grad(7, (1, 256, 3)).astype(np.float64)
+    g = oracle.render_bwd(recs, off, ent, 0, 1, 16, 16, w)
+    assert np.all(g[0, 0:6] == 0.0), g[0, :6]
+    np.testing.assert_allclose(g[0, 6:9], 0.99 * w[0].sum(0), rtol=1e-12)
+    base = oracle.render_fwd(recs, off, ent, 0, 1, 16, 16)
+    for col in (0, 1, 3, 4, 5, 6):
+        h = 1e-7 if col in (3, 4, 5) else 1e-4
+        for sg in (1, -1):
+            rf = recs.rec_f.copy()
+            rf[0, col] += sg * h
+            f = oracle.render_fwd(oracle.Records(rf, recs.rec_i, None, None), off, ent, 0, 1, 16, 16)
+            assert np.array_equal(f["c"], base["c"]), col  # the image does not move
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_r6_partly_capped_finite_difference(seed):
+    """Entries with o in (0.99, 1] centred on pixels: capped near the centre, uncapped on the
+    rim.  fp64 central differences of the image agree with the oracle's gradients, which take
+    the zero derivative on the capped pixels; back-propagating through the cap as if it were
+    absent (the 3DGS convention, SURVEY #15) would not (checked by comparing with a variant
+    of the same scene below the cap).  Probes within 1e-4 of the cap at any pixel are
+    skipped (the cap is a kink)."""
+    rng = np.random.default_rng(50 + seed)
+    n = 3
+    rec_f = np.zeros((n, 10))
+    rec_f[:, 0:2] = rng.integers(4, 12, (n, 2)) + rng.uniform(-0.2, 0.2, (n, 2))  # near pixel centres
+    rec_f[:, 2] = [1.0, 2.0, 3.0]
+    sig = rng.uniform(2.5, 4.0, n)
+    rho = rng.uniform(-0.3, 0.3, n)
+    cov = np.stack([sig ** 2, rho * sig * sig, (sig * rng.uniform(0.8, 1.2, n)) ** 2], 1)
+    det = cov[:, 0] * cov[:, 2] - cov[:, 1] ** 2
+    rec_f[:, 3], rec_f[:, 4], rec_f[:, 5] = cov[:, 2] / det, -cov[:, 1] / det, cov[:, 0] / det
+    rec_f[:, 6] = rng.uniform(0.995, 1.0, n)
+    rec_f[:, 7:10] = rng.uniform(0, 1, (n, 3))
+    recs = oracle.Records(rec_f, np.stack([np.arange(n)] + [np.zeros(n, np.int64)] * 5, 1), None, None)
+    off, ent = oracle.tile_lists(recs, 0, 1, 1, 1)
+    bg = (0.2, 0.5, 0.8)
+    w = synth.upstream_grad(20 + seed, (1, 256, 3)).astype(np.float64)
+    g = oracle.render_bwd(recs, off, ent, 0, 1, 16, 16, w, bg)
+
+    px = np.arange(256) % 16
+    py = np.arange(256) // 16
+
+    def raw_alpha(rf):
+        dx = rf[:, 0:1] - px
+        dy = rf[:, 1:2] - py
+        pw = -0.5 * (rf[:, 3:4] * dx * dx + rf[:, 5:6] * dy * dy) - rf[:, 4:5] * dx * dy
+        return rf[:, 6:7] * np.exp(pw)
+
+    ra = raw_alpha(rec_f)
+    assert np.any(ra > 0.99) and np.any((ra < 0.99) & (ra > 1 / 255))  # both regimes present
+    checked = 0
+    for j in range(n):
+        for k, col in enumerate([0, 1, 3, 4, 5, 6]):
+            h = 1e-6 * max(1.0, abs(rec_f[j, col]))
+            vals, ok = [], True
+            for sg in (1, -1):
+                rf = rec_f.copy()
+                rf[j, col] += sg * h
+                if np.any(np.abs(raw_alpha(rf) - 0.99) < 1e-4):
+                    ok = False
+                f = oracle.render_fwd(oracle.Records(rf, recs.rec_i, None, None), off, ent, 0, 1, 16, 16, bg)
+                vals.append(np.sum(f["c"] * w))
+            if not ok:
+                continue
+            fd = (vals[0] - vals[1]) / (2 * h)
+            gk = [0, 1, 2, 3, 4, 5][k]
+            assert abs(fd - g[j, gk]) <= 1e-5 * max(abs(fd), 1e-3) + 1e-7, (j, col, fd, g[j, gk])
+            checked += 1
+    assert checked >= 12
+    # the capped pixels contribute nothing to the opacity gradient: the same scene with the
+    # opacities scaled below the cap has a clearly different opacity gradient
+    rf2 = rec_f.copy()
+    rf2[:, 6] *= 0.9
+    g2 = oracle.render_bwd(oracle.Records(rf2, recs.rec_i, None, None), off, ent, 0, 1, 16, 16, w, bg)
+    assert np.any(np.abs(g2[:, 5] - g[:, 5]) > 1e-3 * np.abs(g2[:, 5]).max())
+
+
 # ---------------------------------------------------------------- P13 projection backward FD
 def _small_scene(seed, n=12):
     rng = np.random.default_rng(seed)
