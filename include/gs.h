@@ -221,7 +221,9 @@ gs_status gs_exchange_grads(gs_ctx* ctx, const float* dL_drec, const int64_t* re
  * With GS_ADAM_GRAD | GS_ADAM_APPLY and a non-NULL g, g is used as the gradient buffer: the
  * transformation backward writes it and an elementwise Adam pass applies it (the faster path
  * on B200); with g == NULL both happen in one fused kernel with the gradient in registers.
- * m, v, g use the same float4-plane layout as p (unused lanes ignored).                  */
+ * m, v, g use the same float4-plane layout as p (unused lanes ignored).  A non-NULL g must
+ * have g->n == p->n; g is required for GS_ADAM_WRITE_GRAD and for GS_ADAM_APPLY without
+ * GS_ADAM_GRAD (GS_EINVAL otherwise).                                                     */
 gs_status gs_adam_step(gs_ctx* ctx, gs_params* p, gs_params* m, gs_params* v, gs_params* g,
                        const gs_camera* cams_h, int n_views, const int64_t* dp_h,
                        const float* dL_dsend, const void* bwd_index, const gs_adam_hparams* hp,

@@ -369,7 +369,9 @@ extern "C" gs_status gs_adam_step(gs_ctx* c, gs_params* p, gs_params* m, gs_para
   GS_REQUIRE(c, flags & (GS_ADAM_GRAD | GS_ADAM_APPLY), "flags select nothing");
   const bool grad = flags & GS_ADAM_GRAD, apply = flags & GS_ADAM_APPLY, wgrad = flags & GS_ADAM_WRITE_GRAD;
   GS_REQUIRE(c, !apply || (m && v && m->n == p->n && v->n == p->n), "m/v missing or mis-sized");
-  GS_REQUIRE(c, (!wgrad && grad) || (g && g->n == p->n), "g missing or mis-sized");
+  GS_REQUIRE(c, !g || g->n == p->n, "g mis-sized (%lld rows for %lld Gaussians)", (long long)(g ? g->n : 0),
+             (long long)p->n);
+  GS_REQUIRE(c, g || (grad && !wgrad), "g required (apply-only or WRITE_GRAD)");
   GS_REQUIRE(c, hp->batch >= 1 && hp->step >= 1, "batch and step must be >= 1");
   cudaStream_t st = (cudaStream_t)stream;
   if (p->n == 0) return GS_OK;
@@ -409,53 +411,22 @@ extern "C" gs_status gs_adam_step(gs_ctx* c, gs_params* p, gs_params* m, gs_para
     // the parameter gradient, then an elementwise Adam pass streams p, m, v, g at full
     // occupancy; the fused kernel's register footprint caps its memory parallelism
     ++c->launches;
-    // A/B knob: GS_ADAM_SPLIT_MINB = minimum resident CTAs per SM of the gradient kernel
-    static int sminb = -1;
-    if (sminb < 0) {
-      const char* e = getenv("GS_ADAM_SPLIT_MINB");
-      sminb = e ? atoi(e) : 5;  // 5: C2 4.97 -> 4.83 ms vs 4 (126 registers; 1: 188 registers, 8 warps/SM: 6.7 ms)
-    }
-    if (sminb >= 6)
-      k_bwd_adam<true, false, 6><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base,
-                                                          L.ncta, dL_dsend, h);
-    else if (sminb >= 5)
-      k_bwd_adam<true, false, 5><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base,
-                                                          L.ncta, dL_dsend, h);
-    else if (sminb >= 4)
-      k_bwd_adam<true, false, 4><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base,
-                                                          L.ncta, dL_dsend, h);
-    else if (sminb >= 3)
-      k_bwd_adam<true, false, 3><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base,
-                                                          L.ncta, dL_dsend, h);
-    else if (sminb >= 2)
-      k_bwd_adam<true, false, 2><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base,
-                                                          L.ncta, dL_dsend, h);
-    else
-      k_bwd_adam<true, false, 1><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base,
-                                                          L.ncta, dL_dsend, h);
+    // 5 resident CTAs per SM: C2 4.97 -> 4.83 ms against 4 (126 registers; 1: 188 registers,
+    // 8 warps/SM: 6.7 ms; 6: 4.94 ms)
+    k_bwd_adam<true, false, 5><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base, L.ncta,
+                                                        dL_dsend, h);
     ++c->launches;
     k_adam_apply<<<dim3((unsigned)((p->n + 255) / 256), 15), 256, 0, st>>>(P, Mo, Vo, Go, p->n, h);
     GS_LAUNCH_CHECK(c, "bwd + adam_apply");
     return GS_OK;
   }
   ++c->launches;
-  if (wgrad && apply)
-    k_bwd_adam<true, true, 1><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base, L.ncta, dL_dsend, h);
-  else if (wgrad)
-    k_bwd_adam<true, false, 1><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base, L.ncta, dL_dsend, h);
-  else
-  {
-    // A/B knob: GS_ADAM_MINB = minimum resident CTAs per SM requested from ptxas (1 or 4)
-    static int minb = -1;
-    if (minb < 0) {
-      const char* e = getenv("GS_ADAM_MINB");
-      minb = e ? atoi(e) : 1;
-    }
-    if (minb >= 4)
-      k_bwd_adam<false, true, 4><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base, L.ncta, dL_dsend, h);
-    else
-      k_bwd_adam<false, true, 1><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base, L.ncta, dL_dsend, h);
-  }
+  if (!apply)  // parity mode: the parameter gradient only
+    k_bwd_adam<true, false, 5><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base, L.ncta,
+                                                        dL_dsend, h);
+  else  // no gradient buffer: backward and Adam fused in registers (tests/test_gpu_multiview.py)
+    k_bwd_adam<false, true, 1><<<grid, kBlock, 0, st>>>(P, Mo, Vo, Go, p->n, cams, G, nb, L.NW, maskw, base, L.ncta,
+                                                        dL_dsend, h);
   GS_LAUNCH_CHECK(c, "bwd_adam");
   return GS_OK;
 }
