@@ -232,6 +232,74 @@ def run_reference(args, cfg):
     return 0
 
 
+# ----------------------------------------------------------------------------- load-balance study
+
+def run_virtual(args, cfg):
+    """--virtual-ranks G: the E7 analogue (§3.2, §5.3) on one GPU.  The
+    config's batch is split over G virtual ranks' pixel ranges (engine.VirtualGrendel); each
+    rank's render fwd + bwd is timed with CUDA events; the ranks' max / mean time is the
+    imbalance.  Compared: uniform division points (no rebalancing) against Algorithm 1 on
+    MEASURED (SM cycles), WORK (evaluations) and PAPER_AVG (the rank's per-pixel average)
+    costs, each from the same initial scene for `--epochs` passes over the camera pool; the
+    first epoch fills the cost history ("after the first few" epochs) and is not
+    reported."""
+    import torch
+    import paper_2406_18533_b200._lib as L
+    from paper_2406_18533_b200.engine import DEFAULT_LR, VirtualGrendel
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    G = args.virtual_ranks
+    cams = make_cameras(cfg)
+    W, H = cams[0].width, cams[0].height
+    per_epoch = len(cams) // cfg["b"]
+    steps = per_epoch * args.epochs
+    sched = batches(cfg, steps + 1)
+    scene = make_scene(cfg, 0, cfg["n"])
+    if not args.no_morton:
+        from paper_2406_18533_b200.layout import reorder_scene
+        scene = reorder_scene(scene)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(cfg["seed"] + 200)
+    gt_pool = torch.randint(0, 256, (len(cams), H, W, 3), dtype=torch.uint8, device=dev, generator=gen)
+    gt_batch = torch.empty((cfg["b"], H, W, 3), dtype=torch.uint8, device=dev)
+    modes = [("uniform", L.COST_MEASURED, False), ("measured", L.COST_MEASURED, True),
+             ("work", L.COST_WORK, True), ("paper_avg", L.COST_PAPER_AVG, True)]
+    out = {}
+    for name, cm, reb in modes:
+        p = L.GaussianParams.from_arrays(scene.pos, scene.log_scale, scene.rot, scene.opac_logit, scene.sh, dev)
+        lr = tuple(args.study_lr_scale * x for x in DEFAULT_LR)
+        vg = VirtualGrendel(p, W, H, cfg["b"], len(cams), G, cost_mode=cm, rebalance=reb, device=dev, lr=lr)
+        ratios, per_rank = [], []
+        for k in range(steps):
+            for i, j in enumerate(sched[k]):
+                gt_batch[i].copy_(gt_pool[j])
+            t = vg.step([cams[i] for i in sched[k]], gt_batch, [cams[i] for i in sched[k + 1]])
+            if k >= per_epoch:
+                ratios.append(float(t.max() / t.mean()))
+                per_rank.append(t)
+        pr = np.mean(per_rank, 0)
+        out[name] = {"max_over_mean": round(float(np.mean(ratios)), 4),
+                     "max_over_mean_per_step": [round(x, 3) for x in ratios],
+                     "rank_ms_mean": [round(float(x), 3) for x in pr],
+                     "raster_ms_per_step_max_rank": round(float(np.mean([t.max() for t in per_rank])), 3),
+                     "final_dp": [int(x) for x in vg.dp]}
+        print("%-10s imbalance %.3f  max-rank %.2f ms  ranks %s" % (name, out[name]["max_over_mean"],
+              out[name]["raster_ms_per_step_max_rank"], out[name]["rank_ms_mean"]), file=sys.stderr, flush=True)
+        del vg, p
+        torch.cuda.empty_cache()
+    line = {"study": "load_balance", "metric": "imbalance = max / mean over virtual ranks of render fwd+bwd time",
+            "unit": "ratio", "higher_is_better": False, "n_gpus": 1, "virtual_ranks": G,
+            "config": {"workload": cfg["workload"], "batch": cfg["b"], "epochs": args.epochs,
+                       "lr_scale": args.study_lr_scale,
+                       "reported": "epochs 2..%d (%d steps)" % (args.epochs, steps - per_epoch)},
+            "data": "synthetic", "imbalance": out}
+    print(json.dumps(line), flush=True)
+    if args.json_out:
+        with open(args.json_out, "w") as f:
+            json.dump(line, f)
+    return 0
+
+
 # ----------------------------------------------------------------------------- libgs arm
 
 def main():
@@ -241,7 +309,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="libgs", choices=["libgs", "reference"])
-    ap.add_argument("--cost-mode", default="measured", choices=["measured", "work", "paper_avg"])
+    ap.add_argument("--cost-mode", default="paper_avg", choices=["measured", "work", "paper_avg"],
+                    help="A9 cost estimate (N > 1): paper_avg = the rank's measured render time per pixel (P:210, "
+                         "the best of the three in the --virtual-ranks study), measured = per-block SM cycles, "
+                         "work = per-block walked entries")
     ap.add_argument("--no-rebalance", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-morton", action="store_true", help="keep the generator's (random) Gaussian order")
@@ -256,11 +327,19 @@ def main():
                          "render-backward kernels over peer memory (CUDA IPC / NVLink)")
     ap.add_argument("--loss", default="l1", choices=["l1", "ssim"],
                     help="l1: the hot-path loss (R11); ssim: L1 + D-SSIM, lambda 0.2 (NEXT-1)")
+    ap.add_argument("--virtual-ranks", type=int, default=0,
+                    help="load-balance study on one GPU: the config's batch over this many virtual ranks, "
+                         "uniform DP vs Algorithm 1 on MEASURED / WORK / PAPER_AVG costs (an 'imbalance' line)")
+    ap.add_argument("--epochs", type=int, default=3, help="--virtual-ranks: passes over the camera pool")
+    ap.add_argument("--study-lr-scale", type=float, default=1.0,
+                    help="--virtual-ranks: learning rates x this (0: parameters frozen, costs repeat exactly)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.virtual_ranks:
+        return run_virtual(args, cfg)
 
     import torch
     import torch.distributed as dist
@@ -530,7 +609,8 @@ def main():
                            "l2_policy": "inputs larger than L2 (params+Adam state %.1f GB, GT %.2f GB/step)" % (
                                3 * 240 * n / 1e9, cfg["b"] * W * H * 3 / 1e9),
                            "loss": "l1" if args.loss == "l1" else "l1+dssim(0.2)",
-                           "cost_mode": args.cost_mode, "rebalance": not args.no_rebalance,
+                           "cost_mode": args.cost_mode if world > 1 else "n/a (one rank)",
+                           "rebalance": (not args.no_rebalance) if world > 1 else "n/a (one rank: DP = [0, B])",
                            "exchange": args.exchange if world > 1 else "none (one rank)",
                            "shard_layout": "random" if args.no_morton else "morton"},
                 "raster_ms_per_view": round(raster_ms_view, 3),

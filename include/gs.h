@@ -236,14 +236,25 @@ gs_status gs_adam_step(gs_ctx* ctx, gs_params* p, gs_params* m, gs_params* v, gs
  * 2. converts costs to estimates (MEASURED/WORK: the cost; PAPER_AVG: the rank's average
  *    per-pixel cost times the block's pixels) and stores them in
  *    history[image_id][Wt*Ht] (device int64, initialise to -1 = never rendered);
- * 3. builds ET for the next batch from the history, unseen images costing their pixel
- *    count, and runs Algorithm 1 in exact int64 (R8): CT = cumsum(ET),
+ * 3. builds ET for the next batch from the history, an unseen image's blocks at the batch's
+ *    per-pixel rate (R17), and runs Algorithm 1 in exact int64 (R8): CT = cumsum(ET),
  *    DP[g] = #{i : CT[i] G <= g CT[B-1]}, DP[0] = 0, DP[G] = B (uniform if all zero).
  * dp_next_h[G+1] is written on the host (host sync).                                     */
 gs_status gs_rebalance(gs_ctx* ctx, const int64_t* owned_tile_cost, const gs_camera* cams_h,
                        int n_views, const int64_t* dp_h, int64_t* history, int64_t n_images,
                        int cost_mode, const gs_camera* next_cams_h, int n_next,
                        int64_t* dp_next_h, void* stream);
+
+/* gs_rebalance_row -- the local part of gs_rebalance (steps 2-3) given the whole batch's
+ * cost row cost_row[B] (device int64, B = n_views Wt Ht, the blocks of every rank): no
+ * communication, so virtual contexts (world > 1 without a communicator) can run Algorithm 1
+ * and tests can drive it with any row.  Unseen images of the next batch are estimated at the
+ * batch's per-pixel rate sum(cost_row) / sum(in-image pixels) times the block's pixels
+ * (floor), in the cost mode's own units (R17), or their pixel count while every cost is 0.
+ * dp_next_h[G+1] on the host (host sync).                                               */
+gs_status gs_rebalance_row(gs_ctx* ctx, const int64_t* cost_row, const gs_camera* cams_h, int n_views,
+                           const int64_t* dp_h, int64_t* history, int64_t n_images, int cost_mode,
+                           const gs_camera* next_cams_h, int n_next, int64_t* dp_next_h, void* stream);
 
 /* Algorithm 1 alone, pure host function: DP_h[G+1] from ET_h[B].
  * GS_EINVAL if G < 1, B < 0, any ET < 0, or the int64 guard B*max(ET)*G < 2^63 fails.    */

@@ -276,6 +276,23 @@ def costs_to_et(mode, dp, cost, npix):
     return et
 
 
+def next_et(hist, npix, rate_num, rate_den):
+    """A9 step 3 (R17): ET of the next batch from history rows (-1: never rendered)."""
+    hist = np.ascontiguousarray(hist, np.int64)
+    npix = np.ascontiguousarray(npix, np.int64)
+    et = np.zeros_like(hist)
+    lib().orc_next_et(C.c_int64(hist.size), _p(hist), _p(npix), C.c_int64(int(rate_num)), C.c_int64(int(rate_den)),
+                      _p(et))
+    return et
+
+
+def block_npix(W, H):
+    """In-image pixels of each block of one W x H view (R18: partial edge blocks)."""
+    Wt, Ht = (W + 15) // 16, (H + 15) // 16
+    tx, ty = np.arange(Wt * Ht) % Wt, np.arange(Wt * Ht) // Wt
+    return (np.minimum(16, W - 16 * tx) * np.minimum(16, H - 16 * ty)).astype(np.int64)
+
+
 # ------------------------------------------------------------------ whole-step definition
 
 GROUP_SLICES = {"pos": slice(0, 3), "scale": slice(3, 6), "rot": slice(6, 10),

@@ -538,7 +538,6 @@ void orc_render_fwd(int64_t n_rec, const double* rec_f, const int64_t* offsets,
       for (int ch = 0; ch < 3; ch++) out_c[3 * o + ch] = C[ch];
       out_T[o] = T;
       out_nlast[o] = nlast;
-      work[kb] += counts[4 * o] + nlast;
       if (gt) {
         const uint8_t* g = gt + (((int64_t)v * H + py) * W + px) * 3;
         for (int ch = 0; ch < 3; ch++) {
@@ -589,6 +588,18 @@ void orc_render_fwd(int64_t n_rec, const double* rec_f, const int64_t* offsets,
         n_paths[o] = nq;
       }
       flags[o] = flag;
+    }
+    /* WORK cost (R17): the renderer walks a 16x16 block as two 8x16 halves, each until its
+     * last pixel is done -- forward the half's largest E_f, backward its largest n_last */
+    for (int h = 0; h < 2; h++) {
+      int64_t ef = 0, nl = 0;
+      for (int p = 0; p < 256; p++) {
+        if ((p % 16) / 8 != h) continue;
+        int64_t o = kb * 256 + p;
+        if (counts[4 * o] > ef) ef = counts[4 * o];
+        if (out_nlast[o] > nl) nl = out_nlast[o];
+      }
+      work[kb] += ef + nl;
     }
   }
   free(queue);
@@ -804,6 +815,24 @@ void orc_costs_to_et(int32_t mode, int64_t B, int32_t G, const int64_t* DP, cons
     for (int64_t i = DP[g]; i < DP[g + 1]; i++) { Cg += cost[i]; Ng += npix[i]; }
     for (int64_t i = DP[g]; i < DP[g + 1]; i++)
       et[i] = Ng > 0 ? (int64_t)((__int128)Cg * npix[i] / Ng) : 0;
+  }
+}
+
+/* A9 step 3 (R17; "uniform estimate" for images not seen yet): ET of the next
+ * batch's B_next blocks from their images' history rows (hist[k] >= 0: the estimate stored
+ * when that block was last rendered; -1: never rendered), an unseen block costing the rendered
+ * batch's per-pixel rate times its in-image pixels, floor(rate_num * npix / rate_den), with
+ * rate_num = the sum of the rendered batch's costs and rate_den its in-image pixels, or npix
+ * itself while rate_num == 0. */
+void orc_next_et(int64_t B_next, const int64_t* hist, const int64_t* npix, int64_t rate_num, int64_t rate_den,
+                 int64_t* et) {
+  for (int64_t k = 0; k < B_next; k++) {
+    if (hist[k] >= 0)
+      et[k] = hist[k];
+    else if (rate_num > 0 && rate_den > 0)
+      et[k] = (int64_t)((__int128)rate_num * npix[k] / rate_den);
+    else
+      et[k] = npix[k];
   }
 }
 

@@ -65,7 +65,8 @@ void orc_tile_lists(int64_t n_rec, const double* rec_f, const int64_t* rec_i, in
  *   flags[nb][256] (bit0: a skip decision alpha < 1/255 within the margin, bit1: a stop
  *                   decision T' < 1e-4 within the margin, bit2: power > 0 met, bit4: more
  *                   outcome paths than max_paths),
- *   counts[nb][256][4] = (E_f, E_fc, E_fs, E_stop), work[nb] = sum_px (E_f + n_last),
+ *   counts[nb][256][4] = (E_f, E_fc, E_fs, E_stop), work[nb] = the WORK cost (R17): over the
+ *   block's two 8x16 halves (px % 16 < 8, >= 8), the sum of max E_f + max n_last of each half,
  *   dl_dc[nb][256][3] = sign(C-GT)/(3 H W b_total) (only if gt), *loss += sum |C-GT|/(3HWb).
  * margins[4] = (alpha_eps, t_eps, cond_eps, alpha_abs), see gs_oracle.c orc_margins_t.
  * max_paths > 0: every outcome path of the flagged decisions, up to max_paths per pixel
@@ -108,6 +109,12 @@ int orc_division_points(const int64_t* ET, int64_t B, int32_t G, int64_t* DP);
  * cost itself; mode 2 PAPER_AVG: floor(C_g * npix_b / npix_g)).            */
 void orc_costs_to_et(int32_t mode, int64_t B, int32_t G, const int64_t* DP, const int64_t* cost,
                      const int64_t* npix, int64_t* et);
+
+/* A9 step 3 (R17): ET of the next batch from history rows (-1 = never rendered) and the
+ * rendered batch's per-pixel rate rate_num / rate_den (unseen: floor(rate_num npix / rate_den),
+ * or npix while rate_num == 0).                                                          */
+void orc_next_et(int64_t B_next, const int64_t* hist, const int64_t* npix, int64_t rate_num, int64_t rate_den,
+                 int64_t* et);
 
 /* NEXT-1 (reading R12): L = (1-lambda) L1 + lambda (1 - SSIM) of one
  * image, img/gt [H][W][3] in [0,1]; SSIM = mean over pixels and channels of the 11x11

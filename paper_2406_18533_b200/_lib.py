@@ -84,6 +84,8 @@ _sig = {
     "gs_rebalance": (C.c_int, [_vp, _vp, C.POINTER(Camera), C.c_int, _P64, _vp, _i64, C.c_int,
                                C.POINTER(Camera), C.c_int, _P64, _vp]),
     "gs_division_points": (C.c_int, [_P64, _i64, C.c_int, _P64]),
+    "gs_rebalance_row": (C.c_int, [_vp, _vp, C.POINTER(Camera), C.c_int, _P64, _vp, _i64, C.c_int,
+                                   C.POINTER(Camera), C.c_int, _P64, _vp]),
     "gs_exchange_plan": (C.c_int, [_P64, C.c_int, C.c_int, _P64, _P64]),
     "gs_halo_plan": (C.c_int, [_vp, C.POINTER(Camera), C.c_int, _P64, _P64, _i64, _P64]),
     "gs_halo_exchange": (C.c_int, [_vp, _vp, C.c_int, C.POINTER(Camera), C.c_int, _P64, _vp, _vp, _i64, _P64,
@@ -537,6 +539,18 @@ def rebalance(ctx, owned_tile_cost, cams, dp, history, n_images, cost_mode, next
     out, outp = _i64arr(np.zeros(ctx.world + 1))
     st = _lib.gs_rebalance(ctx.handle, _ptr(owned_tile_cost), ca, len(cams), dpp, _ptr(history), int(n_images),
                            int(cost_mode), na, len(next_cams), outp, _stream(stream))
+    ctx.check(st)
+    return out
+
+
+def rebalance_row(ctx, cost_row, cams, dp, history, n_images, cost_mode, next_cams, stream=None):
+    """A9's local part on the whole batch's cost row (no communication; virtual contexts).
+    Returns dp_next (numpy int64[G+1])."""
+    ca, na = cameras(cams), cameras(next_cams)
+    _, dpp = _i64arr(dp)
+    out, outp = _i64arr(np.zeros(ctx.world + 1))
+    st = _lib.gs_rebalance_row(ctx.handle, _ptr(cost_row), ca, len(cams), dpp, _ptr(history), int(n_images),
+                               int(cost_mode), na, len(next_cams), outp, _stream(stream))
     ctx.check(st)
     return out
 

@@ -177,12 +177,42 @@ __global__ void k_costs_to_history(const int64_t* row, int64_t B, gs_geom geo, g
   history[(int64_t)ids.id[v] * geo.per_view + loc] = et;
 }
 
-__global__ void k_next_et(const int64_t* history, int64_t Bn, gs_geom geo, gs_ids ids, int64_t* et) {
+// Per-pixel rate of the batch just rendered (R17): rate[0] = sum of its block estimates,
+// rate[1] = its in-image pixels (one CTA).
+__global__ void k_batch_rate(const int64_t* row, int64_t B, gs_geom geo, int64_t* rate) {
+  __shared__ long long s[2][256];
+  long long cs = 0, ns = 0;
+  for (long long i = threadIdx.x; i < B; i += blockDim.x) {
+    cs += row[i];
+    ns += block_npix(i % geo.per_view, geo);
+  }
+  s[0][threadIdx.x] = cs;
+  s[1][threadIdx.x] = ns;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      s[0][threadIdx.x] += s[0][threadIdx.x + o];
+      s[1][threadIdx.x] += s[1][threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    rate[0] = s[0][0];
+    rate[1] = s[1][0];
+  }
+}
+
+// ET of the next batch: the history, or for an image never rendered the batch's per-pixel
+// rate times the block's pixels, in the cost mode's own units (R17; "uniform":
+// equal cost per pixel); its pixel count when no cost was recorded yet (rate[0] == 0).
+__global__ void k_next_et(const int64_t* history, int64_t Bn, gs_geom geo, gs_ids ids, const int64_t* rate,
+                          int64_t* et) {
   int64_t beta = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (beta >= Bn) return;
   int64_t v = beta / geo.per_view, loc = beta % geo.per_view;
   int64_t h = history[(int64_t)ids.id[v] * geo.per_view + loc];
-  et[beta] = h >= 0 ? h : block_npix(loc, geo);  // unseen image: its pixel count
+  const int64_t npix = block_npix(loc, geo);
+  et[beta] = h >= 0 ? h : (rate[0] > 0 && rate[1] > 0 ? (int64_t)(((__int128)rate[0] * npix) / rate[1]) : npix);
 }
 
 __global__ void k_division_points(const int64_t* CT, int64_t B, int G, int64_t* dp) {
@@ -207,6 +237,8 @@ extern "C" gs_status gs_rebalance(gs_ctx* c, const int64_t* owned_tile_cost, con
                                   int cost_mode, const gs_camera* next_cams_h, int n_next,
                                   int64_t* dp_next_h, void* stream) {
   if (!c) return GS_EINVAL;
+  // every argument check before the collective, so no rank can fail it alone (the checks see
+  // the same arguments on every rank)
   gs_status s = gs_check_batch(c, cams_h, n_views, dp_h);
   if (s != GS_OK) return s;
   GS_REQUIRE(c, next_cams_h && n_next >= 1 && n_next <= GS_MAX_VIEWS && dp_next_h && history,
@@ -215,26 +247,16 @@ extern "C" gs_status gs_rebalance(gs_ctx* c, const int64_t* owned_tile_cost, con
   for (int v = 0; v < n_next; v++)
     GS_REQUIRE(c, next_cams_h[v].width == cams_h[0].width && next_cams_h[v].height == cams_h[0].height,
                "all images must share one size");
-  gs_ids ids, nids;
-  for (int v = 0; v < n_views; v++) {
+  for (int v = 0; v < n_views; v++)
     GS_REQUIRE(c, cams_h[v].image_id >= 0 && cams_h[v].image_id < n_images, "image_id out of range");
-    ids.id[v] = cams_h[v].image_id;
-  }
-  for (int v = 0; v < n_next; v++) {
-    GS_REQUIRE(c, next_cams_h[v].image_id >= 0 && next_cams_h[v].image_id < n_images,
-               "image_id out of range");
-    nids.id[v] = next_cams_h[v].image_id;
-  }
+  for (int v = 0; v < n_next; v++)
+    GS_REQUIRE(c, next_cams_h[v].image_id >= 0 && next_cams_h[v].image_id < n_images, "image_id out of range");
   cudaStream_t st = (cudaStream_t)stream;
   const int G = c->world, r = c->rank;
   gs_geom geo = gs_make_geom(&cams_h[0]);
-  gs_dp_arg dp = gs_make_dp(c, dp_h);
-  const int64_t B = geo.per_view * n_views, Bn = geo.per_view * n_next;
+  const int64_t B = geo.per_view * n_views;
   int64_t* row = (int64_t*)gs_slot_get(c, SLOT_ROW, B * sizeof(int64_t), st);
-  int64_t* et = (int64_t*)gs_slot_get(c, SLOT_ET, Bn * sizeof(int64_t), st);
-  int64_t* ct = (int64_t*)gs_slot_get(c, SLOT_CT, Bn * sizeof(int64_t), st);
-  int64_t* misc = (int64_t*)gs_slot_get(c, SLOT_MISC, (4 * GS_MAX_WORLD + 8) * sizeof(int64_t), st);
-  if (!row || !et || !ct || !misc) return gs_fail(c, GS_ECUDA, "scratch");
+  if (!row) return gs_fail(c, GS_ECUDA, "scratch");
   // 1. the whole cost row: own segment, then all-gather of the others' (allgatherv)
   int64_t cnt[GS_MAX_WORLD], off[GS_MAX_WORLD + 1];
   for (int g = 0; g < G; g++) {
@@ -258,23 +280,62 @@ extern "C" gs_status gs_rebalance(gs_ctx* c, const int64_t* owned_tile_cost, con
     s = p2p_exchange(c, (const char*)row, soff, scnt, (char*)row, off, rc, sizeof(int64_t), st);
     if (s != GS_OK) return s;
   }
-  // 2. estimates of the rendered blocks -> history
+  return gs_rebalance_row(c, row, cams_h, n_views, dp_h, history, n_images, cost_mode, next_cams_h, n_next,
+                          dp_next_h, stream);
+}
+
+extern "C" gs_status gs_rebalance_row(gs_ctx* c, const int64_t* cost_row, const gs_camera* cams_h, int n_views,
+                                      const int64_t* dp_h, int64_t* history, int64_t n_images, int cost_mode,
+                                      const gs_camera* next_cams_h, int n_next, int64_t* dp_next_h, void* stream) {
+  if (!c) return GS_EINVAL;
+  gs_status s = gs_check_batch(c, cams_h, n_views, dp_h);
+  if (s != GS_OK) return s;
+  GS_REQUIRE(c, next_cams_h && n_next >= 1 && n_next <= GS_MAX_VIEWS && dp_next_h && history,
+             "bad next batch / null argument");
+  GS_REQUIRE(c, cost_mode >= 0 && cost_mode <= 2, "cost_mode %d", cost_mode);
+  for (int v = 0; v < n_next; v++)
+    GS_REQUIRE(c, next_cams_h[v].width == cams_h[0].width && next_cams_h[v].height == cams_h[0].height,
+               "all images must share one size");
+  gs_ids ids, nids;
+  for (int v = 0; v < n_views; v++) {
+    GS_REQUIRE(c, cams_h[v].image_id >= 0 && cams_h[v].image_id < n_images, "image_id out of range");
+    ids.id[v] = cams_h[v].image_id;
+  }
+  for (int v = 0; v < n_next; v++) {
+    GS_REQUIRE(c, next_cams_h[v].image_id >= 0 && next_cams_h[v].image_id < n_images,
+               "image_id out of range");
+    nids.id[v] = next_cams_h[v].image_id;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int G = c->world;
+  gs_geom geo = gs_make_geom(&cams_h[0]);
+  gs_dp_arg dp = gs_make_dp(c, dp_h);
+  const int64_t B = geo.per_view * n_views, Bn = geo.per_view * n_next;
+  GS_REQUIRE(c, B == 0 || cost_row != nullptr, "null cost_row");
+  int64_t* et = (int64_t*)gs_slot_get(c, SLOT_ET, Bn * sizeof(int64_t), st);
+  int64_t* ct = (int64_t*)gs_slot_get(c, SLOT_CT, Bn * sizeof(int64_t), st);
+  int64_t* misc = (int64_t*)gs_slot_get(c, SLOT_MISC, (4 * GS_MAX_WORLD + 8) * sizeof(int64_t), st);
+  if (!et || !ct || !misc) return gs_fail(c, GS_ECUDA, "scratch");
+  int64_t* rate = misc + 2 * GS_MAX_WORLD;  // [2]
+  int64_t* ddp = misc + 2 * GS_MAX_WORLD + 2;
+  // 2. estimates of the rendered blocks -> history, and the batch's per-pixel rate
   if (cost_mode == GS_COST_PAPER_AVG) {
     ++c->launches;
-    k_rank_sums<<<G, 256, 0, st>>>(row, dp, geo, misc);
+    k_rank_sums<<<G, 256, 0, st>>>(cost_row, dp, geo, misc);
   }
   if (B > 0) {
     ++c->launches;
-    k_costs_to_history<<<(unsigned)((B + 255) / 256), 256, 0, st>>>(row, B, geo, ids, cost_mode, dp,
+    k_costs_to_history<<<(unsigned)((B + 255) / 256), 256, 0, st>>>(cost_row, B, geo, ids, cost_mode, dp,
                                                                      misc, history);
   }
+  ++c->launches;
+  k_batch_rate<<<1, 256, 0, st>>>(cost_row, B, geo, rate);
   // 3. ET of the next batch, Algorithm 1
   ++c->launches;
-  k_next_et<<<(unsigned)((Bn + 255) / 256), 256, 0, st>>>(history, Bn, geo, nids, et);
+  k_next_et<<<(unsigned)((Bn + 255) / 256), 256, 0, st>>>(history, Bn, geo, nids, rate, et);
   GS_LAUNCH_CHECK(c, "rebalance");
   s = gs_scan_i64(c, et, ct, Bn, 1, st);
   if (s != GS_OK) return s;
-  int64_t* ddp = misc + 2 * GS_MAX_WORLD + 2;
   ++c->launches;
   k_division_points<<<1, 64, 0, st>>>(ct, Bn, G, ddp);
   GS_LAUNCH_CHECK(c, "division_points");

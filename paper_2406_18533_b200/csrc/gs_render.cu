@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_fwd(
   }
   // evaluations: an in-image pixel evaluates every entry up to its stopping entry (or all)
   const int n = end - beg;
-  int ef = 0, nstop = 0;
+  int ef = 0, efmax = 0, nstop = 0;
   double lsum = 0.0;
 #pragma unroll
   for (int j = 0; j < kPPT; j++) {
@@ -303,7 +303,9 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_fwd(
     const int p = (y0 + kRS * j) * 16 + x;
     const int64_t o = lb * 256 + p;
     if (in) {
-      ef += sp[j] >= 0 ? sp[j] + 1 : n;
+      const int e = sp[j] >= 0 ? sp[j] + 1 : n;
+      ef += e;
+      efmax = max(efmax, e);
       nstop += sp[j] >= 0;
     }
     const float col[3] = {fmaf(T[j], bg0, C0[j]), fmaf(T[j], bg1, C1[j]), fmaf(T[j], bg2, C2[j])};
@@ -341,7 +343,9 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_fwd(
   }
   if (tile_cost) {
     if (cost_mode == GS_COST_WORK) {
-      long long w = block_sum<long long>(ef, s_red);
+      // R17: the entries each warp walks (its half's largest E_f), summed over the two warps
+      const int wmax = __reduce_max_sync(0xffffffffu, efmax);
+      const long long w = block_sum<long long>(lane == 0 ? wmax : 0, s_red);
       if (tid == 0) tile_cost[lb] += w;
     } else {
       __syncthreads();
@@ -594,7 +598,8 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_bwd(
   }
   if (tile_cost) {
     if (cost_mode == GS_COST_WORK) {
-      long long w = block_sum<long long>(nlsum, s_red);
+      // R17: the entries each warp walks back (its half's largest n_last), over the two warps
+      const long long w = block_sum<long long>(lane == 0 ? maxn : 0, s_red);
       if (tid == 0) tile_cost[lb] += w;
     } else {
       __syncthreads();

@@ -279,14 +279,21 @@ class GrendelTrainer:
         if collect_stats:
             self.stats.zero_()
             stats = self.stats
+        # PAPER_AVG ("the per-GPU average of measured time"): the rank's render time from
+        # CUDA events, spread over its pixels by gs_rebalance; the kernels' counters are unused
+        paper_avg = self.cost_mode == L.COST_PAPER_AVG
+        cost_t = None if paper_avg else self.cost.t
+        if paper_avg:
+            self._pa_ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            self._pa_ev[0].record(torch.cuda.current_stream() if st is None else st)
         rec("render_fwd", 0)
         if self.loss_kind == "l1":  # L1 fused into the forward's epilogue (O13)
             L.render_fwd(ctx, recv_t, self.sorted.t, self.range.t, cams, dp, self.bg, gt, self.b, None, self.T.t,
-                         self.nl.t, self.dpix.t, self.loss, self.cost.t, self.cost_mode, stats, st)
+                         self.nl.t, self.dpix.t, self.loss, cost_t, self.cost_mode, stats, st)
         else:
             self.rgb.ensure(no)
             L.render_fwd(ctx, recv_t, self.sorted.t, self.range.t, cams, dp, self.bg, None, self.b, self.rgb.t,
-                         self.T.t, self.nl.t, None, None, self.cost.t, self.cost_mode, stats, st)
+                         self.T.t, self.nl.t, None, None, cost_t, self.cost_mode, stats, st)
         rec("render_fwd", 1)
         if self.loss_kind == "ssim":  # NEXT-1: L1 + D-SSIM in two passes around halo exchanges
             rec("loss", 0)
@@ -302,11 +309,13 @@ class GrendelTrainer:
         rec("render_bwd", 0)
         if p2p:  # A5 + A6 fused: gradient sums reduced straight into the owners' buffers
             L.render_bwd_put(ctx, recv_t, n_recv, self.sorted.t, self.range.t, cams, dp, self.dpix.t, self.T.t,
-                             self.nl.t, self.cost.t, self.cost_mode, stats, st)
+                             self.nl.t, cost_t, self.cost_mode, stats, st)
         else:
             L.render_bwd(ctx, recv_t, n_recv, self.sorted.t, self.range.t, cams, dp, self.bg, self.dpix.t,
-                         self.T.t, self.nl.t, self.drec.t, self.cost.t, self.cost_mode, stats, st)
+                         self.T.t, self.nl.t, self.drec.t, cost_t, self.cost_mode, stats, st)
         rec("render_bwd", 1)
+        if paper_avg:
+            self._pa_ev[1].record(torch.cuda.current_stream() if st is None else st)
         # A6 reverse exchange
         rec("exchange_grads", 0)
         if p2p:
@@ -330,7 +339,14 @@ class GrendelTrainer:
         rec("adam", 1)
         # A9 rebalance for the next batch
         rec("rebalance", 0)
-        if self.do_rebalance and next_cams is not None:
+        # one rank owns every block (DP = [0, B]): there is nothing to balance
+        if self.do_rebalance and next_cams is not None and self.G > 1:
+            if paper_avg:  # the rank's measured render time (ns) into its first owned block
+                self._pa_ev[1].synchronize()
+                ns = int(self._pa_ev[0].elapsed_time(self._pa_ev[1]) * 1e6)
+                if no:
+                    self.cost.t[:no].zero_()
+                    self.cost.t[0] = ns
             self.dp = L.rebalance(ctx, self.cost.t, cams, dp, self.history, self.n_images, self.cost_mode,
                                   next_cams, st)
         rec("rebalance", 1)
@@ -358,3 +374,95 @@ def position_lr(step, lr_init=1.6e-4, lr_final=1.6e-6, max_steps=30000, extent=1
     """Host-side exponential position-lr schedule, log-linear interpolation."""
     t = min(max(step / max(max_steps, 1), 0.0), 1.0)
     return extent * math.exp(math.log(lr_init) * (1 - t) + math.log(lr_final) * t)
+
+
+class VirtualGrendel:
+    """G ranks' pixel partition simulated on one GPU (the load-balancing study, §3.2,
+    the paper's Fig. E7 analogue): every rank is a world-G context without a communicator.  One
+    owner context projects all Gaussians into G destination buckets (A1 + A2: rank r's receive
+    buffer is bucket r of the owner's send buffer), each virtual rank bins and renders its DP
+    range (A3-A5, timed separately with CUDA events), the record gradients land in the owner's
+    send order (A6: rank r's rows are a slice of dL/dsend), the owner runs A7 + A8, and A9 runs
+    Algorithm 1 on the whole batch's cost row (gs_rebalance_row; the row is the ranks' owned
+    segments side by side, what gs_rebalance's all-gather assembles).  Per step it returns each
+    rank's render fwd + bwd time: imbalance = max / mean over ranks."""
+
+    def __init__(self, params: L.GaussianParams, width: int, height: int, n_views: int, n_images: int, G: int,
+                 cost_mode=L.COST_MEASURED, rebalance=True, lr=DEFAULT_LR, device=None):
+        self.p, self.G, self.b = params, G, n_views
+        self.W, self.H = width, height
+        self.Wt, self.Ht = (width + 15) // 16, (height + 15) // 16
+        self.B = n_views * self.Wt * self.Ht
+        self.cost_mode, self.do_rebalance, self.lr = cost_mode, rebalance, tuple(lr)
+        dev = self.device = device or params.pos_op.device
+        self.owner = L.Context(dev.index or 0, 0, G)
+        self.ranks = [L.Context(dev.index or 0, r, G) for r in range(G)]
+        self.dp = uniform_dp(self.B, G)
+        self.m, self.v, self.g = params.zeros_like(), params.zeros_like(), params.zeros_like()
+        self.history = torch.full((n_images, self.Wt * self.Ht), -1, dtype=torch.int64, device=dev)
+        self.n_images = n_images
+        self.bwd_index = torch.empty(L.project_index_bytes(self.owner, params.n, n_views), dtype=torch.uint8,
+                                     device=dev)
+        self.send = _Buf(dev, torch.uint8, (L.RECORD_BYTES,))
+        self.dsend = _Buf(dev, torch.float32, (L.GRAD_FLOATS,))
+        self.sorted = _Buf(dev, torch.int32)
+        self.range = _Buf(dev, torch.int32, (), self.B + 1)
+        self.T = _Buf(dev, torch.float32, (256,), self.B)
+        self.nl = _Buf(dev, torch.int32, (256,), self.B)
+        self.dpix = _Buf(dev, torch.float32, (3, 256), self.B)
+        self.row = torch.zeros(self.B, dtype=torch.int64, device=dev)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
+        self.step_count = 0
+
+    def step(self, cams, gt, next_cams=None):
+        """One step; returns [G] render fwd + bwd milliseconds of each virtual rank."""
+        dp = self.dp
+        self.step_count += 1
+        while True:
+            try:
+                counts = L.project(self.owner, self.p, cams, dp, self.send.t, self.send.cap, self.bwd_index)
+                break
+            except L.CapacityError as e:
+                self.send.ensure(int(e.counts.sum()))
+        off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        self.dsend.ensure(int(off[-1]))
+        self.row.zero_()
+        self.loss.zero_()
+        ms = []
+        for r, ctx in enumerate(self.ranks):
+            n_recv = int(off[r + 1] - off[r])
+            no = int(dp[r + 1] - dp[r])
+            recv = self.send.t[off[r]:]
+            while True:
+                try:
+                    L.bin_sort(ctx, recv, n_recv, cams, dp, self.sorted.t, self.sorted.cap, self.range.t)
+                    break
+                except L.CapacityError as e:
+                    self.sorted.ensure(e.needed)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            # PAPER_AVG (P:210): the rank's measured render time, spread by gs_rebalance_row over
+            # its pixels; the kernels' per-block counters are not used
+            cost = None if self.cost_mode == L.COST_PAPER_AVG else (self.row[dp[r]:] if no else self.row)
+            e0.record()
+            L.render_fwd(ctx, recv, self.sorted.t, self.range.t, cams, dp, (0, 0, 0), gt, self.b, None, self.T.t,
+                         self.nl.t, self.dpix.t, self.loss, cost, self.cost_mode, None)
+            L.render_bwd(ctx, recv, n_recv, self.sorted.t, self.range.t, cams, dp, (0, 0, 0), self.dpix.t,
+                         self.T.t, self.nl.t, self.dsend.t[off[r]:], cost, self.cost_mode, None)
+            e1.record()
+            ms.append((e0, e1))
+        ms_r = None
+        if self.cost_mode == L.COST_PAPER_AVG:
+            torch.cuda.synchronize()
+            ms_r = np.array([a.elapsed_time(b) for a, b in ms])
+            for r in range(self.G):
+                if dp[r + 1] > dp[r]:
+                    self.row[int(dp[r])] = int(ms_r[r] * 1e6)  # ns
+        if any(self.lr):
+            hp = L.adam_hparams(self.lr, self.b, self.step_count)
+            L.adam_step(self.owner, self.p, self.m, self.v, self.g, cams, dp, self.dsend.t, self.bwd_index, hp,
+                        L.ADAM_GRAD | L.ADAM_APPLY)
+        if self.do_rebalance and next_cams is not None:
+            self.dp = L.rebalance_row(self.owner, self.row, cams, dp, self.history, self.n_images, self.cost_mode,
+                                      next_cams)
+        torch.cuda.synchronize()
+        return ms_r if ms_r is not None else np.array([a.elapsed_time(b) for a, b in ms])

@@ -181,12 +181,17 @@ def test_render_fwd(case):
     if n_multi == 0:
         assert abs(loss_path - fwd["loss"]) <= 1e-12
     assert abs(run.loss.item() - loss_path) <= 1e-5 * abs(loss_path) + 1e-9
-    # work counters of the matched paths: E_f totals and per-block WORK cost (fwd E_f + bwd n_last)
+    # work counters of the matched paths: E_f totals, and the per-block WORK cost (R17): over
+    # the block's two 8x16 halves, the half's largest E_f (forward) + largest n_last (backward)
     cnt = np.take_along_axis(fwd["path_counts"], first[..., None, None], 2)[:, :, 0]
     st = run.stats.cpu().numpy()
     assert st[0] == cnt[..., 0].sum() and st[1] == cnt[..., 1].sum() and st[3] == cnt[..., 3].sum()
     nl = np.take_along_axis(fwd["path_nl"], first[..., None], 2)[..., 0]
-    np.testing.assert_array_equal(run.cost.cpu().numpy(), cnt[..., 0].sum(1) + nl.sum(1))
+    half = (np.arange(256) % 16) // 8
+    work = sum(cnt[:, half == h, 0].max(1) + nl[:, half == h].max(1) for h in (0, 1))
+    np.testing.assert_array_equal(run.cost.cpu().numpy(), work)
+    if n_multi == 0:
+        np.testing.assert_array_equal(fwd["work"], work)
 
 
 # ---------------------------------------------------------------- A5 backward
@@ -305,35 +310,3 @@ def test_virtual_partition_equals_whole(G):
         lo, hi = dp[r], dp[r + 1]
         np.testing.assert_array_equal(block_major(rr.rgb, rr.no, 3), rgb_whole[lo:hi])
         np.testing.assert_array_equal(block_major(rr.nl, rr.no), nl_whole[lo:hi])
-
-
-# ---------------------------------------------------------------- A9
-def test_division_points_host_and_device():
-    rng = np.random.default_rng(0)
-    for _ in range(500):
-        B, G = int(rng.integers(1, 300)), int(rng.integers(1, 17))
-        et = rng.integers(0, 1000, B) * (rng.random(B) < 0.7)
-        np.testing.assert_array_equal(L.division_points(et, G), oracle.division_points(et, G))
-
-
-@pytest.mark.parametrize("mode", [L.COST_WORK, L.COST_PAPER_AVG])
-def test_rebalance_device(mode):
-    sc = synth.scene_c0(0)
-    cams = synth.cameras_c0()
-    run = Run(sc, cams, (0, 0, 0), None, cost_mode=L.COST_WORK)
-    run.render(run.send, run.n_send)
-    hist = torch.full((4, 16), -1, dtype=torch.int64, device=DEV)
-    # G=1: DP is trivially [0, B]; the history must hold the estimates of image 0
-    dpn = L.rebalance(run.ctx, run.cost, cams, run.dp, hist, 4, mode, cams)
-    assert list(dpn) == [0, 16]
-    cost = run.cost.cpu().numpy()
-    npix = np.full(16, 256)
-    et = oracle.costs_to_et(mode, run.dp, cost, npix)
-    np.testing.assert_array_equal(hist[0].cpu().numpy(), et)
-    assert (hist[1:] == -1).all()
-
-
-def test_rebalance_virtual_world_needs_comm():
-    ctx = L.Context(0, 0, 2)
-    with pytest.raises(L.GSError):
-        L.exchange(ctx, None, [0, 0], None, 0)
