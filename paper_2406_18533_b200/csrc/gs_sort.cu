@@ -25,12 +25,15 @@ using namespace gsd;
 
 namespace {
 
-constexpr int kRadixThreads = 256;
+#ifndef GS_RADIX_THREADS
+#define GS_RADIX_THREADS 256
+#endif
+constexpr int kRadixThreads = GS_RADIX_THREADS;  // 256 (4096-element tiles): 512 (8192) measured slower
 #ifndef GS_RADIX_ITEMS
 #define GS_RADIX_ITEMS 16
 #endif
 constexpr int kRadixItems = GS_RADIX_ITEMS;  // elements per thread (A/B builds may vary it)
-constexpr int kRadixTile = kRadixThreads * kRadixItems;  // 4096 elements per CTA
+constexpr int kRadixTile = kRadixThreads * kRadixItems;  // elements per CTA
 constexpr int kRadixWarps = kRadixThreads / 32;
 constexpr int kRadixPerWarp = kRadixTile / kRadixWarps;   // 512 consecutive elements per warp
 constexpr int kEmitThreads = 256;
@@ -307,16 +310,18 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const uint32_t* __
 // segmented layout; kLast (kSeg only): values go to sorted_idx at their compact position
 // (kcum of the segment + position in it), the sentinel's are dropped; keys to kout (all).
 template <bool kSeg, bool kLast>
-__global__ void __launch_bounds__(kRadixThreads, 5) k_radix_scatter(
+__global__ void __launch_bounds__(kRadixThreads, 5 * 256 / kRadixThreads) k_radix_scatter(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
     uint32_t* __restrict__ vout, int64_t n, int shift, int bits, int64_t ntiles, seg_arg g,
     const unsigned long long* __restrict__ off, int64_t vcap) {
   const int bins = 1 << bits;
   __shared__ int s_wh[kRadixWarps][257];
-  __shared__ int s_toff[256];
+  __shared__ int s_toff[kRadixThreads];
   __shared__ int s_wsum[kRadixWarps];
   __shared__ long long s_gbase[256];
-  __shared__ uint32_t s_k[kRadixTile], s_v[kRadixTile];
+  extern __shared__ uint32_t s_kv[];  // dynamic: the tile's keys, then its values
+  uint32_t* const s_k = s_kv;
+  uint32_t* const s_v = s_kv + kRadixTile;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t mask = (uint32_t)(bins - 1);
   const int64_t base = (int64_t)blockIdx.x * kRadixTile;
@@ -426,6 +431,22 @@ __global__ void k_seg_ranges(const uint32_t* __restrict__ keys, seg_arg g, int64
   }
 }
 
+constexpr int kScatterSmem = 2 * kRadixTile * (int)sizeof(uint32_t);
+// the scatter kernels' dynamic shared memory above the 48 KB default (once per process)
+bool scatter_smem_ready() {
+  static const bool ok = [] {
+    bool r = true;
+    r &= cudaFuncSetAttribute(k_radix_scatter<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kScatterSmem) == cudaSuccess;
+    r &= cudaFuncSetAttribute(k_radix_scatter<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kScatterSmem) == cudaSuccess;
+    r &= cudaFuncSetAttribute(k_radix_scatter<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kScatterSmem) == cudaSuccess;
+    return r;
+  }();
+  return ok;
+}
+
 // One stable LSD pass over n (key, value) elements on `bits` digit bits at `shift` (record
 // passes: digit-major histogram over tiles).  Scratch: SLOT_RADIX_HIST.
 gs_status radix_pass(gs_ctx* c, const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout, int64_t n,
@@ -441,7 +462,7 @@ gs_status radix_pass(gs_ctx* c, const uint32_t* kin, const uint32_t* vin, uint32
   gs_status s = gs_scan_i64(c, (const int64_t*)hist, (int64_t*)hist, (int64_t)bins * ntiles, 0, st);
   if (s != GS_OK) return s;
   ++c->launches;
-  k_radix_scatter<false, false><<<(unsigned)ntiles, kRadixThreads, 0, st>>>(kin, vin, kout, vout, n, shift, bits,
+  k_radix_scatter<false, false><<<(unsigned)ntiles, kRadixThreads, kScatterSmem, st>>>(kin, vin, kout, vout, n, shift, bits,
                                                                             ntiles, g, hist, 0);
   GS_LAUNCH_CHECK(c, "radix pass");
   return GS_OK;
@@ -471,6 +492,7 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
     return GS_OK;
   }
   GS_REQUIRE(c, recv_rec != nullptr, "null recv_rec");
+  if (!scatter_smem_ready()) return gs_fail(c, GS_ECUDA, "radix scatter shared-memory attribute");
   const gs_rec* rec = (const gs_rec*)recv_rec;
   const int64_t pv = geo.per_view;
   seg_arg g;
@@ -576,10 +598,10 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
     if (s != GS_OK) return s;
     ++c->launches;
     if (p == passes - 1)
-      k_radix_scatter<true, true><<<(unsigned)ntl, kRadixThreads, 0, st>>>(kin, vin, kout, sorted_idx, n_pad, shift,
+      k_radix_scatter<true, true><<<(unsigned)ntl, kRadixThreads, kScatterSmem, st>>>(kin, vin, kout, sorted_idx, n_pad, shift,
                                                                           bits, ntl, g, hist, pair_cap);
     else
-      k_radix_scatter<true, false><<<(unsigned)ntl, kRadixThreads, 0, st>>>(kin, vin, kout, vout, n_pad, shift, bits,
+      k_radix_scatter<true, false><<<(unsigned)ntl, kRadixThreads, kScatterSmem, st>>>(kin, vin, kout, vout, n_pad, shift, bits,
                                                                            ntl, g, hist, 0);
     GS_LAUNCH_CHECK(c, "bin_sort pass");
     std::swap(kin, kout);
