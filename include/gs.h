@@ -140,7 +140,12 @@ size_t gs_project_index_bytes(const gs_ctx* ctx, int64_t n, int n_views);
  * per-destination record counts (host sync).  If the total exceeds send_cap, returns
  * GS_ECAPACITY with the counts written and send_rec untouched.  bwd_index must hold
  * gs_project_index_bytes(ctx, p->n, n_views) bytes; it is read back by gs_adam_step.
- * Invisible Gaussians (behind near plane 0.01, det <= 0, empty rectangle) produce nothing. */
+ * Invisible Gaussians (behind near plane 0.01, det <= 0, empty rectangle) produce nothing.
+ * A non-finite position, opacity logit, log-scale or rotation returns GS_ENONFINITE
+ * with the lowest offending gid in gs_last_error, before any record is written; a non-finite
+ * SH coefficient of a Gaussian visible in some view is found while its colour is evaluated and
+ * reported the same way by the next gs_project / gs_project_count of the context (the check
+ * rides on the count read-back: no extra sync).  gs_check_finite checks every parameter.   */
 gs_status gs_project(gs_ctx* ctx, const gs_params* p, const gs_camera* cams_h, int n_views,
                      const int64_t* dp_h, void* send_rec, int64_t send_cap,
                      int64_t* send_counts_h, void* bwd_index, void* stream);

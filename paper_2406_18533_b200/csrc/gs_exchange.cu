@@ -608,7 +608,7 @@ extern "C" gs_status gs_redistribute(gs_ctx* c, const gs_params* p, const gs_par
   GS_REQUIRE(c, recv_buf == nullptr || (send_buf != nullptr || p->n == 0) && send_cap >= p->n,
              "send buffer must hold the shard");
   // shard sizes -> N and this rank's global base (every rank's gid ranges are contiguous)
-  int64_t* dbuf = (int64_t*)gs_slot_get(c, SLOT_COUNT_GATHER, (G + G * G + 2) * sizeof(int64_t), st);
+  int64_t* dbuf = (int64_t*)gs_slot_get(c, SLOT_COUNT_GATHER, (G + 1) * (G + 2) * sizeof(int64_t), st);
   if (!dbuf) return gs_fail(c, GS_ECUDA, "scratch");
   c->pinned[0] = p->n;
   GS_CUDA(c, cudaMemcpyAsync(dbuf, c->pinned, sizeof(int64_t), cudaMemcpyHostToDevice, st));
@@ -621,36 +621,58 @@ extern "C" gs_status gs_redistribute(gs_ctx* c, const gs_params* p, const gs_par
     N += c->pinned[64 + g];
   }
   *n_total_h = N;
-  GS_REQUIRE(c, p->gid_base == base, "gid_base must be the rank's offset in the global order");
   const int64_t n_out = range_lo(r + 1, N, G) - range_lo(r, N, G);
   *n_out_h = n_out;
   if (recv_buf == nullptr) return GS_OK;  // size query (every rank passes NULL together)
-  // recv_cap below the queried size is a contract violation (the other ranks continue)
-  GS_REQUIRE(c, recv_cap >= n_out, "receive capacity %lld < %lld (query the size first)", (long long)recv_cap,
-             (long long)n_out);
-  GS_REQUIRE(c, p_out && m_out && v_out && p_out->n == n_out && m_out->n == n_out && v_out->n == n_out,
-             "output planes must be laid out for the queried size");
-  int64_t scnt[GS_MAX_WORLD];
-  gs_status s = gs_redistribute_pack(c, p, m, v, N, seed, send_buf, send_cap, scnt, stream);
-  if (s != GS_OK) return s;
-  // count matrix (all-gather of every rank's send counts)
+  // The rank's global base comes from the gathered sizes (the caller's gid_base may be stale
+  // after a densify changed the shard sizes).  Local checks that can differ between ranks are
+  // agreed on before the next collective: every rank all-gathers its send counts plus a
+  // status word, and all return the same error if any rank failed (no rank is left waiting).
+  gs_params pb = *p;
+  pb.gid_base = base;
+  int64_t scnt[GS_MAX_WORLD] = {0};
+  int64_t st_local = 0;
+  std::string why;
+  if (recv_cap < n_out) {
+    st_local = GS_EINVAL;
+    why = "receive capacity below the queried size";
+  } else if (!(p_out && m_out && v_out && p_out->n == n_out && m_out->n == n_out && v_out->n == n_out)) {
+    st_local = GS_EINVAL;
+    why = "output planes not laid out for the queried size";
+  } else {
+    gs_status s = gs_redistribute_pack(c, &pb, m, v, N, seed, send_buf, send_cap, scnt, stream);
+    if (s != GS_OK) {
+      st_local = s;
+      why = c->err;
+      for (int g = 0; g < G; g++) scnt[g] = 0;
+    }
+  }
+  // count matrix + status (all-gather of every rank's G send counts and its status)
   for (int g = 0; g < G; g++) c->pinned[g] = scnt[g];
-  GS_CUDA(c, cudaMemcpyAsync(dbuf, c->pinned, G * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  GS_NCCL(c, ncclAllGather(dbuf, dbuf + G, G, ncclInt64, c->comm, st));
-  GS_CUDA(c, cudaMemcpyAsync(c->pinned + 64, dbuf + G, G * G * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  c->pinned[G] = st_local;
+  GS_CUDA(c, cudaMemcpyAsync(dbuf, c->pinned, (G + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  GS_NCCL(c, ncclAllGather(dbuf, dbuf + G + 1, G + 1, ncclInt64, c->comm, st));
+  GS_CUDA(c, cudaMemcpyAsync(c->pinned + 64, dbuf + G + 1, G * (G + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                             st));
   GS_CUDA(c, cudaStreamSynchronize(st));
+  for (int g = 0; g < G; g++) {
+    const int64_t sg = c->pinned[64 + g * (G + 1) + G];
+    if (sg != 0)
+      return gs_fail(c, (gs_status)sg, "redistribution failed on rank %d%s%s", g, g == r ? ": " : "",
+                     g == r ? why.c_str() : "");
+  }
   int64_t soff[GS_MAX_WORLD], roff[GS_MAX_WORLD], rcnt[GS_MAX_WORLD];
   int64_t so = 0, ro = 0;
   for (int g = 0; g < G; g++) {
     soff[g] = so;
     so += scnt[g];
-    rcnt[g] = c->pinned[64 + g * G + r];
+    rcnt[g] = c->pinned[64 + g * (G + 1) + r];
     roff[g] = ro;
     ro += rcnt[g];
   }
   if (ro != n_out) return gs_fail(c, GS_EINVAL, "redistribution counts inconsistent (%lld != %lld)", (long long)ro,
                                   (long long)n_out);
-  s = p2p_exchange(c, (const char*)send_buf, soff, scnt, (char*)recv_buf, roff, rcnt, kRedistFloats * sizeof(float),
+  gs_status s = p2p_exchange(c, (const char*)send_buf, soff, scnt, (char*)recv_buf, roff, rcnt, kRedistFloats * sizeof(float),
                    st);
   if (s != GS_OK) return s;
   p_out->gid_base = m_out->gid_base = v_out->gid_base = range_lo(r, N, G);

@@ -42,6 +42,7 @@ enum {
   SLOT_HALO_IDX,      // halo exchange: owned-block indices to pack
   SLOT_DENSIFY,       // densify keep flags [4][n]
   SLOT_DENSIFY_OFF,   // densify output positions
+  SLOT_NONFINITE,     // gs_project: lowest gid with a non-finite parameter (atomicMin word)
   SLOT_N
 };
 

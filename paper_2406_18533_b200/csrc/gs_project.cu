@@ -28,7 +28,8 @@ struct gs_outs {
 __global__ void __launch_bounds__(kBlock) k_project_count(
     const float4* __restrict__ pos_op, const float4* __restrict__ log_scale,
     const float4* __restrict__ rot, int64_t n, gs_cams_arg cams, gs_geom geo, gs_dp_arg dp,
-    int nb, int NW, uint32_t* __restrict__ maskw, int64_t* __restrict__ cta_cnt, int64_t ncta) {
+    int nb, int NW, uint32_t* __restrict__ maskw, int64_t* __restrict__ cta_cnt, int64_t ncta, int64_t gid_base,
+    unsigned long long* __restrict__ bad) {
   __shared__ int s_c[kMaxBuckets];
   for (int k = threadIdx.x; k < nb; k += kBlock) s_c[k] = 0;
   __syncthreads();
@@ -38,7 +39,12 @@ __global__ void __launch_bounds__(kBlock) k_project_count(
   for (int w = 0; w < kMaxWords; w++) m[w] = 0;
   if (i < n) {
     float4 X = pos_op[i];
-    gs_cov3 cv = cov3_of(log_scale[i], rot[i]);
+    const float4 ls = log_scale[i], q = rot[i];
+    // a non-finite parameter is an error naming the Gaussian (lowest gid wins)
+    if (!(isfinite(X.x) && isfinite(X.y) && isfinite(X.z) && isfinite(X.w) && isfinite(ls.x) && isfinite(ls.y) &&
+          isfinite(ls.z) && isfinite(q.x) && isfinite(q.y) && isfinite(q.z) && isfinite(q.w)))
+      atomicMin(bad, (unsigned long long)(gid_base + i));
+    gs_cov3 cv = cov3_of(ls, q);
     for (int v = 0; v < cams.n; v++) {
       gs_memb mb = membership(cv, X.x, X.y, X.z, cams.c[v], geo.Wt, geo.Ht);
       if (!mb.vis) continue;
@@ -66,7 +72,7 @@ __global__ void __launch_bounds__(kBlock) k_project_write(
     const float4* __restrict__ pos_op, const float4* __restrict__ log_scale,
     const float4* __restrict__ rot, const float4* __restrict__ sh, int64_t n, int64_t gid_base,
     gs_cams_arg cams, gs_geom geo, int G, int nb, int NW, const uint32_t* __restrict__ maskw,
-    const int64_t* __restrict__ base, int64_t ncta, gs_outs outs) {
+    const int64_t* __restrict__ base, int64_t ncta, gs_outs outs, unsigned long long* __restrict__ bad) {
   __shared__ int s_cnt[kWarps * kMaxBuckets];
   const int b = cams.n;
   int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
@@ -121,15 +127,19 @@ __global__ void __launch_bounds__(kBlock) k_project_write(
       sh_basis(dx * inv, dy * inv, dz * inv, Y);
       float col[3];
       col[0] = col[1] = col[2] = 0.5f;
+      bool shf = true;
 #pragma unroll
       for (int k = 0; k < 12; k++) {  // SH planes read only for visible (i, v)
         const float4 s4 = sh[(int64_t)k * n + i];
+        shf = shf && isfinite(s4.x) && isfinite(s4.y) && isfinite(s4.z) && isfinite(s4.w);
         const float e[4] = {s4.x, s4.y, s4.z, s4.w};
 #pragma unroll
         for (int j = 0; j < 4; j++) col[(4 * k + j) % 3] = fmaf(Y[(4 * k + j) / 3], e[j], col[(4 * k + j) % 3]);
       }
 #pragma unroll
       for (int ch = 0; ch < 3; ch++) col[ch] = fmaxf(col[ch], 0.0f);
+      // SH coefficients are read here only (visible Gaussians): reported by the next call's sync
+      if (!shf) atomicMin(bad, (unsigned long long)(gid_base + i));
       unsigned meta = (unsigned)((gid_base + i) * 32 + v);
       rec.a = make_float4(mb.mx, mb.my, mb.depth, mb.r);
       rec.b = make_float4(lh[0], lh[1], lh[2], opac);
@@ -151,6 +161,14 @@ __global__ void __launch_bounds__(kBlock) k_project_write(
 }
 
 }  // namespace
+
+// The context's non-finite word (lowest offending gid, ~0 = none), initialised on first use.
+static unsigned long long* nonfinite_word(gs_ctx* c, cudaStream_t st) {
+  const bool fresh = c->slot[SLOT_NONFINITE].ptr == nullptr;
+  unsigned long long* w = (unsigned long long*)gs_slot_get(c, SLOT_NONFINITE, sizeof(unsigned long long), st);
+  if (w && fresh && cudaMemsetAsync(w, 0xff, sizeof(unsigned long long), st) != cudaSuccess) return nullptr;
+  return w;
+}
 
 extern "C" size_t gs_project_index_bytes(const gs_ctx* c, int64_t n, int n_views) {
   if (!c || n < 0 || n_views < 1) return 0;
@@ -178,10 +196,12 @@ static gs_status project_count_phase(gs_ctx* c, const gs_params* p, const gs_cam
   gs_geom geo = gs_make_geom(&cams_h[0]);
   gs_dp_arg dp = gs_make_dp(c, dp_h);
   GS_CUDA(c, cudaMemsetAsync(base + (int64_t)nb * L.ncta, 0, sizeof(int64_t), st));
+  unsigned long long* bad = nonfinite_word(c, st);
+  if (!bad) return gs_fail(c, GS_ECUDA, "scratch");
   ++c->launches;
   k_project_count<<<(unsigned)L.ncta, kBlock, 0, st>>>(
       (const float4*)p->pos_op, (const float4*)p->log_scale, (const float4*)p->rot, p->n, cams, geo,
-      dp, nb, L.NW, maskw, base, L.ncta);
+      dp, nb, L.NW, maskw, base, L.ncta, p->gid_base, bad);
   GS_LAUNCH_CHECK(c, "project_count");
   s = gs_scan_i64(c, base, base, (int64_t)nb * L.ncta + 1, 0, st);
   if (s != GS_OK) return s;
@@ -190,7 +210,13 @@ static gs_status project_count_phase(gs_ctx* c, const gs_params* p, const gs_cam
   ++c->launches;
   k_gather_totals<<<1, 64, 0, st>>>(base, L.ncta, b, G, tot);
   GS_CUDA(c, cudaMemcpyAsync(c->pinned, tot, (G + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(c, cudaMemcpyAsync(c->pinned + GS_MAX_WORLD + 1, bad, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GS_CUDA(c, cudaStreamSynchronize(st));
+  const unsigned long long badv = (unsigned long long)c->pinned[GS_MAX_WORLD + 1];
+  if (badv != ~0ull) {  // this call's position / scale / rotation / opacity, or an earlier call's SH
+    GS_CUDA(c, cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
+    return gs_fail(c, GS_ENONFINITE, "non-finite parameter at gid %lld", (long long)badv);
+  }
   for (int d = 0; d < G; d++) send_counts_h[d] = c->pinned[d + 1] - c->pinned[d];
   *total_h = c->pinned[G];
   if (*total_h >= (1ll << 31))
@@ -210,7 +236,8 @@ static gs_status project_write_phase(gs_ctx* c, const gs_params* p, const gs_cam
   ++c->launches;
   k_project_write<<<(unsigned)L.ncta, kBlock, 0, st>>>(
       (const float4*)p->pos_op, (const float4*)p->log_scale, (const float4*)p->rot,
-      (const float4*)p->sh, p->n, p->gid_base, cams, geo, G, nb, L.NW, maskw, base, L.ncta, outs);
+      (const float4*)p->sh, p->n, p->gid_base, cams, geo, G, nb, L.NW, maskw, base, L.ncta, outs,
+      nonfinite_word(c, st));
   GS_LAUNCH_CHECK(c, "project_write");
   return GS_OK;
 }

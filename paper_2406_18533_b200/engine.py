@@ -148,6 +148,14 @@ class GrendelTrainer:
         if noise is None:
             noise = torch.randn((n, 2, 3), dtype=torch.float32, device=self.device, generator=generator)
         p2, m2, v2, counts = L.densify(self.ctx, self.p, self.m, self.v, *self.dstats, noise, cfg, events=events)
+        if self.G > 1:
+            # the shards changed size: the rank's global base is the exclusive prefix of the new
+            # sizes (contiguous gid ranges), agreed through torch.distributed
+            import torch.distributed as dist
+            sizes = [None] * self.G
+            dist.all_gather_object(sizes, int(p2.n))
+            base = int(sum(sizes[: self.rank]))
+            p2.gid_base = m2.gid_base = v2.gid_base = base
         self._replace_shard(p2, m2, v2)
         return counts
 

@@ -310,3 +310,30 @@ def test_virtual_partition_equals_whole(G):
         lo, hi = dp[r], dp[r + 1]
         np.testing.assert_array_equal(block_major(rr.rgb, rr.no, 3), rgb_whole[lo:hi])
         np.testing.assert_array_equal(block_major(rr.nl, rr.no), nl_whole[lo:hi])
+
+
+# ---------------------------------------------------------------- S:149 non-finite parameters
+def test_project_reports_non_finite_parameters():
+    """gs_project fails with GS_ENONFINITE naming the lowest offending gid for a non-finite
+    position / opacity / scale / rotation in the same call, and for a non-finite SH coefficient
+    of a visible Gaussian in the next call; clean parameters pass again afterwards."""
+    sc = synth.scene_c0(0)
+    cams = synth.cameras_c0()
+    mb = oracle.membership(sc, cams[0])
+    vis = np.nonzero(mb["vis"])[0]
+    for field, gid in (("rot", 417), ("pos", 33), ("log_scale", 902), ("opac_logit", 5)):
+        bad = synth.Scene(sc.pos.copy(), sc.log_scale.copy(), sc.rot.copy(), sc.opac_logit.copy(), sc.sh.copy())
+        getattr(bad, field)[gid] = np.nan if field != "opac_logit" else np.inf
+        if field != "opac_logit":
+            getattr(bad, field)[gid + 3] = np.inf
+        with pytest.raises(L.GSError) as ei:
+            Run(bad, cams)
+        assert ei.value.status == L.GS_ENONFINITE and ("gid %d" % gid) in str(ei.value), str(ei.value)
+    bad = synth.Scene(sc.pos.copy(), sc.log_scale.copy(), sc.rot.copy(), sc.opac_logit.copy(), sc.sh.copy())
+    g = int(vis[10])
+    bad.sh[g, 7, 1] = np.nan
+    run = Run(bad, cams)  # the SH are read while the records are written
+    with pytest.raises(L.GSError) as ei:
+        L.project(run.ctx, run.p, cams, run.dp, run.send, run.n_send, run.idx)
+    assert ei.value.status == L.GS_ENONFINITE and ("gid %d" % g) in str(ei.value)
+    Run(sc, cams)  # a clean shard passes
