@@ -476,6 +476,38 @@ def main():
             counts[kname] += tr.last[kname] / args.breakdown_steps
     stats = stats / args.breakdown_steps
 
+    # ---------------- N > 1: exchange volumes, NVLink rates and raster imbalance
+    multi = None
+    if world > 1:
+        sc_, rc_ = np.asarray(tr.last["send_counts"]), np.asarray(tr.last["recv_counts"])
+        vec = torch.tensor([calls.get("exchange", 0.0), calls.get("exchange_grads", 0.0),
+                            calls.get("render_fwd", 0.0) + calls.get("render_bwd", 0.0),
+                            float(sc_.sum() - sc_[rank]), float(rc_.sum() - rc_[rank]), float(sc_.sum())],
+                           dtype=torch.float64, device=dev)
+        allv = [torch.zeros_like(vec) for _ in range(world)]
+        dist.all_gather(allv, vec)
+        a = torch.stack(allv).cpu().numpy()  # [rank][fwd_ms, rev_ms, raster_ms, sent, recvd, all sent]
+        rb, gb = L.RECORD_BYTES, 4 * L.GRAD_FLOATS
+
+        def rate(nbytes, ms):
+            return [round(float(x) / (float(t) / 1e3) / 1e9, 2) if t > 0 else None for x, t in zip(nbytes, ms)]
+
+        multi = {
+            "forward_exchange": {"bytes_sent_remote": [int(x * rb) for x in a[:, 3]],
+                                 "bytes_recv_remote": [int(x * rb) for x in a[:, 4]],
+                                 "ms": [round(float(x), 4) for x in a[:, 0]],
+                                 "GBps_sent_per_rank": rate(a[:, 3] * rb, a[:, 0]),
+                                 "GBps_max_over_ranks": max([x for x in rate(a[:, 3] * rb, a[:, 0]) if x] or [0])},
+            "reverse_exchange": {"bytes_sent_remote": [int(x * gb) for x in a[:, 4]],
+                                 "ms": [round(float(x), 4) for x in a[:, 1]],
+                                 "GBps_sent_per_rank": rate(a[:, 4] * gb, a[:, 1]),
+                                 "GBps_max_over_ranks": max([x for x in rate(a[:, 4] * gb, a[:, 1]) if x] or [0])},
+            "records_vs_dense_bound": round(float(a[:, 5].sum()) / (world * n * cfg["b"]), 5),
+            "raster_ms_per_rank": [round(float(x), 3) for x in a[:, 2]],
+            "raster_imbalance_max_over_mean": round(float(a[:, 2].max() / max(a[:, 2].mean(), 1e-9)), 4),
+            "note": "per-call CUDA-event times of the breakdown steps on each rank's stream; bytes = records "
+                    "(or 9-float gradients) exchanged with other ranks; dense bound = G x N records per view"}
+
     # ---------------- e2e: host (pinned) ground truth in, loss out, through the same API
     e2e = None
     if not args.no_e2e:
@@ -626,6 +658,8 @@ def main():
                 "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "setup_s": round(setup_s, 1)}
         if dens is not None:
             line["densify"] = dens
+        if multi is not None:
+            line["multi_gpu"] = multi
         s = json.dumps(line)
         print(s, flush=True)
         if args.json_out:

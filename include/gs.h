@@ -424,7 +424,7 @@ gs_status gs_p2p_offsets(const int64_t* counts_h, int G, int rank, int64_t* recv
                          int64_t* send_off_h, int64_t* owner_off_h);
 
 /* gs_sym_alloc -- (re)allocates the context's symmetric buffer `which` (0: receive records,
- * 1: dL/dsend floats, 2: barrier flags, zeroed) of at least `bytes`, returns its device
+ * 1: dL/dsend floats, 2: barrier flags, zeroed, 3: count matrix, 4: cost row) of at least `bytes`, returns its device
  * pointer and its 64-byte CUDA IPC handle (for the peers' gs_ipc_open).  Owned by the
  * context (freed by gs_destroy).  Growing invalidates the peers' mappings: re-exchange and
  * re-attach.                                                                               */
@@ -474,6 +474,36 @@ gs_status gs_p2p_barrier(gs_ctx* ctx, void* stream);
 /* gs_p2p_status -- GS_ECUDA if a barrier of this context timed out since the last call (and
  * clears it), else GS_OK.  Host sync on `stream`.                                         */
 gs_status gs_p2p_status(gs_ctx* ctx, void* stream);
+
+/* Sync-free variant of the forward half (no host round trip between counting and writing):
+ *   gs_project_put_dev -> gs_p2p_counts -> gs_p2p_barrier -> gs_bin_sort / gs_render_fwd ->
+ *   gs_render_bwd_put -> gs_p2p_put_costs -> gs_p2p_barrier -> gs_adam_step ->
+ *   gs_rebalance_row (on the attached own cost row, identical on every rank).
+ * The count matrix is exchanged on the devices (row stores + barrier), the record offsets are
+ * computed from it inside the writing kernel, and the host reads the matrix (for the sizes
+ * the downstream calls take) asynchronously while the records are being written.           */
+/* gs_p2p_attach_counts -- the G ranks' count-matrix buffers (G x G int64 each, symmetric
+ * buffer 3) and cost-row buffers (row_cap int64 each, symmetric buffer 4; row_cap = 0: none),
+ * as device pointers valid in this process.                                                 */
+gs_status gs_p2p_attach_counts(gs_ctx* ctx, void* const* cmat_h, void* const* row_h, int64_t row_cap);
+/* gs_project_put_dev -- gs_project_count + the count exchange + gs_project_put without a host
+ * sync: counts this rank's records per destination into bwd_index, stores the row into every
+ * rank's count matrix, device barrier, then writes the records to their destinations'
+ * receive buffers at offsets taken from the device matrix and zeroes the own dL/dsend rows.
+ * Nothing is written if any destination's receive capacity is too small (gs_p2p_counts then
+ * returns GS_ECAPACITY on every rank: grow, re-attach and call again).  Peers may read the
+ * records only after the next gs_p2p_barrier.                                              */
+gs_status gs_project_put_dev(gs_ctx* ctx, const gs_params* p, const gs_camera* cams_h, int n_views,
+                             const int64_t* dp_h, void* bwd_index, void* stream);
+/* gs_p2p_counts -- waits for the matrix read-back of the last gs_project_put_dev (host waits
+ * on an event, not on the stream), copies it to counts_h[G x G] and sets the plan
+ * (gs_p2p_plan: *n_recv_h, GS_ECAPACITY).  GS_ENONFINITE (lowest gid) if that projection saw
+ * a non-finite parameter.                                                                   */
+gs_status gs_p2p_counts(gs_ctx* ctx, int64_t* counts_h, int64_t* n_recv_h);
+/* gs_p2p_put_costs -- this rank's owned cost row (dp_h[rank+1] - dp_h[rank] int64) into every
+ * rank's attached cost row at [dp_h[rank], ...); complete on every rank after the next
+ * gs_p2p_barrier.  GS_EINVAL if dp_h[G] exceeds the row capacity.                           */
+gs_status gs_p2p_put_costs(gs_ctx* ctx, const int64_t* owned_cost, const int64_t* dp_h, void* stream);
 
 /* --------------------------------------------------------------------------- self-check */
 /* gs_selftest_ex2 -- the maximum relative error of the renderer's exp2 (ex2.approx.ftz.f32,

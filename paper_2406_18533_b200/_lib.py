@@ -121,6 +121,10 @@ _sig = {
                                     _vp, C.c_int, _vp, _vp]),
     "gs_p2p_barrier": (C.c_int, [_vp, _vp]),
     "gs_p2p_status": (C.c_int, [_vp, _vp]),
+    "gs_p2p_attach_counts": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp), _i64]),
+    "gs_project_put_dev": (C.c_int, [_vp, C.POINTER(Params), C.POINTER(Camera), C.c_int, _P64, _vp, _vp]),
+    "gs_p2p_counts": (C.c_int, [_vp, _P64, _P64]),
+    "gs_p2p_put_costs": (C.c_int, [_vp, _vp, _P64, _vp]),
     "gs_selftest_ex2": (C.c_int, [_vp, C.c_float, C.c_float, C.POINTER(C.c_double), _vp]),
 }
 for _name, (_res, _args) in _sig.items():
@@ -171,6 +175,7 @@ class Context:
         self._h = C.c_void_p()
         st = _lib.gs_create(C.byref(self._h), device, rank, world, nccl_id)
         self.device, self.rank, self.world = device, rank, world
+        self.has_comm = world > 1 and nccl_id is not None  # NCCL communicator (collective calls)
         if st != GS_OK:
             msg = self.last_error()
             _lib.gs_destroy(self._h)
@@ -576,7 +581,7 @@ def exchange_plan(counts, G, rank):
 
 
 # ------------------------------------------------------------------ NEXT-3 peer-memory exchange
-SYM_RECV, SYM_DSEND, SYM_FLAGS = 0, 1, 2
+SYM_RECV, SYM_DSEND, SYM_FLAGS, SYM_COUNTS, SYM_ROW = 0, 1, 2, 3, 4
 
 
 def p2p_offsets(counts, G, rank):
@@ -669,6 +674,46 @@ def p2p_barrier(ctx, stream=None):
 
 def p2p_status(ctx, stream=None):
     ctx.check(_lib.gs_p2p_status(ctx.handle, _stream(stream)))
+
+
+def p2p_attach_counts(ctx, cmat_ptrs, row_ptrs, row_cap):
+    """The G ranks' count-matrix buffers and cost-row buffers (row_cap int64 each; 0: none)."""
+    G = ctx.world
+    arr = lambda ps: (C.c_void_p * G)(*[C.c_void_p(int(q)) for q in ps])  # noqa: E731
+    ctx.check(_lib.gs_p2p_attach_counts(ctx.handle, arr(cmat_ptrs), arr(row_ptrs) if row_cap else None,
+                                        int(row_cap)))
+
+
+def project_put_dev(ctx, params, cams, dp, bwd_index, stream=None):
+    """A1 + A2 fused without a host sync: counts, device-side count exchange, records into the
+    destinations' receive buffers (offsets from the device matrix).  Follow with p2p_counts."""
+    ca = cameras(cams)
+    _, dpp = _i64arr(dp)
+    ps = params.struct()
+    ctx.check(_lib.gs_project_put_dev(ctx.handle, C.byref(ps), ca, len(cams), dpp, _ptr(bwd_index),
+                                      _stream(stream)))
+
+
+def p2p_counts(ctx):
+    """The count matrix of the last project_put_dev (event wait) and the plan it sets:
+    (counts numpy int64 [G, G], n_recv).  CapacityError on every rank together."""
+    G = ctx.world
+    cm = np.zeros(G * G, np.int64)
+    nr = C.c_int64(0)
+    st = _lib.gs_p2p_counts(ctx.handle, cm.ctypes.data_as(_P64), C.byref(nr))
+    if st == GS_ECAPACITY:
+        e = CapacityError(st, ctx.last_error())
+        e.needed = int(nr.value)
+        e.counts = cm.reshape(G, G)
+        raise e
+    ctx.check(st)
+    return cm.reshape(G, G), int(nr.value)
+
+
+def p2p_put_costs(ctx, owned_cost, dp, stream=None):
+    """This rank's owned cost segment into every rank's attached cost row."""
+    _, dpp = _i64arr(dp)
+    ctx.check(_lib.gs_p2p_put_costs(ctx.handle, _ptr(owned_cost), dpp, _stream(stream)))
 
 
 def selftest_ex2(ctx, lo, hi, stream=None):

@@ -117,6 +117,7 @@ void gs_destroy(gs_ctx* c) {
   cudaSetDevice(c->device);
   for (int s = 0; s < SLOT_N; s++)
     if (c->slot[s].ptr) cudaFree(c->slot[s].ptr);
+  if (c->p2p.counts_ev) cudaEventDestroy(c->p2p.counts_ev);
   if (c->pinned) cudaFreeHost(c->pinned);
   for (void* q : c->p2p.opened) cudaIpcCloseMemHandle(q);
   if (c->p2p.err) cudaFree(c->p2p.err);

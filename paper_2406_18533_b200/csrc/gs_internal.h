@@ -49,8 +49,13 @@ enum {
 // NEXT-3 peer-memory exchange state (gs_p2p.cu): symmetric buffers this context allocated,
 // peers' buffers opened from IPC handles, the attached per-rank pointers and the current plan.
 struct gs_p2p_state {
-  void* sym[3] = {nullptr, nullptr, nullptr};  // own symmetric buffers: records, dL/dsend, flags
-  size_t sym_bytes[3] = {0, 0, 0};
+  // own symmetric buffers: records, dL/dsend, flags, count matrices, cost rows
+  void* sym[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  size_t sym_bytes[5] = {0, 0, 0, 0, 0};
+  int64_t* cmat[32] = {};                      // per rank: G x G count matrix (device counts)
+  int64_t* row[32] = {};                       // per rank: the batch's cost row
+  int64_t row_cap = 0;                         // cost-row capacity (blocks)
+  cudaEvent_t counts_ev = nullptr;             // the own matrix is in pinned[kCountsPinned..]
   std::vector<void*> opened;                   // cudaIpcOpenMemHandle'd peer buffers
   bool attached = false, planned = false;
   void* recv[32] = {};                         // per rank: receive buffer (gs_rec)
@@ -74,6 +79,13 @@ struct gs_ctx {
   ncclComm_t comm = nullptr;
 #endif
 };
+
+// pinned[kCountsPinned ..] holds the NEXT-3 count matrix read back asynchronously, then the
+// non-finite word of the sync-free projection (gs_project_put_dev)
+constexpr int kCountsPinned = 4096;
+// NEXT-3 device-side count exchange (gs_p2p.cu): this rank's per-destination prefix tot_dev
+// (G + 1 device int64) into every rank's matrix, barrier, async copy of the own matrix
+gs_status gs_p2p_counts_exchange(gs_ctx* c, const int64_t* tot_dev, cudaStream_t st);
 
 gs_status gs_fail(gs_ctx* c, gs_status s, const char* fmt, ...);
 void* gs_slot_get(gs_ctx* c, int slot, size_t bytes, cudaStream_t st);

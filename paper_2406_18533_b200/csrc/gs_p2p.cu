@@ -3,6 +3,7 @@
 // projection's record write (gs_project_put, gs_project.cu) and the reverse exchange into the
 // render backward's gradient reduction (gs_render_bwd_put, gs_render.cu); this file holds the
 // plan arithmetic, the symmetric buffers, IPC mapping and the device-side barrier.
+#include <algorithm>
 #include <cstring>
 
 #include "gs_device.cuh"
@@ -70,7 +71,7 @@ extern "C" gs_status gs_p2p_offsets(const int64_t* C, int G, int r, int64_t* seg
 
 extern "C" gs_status gs_sym_alloc(gs_ctx* c, int which, size_t bytes, void** ptr_h, uint8_t handle_h[64]) {
   if (!c) return GS_EINVAL;
-  GS_REQUIRE(c, which >= 0 && which < 3 && ptr_h, "bad argument");
+  GS_REQUIRE(c, which >= 0 && which < 5 && ptr_h, "bad argument");
   GS_CUDA(c, cudaSetDevice(c->device));
   gs_p2p_state& P = c->p2p;
   if (bytes == 0) bytes = 256;
@@ -83,7 +84,7 @@ extern "C" gs_status gs_sym_alloc(gs_ctx* c, int which, size_t bytes, void** ptr
     }
     GS_CUDA(c, cudaMalloc(&P.sym[which], bytes));
     P.sym_bytes[which] = bytes;
-    if (which == 2) GS_CUDA(c, cudaMemset(P.sym[which], 0, bytes));
+    if (which == 2 || which == 3) GS_CUDA(c, cudaMemset(P.sym[which], 0, bytes));
     P.attached = false;  // peers must re-open and re-attach
   }
   *ptr_h = P.sym[which];
@@ -150,6 +151,91 @@ extern "C" gs_status gs_p2p_plan(gs_ctx* c, const int64_t* C, int64_t* n_recv_h)
   }
   P.counts.assign(C, C + (size_t)G * G);
   P.planned = true;
+  return GS_OK;
+}
+
+// ------------------------------------------------------------------ device-side counts
+namespace {
+struct gs_ptrs64 {
+  int64_t* p[GS_MAX_WORLD];
+};
+// This rank's row of the count matrix (tot = its per-destination prefix, G + 1 entries) into
+// row `rank` of every rank's matrix (NVLink stores); visible to them after the next barrier.
+__global__ void k_p2p_counts_put(const int64_t* __restrict__ tot, gs_ptrs64 cm, int G, int rank) {
+  const int q = blockIdx.x, d = threadIdx.x;
+  if (q < G && d < G) cm.p[q][rank * G + d] = tot[d + 1] - tot[d];
+}
+// The owned segment of the batch's cost row into every rank's row at [B_lo, B_lo + n).
+__global__ void k_p2p_row_put(const int64_t* __restrict__ cost, int64_t n, int64_t B_lo, gs_ptrs64 rows, int G) {
+  const int q = blockIdx.y;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    rows.p[q][B_lo + i] = cost[i];
+}
+}  // namespace
+
+extern "C" gs_status gs_p2p_attach_counts(gs_ctx* c, void* const* cmat_h, void* const* row_h, int64_t row_cap) {
+  if (!c) return GS_EINVAL;
+  GS_REQUIRE(c, cmat_h, "null argument");
+  GS_REQUIRE(c, row_cap >= 0 && (row_cap == 0 || row_h), "row pointers required with a capacity");
+  gs_p2p_state& P = c->p2p;
+  for (int g = 0; g < c->world; g++) {
+    GS_REQUIRE(c, cmat_h[g] != nullptr, "rank %d has no count matrix", g);
+    P.cmat[g] = (int64_t*)cmat_h[g];
+    P.row[g] = row_cap ? (int64_t*)row_h[g] : nullptr;
+  }
+  P.row_cap = row_cap;
+  if (!P.counts_ev) GS_CUDA(c, cudaEventCreateWithFlags(&P.counts_ev, cudaEventDisableTiming));
+  return GS_OK;
+}
+
+// Device-side count exchange (gs_project_put_dev's first half): the row to every peer, the
+// barrier, then an asynchronous copy of the own (now complete) matrix to pinned memory whose
+// completion gs_p2p_counts waits for.
+gs_status gs_p2p_counts_exchange(gs_ctx* c, const int64_t* tot_dev, cudaStream_t st) {
+  gs_p2p_state& P = c->p2p;
+  const int G = c->world;
+  gs_ptrs64 cm;
+  for (int g = 0; g < GS_MAX_WORLD; g++) cm.p[g] = g < G ? P.cmat[g] : nullptr;
+  ++c->launches;
+  k_p2p_counts_put<<<G, 32, 0, st>>>(tot_dev, cm, G, c->rank);
+  GS_LAUNCH_CHECK(c, "p2p counts");
+  gs_status s = gs_p2p_barrier(c, st);
+  if (s != GS_OK) return s;
+  GS_CUDA(c, cudaMemcpyAsync(c->pinned + kCountsPinned, P.cmat[c->rank], (size_t)G * G * sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, st));
+  return GS_OK;
+}
+
+extern "C" gs_status gs_p2p_counts(gs_ctx* c, int64_t* counts_h, int64_t* n_recv_h) {
+  if (!c) return GS_EINVAL;
+  GS_REQUIRE(c, counts_h && n_recv_h, "null argument");
+  gs_p2p_state& P = c->p2p;
+  GS_REQUIRE(c, P.counts_ev, "gs_p2p_counts before gs_p2p_attach_counts");
+  GS_CUDA(c, cudaEventSynchronize(P.counts_ev));
+  const int G = c->world;
+  for (int k = 0; k < G * G; k++) counts_h[k] = c->pinned[kCountsPinned + k];
+  const unsigned long long badv = (unsigned long long)c->pinned[kCountsPinned + GS_MAX_WORLD * GS_MAX_WORLD];
+  if (badv != ~0ull)  // the projection saw a non-finite parameter: its records are garbage
+    return gs_fail(c, GS_ENONFINITE, "non-finite parameter at gid %lld", (long long)badv);
+  return gs_p2p_plan(c, counts_h, n_recv_h);
+}
+
+extern "C" gs_status gs_p2p_put_costs(gs_ctx* c, const int64_t* owned_cost, const int64_t* dp_h, void* stream) {
+  if (!c) return GS_EINVAL;
+  gs_p2p_state& P = c->p2p;
+  GS_REQUIRE(c, dp_h && P.row_cap > 0, "no cost rows attached");
+  const int G = c->world;
+  const int64_t lo = dp_h[c->rank], n = dp_h[c->rank + 1] - lo;
+  GS_REQUIRE(c, dp_h[G] <= P.row_cap, "cost row capacity %lld < %lld blocks", (long long)P.row_cap,
+             (long long)dp_h[G]);
+  if (n == 0) return GS_OK;
+  GS_REQUIRE(c, owned_cost != nullptr, "null owned_cost");
+  gs_ptrs64 rows;
+  for (int g = 0; g < GS_MAX_WORLD; g++) rows.p[g] = g < G ? P.row[g] : nullptr;
+  ++c->launches;
+  k_p2p_row_put<<<dim3((unsigned)std::min<int64_t>((n + 255) / 256, 148), G), 256, 0, (cudaStream_t)stream>>>(
+      owned_cost, n, lo, rows, G);
+  GS_LAUNCH_CHECK(c, "p2p cost row");
   return GS_OK;
 }
 

@@ -11,6 +11,8 @@
 //          ballots (thread order = gid order), write 64-byte records.
 // Placement is therefore deterministic and gid-ordered within each (d, v) bucket, which the
 // stable (depth, gid) order of A3 relies on; no placement atomics.
+#include <cstring>
+
 #include "gs_device.cuh"
 #include "gs_index.cuh"
 
@@ -68,12 +70,48 @@ __global__ void k_gather_totals(const int64_t* base, int64_t ncta, int b, int G,
   if (d <= G) out[d] = base[(int64_t)d * b * ncta];
 }
 
+// NEXT-3 sync-free put: the destinations' receive buffers and capacities; the record offsets
+// come from the G x G count matrix on the device (this rank's copy, complete after the
+// count-exchange barrier).
+struct gs_devouts {
+  gs_rec* recv[GS_MAX_WORLD];
+  long long cap[GS_MAX_WORLD];
+  const int64_t* cmat;
+  int rank;
+};
+
+template <bool kDev>
 __global__ void __launch_bounds__(kBlock) k_project_write(
     const float4* __restrict__ pos_op, const float4* __restrict__ log_scale,
     const float4* __restrict__ rot, const float4* __restrict__ sh, int64_t n, int64_t gid_base,
     gs_cams_arg cams, gs_geom geo, int G, int nb, int NW, const uint32_t* __restrict__ maskw,
-    const int64_t* __restrict__ base, int64_t ncta, gs_outs outs, unsigned long long* __restrict__ bad) {
+    const int64_t* __restrict__ base, int64_t ncta, gs_outs outs, unsigned long long* __restrict__ bad,
+    gs_devouts dv) {
   __shared__ int s_cnt[kWarps * kMaxBuckets];
+  __shared__ gs_rec* s_out[GS_MAX_WORLD];  // kDev: destination d's base for this rank's records
+  if constexpr (kDev) {
+    // every destination's records: this rank's bucket for d starts at put[d] = sum over
+    // s < rank of C[s][d] in d's buffer and at soff[d] = sum over d' < d of C[rank][d'] in the
+    // send order; nothing is written if any destination would overflow (every rank sees the
+    // same matrix: all skip together, gs_p2p_counts reports it)
+    __shared__ int s_ok;
+    if (threadIdx.x == 0) s_ok = 1;
+    __syncthreads();
+    if ((int)threadIdx.x < G) {
+      const int d = threadIdx.x;
+      long long put = 0, in = 0, soff = 0;
+      for (int q = 0; q < G; q++) {
+        const long long x = dv.cmat[q * G + d];
+        in += x;
+        if (q < dv.rank) put += x;
+      }
+      for (int e = 0; e < d; e++) soff += dv.cmat[dv.rank * G + e];
+      if (in > dv.cap[d]) s_ok = 0;
+      s_out[d] = dv.recv[d] + (put - soff);
+    }
+    __syncthreads();
+    if (!s_ok) return;
+  }
   const int b = cams.n;
   int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
   uint32_t m[kMaxWords], u[kMaxWords];
@@ -154,7 +192,7 @@ __global__ void __launch_bounds__(kBlock) k_project_write(
       if (bit) {
         int64_t pos = base[(int64_t)k * ncta + blockIdx.x] + warp_prefix(s_cnt, wid, nb, k) +
                       __popc(bal & lt);
-        outs.d[d][pos] = rec;  // own send buffer, or (NEXT-3) destination d's receive buffer
+        (kDev ? s_out[d] : outs.d[d])[pos] = rec;  // own send buffer, or (NEXT-3) d's receive buffer
       }
     }
   }
@@ -175,19 +213,23 @@ extern "C" size_t gs_project_index_bytes(const gs_ctx* c, int64_t n, int n_views
   return index_layout(n, n_views, c->world).bytes;
 }
 
-// Counting half (shared by gs_project and gs_project_count): bwd_index masks and per-CTA
-// bucket bases, per-destination counts to the host (one sync).
-static gs_status project_count_phase(gs_ctx* c, const gs_params* p, const gs_camera* cams_h, int n_views,
-                                     const int64_t* dp_h, int64_t* send_counts_h, void* bwd_index,
-                                     cudaStream_t st, int64_t* total_h) {
+// Counting half, device part (gs_project, gs_project_count, gs_project_put_dev): bwd_index
+// masks and per-CTA bucket bases, and *tot_dev = this rank's per-destination prefix [G + 1]
+// on the device.  No host sync.
+static gs_status project_count_launch(gs_ctx* c, const gs_params* p, const gs_camera* cams_h, int n_views,
+                                      const int64_t* dp_h, void* bwd_index, cudaStream_t st, int64_t** tot_dev) {
   gs_status s = gs_check_batch(c, cams_h, n_views, dp_h);
   if (s != GS_OK) return s;
-  GS_REQUIRE(c, p && send_counts_h, "null argument");
+  GS_REQUIRE(c, p, "null argument");
   const int G = c->world, b = n_views, nb = b * G;
   GS_REQUIRE(c, nb <= kMaxBuckets, "n_views * world = %d exceeds %d", nb, kMaxBuckets);
-  for (int d = 0; d < G; d++) send_counts_h[d] = 0;
-  *total_h = 0;
-  if (p->n == 0) return GS_OK;
+  int64_t* tot = (int64_t*)gs_slot_get(c, SLOT_PROJ_TMP, (GS_MAX_WORLD + 1) * sizeof(int64_t), st);
+  if (!tot) return gs_fail(c, GS_ECUDA, "scratch");
+  *tot_dev = tot;
+  if (p->n == 0) {
+    GS_CUDA(c, cudaMemsetAsync(tot, 0, (GS_MAX_WORLD + 1) * sizeof(int64_t), st));
+    return GS_OK;
+  }
   GS_REQUIRE(c, bwd_index && p->pos_op && p->log_scale && p->rot && p->sh, "null buffer");
   gs_index_layout L = index_layout(p->n, b, G);
   uint32_t* maskw = (uint32_t*)bwd_index;
@@ -205,18 +247,41 @@ static gs_status project_count_phase(gs_ctx* c, const gs_params* p, const gs_cam
   GS_LAUNCH_CHECK(c, "project_count");
   s = gs_scan_i64(c, base, base, (int64_t)nb * L.ncta + 1, 0, st);
   if (s != GS_OK) return s;
-  int64_t* tot = (int64_t*)gs_slot_get(c, SLOT_PROJ_TMP, (GS_MAX_WORLD + 1) * sizeof(int64_t), st);
-  if (!tot) return gs_fail(c, GS_ECUDA, "scratch");
   ++c->launches;
   k_gather_totals<<<1, 64, 0, st>>>(base, L.ncta, b, G, tot);
+  GS_LAUNCH_CHECK(c, "project totals");
+  return GS_OK;
+}
+
+// The non-finite word read back with a count sync: GS_ENONFINITE naming the lowest gid (and
+// the word reset) if set.
+static gs_status nonfinite_result(gs_ctx* c, unsigned long long badv, cudaStream_t st) {
+  if (badv == ~0ull) return GS_OK;  // this call's position / scale / rotation / opacity, or an earlier call's SH
+  unsigned long long* bad = nonfinite_word(c, st);
+  if (bad) GS_CUDA(c, cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
+  return gs_fail(c, GS_ENONFINITE, "non-finite parameter at gid %lld", (long long)badv);
+}
+
+// Counting half with the read-back (gs_project, gs_project_count): per-destination counts to
+// the host (one sync).
+static gs_status project_count_phase(gs_ctx* c, const gs_params* p, const gs_camera* cams_h, int n_views,
+                                     const int64_t* dp_h, int64_t* send_counts_h, void* bwd_index,
+                                     cudaStream_t st, int64_t* total_h) {
+  GS_REQUIRE(c, send_counts_h, "null argument");
+  const int G = c->world;
+  for (int d = 0; d < G; d++) send_counts_h[d] = 0;
+  *total_h = 0;
+  int64_t* tot = nullptr;
+  gs_status s = project_count_launch(c, p, cams_h, n_views, dp_h, bwd_index, st, &tot);
+  if (s != GS_OK) return s;
+  if (p->n == 0) return GS_OK;
+  unsigned long long* bad = nonfinite_word(c, st);
+  if (!bad) return gs_fail(c, GS_ECUDA, "scratch");
   GS_CUDA(c, cudaMemcpyAsync(c->pinned, tot, (G + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GS_CUDA(c, cudaMemcpyAsync(c->pinned + GS_MAX_WORLD + 1, bad, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GS_CUDA(c, cudaStreamSynchronize(st));
-  const unsigned long long badv = (unsigned long long)c->pinned[GS_MAX_WORLD + 1];
-  if (badv != ~0ull) {  // this call's position / scale / rotation / opacity, or an earlier call's SH
-    GS_CUDA(c, cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
-    return gs_fail(c, GS_ENONFINITE, "non-finite parameter at gid %lld", (long long)badv);
-  }
+  s = nonfinite_result(c, (unsigned long long)c->pinned[GS_MAX_WORLD + 1], st);
+  if (s != GS_OK) return s;
   for (int d = 0; d < G; d++) send_counts_h[d] = c->pinned[d + 1] - c->pinned[d];
   *total_h = c->pinned[G];
   if (*total_h >= (1ll << 31))
@@ -234,10 +299,12 @@ static gs_status project_write_phase(gs_ctx* c, const gs_params* p, const gs_cam
   gs_cams_arg cams = make_cams(cams_h, n_views);
   gs_geom geo = gs_make_geom(&cams_h[0]);
   ++c->launches;
-  k_project_write<<<(unsigned)L.ncta, kBlock, 0, st>>>(
+  gs_devouts dv;
+  memset(&dv, 0, sizeof(dv));
+  k_project_write<false><<<(unsigned)L.ncta, kBlock, 0, st>>>(
       (const float4*)p->pos_op, (const float4*)p->log_scale, (const float4*)p->rot,
       (const float4*)p->sh, p->n, p->gid_base, cams, geo, G, nb, L.NW, maskw, base, L.ncta, outs,
-      nonfinite_word(c, st));
+      nonfinite_word(c, st), dv);
   GS_LAUNCH_CHECK(c, "project_write");
   return GS_OK;
 }
@@ -294,4 +361,64 @@ extern "C" gs_status gs_project_put(gs_ctx* c, const gs_params* p, const gs_came
       outs.d[d] = (gs_rec*)c->p2p.recv[d] + (put[d] - soff[d]);
     }
   return project_write_phase(c, p, cams_h, n_views, bwd_index, outs, st);
+}
+
+namespace {
+// dL/dsend rows [0, n_send) of this rank zeroed for the peers' reductions, n_send from the
+// device matrix (row `rank`); nothing if it exceeds the capacity (gs_p2p_counts reports it).
+__global__ void k_zero_dsend(float* __restrict__ dsend, const int64_t* __restrict__ cmat, int G, int rank,
+                             long long cap) {
+  long long n = 0;
+  for (int d = 0; d < G; d++) n += cmat[rank * G + d];
+  if (n > cap) return;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < 9 * n; i += (long long)gridDim.x * blockDim.x)
+    dsend[i] = 0.f;
+}
+}  // namespace
+
+extern "C" gs_status gs_project_put_dev(gs_ctx* c, const gs_params* p, const gs_camera* cams_h, int n_views,
+                                        const int64_t* dp_h, void* bwd_index, void* stream) {
+  if (!c) return GS_EINVAL;
+  GS_REQUIRE(c, p, "null argument");
+  gs_p2p_state& P = c->p2p;
+  GS_REQUIRE(c, P.attached && P.counts_ev, "gs_project_put_dev needs gs_p2p_attach and gs_p2p_attach_counts");
+  const int G = c->world, r = c->rank, b = n_views, nb = b * G;
+  cudaStream_t st = (cudaStream_t)stream;
+  P.planned = false;
+  int64_t* tot = nullptr;
+  gs_status s = project_count_launch(c, p, cams_h, n_views, dp_h, bwd_index, st, &tot);
+  if (s != GS_OK) return s;
+  // the count matrix on every rank's device: row r to every peer, barrier, async read-back
+  s = gs_p2p_counts_exchange(c, tot, st);
+  if (s != GS_OK) return s;
+  unsigned long long* bad = nonfinite_word(c, st);
+  if (!bad) return gs_fail(c, GS_ECUDA, "scratch");
+  GS_CUDA(c, cudaMemcpyAsync(c->pinned + kCountsPinned + GS_MAX_WORLD * GS_MAX_WORLD, bad, sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, st));
+  GS_CUDA(c, cudaEventRecord(P.counts_ev, st));
+  GS_REQUIRE(c, P.dsend[r] != nullptr, "null dL/dsend");
+  ++c->launches;
+  k_zero_dsend<<<148 * 4, 256, 0, st>>>(P.dsend[r], P.cmat[r], G, r, (long long)P.dsend_cap[r]);
+  if (p->n > 0) {
+    gs_devouts dv;
+    memset(&dv, 0, sizeof(dv));
+    for (int d = 0; d < G; d++) {
+      dv.recv[d] = (gs_rec*)P.recv[d];
+      dv.cap[d] = P.recv_cap[d];
+    }
+    dv.cmat = P.cmat[r];
+    dv.rank = r;
+    gs_index_layout L = index_layout(p->n, b, G);
+    gs_outs outs;
+    memset(&outs, 0, sizeof(outs));
+    gs_cams_arg cams = make_cams(cams_h, n_views);
+    gs_geom geo = gs_make_geom(&cams_h[0]);
+    ++c->launches;
+    k_project_write<true><<<(unsigned)L.ncta, kBlock, 0, st>>>(
+        (const float4*)p->pos_op, (const float4*)p->log_scale, (const float4*)p->rot, (const float4*)p->sh, p->n,
+        p->gid_base, cams, geo, G, nb, L.NW, (const uint32_t*)bwd_index,
+        (const int64_t*)((const char*)bwd_index + L.base_off), L.ncta, outs, bad, dv);
+  }
+  GS_LAUNCH_CHECK(c, "project_put_dev");
+  return GS_OK;
 }

@@ -46,7 +46,7 @@ class GrendelTrainer:
     def __init__(self, ctx: L.Context, params: L.GaussianParams, width: int, height: int, n_views: int,
                  n_images: int, lr=DEFAULT_LR, cost_mode=L.COST_MEASURED, bg=(0.0, 0.0, 0.0),
                  rebalance=True, dp=None, device=None, split_adam=True, loss="l1", ssim_lambda=0.2,
-                 densify_stats=False, exchange="nccl", count_gather="nccl"):
+                 densify_stats=False, exchange="nccl", count_gather="nccl", sync_free=True):
         self.ctx, self.p = ctx, params
         self.device = device or params.pos_op.device
         self.W, self.H, self.b = width, height, n_views
@@ -66,6 +66,9 @@ class GrendelTrainer:
         if self.exchange_kind == "p2p" and (loss != "l1" or densify_stats or any(bg)):
             raise ValueError("exchange='p2p' supports the L1 loss, black background, no densification statistics")
         self.p2p = None  # (recv_ptr, dsend_ptr, recv_cap, dsend_cap) once attached
+        # p2p: the count matrix and the cost row exchanged on the devices (gs_project_put_dev,
+        # gs_p2p_put_costs) instead of through the host (count_gather)
+        self.sync_free = bool(sync_free)
         # which collective carries the G x G count matrix (G^2 int64): the context's NCCL
         # communicator, or torch.distributed's process group (contexts without one)
         self.count_gather = count_gather
@@ -190,12 +193,37 @@ class GrendelTrainer:
         rp, rh = L.sym_alloc(ctx, L.SYM_RECV, recv_cap * L.RECORD_BYTES)
         dp_, dh = L.sym_alloc(ctx, L.SYM_DSEND, dsend_cap * L.GRAD_FLOATS * 4)
         fp, fh = L.sym_alloc(ctx, L.SYM_FLAGS, G * 8)
+        # sync-free forward (gs_project_put_dev): the count matrices and the batch cost rows
+        cp, ch = L.sym_alloc(ctx, L.SYM_COUNTS, G * G * 8)
+        wp, wh = L.sym_alloc(ctx, L.SYM_ROW, self.B * 8)
         allh = [None] * G
-        dist.all_gather_object(allh, (rh, dh, fh))
-        own = (rp, dp_, fp)
-        ptrs = [[own[k] if g == self.rank else L.ipc_open(ctx, allh[g][k]) for g in range(G)] for k in range(3)]
+        dist.all_gather_object(allh, (rh, dh, fh, ch, wh))
+        own = (rp, dp_, fp, cp, wp)
+        ptrs = [[own[k] if g == self.rank else L.ipc_open(ctx, allh[g][k]) for g in range(G)] for k in range(5)]
         L.p2p_attach(ctx, ptrs[0], [recv_cap] * G, ptrs[1], [dsend_cap] * G, ptrs[2])
+        L.p2p_attach_counts(ctx, ptrs[3], ptrs[4], self.B)
         self.p2p = (rp, dp_, recv_cap, dsend_cap)
+        self.p2p_row = wp
+
+    def _p2p_exchange_dev(self, cams, dp, st):
+        """A1 + A2 fused without a host round trip between counting and writing: the count
+        matrix is exchanged on the devices, the records written at offsets computed from it,
+        and the host reads the matrix while they are being written.  On a capacity shortfall
+        (every rank sees it together) the buffers grow and the projection runs again."""
+        ctx = self.ctx
+        if self.p2p is None:
+            self._p2p_setup(1 << 16, 1 << 16)
+        while True:
+            L.project_put_dev(ctx, self.p, cams, dp, self.bwd_index, st)
+            L.p2p_barrier(ctx, st)  # records visible to their destinations
+            try:
+                C, n_recv = L.p2p_counts(ctx)
+                break
+            except L.CapacityError as e:
+                n_in, n_out = e.counts.sum(0), e.counts.sum(1)
+                self._p2p_setup(max(int(n_in.max() * 1.25) + 1024, self.p2p[2]),
+                                max(int(n_out.max() * 1.25) + 1024, self.p2p[3]))
+        return C[self.rank].copy(), C[:, self.rank].copy(), n_recv
 
     def _p2p_exchange(self, cams, dp, st):
         """A1 + A2 fused: count, all-gather the count matrix, put the records into the
@@ -217,6 +245,23 @@ class GrendelTrainer:
         L.p2p_barrier(ctx, st)
         return send_counts, C[:, self.rank].copy(), n_recv
 
+    def _gather_cost_row(self, dp, no):
+        """The whole batch's cost row from every rank's owned segment (torch.distributed
+        all-gather of equal-size padded segments; what gs_rebalance's NCCL allgatherv does)."""
+        import torch.distributed as dist
+        seg = int(max(dp[g + 1] - dp[g] for g in range(self.G)))
+        mine = torch.zeros(max(seg, 1), dtype=torch.int64, device=self.device)
+        mine[:no].copy_(self.cost.t[:no])
+        parts = [torch.zeros_like(mine) for _ in range(self.G)]
+        if dist.get_backend() == "gloo":  # gloo: host tensors
+            mine_h = mine.cpu()
+            parts_h = [torch.zeros_like(mine_h) for _ in range(self.G)]
+            dist.all_gather(parts_h, mine_h)
+            parts = [x.to(self.device) for x in parts_h]
+        else:
+            dist.all_gather(parts, mine)
+        return torch.cat([parts[g][: int(dp[g + 1] - dp[g])] for g in range(self.G)])
+
     @property
     def n_owned(self):
         return int(self.dp[self.rank + 1] - self.dp[self.rank])
@@ -237,7 +282,9 @@ class GrendelTrainer:
         # A1 project (retry on capacity)
         rec("project", 0)
         cap = self.send.cap
-        if p2p:  # NEXT-3: projection writes straight into the destinations (A1 + A2 fused)
+        if p2p and self.sync_free:  # NEXT-3, counts exchanged on the devices
+            send_counts, recv_counts, n_recv = self._p2p_exchange_dev(cams, dp, st)
+        elif p2p:  # NEXT-3: projection writes straight into the destinations (A1 + A2 fused)
             send_counts, recv_counts, n_recv = self._p2p_exchange(cams, dp, st)
         while not p2p:
             try:
@@ -327,6 +374,10 @@ class GrendelTrainer:
         # A6 reverse exchange
         rec("exchange_grads", 0)
         if p2p:
+            # the owned cost segment rides on the same barrier (A9's all-gather, sync-free form)
+            row_put = self.sync_free and self.do_rebalance and next_cams is not None and not paper_avg
+            if row_put:
+                L.p2p_put_costs(ctx, self.cost.t, dp, st)
             L.p2p_barrier(ctx, st)
             dsend = self.p2p[1]
         elif self.G == 1:
@@ -355,8 +406,18 @@ class GrendelTrainer:
                 if no:
                     self.cost.t[:no].zero_()
                     self.cost.t[0] = ns
-            self.dp = L.rebalance(ctx, self.cost.t, cams, dp, self.history, self.n_images, self.cost_mode,
-                                  next_cams, st)
+            if p2p and self.sync_free:  # the row is already on this device (p2p_put_costs)
+                if paper_avg:
+                    L.p2p_put_costs(ctx, self.cost.t, dp, st)
+                    L.p2p_barrier(ctx, st)
+                self.dp = L.rebalance_row(ctx, self.p2p_row, cams, dp, self.history, self.n_images,
+                                          self.cost_mode, next_cams, st)
+            elif ctx.has_comm:
+                self.dp = L.rebalance(ctx, self.cost.t, cams, dp, self.history, self.n_images, self.cost_mode,
+                                      next_cams, st)
+            else:  # processes without a communicator (IPC exchange): the row through torch.distributed
+                self.dp = L.rebalance_row(ctx, self._gather_cost_row(dp, no), cams, dp, self.history, self.n_images,
+                                          self.cost_mode, next_cams, st)
         rec("rebalance", 1)
         self.last = dict(n_send=n_send, n_recv=n_recv, n_pairs=n_pairs, send_counts=send_counts,
                          recv_counts=recv_counts, n_owned=no)
