@@ -48,7 +48,7 @@ float orc_exp_rn(float x) {
   float z = r * r;
   float p = 1.9875691500e-4f;
   p = p * r + 1.3981999507e-3f;
-  p = p * r + 8.3333451907e-3f;
+  p = p * r + 8.3334519073e-3f;
   p = p * r + 4.1665795894e-2f;
   p = p * r + 1.6666665459e-1f;
   p = p * r + 5.0000001201e-1f;

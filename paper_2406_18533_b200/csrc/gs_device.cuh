@@ -59,7 +59,7 @@ __device__ __forceinline__ float exp_rn(float x) {
   float z = mul(r, r);
   float p = 1.9875691500e-4f;
   p = add(mul(p, r), 1.3981999507e-3f);
-  p = add(mul(p, r), 8.3333451907e-3f);
+  p = add(mul(p, r), 8.3334519073e-3f);
   p = add(mul(p, r), 4.1665795894e-2f);
   p = add(mul(p, r), 1.6666665459e-1f);
   p = add(mul(p, r), 5.0000001201e-1f);
