@@ -24,7 +24,7 @@ struct gs_slot {
 enum {
   SLOT_SCAN = 0,      // scan partials
   SLOT_PROJ_TMP,      // projection per-destination totals
-  SLOT_DIFF,          // bin_sort 2D difference arrays
+  SLOT_DIFF,          // bin_sort 2D difference arrays of the tile rectangles
   SLOT_COUNTS,        // bin_sort per-block counts (int64)
   SLOT_CURSOR,        // bin_sort per-block cursors
   SLOT_KEYS,          // bin_sort (depth, recv idx) keys
@@ -35,7 +35,7 @@ enum {
   SLOT_CT,            // rebalance prefix sums
   SLOT_MISC,          // small counters / dp
   SLOT_COUNT_GATHER,  // exchange count matrix
-  SLOT_RECTILES,      // bin_sort per-record tile counts -> pair starts
+  SLOT_RECTILES,      // bin_sort per-record coarse counts
   SLOT_RADIX_HIST,    // bin_sort radix per-tile digit histograms -> offsets
   SLOT_PSTART,        // bin_sort pair starts in depth order
   SLOT_HALO_SEND,     // halo exchange: packed blocks to send
@@ -43,6 +43,10 @@ enum {
   SLOT_DENSIFY,       // densify keep flags [4][n]
   SLOT_DENSIFY_OFF,   // densify output positions
   SLOT_NONFINITE,     // gs_project: lowest gid with a non-finite parameter (atomicMin word)
+  SLOT_BCOUNT,        // bin_sort per-owned-block pair counts -> offsets (int64)
+  SLOT_CLIST,         // bin_sort coarse lists (record indices by super-tile)
+  SLOT_CRANGE,        // bin_sort coarse-list ranges per super-tile
+  SLOT_RECT8,         // bin_sort packed tile rectangle + view per record
   SLOT_N
 };
 

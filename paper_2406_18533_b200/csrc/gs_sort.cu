@@ -1,19 +1,28 @@
 // gs_sort.cu -- A3: Z-buffer build ("iterates over intersecting Gaussians in
 // increasing depth"; App. A.2 "indices of intersecting gaussians for each pixel").
 //
-// B200 design (differs from the prior art's global 64-bit (tile | depth) radix sort of the
-// pairs): the RECORDS are sorted by (view, depth) -- stable LSD radix over the 32 depth bits,
-// then the view -- so equal depths stay in receive order (= gid order within a view, R7); the
-// (block, record) pairs are emitted in that order, each view's pairs into its own segment of
-// the pair array, padded to whole radix tiles; then the pairs of every segment are stably
-// radix-sorted by their VIEW-LOCAL block index (16 bits for a 4591x3436 view: 2 passes of 8;
-// 13 bits at 1080p: 7 + 6) with one digit histogram laid out [view][digit][tile], so one
-// exclusive scan keeps every segment in place.  Each block's list then comes out in exact
-// (depth, gid) order (O11) with no per-block sort and traffic linear in the pairs; tile_range
-// is read off the sorted keys.  Pairs of blocks the rank does not own (G > 1: rectangles
-// straddling the partition) and the padding carry the sentinel key 2^nbits - 1, sort to the
-// end of their segment and are never written.  One host sync per call: the per-view pair
-// counts (scratch sizing, segment layout, the capacity check and *n_pairs_h).
+// B200 design (differs from the prior art's global 64-bit (tile | depth) radix sort of every
+// (tile, Gaussian) pair): two levels.
+//  1. The RECORDS are sorted by (view, depth) -- stable LSD radix over the 32 depth bits, then
+//     the view -- so equal depths stay in receive order (= gid order within a view, R7).
+//  2. Coarse binning: each record is paired with the SUPER-TILES (8 x 8 blocks, 128 x 128 px)
+//     its tile rectangle touches (~2 per record instead of ~17 blocks), emitted in (view,
+//     depth) order into per-view segments padded to radix tiles and stably radix-sorted by the
+//     view-local super-tile index (10 bits at 4591x3436: 2 passes of 5; 8 bits at 1080p: one
+//     pass) with one digit histogram laid out [view][digit][tile].  Each super-tile's coarse
+//     list is then in (depth, gid) order.
+//  3. Block offsets without reading any pair: every record adds its rectangle to a per-view 2D
+//     difference array (4 atomics), a 2D prefix gives each block's pair count, and an
+//     exclusive scan over the owned blocks gives tile_range.
+//  4. Fine emission: one CTA per super-tile walks its coarse list in order, 128 records at a
+//     time; each record's blocks inside the super-tile are a 64-bit mask, the in-order rank of
+//     a record among those hitting a block is a ballot popcount (plus the earlier warps'
+//     counts), and the record index is stored at tile_range[block] + rank.  Block lists come
+//     out in exact (depth, gid) order (O11) with no per-block sort, no pair keys and no pass
+//     over the pairs besides the one store of each.
+// Blocks the rank does not own (G > 1: rectangles straddling the partition) are masked out in
+// step 4 and never counted in step 3.  One host sync per call: the per-view coarse and owned
+// pair counts (scratch sizing, segment layout, the capacity check and *n_pairs_h).
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -38,6 +47,35 @@ constexpr int kRadixWarps = kRadixThreads / 32;
 constexpr int kRadixPerWarp = kRadixTile / kRadixWarps;   // 512 consecutive elements per warp
 constexpr int kEmitThreads = 256;
 constexpr int kEmitPairs = 1024;  // pairs per emission CTA
+constexpr int kSTShift = 3;        // super-tile side: 2^3 = 8 blocks (64 blocks: one 64-bit mask)
+constexpr int kST = 1 << kSTShift;
+constexpr int kFineThreads = 128;  // fine emission: records per chunk (4 warps)
+
+// The coarse grid: super-tile (sx, sy) = blocks [8 sx, 8 sx + 7] x [8 sy, 8 sy + 7] of the
+// view, view-local index sy * Cw + sx.
+struct cgrid {
+  int Cw, Ch;
+};
+// A record's tile rectangle and view packed into 8 bytes (k_tile_counts, read by the emission
+// kernels instead of the 64-byte record): x = tx0 | tx1 << 16, y = ty0 | ty1 << 13 | view << 26
+// (Wt < 2^16, Ht < 2^13); an empty rectangle has tx0 > tx1.
+__device__ __forceinline__ uint2 pack_rect(int tx0, int tx1, int ty0, int ty1, int v) {
+  return make_uint2((unsigned)tx0 | (unsigned)tx1 << 16, (unsigned)ty0 | (unsigned)ty1 << 13 | (unsigned)v << 26);
+}
+__device__ __forceinline__ void unpack_rect(uint2 r, int& tx0, int& tx1, int& ty0, int& ty1, int& v) {
+  tx0 = (int)(r.x & 0xffffu);
+  tx1 = (int)(r.x >> 16);
+  ty0 = (int)(r.y & 0x1fffu);
+  ty1 = (int)((r.y >> 13) & 0x1fffu);
+  v = (int)(r.y >> 26);
+}
+__device__ __forceinline__ void coarse_rect(int tx0, int tx1, int ty0, int ty1, int& sx0, int& sx1, int& sy0,
+                                            int& sy1) {
+  sx0 = tx0 >> kSTShift;
+  sx1 = tx1 >> kSTShift;
+  sy0 = ty0 >> kSTShift;
+  sy1 = ty1 >> kSTShift;
+}
 
 // The segment layout of the rank's views v_lo .. v_lo + nv - 1 (host-computed after the sync):
 // view k's pairs occupy padded positions [seg[k], seg[k+1]) (tile-aligned), its owned pairs
@@ -63,12 +101,15 @@ __device__ __forceinline__ long long seg_hidx(const seg_arg& g, int k, int d, lo
   return t0 * bins + (long long)d * nt + (t - t0);
 }
 
-// Per-record tile count of its rectangle in its view (all blocks: the emission enumerates the
-// rectangle), and per view the pair total and the owned-pair total (owned = view-local block in
-// [lo, hi): per rectangle row an interval intersection).  cnt[k] / own[k] over the rank's views.
+// Per record: its coarse-pair count (super-tiles its tile rectangle touches), its rectangle
+// added to the view's 2D difference array diff[k][Ht + 1][Wt + 1] (the prefix sums of which
+// count each block's pairs), and per view the coarse-pair total and the owned-pair total
+// (owned = view-local block in [lo, hi): per rectangle row an interval intersection).
+// cnt[k] / own[k] over the rank's views; g.lo / g.hi are the FINE ownership bounds here.
 __global__ void k_tile_counts(const gs_rec* __restrict__ rec, int64_t n_recv, gs_geom geo, seg_arg g,
-                              int64_t* __restrict__ n_tiles, unsigned long long* __restrict__ cnt,
-                              unsigned long long* __restrict__ own) {
+                              int64_t* __restrict__ n_coarse, unsigned long long* __restrict__ cnt,
+                              unsigned long long* __restrict__ own, int* __restrict__ diff,
+                              uint2* __restrict__ rect8) {
   __shared__ unsigned long long s_c[GS_MAX_VIEWS], s_o[GS_MAX_VIEWS];
   if (threadIdx.x < GS_MAX_VIEWS) s_c[threadIdx.x] = s_o[threadIdx.x] = 0;
   __syncthreads();
@@ -77,19 +118,30 @@ __global__ void k_tile_counts(const gs_rec* __restrict__ rec, int64_t n_recv, gs
   int k = -1;
   if (j < n_recv) {
     const float4 a = rec[j].a;
-    k = (int)(__float_as_uint(rec[j].d.w) & 31u) - g.v_lo;
+    const int v = (int)(__float_as_uint(rec[j].d.w) & 31u);
+    k = v - g.v_lo;
     int tx0, tx1, ty0, ty1;
-    if (k >= 0 && k < g.nv && rect_of(a.x, a.y, a.w, geo.Wt, geo.Ht, tx0, tx1, ty0, ty1)) {
-      t = (unsigned)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+    const bool ok = k >= 0 && k < g.nv && rect_of(a.x, a.y, a.w, geo.Wt, geo.Ht, tx0, tx1, ty0, ty1);
+    rect8[j] = ok ? pack_rect(tx0, tx1, ty0, ty1, v) : pack_rect(1, 0, 0, 0, v);
+    if (ok) {
+      int sx0, sx1, sy0, sy1;
+      coarse_rect(tx0, tx1, ty0, ty1, sx0, sx1, sy0, sy1);
+      t = (unsigned)((sx1 - sx0 + 1) * (sy1 - sy0 + 1));
       for (int ty = ty0; ty <= ty1; ty++) {
         const long long r0 = (long long)ty * geo.Wt + tx0, r1 = (long long)ty * geo.Wt + tx1 + 1;
         o += (unsigned)max(0ll, min(r1, (long long)g.hi[k]) - max(r0, (long long)g.lo[k]));
       }
+      int* D = diff + (int64_t)k * (geo.Ht + 1) * (geo.Wt + 1);
+      const int W1 = geo.Wt + 1;
+      atomicAdd(D + ty0 * W1 + tx0, 1);
+      atomicAdd(D + ty0 * W1 + tx1 + 1, -1);
+      atomicAdd(D + (ty1 + 1) * W1 + tx0, -1);
+      atomicAdd(D + (ty1 + 1) * W1 + tx1 + 1, 1);
     } else {
       k = -1;
     }
   }
-  if (j <= n_recv) n_tiles[j] = t;
+  if (j <= n_recv) n_coarse[j] = t;
   // per view: the lanes of a view add their counts once (a warp's records mostly share a view)
   const unsigned peers = __match_any_sync(0xffffffffu, k);
   const int leader = __ffs(peers) - 1;
@@ -137,17 +189,17 @@ __global__ void k_cta_first(const int64_t* __restrict__ ps, int64_t n, int64_t* 
   for (int64_t c = (a + kEmitPairs - 1) / kEmitPairs; c * kEmitPairs < b; c++) first[c] = s;
 }
 
-// Emit the pairs of the ordered records: CTA c enumerates unpadded pairs [c*kEmitPairs, ...)
-// of pair_start (= scan of the tile counts in (view, depth) order) and stores each at its
-// padded position (+ shift of its view's segment): key = view-local block index if the rank
-// owns the block, else the sentinel; value = recv_idx.  The histogram of the first digit
+// Emit the coarse pairs of the ordered records: CTA c enumerates unpadded pairs
+// [c*kEmitPairs, ...) of pair_start (= scan of the coarse counts in (view, depth) order) and
+// stores each at its padded position (+ shift of its view's segment): key = view-local
+// super-tile index; value = recv_idx.  The histogram of the first digit
 // pass (bits [0, bits0)) is accumulated on the way ([segment][digit][tile] layout).  Every
 // received record has >= 1 tile (A1 emits a record only for a rectangle with an owned block),
 // so at most kEmitPairs + 1 records overlap a CTA.
 __global__ void __launch_bounds__(kEmitThreads) k_emit(
-    const gs_rec* __restrict__ rec, const uint32_t* __restrict__ order, int64_t n_recv,
+    const uint2* __restrict__ rect8, const uint32_t* __restrict__ order, int64_t n_recv,
     const int64_t* __restrict__ pair_start, const int64_t* __restrict__ first, int64_t n_full, gs_geom geo,
-    seg_arg g, int bits0, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+    cgrid cg, seg_arg g, int bits0, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
     unsigned long long* __restrict__ hist) {
   __shared__ int64_t s_start[kEmitPairs + 2];
   __shared__ int s_tx0[kEmitPairs + 1], s_ty0[kEmitPairs + 1], s_w[kEmitPairs + 1], s_k[kEmitPairs + 1];
@@ -177,13 +229,13 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(
     const int64_t sidx = slo + r;
     s_start[r] = pair_start[sidx];
     const uint32_t j = order[sidx];
-    const float4 a = rec[j].a;
-    int tx0, tx1, ty0, ty1;
-    rect_of(a.x, a.y, a.w, geo.Wt, geo.Ht, tx0, tx1, ty0, ty1);
-    s_tx0[r] = tx0;
-    s_ty0[r] = ty0;
-    s_w[r] = tx1 - tx0 + 1;
-    s_k[r] = (int)(__float_as_uint(rec[j].d.w) & 31u) - g.v_lo;
+    int tx0, tx1, ty0, ty1, v, sx0, sx1, sy0, sy1;
+    unpack_rect(rect8[j], tx0, tx1, ty0, ty1, v);
+    coarse_rect(tx0, tx1, ty0, ty1, sx0, sx1, sy0, sy1);
+    s_tx0[r] = sx0;
+    s_ty0[r] = sy0;
+    s_w[r] = sx1 - sx0 + 1;
+    s_k[r] = v - g.v_lo;
     s_j[r] = j;
   }
   if (threadIdx.x == 0) s_start[nr] = pair_start[slo + nr];
@@ -242,7 +294,7 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(
     int rm = t - q * w;
     if (rm < 0) q--, rm += w;
     else if (rm >= w) q++, rm -= w;
-    const int local = (s_ty0[lo] + q) * geo.Wt + s_tx0[lo] + rm;
+    const int local = (s_ty0[lo] + q) * cg.Cw + s_tx0[lo] + rm;
     const uint32_t key = (local >= g.lo[k] && local < g.hi[k]) ? (uint32_t)local : g.sentinel;
     const int64_t pos = pp + g.shift[k];
     keys[pos] = key;
@@ -431,6 +483,167 @@ __global__ void k_seg_ranges(const uint32_t* __restrict__ keys, seg_arg g, int64
   }
 }
 
+// 2D prefix of the difference arrays, rows first: warp per row of Wt + 1 entries.
+__global__ void k_diff_rows(int* __restrict__ diff, int64_t nrows, int W1) {
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= nrows) return;
+  int* row = diff + r * W1;
+  int carry = 0;
+  for (int x0 = 0; x0 < W1; x0 += 32) {
+    const int x = x0 + lane;
+    int v = x < W1 ? row[x] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    v += carry;
+    if (x < W1) row[x] = v;
+    carry = __shfl_sync(0xffffffffu, v, 31);
+  }
+}
+
+// ... then columns: thread per column x < Wt of view k = blockIdx.y; the running sum is block
+// (x, y)'s pair count, stored for owned blocks at their owned index (b - B_lo).
+__global__ void k_diff_cols(const int* __restrict__ diff, gs_geom geo, seg_arg g, int64_t* __restrict__ bcnt) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
+  if (x >= geo.Wt) return;
+  const int W1 = geo.Wt + 1;
+  const int* D = diff + (int64_t)k * (geo.Ht + 1) * W1 + x;
+  int64_t* out = bcnt + ((int64_t)(g.v_lo + k) * geo.per_view - g.B_lo);
+  const int lo = g.lo[k], hi = g.hi[k];
+  int run = 0;
+#pragma unroll 4
+  for (int y = 0; y < geo.Ht; y++) {
+    run += D[(int64_t)y * W1];
+    const int loc = y * geo.Wt + x;
+    if (loc >= lo && loc < hi) out[loc] = run;
+  }
+}
+
+__global__ void k_to_i32(const int64_t* __restrict__ in, int64_t n, int32_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (int32_t)in[i];
+}
+
+// 32 x 32 bit-matrix transpose across a warp: lane i holds row i (bit k = column k); lane k
+// gets column k (bit i = row i's bit k).  Five stages; stage j swaps the off-diagonal j x j
+// blocks between lanes i and i ^ j.
+__device__ __forceinline__ unsigned warp_transpose32(unsigned v, int lane) {
+  const unsigned masks[5] = {0x0000ffffu, 0x00ff00ffu, 0x0f0f0f0fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int s = 0; s < 5; s++) {
+    const int j = 16 >> s;
+    const unsigned m = masks[s];
+    const unsigned o = __shfl_xor_sync(0xffffffffu, v, j);
+    v = (lane & j) ? ((v & ~m) | ((o >> j) & m)) : ((v & m) | ((o << j) & ~m));
+  }
+  return v;
+}
+
+// Fine emission, one CTA per (view k, super-tile): the super-tile's coarse list (crange, in
+// (depth, gid) order) in chunks of 128 records, one per thread.  A record's owned blocks
+// inside the super-tile form a 64-bit mask (bit 8 j + i = block (8 sx + i, 8 sy + j)).  Each
+// warp transposes its 32 masks, so lane l holds the 32-bit sets of its lanes (= records, in
+// order) hitting block l and block l + 32; their popcounts are the warp's counts (phase 1),
+// which phase 2 turns into chunk-local offsets per block; in phase 3 lane l places the record
+// indices of its two blocks, in lane order, into the chunk's per-block staging rows; in phase
+// 4 each block's run is appended to its list with contiguous stores (the block cursors start
+// at tile_range).  Every block list keeps the coarse (depth, gid) order.
+struct fine_arg {
+  int nv, v_lo, nST;
+  int lo[GS_MAX_VIEWS], hi[GS_MAX_VIEWS];  // owned view-local blocks [lo, hi) of view k
+  long long B_lo;
+};
+__global__ void __launch_bounds__(kFineThreads) k_fine(const uint2* __restrict__ rect8,
+                                                       const uint32_t* __restrict__ clist,
+                                                       const int32_t* __restrict__ crange, gs_geom geo, cgrid cg,
+                                                       fine_arg f, const int32_t* __restrict__ range,
+                                                       uint32_t* __restrict__ out) {
+  constexpr int kW = kFineThreads / 32, kB = kST * kST;
+  __shared__ int s_cur[kB], s_cnt[kB];
+  __shared__ int s_wc[kW][kB];
+  __shared__ uint32_t s_stage[kB][kFineThreads + 1];  // +1: lanes of one position hit different banks
+  const int bid = blockIdx.x;
+  const int cs = crange[bid], ce = crange[bid + 1];
+  if (cs >= ce) return;
+  const int k = bid / f.nST, sidx = bid - k * f.nST;
+  const int bx0 = (sidx % cg.Cw) * kST, by0 = (sidx / cg.Cw) * kST;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  // the super-tile's owned blocks (every warp computes the same mask)
+  bool ob[2];
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const int b = lane + 32 * h, bx = bx0 + (b & (kST - 1)), by = by0 + (b >> kSTShift);
+    const int loc = by * geo.Wt + bx;
+    ob[h] = bx < geo.Wt && by < geo.Ht && loc >= f.lo[k] && loc < f.hi[k];
+  }
+  const unsigned own_lo = __ballot_sync(0xffffffffu, ob[0]), own_hi = __ballot_sync(0xffffffffu, ob[1]);
+  if ((own_lo | own_hi) == 0) return;
+  if (tid < kB) {
+    const int loc = (by0 + (tid >> kSTShift)) * geo.Wt + bx0 + (tid & (kST - 1));
+    s_cur[tid] = ob[tid >> 5] ? range[(int64_t)(f.v_lo + k) * geo.per_view + loc - f.B_lo] : 0;
+  }
+  for (int c0 = cs; c0 < ce; c0 += kFineThreads) {
+    __syncthreads();  // s_cur initialised / the previous chunk's staging written out
+    const int i = c0 + tid;
+    uint32_t j = 0;
+    unsigned mlo = 0, mhi = 0;
+    if (i < ce) {
+      j = clist[i];
+      int tx0, tx1, ty0, ty1, v;
+      unpack_rect(__ldg(&rect8[j]), tx0, tx1, ty0, ty1, v);
+      const int ix0 = max(tx0 - bx0, 0), ix1 = min(tx1 - bx0, kST - 1);
+      const int iy0 = max(ty0 - by0, 0), iy1 = min(ty1 - by0, kST - 1);
+      if (ix0 <= ix1 && iy0 <= iy1) {
+        const unsigned long long cols =
+            (unsigned long long)((0xffu << ix0) & (0xffu >> (kST - 1 - ix1))) * 0x0101010101010101ull;
+        const unsigned long long rows = (~0ull << (8 * iy0)) & (~0ull >> (8 * (kST - 1 - iy1)));
+        const unsigned long long m = cols & rows;
+        mlo = (unsigned)m & own_lo;
+        mhi = (unsigned)(m >> 32) & own_hi;
+      }
+    }
+    // lane l: which of the warp's records hit block l (tlo) and block l + 32 (thi)
+    unsigned tlo = warp_transpose32(mlo, lane), thi = warp_transpose32(mhi, lane);
+    s_wc[w][lane] = __popc(tlo);  // phase 1
+    s_wc[w][lane + 32] = __popc(thi);
+    __syncthreads();
+    if (tid < kB) {  // phase 2: chunk-local warp offsets per block
+      int run = 0;
+#pragma unroll
+      for (int ww = 0; ww < kW; ww++) {
+        const int t = s_wc[ww][tid];
+        s_wc[ww][tid] = run;
+        run += t;
+      }
+      s_cnt[tid] = run;
+    }
+    __syncthreads();
+    int plo = s_wc[w][lane], phi = s_wc[w][lane + 32];
+    while (__any_sync(0xffffffffu, (tlo | thi) != 0)) {  // phase 3: lane order = record order
+      const int ra = tlo ? __ffs(tlo) - 1 : 0, rb = thi ? __ffs(thi) - 1 : 0;
+      const uint32_t ja = __shfl_sync(0xffffffffu, j, ra), jb = __shfl_sync(0xffffffffu, j, rb);
+      if (tlo) {
+        s_stage[lane][plo++] = ja;
+        tlo &= tlo - 1;
+      }
+      if (thi) {
+        s_stage[lane + 32][phi++] = jb;
+        thi &= thi - 1;
+      }
+    }
+    __syncthreads();
+    for (int b = w; b < kB; b += kW) {  // phase 4: each block's run, contiguous
+      const int n = s_cnt[b], base = s_cur[b];
+      for (int t = lane; t < n; t += 32) out[base + t] = s_stage[b][t];
+      __syncwarp();
+      if (lane == 0) s_cur[b] = base + n;
+    }
+  }
+}
+
 constexpr int kScatterSmem = 2 * kRadixTile * (int)sizeof(uint32_t);
 // the scatter kernels' dynamic shared memory above the 48 KB default (once per process)
 bool scatter_smem_ready() {
@@ -505,46 +718,89 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
     g.lo[k] = (int)std::max<int64_t>(B_lo - v * pv, 0);
     g.hi[k] = (int)std::min<int64_t>(B_hi - v * pv, pv);
   }
-  const int nbits = 32 - __builtin_clz((unsigned)pv);  // 2^nbits > pv: the sentinel exceeds every key
-  g.sentinel = (nbits >= 32) ? 0xffffffffu : ((1u << nbits) - 1u);
-  const int passes = (nbits + 7) / 8, width = (nbits + passes - 1) / passes;
-  // 1. per-record tile counts, per-view pair and owned-pair totals (one host sync)
-  int64_t* ntiles = (int64_t*)gs_slot_get(c, SLOT_RECTILES, (n_recv + 1) * sizeof(int64_t), st);
+  // the coarse grid (super-tiles of 8 x 8 blocks) and its segment layout arguments
+  cgrid cg;
+  cg.Cw = (geo.Wt + kST - 1) / kST;
+  cg.Ch = (geo.Ht + kST - 1) / kST;
+  const int nST = cg.Cw * cg.Ch;
+  fine_arg fa;
+  memset(&fa, 0, sizeof(fa));
+  fa.nv = g.nv;
+  fa.v_lo = g.v_lo;
+  fa.nST = nST;
+  fa.B_lo = B_lo;
+  for (int k = 0; k < g.nv; k++) fa.lo[k] = g.lo[k], fa.hi[k] = g.hi[k];
+  GS_REQUIRE(c, (int64_t)g.nv * nST < (1ll << 31) - 1, "too many super-tiles");
+  GS_REQUIRE(c, geo.Wt < (1 << 16) && geo.Ht < (1 << 13), "image of %d x %d blocks exceeds the packed rectangle",
+             geo.Wt, geo.Ht);
+  // 1. per-record coarse counts, block-count difference arrays, per-view coarse and owned-pair
+  //    totals (one host sync)
+  const int64_t dsz = (int64_t)g.nv * (geo.Ht + 1) * (geo.Wt + 1);
+  int64_t* ncoarse = (int64_t*)gs_slot_get(c, SLOT_RECTILES, (n_recv + 1) * sizeof(int64_t), st);
   int64_t* ps = (int64_t*)gs_slot_get(c, SLOT_PSTART, (n_recv + 1) * sizeof(int64_t), st);
   unsigned long long* vc = (unsigned long long*)gs_slot_get(c, SLOT_COUNTS, 2 * GS_MAX_VIEWS * sizeof(int64_t), st);
-  if (!ntiles || !ps || !vc) return gs_fail(c, GS_ECUDA, "scratch");
+  int* diff = (int*)gs_slot_get(c, SLOT_DIFF, dsz * sizeof(int), st);
+  uint2* rect8 = (uint2*)gs_slot_get(c, SLOT_RECT8, n_recv * sizeof(uint2), st);
+  if (!ncoarse || !ps || !vc || !diff || !rect8) return gs_fail(c, GS_ECUDA, "scratch");
   GS_CUDA(c, cudaMemsetAsync(vc, 0, 2 * GS_MAX_VIEWS * sizeof(int64_t), st));
+  GS_CUDA(c, cudaMemsetAsync(diff, 0, dsz * sizeof(int), st));
   ++c->launches;
-  k_tile_counts<<<(unsigned)((n_recv + 256) / 256), 256, 0, st>>>(rec, n_recv, geo, g, ntiles, vc,
-                                                                  vc + GS_MAX_VIEWS);
+  k_tile_counts<<<(unsigned)((n_recv + 256) / 256), 256, 0, st>>>(rec, n_recv, geo, g, ncoarse, vc,
+                                                                  vc + GS_MAX_VIEWS, diff, rect8);
   GS_LAUNCH_CHECK(c, "tile counts");
   GS_CUDA(c, cudaMemcpyAsync(c->pinned, vc, 2 * GS_MAX_VIEWS * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GS_CUDA(c, cudaStreamSynchronize(st));
+  // coarse segments: every super-tile key is "owned" ([0, nST)); the sentinel pads
+  seg_arg cgs = g;
+  const int nbits = 32 - __builtin_clz((unsigned)nST);  // 2^nbits > nST: the sentinel exceeds every key
+  cgs.sentinel = (1u << nbits) - 1u;
+  cgs.B_lo = (long long)g.v_lo * nST;
+  const int passes = (nbits + 7) / 8, width = (nbits + passes - 1) / passes;
   int64_t n_full = 0, K = 0;
-  g.seg[0] = 0;
-  g.kcum[0] = 0;
+  cgs.seg[0] = 0;
+  cgs.kcum[0] = 0;
   for (int k = 0; k < g.nv; k++) {
     const int64_t cnt = c->pinned[k], own = c->pinned[GS_MAX_VIEWS + k];
+    cgs.lo[k] = 0;
+    cgs.hi[k] = nST;
     // >= 1 padding sentinel per segment (k_seg_ranges reads the segment's end off it)
-    g.seg[k + 1] = g.seg[k] + (cnt + 1 + kRadixTile - 1) / kRadixTile * kRadixTile;
-    g.shift[k] = g.seg[k] - n_full;
-    g.kcum[k + 1] = g.kcum[k] + own;
+    cgs.seg[k + 1] = cgs.seg[k] + (cnt + 1 + kRadixTile - 1) / kRadixTile * kRadixTile;
+    cgs.shift[k] = cgs.seg[k] - n_full;
+    cgs.kcum[k + 1] = cgs.kcum[k] + cnt;
     n_full += cnt;
     K += own;
   }
-  const int64_t n_pad = g.seg[g.nv];
+  const int64_t n_pad = cgs.seg[g.nv];
   *n_pairs_h = K;
-  if (n_pad >= (1ll << 31))
-    return gs_fail(c, GS_ENOTSUP, "pair total %lld exceeds int32 positions", (long long)n_pad);
+  if (n_pad >= (1ll << 31) || K >= (1ll << 31))
+    return gs_fail(c, GS_ENOTSUP, "pair total %lld exceeds int32 positions", (long long)std::max(n_pad, K));
   if (K > pair_cap) return gs_fail(c, GS_ECAPACITY, "pair capacity %lld < %lld", (long long)pair_cap, (long long)K);
   GS_REQUIRE(c, K == 0 || sorted_idx != nullptr, "null sorted_idx");
+  // 2. block offsets: 2D prefix of the difference arrays, owned counts, exclusive scan
+  int64_t* bcnt = (int64_t*)gs_slot_get(c, SLOT_BCOUNT, (n_owned + 1) * sizeof(int64_t), st);
+  if (!bcnt) return gs_fail(c, GS_ECUDA, "scratch");
+  GS_CUDA(c, cudaMemsetAsync(bcnt + n_owned, 0, sizeof(int64_t), st));
+  const int64_t nrows = (int64_t)g.nv * (geo.Ht + 1);
+  ++c->launches;
+  k_diff_rows<<<(unsigned)((nrows * 32 + 255) / 256), 256, 0, st>>>(diff, nrows, geo.Wt + 1);
+  ++c->launches;
+  k_diff_cols<<<dim3((unsigned)((geo.Wt + 127) / 128), (unsigned)g.nv), 128, 0, st>>>(diff, geo, g, bcnt);
+  GS_LAUNCH_CHECK(c, "block counts");
+  s = gs_scan_i64(c, bcnt, bcnt, n_owned + 1, 0, st);
+  if (s != GS_OK) return s;
+  ++c->launches;
+  k_to_i32<<<(unsigned)((n_owned + 256) / 256), 256, 0, st>>>(bcnt, n_owned + 1, tile_range);
+  GS_LAUNCH_CHECK(c, "block ranges");
+  if (K == 0) return GS_OK;
+  // 3. records by (view, depth): 4 stable 8-bit depth passes (A -> B -> A -> B -> A), then the
+  //    view (-> B -> A, values only kept)
   const int64_t cap = std::max(n_pad, n_recv);
   uint32_t* A = (uint32_t*)gs_slot_get(c, SLOT_KEYS, 2 * cap * sizeof(uint32_t), st);
   uint32_t* Bf = (uint32_t*)gs_slot_get(c, SLOT_KEYS_TMP, 2 * cap * sizeof(uint32_t), st);
-  if (!A || !Bf) return gs_fail(c, GS_ECUDA, "radix scratch (%lld pairs)", (long long)cap);
+  uint32_t* clist = (uint32_t*)gs_slot_get(c, SLOT_CLIST, std::max<int64_t>(n_full, 1) * sizeof(uint32_t), st);
+  int32_t* crange = (int32_t*)gs_slot_get(c, SLOT_CRANGE, ((int64_t)g.nv * nST + 1) * sizeof(int32_t), st);
+  if (!A || !Bf || !clist || !crange) return gs_fail(c, GS_ECUDA, "radix scratch (%lld pairs)", (long long)cap);
   uint32_t *ka = A, *va = A + cap, *kb = Bf, *vb = Bf + cap;
-  // 2. records by (view, depth): 4 stable 8-bit depth passes (A -> B -> A -> B -> A), then the
-  //    view (-> B -> A, values only kept)
   ++c->launches;
   k_depth_keys<<<(unsigned)((n_recv + 255) / 256), 256, 0, st>>>(rec, n_recv, ka, va);
   for (int p = 0; p < 4; p++) {
@@ -560,10 +816,10 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
     std::swap(ka, kb);
     std::swap(va, vb);
   }
-  // 3. pair starts in (view, depth) order; pairs (local block or sentinel, recv_idx) -> B, with
-  //    the first pass's histogram
+  // 4. coarse pair starts in (view, depth) order; coarse pairs (super-tile, recv_idx) -> B,
+  //    with the first pass's histogram
   ++c->launches;
-  k_gather_tiles<<<(unsigned)((n_recv + 256) / 256), 256, 0, st>>>(va, ntiles, n_recv, ps);
+  k_gather_tiles<<<(unsigned)((n_recv + 256) / 256), 256, 0, st>>>(va, ncoarse, n_recv, ps);
   s = gs_scan_i64(c, ps, ps, n_recv + 1, 0, st);
   if (s != GS_OK) return s;
   const int64_t ntl = n_pad / kRadixTile;
@@ -572,44 +828,48 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
       (unsigned long long*)gs_slot_get(c, SLOT_RADIX_HIST, (size_t)(1 << width) * ntl * sizeof(int64_t), st);
   if (!hist) return gs_fail(c, GS_ECUDA, "radix histogram scratch");
   GS_CUDA(c, cudaMemsetAsync(hist, 0, (size_t)bins0 * ntl * sizeof(int64_t), st));
-  if (n_full > 0) {
+  {
     const int64_t nct = (n_full + kEmitPairs - 1) / kEmitPairs;
     int64_t* first = (int64_t*)gs_slot_get(c, SLOT_LARGE, (nct + 1) * sizeof(int64_t), st);
     if (!first) return gs_fail(c, GS_ECUDA, "scratch");
     ++c->launches;
     k_cta_first<<<(unsigned)((n_recv + 255) / 256), 256, 0, st>>>(ps, n_recv, first);
     ++c->launches;
-    k_emit<<<(unsigned)nct, kEmitThreads, 0, st>>>(rec, va, n_recv, ps, first, n_full, geo, g, std::min(width, nbits),
-                                                   kb, vb, hist);
+    k_emit<<<(unsigned)nct, kEmitThreads, 0, st>>>(rect8, va, n_recv, ps, first, n_full, geo, cg, cgs,
+                                                   std::min(width, nbits), kb, vb, hist);
   }
   ++c->launches;
-  k_pad<<<dim3(4, g.nv), 256, 0, st>>>(g, vc, std::min(width, nbits), kb, hist);
+  k_pad<<<dim3(4, g.nv), 256, 0, st>>>(cgs, vc, std::min(width, nbits), kb, hist);
   GS_LAUNCH_CHECK(c, "bin_sort emit");
-  // 4. stable segmented sort by view-local block index; the last pass writes the owned values
-  //    compactly into sorted_idx and the keys into scratch
+  // 5. stable segmented sort by view-local super-tile; the last pass writes the record indices
+  //    compactly into clist and the keys into scratch
   uint32_t *kin = kb, *vin = vb, *kout = ka, *vout = va;
   for (int p = 0; p < passes; p++) {
     const int shift = p * width, bits = std::min(width, nbits - shift), bins = 1 << bits;
     if (p > 0) {
       ++c->launches;
-      k_radix_hist<true><<<(unsigned)ntl, kRadixThreads, 0, st>>>(kin, n_pad, shift, bits, ntl, g, hist);
+      k_radix_hist<true><<<(unsigned)ntl, kRadixThreads, 0, st>>>(kin, n_pad, shift, bits, ntl, cgs, hist);
     }
     s = gs_scan_i64(c, (const int64_t*)hist, (int64_t*)hist, (int64_t)bins * ntl, 0, st);
     if (s != GS_OK) return s;
     ++c->launches;
     if (p == passes - 1)
-      k_radix_scatter<true, true><<<(unsigned)ntl, kRadixThreads, kScatterSmem, st>>>(kin, vin, kout, sorted_idx, n_pad, shift,
-                                                                          bits, ntl, g, hist, pair_cap);
+      k_radix_scatter<true, true><<<(unsigned)ntl, kRadixThreads, kScatterSmem, st>>>(kin, vin, kout, clist, n_pad,
+                                                                                      shift, bits, ntl, cgs, hist,
+                                                                                      n_full);
     else
-      k_radix_scatter<true, false><<<(unsigned)ntl, kRadixThreads, kScatterSmem, st>>>(kin, vin, kout, vout, n_pad, shift, bits,
-                                                                           ntl, g, hist, 0);
+      k_radix_scatter<true, false><<<(unsigned)ntl, kRadixThreads, kScatterSmem, st>>>(kin, vin, kout, vout, n_pad,
+                                                                                       shift, bits, ntl, cgs, hist, 0);
     GS_LAUNCH_CHECK(c, "bin_sort pass");
     std::swap(kin, kout);
     std::swap(vin, vout);
   }
-  // 5. ranges from the sorted keys (now in kin)
+  // 6. super-tile ranges of the coarse lists (sorted keys now in kin), then the fine emission
   ++c->launches;
-  k_seg_ranges<<<(unsigned)(n_pad / 1024), 256, 0, st>>>(kin, g, pv, tile_range);
-  GS_LAUNCH_CHECK(c, "bin_sort ranges");
+  k_seg_ranges<<<(unsigned)(n_pad / 1024), 256, 0, st>>>(kin, cgs, nST, crange);
+  ++c->launches;
+  k_fine<<<(unsigned)((int64_t)g.nv * nST), kFineThreads, 0, st>>>(rect8, clist, crange, geo, cg, fa, tile_range,
+                                                                   sorted_idx);
+  GS_LAUNCH_CHECK(c, "bin_sort fine");
   return GS_OK;
 }
