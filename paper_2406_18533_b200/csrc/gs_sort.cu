@@ -546,11 +546,14 @@ __device__ __forceinline__ unsigned warp_transpose32(unsigned v, int lane) {
 // (depth, gid) order) in chunks of 128 records, one per thread.  A record's owned blocks
 // inside the super-tile form a 64-bit mask (bit 8 j + i = block (8 sx + i, 8 sy + j)).  Each
 // warp transposes its 32 masks, so lane l holds the 32-bit sets of its lanes (= records, in
-// order) hitting block l and block l + 32; their popcounts are the warp's counts (phase 1),
-// which phase 2 turns into chunk-local offsets per block; in phase 3 lane l places the record
-// indices of its two blocks, in lane order, into the chunk's per-block staging rows; in phase
-// 4 each block's run is appended to its list with contiguous stores (the block cursors start
-// at tile_range).  Every block list keeps the coarse (depth, gid) order.
+// order) hitting block l and block l + 32; their popcounts are the warp's counts (phase 1).
+// Phase 2 (warp 0) turns them into offsets: per block the earlier warps' counts, and the
+// block's place in the chunk's staging array (blocks back to back, an exclusive scan of the
+// chunk's per-block totals).  In phase 3 lane l places the record indices of its two blocks,
+// in lane order, into the staging array (and the block of every staged entry); in phase 4 the
+// CTA walks the staged entries linearly and stores each at its block's cursor (started at
+// tile_range) + its place in the block's run: consecutive threads store mostly consecutive
+// addresses.  Every block list keeps the coarse (depth, gid) order.
 struct fine_arg {
   int nv, v_lo, nST;
   int lo[GS_MAX_VIEWS], hi[GS_MAX_VIEWS];  // owned view-local blocks [lo, hi) of view k
@@ -562,9 +565,12 @@ __global__ void __launch_bounds__(kFineThreads) k_fine(const uint2* __restrict__
                                                        fine_arg f, const int32_t* __restrict__ range,
                                                        uint32_t* __restrict__ out) {
   constexpr int kW = kFineThreads / 32, kB = kST * kST;
-  __shared__ int s_cur[kB], s_cnt[kB];
+  __shared__ int s_cur[kB];   // block cursor (next free position of its list)
+  __shared__ int s_dst[kB];   // this chunk: cursor - staging start of the block
   __shared__ int s_wc[kW][kB];
-  __shared__ uint32_t s_stage[kB][kFineThreads + 1];  // +1: lanes of one position hit different banks
+  __shared__ int s_tot;
+  __shared__ uint32_t s_flat[kB * kFineThreads];
+  __shared__ uint8_t s_blk[kB * kFineThreads];
   const int bid = blockIdx.x;
   const int cs = crange[bid], ce = crange[bid + 1];
   if (cs >= ce) return;
@@ -610,37 +616,55 @@ __global__ void __launch_bounds__(kFineThreads) k_fine(const uint2* __restrict__
     s_wc[w][lane] = __popc(tlo);  // phase 1
     s_wc[w][lane + 32] = __popc(thi);
     __syncthreads();
-    if (tid < kB) {  // phase 2: chunk-local warp offsets per block
-      int run = 0;
+    if (w == 0) {  // phase 2: blocks lane and lane + 32
+      int ra = 0, rb = 0;
 #pragma unroll
       for (int ww = 0; ww < kW; ww++) {
-        const int t = s_wc[ww][tid];
-        s_wc[ww][tid] = run;
-        run += t;
+        const int ta = s_wc[ww][lane], tb = s_wc[ww][lane + 32];
+        s_wc[ww][lane] = ra;
+        s_wc[ww][lane + 32] = rb;
+        ra += ta;
+        rb += tb;
       }
-      s_cnt[tid] = run;
+      // staging starts: exclusive scan of the 64 block totals (blocks 0..31, then 32..63)
+      int ia = ra, ib = rb;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int ya = __shfl_up_sync(0xffffffffu, ia, o), yb = __shfl_up_sync(0xffffffffu, ib, o);
+        if (lane >= o) ia += ya, ib += yb;
+      }
+      const int tot_a = __shfl_sync(0xffffffffu, ia, 31);
+      const int sa = ia - ra, sb = tot_a + ib - rb;
+      // the warp offsets become staging positions; s_dst maps them to list positions
+      for (int ww = 0; ww < kW; ww++) s_wc[ww][lane] += sa, s_wc[ww][lane + 32] += sb;
+      const int ca = s_cur[lane], cb = s_cur[lane + 32];
+      s_dst[lane] = ca - sa;
+      s_dst[lane + 32] = cb - sb;
+      s_cur[lane] = ca + ra;
+      s_cur[lane + 32] = cb + rb;
+      if (lane == 31) s_tot = tot_a + ib;
     }
     __syncthreads();
     int plo = s_wc[w][lane], phi = s_wc[w][lane + 32];
     while (__any_sync(0xffffffffu, (tlo | thi) != 0)) {  // phase 3: lane order = record order
-      const int ra = tlo ? __ffs(tlo) - 1 : 0, rb = thi ? __ffs(thi) - 1 : 0;
-      const uint32_t ja = __shfl_sync(0xffffffffu, j, ra), jb = __shfl_sync(0xffffffffu, j, rb);
+      const int ra = __ffs(tlo) - 1, rb = __ffs(thi) - 1;  // -1 (unused) when empty
+      const uint32_t ja = __shfl_sync(0xffffffffu, j, ra & 31), jb = __shfl_sync(0xffffffffu, j, rb & 31);
       if (tlo) {
-        s_stage[lane][plo++] = ja;
+        s_flat[plo] = ja;
+        s_blk[plo] = (uint8_t)lane;
+        plo++;
         tlo &= tlo - 1;
       }
       if (thi) {
-        s_stage[lane + 32][phi++] = jb;
+        s_flat[phi] = jb;
+        s_blk[phi] = (uint8_t)(lane + 32);
+        phi++;
         thi &= thi - 1;
       }
     }
     __syncthreads();
-    for (int b = w; b < kB; b += kW) {  // phase 4: each block's run, contiguous
-      const int n = s_cnt[b], base = s_cur[b];
-      for (int t = lane; t < n; t += 32) out[base + t] = s_stage[b][t];
-      __syncwarp();
-      if (lane == 0) s_cur[b] = base + n;
-    }
+    const int tot = s_tot;
+    for (int e = tid; e < tot; e += kFineThreads) out[s_dst[s_blk[e]] + e] = s_flat[e];  // phase 4
   }
 }
 
