@@ -565,12 +565,13 @@ __global__ void __launch_bounds__(kFineThreads) k_fine(const uint2* __restrict__
                                                        fine_arg f, const int32_t* __restrict__ range,
                                                        uint32_t* __restrict__ out) {
   constexpr int kW = kFineThreads / 32, kB = kST * kST;
+  constexpr int kStage = kB / 2 * kFineThreads;  // staged entries per pass (one half of the blocks)
   __shared__ int s_cur[kB];   // block cursor (next free position of its list)
   __shared__ int s_dst[kB];   // this chunk: cursor - staging start of the block
   __shared__ int s_wc[kW][kB];
-  __shared__ int s_tot;
-  __shared__ uint32_t s_flat[kB * kFineThreads];
-  __shared__ uint8_t s_blk[kB * kFineThreads];
+  __shared__ int s_tot, s_tot_a;
+  __shared__ uint32_t s_flat[kStage + 1];
+  __shared__ uint8_t s_blk[kStage + 1];
   const int bid = blockIdx.x;
   const int cs = crange[bid], ce = crange[bid + 1];
   if (cs >= ce) return;
@@ -642,29 +643,35 @@ __global__ void __launch_bounds__(kFineThreads) k_fine(const uint2* __restrict__
       s_dst[lane + 32] = cb - sb;
       s_cur[lane] = ca + ra;
       s_cur[lane + 32] = cb + rb;
-      if (lane == 31) s_tot = tot_a + ib;
+      if (lane == 31) s_tot = tot_a + ib, s_tot_a = tot_a;
     }
     __syncthreads();
-    int plo = s_wc[w][lane], phi = s_wc[w][lane + 32];
-    while (__any_sync(0xffffffffu, (tlo | thi) != 0)) {  // phase 3: lane order = record order
-      const int ra = __ffs(tlo) - 1, rb = __ffs(thi) - 1;  // -1 (unused) when empty
-      const uint32_t ja = __shfl_sync(0xffffffffu, j, ra & 31), jb = __shfl_sync(0xffffffffu, j, rb & 31);
-      if (tlo) {
-        s_flat[plo] = ja;
-        s_blk[plo] = (uint8_t)lane;
-        plo++;
-        tlo &= tlo - 1;
+    // phases 3 + 4 over the staging array; a chunk with more than kStage entries is staged in
+    // two halves (blocks 0..31, then 32..63: at most 32 x 128 entries each)
+    const int tot = s_tot, tot_a = s_tot_a;
+    const bool split = tot > kStage;
+    for (int half = 0; half < (split ? 2 : 1); half++) {
+      unsigned xa = (split && half == 1) ? 0u : tlo, xb = (split && half == 0) ? 0u : thi;
+      const int sh = (split && half == 1) ? tot_a : 0;  // staging position of the pass's first entry
+      int plo = s_wc[w][lane] - sh, phi = s_wc[w][lane + 32] - sh;
+      while (__any_sync(0xffffffffu, (xa | xb) != 0)) {  // phase 3: lane order = record order
+        const int ra = __ffs(xa) - 1, rb = __ffs(xb) - 1;  // -1 (unused) when empty
+        const uint32_t ja = __shfl_sync(0xffffffffu, j, ra & 31), jb = __shfl_sync(0xffffffffu, j, rb & 31);
+        const int da = xa ? plo : kStage, db = xb ? phi : kStage;  // kStage: a dummy slot
+        s_flat[da] = ja;
+        s_blk[da] = (uint8_t)lane;
+        s_flat[db] = jb;
+        s_blk[db] = (uint8_t)(lane + 32);
+        plo += xa != 0u;
+        phi += xb != 0u;
+        xa &= xa - 1;
+        xb &= xb - 1;
       }
-      if (thi) {
-        s_flat[phi] = jb;
-        s_blk[phi] = (uint8_t)(lane + 32);
-        phi++;
-        thi &= thi - 1;
-      }
+      __syncthreads();
+      const int n = split ? (half ? tot - tot_a : tot_a) : tot;
+      for (int e = tid; e < n; e += kFineThreads) out[s_dst[s_blk[e]] + sh + e] = s_flat[e];  // phase 4
+      if (split && half == 0) __syncthreads();  // the staging is reused by the second half
     }
-    __syncthreads();
-    const int tot = s_tot;
-    for (int e = tid; e < tot; e += kFineThreads) out[s_dst[s_blk[e]] + e] = s_flat[e];  // phase 4
   }
 }
 
