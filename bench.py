@@ -153,52 +153,127 @@ def peaks():
 
 # ----------------------------------------------------------------------------- oracle arm
 
-def oracle_sample(scene, cam, gt_img, n_blocks=16, adam_frac=1.0 / 16, seed=0):
-    """One bounded sample of one view of the workload, run by the CPU oracle as it stands
-    (single thread).  Sample: project ALL Gaussians for the view (O1-O9, measured as is),
-    build the lists of and render forward + L1 + backward a window of `n_blocks` blocks
-    (O11-O15), transformation backward of the records that window touched (O16), Adam over a
-    1/16 slice of the Gaussians (O17).  Render is scaled to all blocks of the view, the
-    transformation backward to all records of the view, Adam to all Gaussians (then shared by
-    the b views of the batch)."""
+def cpu_info():
+    """Host CPU model and logical CPU count (lscpu; os.cpu_count() if lscpu is missing)."""
+    info = {"logical_cpus": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[k.strip()] = v.strip()
+    except Exception:
+        pass
+    return info
+
+
+def _chunks(n, k):
+    return [(n * i // k, n * (i + 1) // k) for i in range(k) if n * (i + 1) // k > n * i // k]
+
+
+def oracle_sample(scene, cam, gt_img, threads=1, n_windows=16, win=64, adam_frac=1.0 / 16, seed=0):
+    """One bounded sample of one view of the workload, run by the CPU oracle as it stands, on
+    `threads` host threads (the C oracle releases the GIL; work is split into disjoint chunks
+    whose results are concatenated in order -- the oracle's arithmetic is untouched).
+    Sample: project ALL Gaussians for the view (O1-O9, measured as is); `n_windows` windows of
+    `win` consecutive blocks, stratified over the view's block rows (window w starts at block
+    ((w + 1/2) / n_windows) * blocks, shifted by `seed`): their lists (O11), render forward + L1
+    + backward (O12-O15); the transformation backward of the records the windows touched (O16);
+    Adam over a 1/16 slice of the Gaussians (O17).  Scaled: render to all blocks of the view,
+    lists to one pass over the view's records (one window's list time), the transformation
+    backward to all records of the view, Adam to all Gaussians (shared by the b views)."""
+    import concurrent.futures as cf
     import oracle
     n = scene.n
     W, H = cam.width, cam.height
     Wt, Ht = (W + 15) // 16, (H + 15) // 16
+    nblk = Wt * Ht
+    ex = cf.ThreadPoolExecutor(max(1, threads))
+    wall0 = time.perf_counter()
+    cpu0 = time.process_time()
+    # O1-O9 over Gaussian chunks (records of a chunk are in gid order, chunks concatenated in order)
     t0 = time.perf_counter()
-    recs = oracle.make_records(scene, [cam], "parity")
+    parts = list(ex.map(lambda lh: (lh[0], oracle.make_records(scene.slice(*lh), [cam], "parity")),
+                        _chunks(n, max(1, threads))))
+    vi = np.concatenate([r.vi + np.array([0, lo]) for lo, r in parts])
+    recs = oracle.Records(np.concatenate([r.rec_f for _, r in parts]), np.concatenate([r.rec_i for _, r in parts]),
+                          vi, np.concatenate([r.clamp for _, r in parts]))
     t1 = time.perf_counter()
-    k = (seed * 7919) % max(1, Wt * Ht - n_blocks)
-    c = max(0, min((Ht // 2) * Wt + Wt // 2 + k - Wt * Ht // 2, Wt * Ht - n_blocks)) if seed else (Ht // 2) * Wt + Wt // 2
-    b0, b1 = c, min(c + n_blocks, Wt * Ht)
-    off, ent = oracle.tile_lists(recs, b0, b1, Wt, Ht)
-    t1b = time.perf_counter()
-    f = oracle.render_fwd(recs, off, ent, b0, b1, W, H, (0, 0, 0), gt_img[None], 1)
-    g = oracle.render_bwd(recs, off, ent, b0, b1, W, H, f["dl_dc"])
+    win = min(win, nblk)
+    n_windows = max(1, min(n_windows, nblk // win))
+    shift = (seed * 7919) % max(1, nblk // n_windows)
+    starts = [min(int((w + 0.5) * nblk / n_windows) - win // 2 + shift, nblk - win) for w in range(n_windows)]
+    starts = [max(0, s0) for s0 in starts]
+
+    def window(b0):
+        tl = time.perf_counter()
+        off, ent = oracle.tile_lists(recs, b0, b0 + win, Wt, Ht)
+        tr = time.perf_counter()
+        f = oracle.render_fwd(recs, off, ent, b0, b0 + win, W, H, (0, 0, 0), gt_img[None], 1)
+        g = oracle.render_bwd(recs, off, ent, b0, b0 + win, W, H, f["dl_dc"])
+        touched = np.unique(ent)
+        return tr - tl, time.perf_counter() - tr, touched, g[touched]
+
+    wres = list(ex.map(window, starts))
     t2 = time.perf_counter()
-    touched = np.unique(ent)
+    touched, inv = np.unique(np.concatenate([w[2] for w in wres]), return_inverse=True)
+    grad = np.zeros((len(touched), 9))
+    np.add.at(grad, inv, np.concatenate([w[3] for w in wres]))
     gidx = recs.vi[touched, 1]
-    sub = synth.Scene(scene.pos[gidx], scene.log_scale[gidx], scene.rot[gidx], scene.opac_logit[gidx],
-                      scene.sh[gidx])
-    sel = oracle.Records(None, None, np.stack([np.zeros(len(touched), np.int64), np.arange(len(touched))], 1), None)
-    oracle.project_bwd(sub, [cam], sel, g[touched])
+
+    def pbwd(lh):
+        lo, hi = lh
+        sub = synth.Scene(scene.pos[gidx[lo:hi]], scene.log_scale[gidx[lo:hi]], scene.rot[gidx[lo:hi]],
+                          scene.opac_logit[gidx[lo:hi]], scene.sh[gidx[lo:hi]])
+        sel = oracle.Records(None, None, np.stack([np.zeros(hi - lo, np.int64), np.arange(hi - lo)], 1), None)
+        return oracle.project_bwd(sub, [cam], sel, grad[lo:hi])
+
+    list(ex.map(pbwd, _chunks(len(touched), max(1, threads))))
     t3 = time.perf_counter()
     m = max(1, int(n * adam_frac))
-    flat = oracle.flatten_params(scene.slice(0, m))
-    oracle.adam(flat, np.zeros_like(flat), np.zeros_like(flat), np.zeros_like(flat), 1e-3, batch=1, step=1)
+
+    def adam(lh):
+        flat = oracle.flatten_params(scene.slice(*lh))
+        return oracle.adam(flat, np.zeros_like(flat), np.zeros_like(flat), np.zeros_like(flat), 1e-3, batch=1, step=1)
+
+    list(ex.map(adam, _chunks(m, max(1, threads))))
     t4 = time.perf_counter()
+    ex.shutdown()
+    sampled = n_windows * win
     proj = t1 - t0
-    lists = t1b - t1  # one pass over all records (the window's lists are its output)
-    rend = (t2 - t1b) * (Wt * Ht) / max(b1 - b0, 1)
+    lists = float(np.mean([w[0] for w in wres]))  # one window's lists ~ one pass over the view's records
+    rend = (t2 - t1) * nblk / sampled
     pb = (t3 - t2) * recs.n / max(len(touched), 1)
-    adam = (t4 - t3) * n / m
-    return dict(sec_per_view_est=proj + lists + rend + pb, adam_per_batch=adam, cpu_s=t4 - t0,
-                parts=dict(project=proj, lists=lists, render=rend, proj_bwd=pb, adam=adam))
+    adam_t = (t4 - t3) * n / m
+    return dict(sec_per_view_est=proj + lists + rend + pb, adam_per_batch=adam_t, wall_s=t4 - wall0,
+                cpu_s=time.process_time() - cpu0, threads=max(1, threads), blocks_sampled=sampled, windows=n_windows, win=win,
+                parts=dict(project=proj, lists=lists, render=rend, proj_bwd=pb, adam=adam_t))
 
 
 def cpu_views_per_s(sample, b):
     per_view = sample["sec_per_view_est"] + sample["adam_per_batch"] / b
     return 1.0 / per_view
+
+
+SAMPLE_TEXT = ("one view: all Gaussians projected (O1-O9); %d blocks in %d windows of %d stratified over the "
+               "view's block rows: lists (O11), render fwd + L1 + bwd (O12-O15), scaled to all blocks; the "
+               "touched records' transformation backward (O16), scaled to all records; Adam over 1/16 of the "
+               "Gaussians (O17), scaled and shared by the batch's b views")
+
+
+def oracle_baseline(scene, cam, gt, b, seed=0):
+    """The oracle on all host cores and on one thread (SURVEY §8(d) "Modes"), same sample."""
+    ncpu = os.cpu_count() or 1
+    s_all = oracle_sample(scene, cam, gt, threads=ncpu, seed=seed)
+    s_one = oracle_sample(scene, cam, gt, threads=1, seed=seed)
+    return {"value": cpu_views_per_s(s_all, b), "unit": "views/s", "cores": s_all["threads"], "kind": "oracle",
+            "sample": SAMPLE_TEXT % (s_all["blocks_sampled"], s_all["windows"], s_all["win"])
+                      + "; %.1f s wall on %d threads, %.1f s on 1" % (s_all["wall_s"], s_all["threads"],
+                                                                      s_one["wall_s"]),
+            "cpu": cpu_info(),
+            "parts_s_per_view": {k: round(v, 3) for k, v in s_all["parts"].items()},
+            "single_thread": {"value": cpu_views_per_s(s_one, b), "cores": 1,
+                              "parts_s_per_view": {k: round(v, 3) for k, v in s_one["parts"].items()}}}
 
 
 def run_reference(args, cfg):
@@ -209,11 +284,12 @@ def run_reference(args, cfg):
     cams = make_cameras(cfg)
     sched = batches(cfg, args.warmup + args.steps)
     times, samples = [], []
+    ncpu = os.cpu_count() or 1
     for k in range(args.warmup + args.steps):
         cam = cams[sched[k][0]]
         gt = synth.gt_image(cfg["seed"], cam)
         t = time.perf_counter()
-        s = oracle_sample(scene, cam, gt, seed=k)
+        s = oracle_sample(scene, cam, gt, threads=ncpu, seed=k)
         if k >= args.warmup:
             times.append(time.perf_counter() - t)
             samples.append(cpu_views_per_s(s, cfg["b"]))
@@ -222,11 +298,10 @@ def run_reference(args, cfg):
             "warmup": args.warmup, "ms_per_step": 1000.0 * float(np.mean(times)), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": cfg["workload"], "global_batch": cfg["b"], "parallelism": "oracle-cpu-1-thread"},
-            "cpu_baseline": {"value": v, "unit": "views/s", "cores": 1, "kind": "oracle",
-                             "sample": "per step: one view; all Gaussians projected; 16 blocks rendered fwd+L1+bwd "
-                                       "(scaled to all blocks); their records' transformation backward (scaled "
-                                       "to all records); Adam over 1/16 of the Gaussians (scaled, shared by b views)"},
+            "config": {"workload": cfg["workload"], "global_batch": cfg["b"],
+                       "parallelism": "oracle-cpu-%d-threads" % ncpu},
+            "cpu_baseline": {"value": v, "unit": "views/s", "cores": ncpu, "kind": "oracle", "cpu": cpu_info(),
+                             "sample": "per step: " + SAMPLE_TEXT % (s["blocks_sampled"], s["windows"], s["win"])},
             "e2e": {"value": v, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -594,12 +669,7 @@ def main():
         full = scene
         cam = batch_cams(0)[0]
         gt = gt_pool[sched[0][0]].cpu().numpy()
-        s = oracle_sample(full, cam, gt)
-        cpu = {"value": cpu_views_per_s(s, cfg["b"]), "unit": "views/s", "cores": 1, "kind": "oracle",
-               "sample": "one view; all Gaussians projected; 16 blocks rendered fwd+L1+bwd (scaled to all "
-                         "blocks); their records' transformation backward (scaled to all records); Adam over 1/16 "
-                         "of the Gaussians (scaled, shared by b views); %.1f s of CPU work" % s["cpu_s"],
-               "parts_s_per_view": {k: round(v, 3) for k, v in s["parts"].items()}}
+        cpu = oracle_baseline(full, cam, gt, cfg["b"])
 
     # ---------------- NEXT-2: one densify-and-prune event over the trained shard (after all
     # other measurements: it changes the shard), plus the per-step statistics kernel

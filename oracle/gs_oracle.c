@@ -9,6 +9,7 @@
  *
  * Compile: gcc -O2 -fno-fast-math -ffp-contract=off -fPIC -shared (x86-64 SSE, no x87).
  */
+#define _GNU_SOURCE /* qsort_r: the O11 comparator takes the record arrays as an argument */
 #include "gs_oracle.h"
 
 #include <math.h>
@@ -339,14 +340,18 @@ void orc_exchange_sets(int64_t n, const int8_t* vis, const int32_t* rect, int32_
 }
 
 /* ------------------------------------------------------------------ O11 tile lists */
-static const double* g_sort_f;
-static const int64_t* g_sort_i;
-static int cmp_depth_gid(const void* pa, const void* pb) {
+typedef struct {
+  const double* f;
+  const int64_t* i;
+} sort_arg_t;
+/* reentrant (no static state), so concurrent calls over disjoint block ranges are safe */
+static int cmp_depth_gid(const void* pa, const void* pb, void* arg) {
+  const sort_arg_t* s = (const sort_arg_t*)arg;
   int64_t a = *(const int64_t*)pa, b = *(const int64_t*)pb;
-  double da = g_sort_f[10 * a + 2], db = g_sort_f[10 * b + 2];
+  double da = s->f[10 * a + 2], db = s->f[10 * b + 2];
   if (da < db) return -1;
   if (da > db) return 1;
-  int64_t ga = g_sort_i[6 * a], gb = g_sort_i[6 * b];
+  int64_t ga = s->i[6 * a], gb = s->i[6 * b];
   return (ga < gb) ? -1 : (ga > gb) ? 1 : 0;
 }
 
@@ -376,10 +381,9 @@ void orc_tile_lists(int64_t n_rec, const double* rec_f, const int64_t* rec_i, in
           if (beta >= b0 && beta < b1) entries[offsets[beta - b0] + cnt[beta - b0]++] = j;
         }
     }
-    g_sort_f = rec_f;
-    g_sort_i = rec_i;
+    sort_arg_t sa = {rec_f, rec_i};
     for (int64_t k = 0; k < nb; k++)
-      qsort(entries + offsets[k], (size_t)(offsets[k + 1] - offsets[k]), sizeof(int64_t), cmp_depth_gid);
+      qsort_r(entries + offsets[k], (size_t)(offsets[k + 1] - offsets[k]), sizeof(int64_t), cmp_depth_gid, &sa);
   }
   free(cnt);
 }
