@@ -78,7 +78,27 @@ __device__ __forceinline__ bool box_may_hit(float mx, float my, float l11, float
   return !(qmin > qmax + 0.05f * (1.0f + qmax));
 }
 
-// Stage records [0, cnt) of the calling warp's walk (sidx: their receive indices in list
+// Receive indices [0, cnt) of a staging round: lane + 32 i (0 past cnt).
+template <int KW>
+__device__ __forceinline__ void load_idx(const uint32_t* __restrict__ sidx, int cnt, uint32_t (&jr)[KW / 32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < KW / 32; i++) jr[i] = lane + 32 * i < cnt ? __ldg(sidx + lane + 32 * i) : 0u;
+}
+
+// u and w of the prescaled factor at the reference point (rx, ry), in fp64 from the
+// double-float factor (hi + lo), rounded to nearest (R16).  Explicit fp64 intrinsics: every
+// kernel that stages a record gets the same bits for the same reference point.
+__device__ __forceinline__ float ref_u(const float4& a, const float4& b, const float4& d, double rx, double ry) {
+  const double dmx = __dsub_rn((double)a.x, rx), dmy = __dsub_rn((double)a.y, ry);
+  return __double2float_rn(__fma_rn(__dadd_rn((double)b.x, (double)d.x), dmx,
+                                    __dmul_rn(__dadd_rn((double)b.y, (double)d.y), dmy)));
+}
+__device__ __forceinline__ float ref_w(const float4& a, const float4& b, const float4& d, double ry) {
+  return __double2float_rn(__dmul_rn(__dadd_rn((double)b.z, (double)d.z), __dsub_rn((double)a.y, ry)));
+}
+
+// Stage records [0, cnt) of the calling warp's walk (jr: their receive indices in list
 // order, list positions pos0 + t), culled against the pixel centres of its 8x16 half
 // [hx0, hx0 + 7] x [hy0, hy0 + 15], compacted by ballot into the warp's slots and padded to a
 // multiple of `pad` with entries no pixel composites.  Slot k is the triple s[3k .. 3k+2]:
@@ -87,20 +107,21 @@ __device__ __forceinline__ bool box_may_hit(float mx, float my, float l11, float
 //   Bq = (l22', o, r, g)
 //   cq = (b, qmax, list position, receive index)
 // No CTA barrier; the caller must have __syncwarp'ed since its last read of the slots.
-template <int KW>
-__device__ __forceinline__ int stage_warp(const gs_rec* __restrict__ rec, const uint32_t* __restrict__ sidx, int cnt,
+// S = 4 (backward): a fourth float4 per slot carries entry constants of the gradient formation,
+//   E = (m_x - r_x, m_y - r_y, 1 / o, l21'^2 + l22'^2)   (mean relative to the half's centre).
+// jr: the round's receive indices (load_idx); the backward loads them one round ahead, so its
+// staging waits on one level of dependent loads (the records), not two.
+template <int KW, int S = 3>
+__device__ __forceinline__ int stage_warp(const gs_rec* __restrict__ rec, const uint32_t (&jr)[KW / 32], int cnt,
                                           int pos0, float4* s, float hx0, float hy0, int pad) {
   constexpr int kI = KW / 32;
   const int lane = threadIdx.x & 31;
-  uint32_t jr[kI];
   unsigned bal[kI];
 #pragma unroll
   for (int i = 0; i < kI; i++) {
     const int t = lane + 32 * i;
     bool keep = false;
-    jr[i] = 0;
     if (t < cnt) {
-      jr[i] = sidx[t];
       const gs_rec* r = rec + jr[i];
       const float4 a = __ldg(&r->a), b = __ldg(&r->b);
       const float qmax = __ldg(&r->c.w);
@@ -117,20 +138,20 @@ __device__ __forceinline__ int stage_warp(const gs_rec* __restrict__ rec, const 
       const int off = base + __popc(bal[i] & lt);
       const gs_rec* r = rec + jr[i];
       const float4 a = __ldg(&r->a), b = __ldg(&r->b), c = __ldg(&r->c), d = __ldg(&r->d);
-      const double dmx = (double)a.x - rx, dmy = (double)a.y - ry;
-      const float uref = __double2float_rn(((double)b.x + (double)d.x) * dmx + ((double)b.y + (double)d.y) * dmy);
-      const float wref = __double2float_rn(((double)b.z + (double)d.z) * dmy);
-      s[3 * off] = make_float4(uref, wref, b.x, b.y);
-      s[3 * off + 1] = make_float4(b.z, b.w, c.x, c.y);
-      s[3 * off + 2] = make_float4(c.z, c.w, __int_as_float(pos0 + lane + 32 * i), __uint_as_float(jr[i]));
+      const float uref = ref_u(a, b, d, rx, ry), wref = ref_w(a, b, d, ry);
+      s[S * off] = make_float4(uref, wref, b.x, b.y);
+      s[S * off + 1] = make_float4(b.z, b.w, c.x, c.y);
+      s[S * off + 2] = make_float4(c.z, c.w, __int_as_float(pos0 + lane + 32 * i), __uint_as_float(jr[i]));
+      if (S == 4)
+        s[S * off + 3] = make_float4(a.x - (hx0 + 3.5f), a.y - (hy0 + 7.5f), __frcp_rn(b.w), fmaf(b.y, b.y, b.z * b.z));
     }
     base += __popc(bal[i]);
   }
   const int padded = (base + pad - 1) / pad * pad;
   for (int t = base + lane; t < padded; t += 32) {
-    s[3 * t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    s[3 * t + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-    s[3 * t + 2] = make_float4(0.f, -1.0f, 0.f, 0.f);  // qmax < 0 <= q: never composited
+    s[S * t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    s[S * t + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    s[S * t + 2] = make_float4(0.f, -1.0f, 0.f, 0.f);  // qmax < 0 <= q: never composited
   }
   __syncwarp();
   return base;
@@ -265,7 +286,11 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_fwd(
   for (int b0 = beg; b0 < end; b0 += kFW) {
     if (__all_sync(0xffffffffu, all_done())) break;
     const int cnt = min(kFW, end - b0);
-    const int kept = stage_warp<kFW>(rec, sorted_idx + b0, cnt, b0 - beg, s, hx0, hy0, kUnroll);
+    // (loading the next round's indices here as the backward does spills at the forward's
+    // 56-register cap: 18.41 -> 18.55 ms)
+    uint32_t jc[kFW / 32];
+    load_idx<kFW>(sorted_idx + b0, cnt, jc);
+    const int kept = stage_warp<kFW>(rec, jc, cnt, b0 - beg, s, hx0, hy0, kUnroll);
     const int kept8 = (kept + kUnroll - 1) & ~(kUnroll - 1);
     for (int k0 = 0; k0 < kept8; k0 += kUnroll) {
       if (all_done()) break;
@@ -397,14 +422,15 @@ __device__ __forceinline__ void bwd_comp_strip(float raw, const float4& Bq, floa
 //   dL/dl11' = -2ln2 l11 sum q_j u_j,  dL/dl21' = -2ln2 sum q_j (l21 u_j + l22 w_j),
 //   dL/dconic-like (gr2..4) = -1/2 sum q dx^2, -sum q dx dy_j, -1/2 sum q dy_j^2,
 //   dL/do = sum G dA = sum q / o (o > 1/255 for any entry that composites).
-__device__ __forceinline__ void strip_grads(const float4& A, const float4& Bq, float dx, float dy0, float u0,
-                                            float w0, const float acc[3], float gr[9]) {
-  const float l11 = A.z, l21 = A.w, l22 = Bq.x, o = Bq.y;
+// E: the staged entry constants (stage_warp<., 4>): E.z = 1 / o, E.w = l21'^2 + l22'^2.
+__device__ __forceinline__ void strip_grads(const float4& A, const float4& Bq, const float4& E, float dx, float dy0,
+                                            float u0, float w0, const float acc[3], float gr[9]) {
+  const float l11 = A.z, l21 = A.w, l22 = Bq.x;
   const float Q0 = acc[0], Q1 = acc[1], Q2 = acc[2];
   const float k = -1.3862943611198906f;
-  gr[5] = Q0 * rcp_approx(o);
+  gr[5] = Q0 * E.z;
   gr[0] = k * l11 * fmaf(u0, Q0, -l21 * Q1);
-  gr[1] = k * fmaf(fmaf(l21, u0, l22 * w0), Q0, -fmaf(l21, l21, l22 * l22) * Q1);
+  gr[1] = k * fmaf(fmaf(l21, u0, l22 * w0), Q0, -E.w * Q1);
   gr[2] = -0.5f * dx * dx * Q0;
   gr[3] = -dx * fmaf(dy0, Q0, -Q1);
   gr[4] = -0.5f * fmaf(dy0, fmaf(dy0, Q0, -2.0f * Q1), Q2);
@@ -468,8 +494,8 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_bwd(
     const float* __restrict__ dL_dpix, const float* __restrict__ T_final,
     const int32_t* __restrict__ n_last, int64_t* __restrict__ tile_cost, int cost_mode,
     long long* __restrict__ stats, gs_gdst gdst) {
-  // the staged entries as (A, Bq, cq) triples, so one pointer walks them
-  __shared__ float4 s_e[3 * 2 * kBW];
+  // the staged entries as (A, Bq, cq, E) quadruples, so one pointer walks them
+  __shared__ float4 s_e[4 * 2 * kBW];
   // per-warp buffered reduction rows (flush_rows)
   __shared__ __align__(128) float s_rows[2 * kF * 9 * 32];
   __shared__ long long s_red[kNT / 32];
@@ -510,14 +536,21 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_bwd(
   float acc[3] = {0.f, 0.f, 0.f};  // per-entry strip moments and colour gradients
   float2 gc01 = make_float2(0.f, 0.f);
   float gc2 = 0.f;
-  float4* const s = s_e + wid * 3 * kBW;  // this warp's slots
-  for (int bi = (maxn + kBW - 1) / kBW - 1; bi >= 0; bi--) {
+  float4* const s = s_e + wid * 4 * kBW;  // this warp's slots
+  uint32_t jn[kBW / 32];
+  const int bi0 = (maxn + kBW - 1) / kBW - 1;
+  if (bi0 >= 0) load_idx<kBW>(sorted_idx + beg + bi0 * kBW, maxn - bi0 * kBW, jn);
+  for (int bi = bi0; bi >= 0; bi--) {
     const int p0 = bi * kBW;  // list position of the batch start
     const int cnt = min(kBW, maxn - p0);
+    uint32_t jc[kBW / 32];
+#pragma unroll
+    for (int i = 0; i < kBW / 32; i++) jc[i] = jn[i];
+    if (bi > 0) load_idx<kBW>(sorted_idx + beg + p0 - kBW, kBW, jn);
     __syncwarp();
-    const int kept = stage_warp<kBW>(rec, sorted_idx + beg + p0, cnt, p0, s, hx0, hy0, 1);
-    const float4* ep = s + 3 * (kept - 1);  // entry k's triple
-    for (int k = kept - 1; k >= 0; k--, ep -= 3) {
+    const int kept = stage_warp<kBW, 4>(rec, jc, cnt, p0, s, hx0, hy0, 1);
+    const float4* ep = s + 4 * (kept - 1);  // entry k's quadruple
+    for (int k = kept - 1; k >= 0; k--, ep -= 4) {
       const float4 cq = ep[2];
       const int pos = __float_as_int(cq.z);
       const float4 A = ep[0], Bq = ep[1];
@@ -558,12 +591,10 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_bwd(
         }
       }
       if (__any_sync(0xffffffffu, any)) {
-        // the mean-to-pixel offset of the thread's first pixel from the exponent terms at the
-        // half's centre: m - r = (dmx, dmy) with w_ref = l22 dmy, u_ref = l11 dmx + l21 dmy
-        const float dmy = A.y * rcp_approx(Bq.x);
-        const float dmx = fmaf(-A.w, dmy, A.x) * rcp_approx(A.z);
+        // the mean-to-pixel offset of the thread's first pixel: (m - r) + (r - p)
+        const float4 E = ep[3];
         float gr[9];
-        strip_grads(A, Bq, dmx + ex, dmy + ey0, e.u[0], e.w[0], acc, gr);
+        strip_grads(A, Bq, E, E.x + ex, E.y + ey0, e.u[0], e.w[0], acc, gr);
         gr[6] = gc01.x;
         gr[7] = gc01.y;
         gr[8] = gc2;
