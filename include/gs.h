@@ -185,26 +185,39 @@ gs_status gs_bin_sort(gs_ctx* ctx, const void* recv_rec, int64_t n_recv, const g
  * dL_dpix[n_owned][3][256] = sign(C - GT) / (3 H W b_loss) and *loss_sum (device double)
  * += sum |C - GT| / (3 H W b_loss).  tile_cost[n_owned] (int64, nullable) += per-block
  * cost (MEASURED: SM cycles of the block; WORK: evaluations E_f).  stats (nullable
- * int64[8], device) += (E_f, E_fc, E_fs, E_stop, 0, 0, 0, 0) totals.                      */
+ * int64[8], device) += (E_f, E_fc, E_fs, E_stop, 0, 0, 0, 0) totals.
+ * cull_bits (nullable, device u32[gs_cull_words(K, n_owned)], K = the lists' total length):
+ * receives, for every list entry the forward staged, whether any pixel centre of each 8x16
+ * half of its block may composite it (a conservative, semantics-free ellipse-box test: an
+ * entry with the bit clear is a no-op for every pixel of that half).  Pass the same buffer
+ * to gs_render_bwd / gs_render_bwd_put on the same lists to skip the test there; contents
+ * are internal to the pair of calls.                                                       */
 gs_status gs_render_fwd(gs_ctx* ctx, const void* recv_rec, const uint32_t* sorted_idx,
                         const int32_t* tile_range, const gs_camera* cams_h, int n_views,
                         const int64_t* dp_h, const float* bg_h, const uint8_t* gt, int b_loss,
                         float* out_rgb, float* T_final, int32_t* n_last, float* dL_dpix,
                         double* loss_sum, int64_t* tile_cost, int cost_mode, int64_t* stats,
-                        void* stream);
+                        uint32_t* cull_bits, void* stream);
+/* Words of the cull_bits buffer for lists of total length n_pairs over n_owned blocks
+ * (2 x (n_pairs / 32 + n_owned + 1): two halves, one bit per entry, 32-entry words aligned
+ * per block).                                                                              */
+int64_t gs_cull_words(int64_t n_pairs, int64_t n_owned);
 
 /* --------------------------------------------------------------------------- A5 */
 /* A5 gs_render_bwd -- backward of compositing (O14-O15).  Walks each pixel's list
  * back to front from n_last, reconstructing T, and accumulates dL/d(record) over all owned
  * pixels into dL_drec[n_recv][9] (zeroed by this call; float atomics, so summation order is
  * not deterministic).  tile_cost += cost (WORK: visited entries = n_last per pixel).
- * stats (nullable) += (0, 0, 0, 0, E_b visited, E_bc contributing, 0, 0).                */
+ * stats (nullable) += (0, 0, 0, 0, E_b visited, E_bc contributing, 0, 0).
+ * cull_bits (nullable): the buffer gs_render_fwd filled for these same lists (sorted_idx,
+ * tile_range, dp unchanged since), read instead of re-running the forward's cull test;
+ * NULL: the test runs here.  Results are identical either way.                             */
 gs_status gs_render_bwd(gs_ctx* ctx, const void* recv_rec, int64_t n_recv,
                         const uint32_t* sorted_idx, const int32_t* tile_range,
                         const gs_camera* cams_h, int n_views, const int64_t* dp_h,
                         const float* bg_h, const float* dL_dpix, const float* T_final,
                         const int32_t* n_last, float* dL_drec, int64_t* tile_cost, int cost_mode,
-                        int64_t* stats, void* stream);
+                        int64_t* stats, const uint32_t* cull_bits, void* stream);
 
 /* --------------------------------------------------------------------------- A6 */
 /* A6 gs_exchange_grads -- reverse sparse all-to-all ("A reversed all-to-all
@@ -463,7 +476,7 @@ gs_status gs_project_put(gs_ctx* ctx, const gs_params* p, const gs_camera* cams_
 gs_status gs_render_bwd_put(gs_ctx* ctx, const void* recv_rec, int64_t n_recv, const uint32_t* sorted_idx,
                             const int32_t* tile_range, const gs_camera* cams_h, int n_views, const int64_t* dp_h,
                             const float* dL_dpix, const float* T_final, const int32_t* n_last, int64_t* tile_cost,
-                            int cost_mode, int64_t* stats, void* stream);
+                            int cost_mode, int64_t* stats, const uint32_t* cull_bits, void* stream);
 /* gs_p2p_barrier -- device-side barrier over the attached flag arrays, asynchronous (no host
  * sync): one kernel writes the next epoch into every rank's flag slot for this rank
  * (system-scope release after the stream's earlier work) and waits until all ranks' slots

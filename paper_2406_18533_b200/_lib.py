@@ -75,9 +75,10 @@ _sig = {
     "gs_exchange": (C.c_int, [_vp, _vp, _P64, _vp, _i64, _P64, _P64, _vp]),
     "gs_bin_sort": (C.c_int, [_vp, _vp, _i64, C.POINTER(Camera), C.c_int, _P64, _vp, _i64, _vp, _P64, _vp]),
     "gs_render_fwd": (C.c_int, [_vp, _vp, _vp, _vp, C.POINTER(Camera), C.c_int, _P64, C.POINTER(C.c_float),
-                                _vp, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
+                                _vp, C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp, _vp]),
+    "gs_cull_words": (C.c_int64, [_i64, _i64]),
     "gs_render_bwd": (C.c_int, [_vp, _vp, _i64, _vp, _vp, C.POINTER(Camera), C.c_int, _P64,
-                                C.POINTER(C.c_float), _vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp]),
+                                C.POINTER(C.c_float), _vp, _vp, _vp, _vp, _vp, C.c_int, _vp, _vp, _vp]),
     "gs_exchange_grads": (C.c_int, [_vp, _vp, _P64, _P64, _vp, _vp]),
     "gs_adam_step": (C.c_int, [_vp, C.POINTER(Params), C.POINTER(Params), C.POINTER(Params), C.POINTER(Params),
                                C.POINTER(Camera), C.c_int, _P64, _vp, _vp, C.POINTER(AdamHparams), C.c_int, _vp]),
@@ -118,7 +119,7 @@ _sig = {
     "gs_project_count": (C.c_int, [_vp, C.POINTER(Params), C.POINTER(Camera), C.c_int, _P64, _P64, _vp, _vp]),
     "gs_project_put": (C.c_int, [_vp, C.POINTER(Params), C.POINTER(Camera), C.c_int, _P64, _vp, _vp]),
     "gs_render_bwd_put": (C.c_int, [_vp, _vp, _i64, _vp, _vp, C.POINTER(Camera), C.c_int, _P64, _vp, _vp, _vp,
-                                    _vp, C.c_int, _vp, _vp]),
+                                    _vp, C.c_int, _vp, _vp, _vp]),
     "gs_p2p_barrier": (C.c_int, [_vp, _vp]),
     "gs_p2p_status": (C.c_int, [_vp, _vp]),
     "gs_p2p_attach_counts": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp), _i64]),
@@ -332,25 +333,31 @@ def _bg(bg):
 
 
 def render_fwd(ctx, recv_rec, sorted_idx, tile_range, cams, dp, bg, gt, b_loss, out_rgb, T_final, n_last,
-               dL_dpix, loss_sum, tile_cost, cost_mode, stats, stream=None):
-    """A4."""
+               dL_dpix, loss_sum, tile_cost, cost_mode, stats, stream=None, cull=None):
+    """A4.  cull: optional uint32 device buffer of cull_words() words the forward fills for
+    render_bwd on the same lists."""
     ca = cameras(cams)
     _, dpp = _i64arr(dp)
     st = _lib.gs_render_fwd(ctx.handle, _ptr(recv_rec), _ptr(sorted_idx), _ptr(tile_range), ca, len(cams), dpp,
                             _bg(bg), _ptr(gt), int(b_loss), _ptr(out_rgb), _ptr(T_final), _ptr(n_last),
                             _ptr(dL_dpix), _ptr(loss_sum), _ptr(tile_cost), int(cost_mode), _ptr(stats),
-                            _stream(stream))
+                            _ptr(cull), _stream(stream))
     ctx.check(st)
 
 
+def cull_words(n_pairs, n_owned):
+    """Words of render_fwd's cull buffer for lists of n_pairs entries over n_owned blocks."""
+    return int(_lib.gs_cull_words(int(n_pairs), int(n_owned)))
+
+
 def render_bwd(ctx, recv_rec, n_recv, sorted_idx, tile_range, cams, dp, bg, dL_dpix, T_final, n_last,
-               dL_drec, tile_cost, cost_mode, stats, stream=None):
-    """A5."""
+               dL_drec, tile_cost, cost_mode, stats, stream=None, cull=None):
+    """A5.  cull: the buffer render_fwd filled for these lists (None: the cull test runs here)."""
     ca = cameras(cams)
     _, dpp = _i64arr(dp)
     st = _lib.gs_render_bwd(ctx.handle, _ptr(recv_rec), int(n_recv), _ptr(sorted_idx), _ptr(tile_range), ca,
                             len(cams), dpp, _bg(bg), _ptr(dL_dpix), _ptr(T_final), _ptr(n_last), _ptr(dL_drec),
-                            _ptr(tile_cost), int(cost_mode), _ptr(stats), _stream(stream))
+                            _ptr(tile_cost), int(cost_mode), _ptr(stats), _ptr(cull), _stream(stream))
     ctx.check(st)
 
 
@@ -658,14 +665,14 @@ def project_put(ctx, params, cams, dp, bwd_index, stream=None):
 
 
 def render_bwd_put(ctx, recv_rec, n_recv, sorted_idx, tile_range, cams, dp, dL_dpix, T_final, n_last, tile_cost,
-                   cost_mode, stats, stream=None, recv_ptr=None):
+                   cost_mode, stats, stream=None, recv_ptr=None, cull=None):
     """A5 fused with A6: gradient sums straight into the owners' dL/dsend buffers."""
     ca = cameras(cams)
     _, dpp = _i64arr(dp)
     rp = C.c_void_p(recv_ptr) if recv_ptr is not None else _ptr(recv_rec)
     ctx.check(_lib.gs_render_bwd_put(ctx.handle, rp, int(n_recv), _ptr(sorted_idx), _ptr(tile_range), ca,
                                      len(cams), dpp, _ptr(dL_dpix), _ptr(T_final), _ptr(n_last), _ptr(tile_cost),
-                                     int(cost_mode), _ptr(stats), _stream(stream)))
+                                     int(cost_mode), _ptr(stats), _ptr(cull), _stream(stream)))
 
 
 def p2p_barrier(ctx, stream=None):

@@ -24,9 +24,9 @@ struct gs_slot {
 enum {
   SLOT_SCAN = 0,      // scan partials
   SLOT_PROJ_TMP,      // projection per-destination totals
-  SLOT_DIFF,          // bin_sort 2D difference arrays of the tile rectangles
+  SLOT_DIFF,          // (unused)
   SLOT_COUNTS,        // bin_sort per-block counts (int64)
-  SLOT_CURSOR,        // bin_sort per-block cursors
+  SLOT_CURSOR,        // bin_sort fine emission: first segment of each super-tile (int64)
   SLOT_KEYS,          // bin_sort (depth, recv idx) keys
   SLOT_KEYS_TMP,      // merge ping-pong for long lists
   SLOT_LARGE,         // list of long blocks + counters
@@ -47,6 +47,7 @@ enum {
   SLOT_CLIST,         // bin_sort coarse lists (record indices by super-tile)
   SLOT_CRANGE,        // bin_sort coarse-list ranges per super-tile
   SLOT_RECT8,         // bin_sort packed tile rectangle + view per record
+  SLOT_FSEG_CNT,      // bin_sort fine emission: per-segment block counts -> offsets
   SLOT_N
 };
 

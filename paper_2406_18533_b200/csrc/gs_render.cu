@@ -48,6 +48,10 @@ constexpr int kUnroll = 4;  // forward entries per unrolled group (4 measured fa
 #ifndef GS_BWD_MINB
 #define GS_BWD_MINB 14
 #endif
+// 0: the backward ignores the forward's cull bits and repeats the test (A/B builds only)
+#ifndef GS_CULL_REUSE
+#define GS_CULL_REUSE 1
+#endif
 
 // Could any pixel centre of the box [bx0, bx0 + ex] x [by0, by0 + ey] see the record (mean
 // (mx, my), prescaled factor l11, l21, l22) with alpha >= 1/255?  Minimum of q(d) = |L'^T d|^2
@@ -111,23 +115,42 @@ __device__ __forceinline__ float ref_w(const float4& a, const float4& b, const f
 //   E = (m_x - r_x, m_y - r_y, 1 / o, l21'^2 + l22'^2)   (mean relative to the half's centre).
 // jr: the round's receive indices (load_idx); the backward loads them one round ahead, so its
 // staging waits on one level of dependent loads (the records), not two.
+// Cull bits (gs_render_fwd's cull_bits): word k of the round holds the keep ballot of entries
+// 32k .. 32k + 31; bits_out (forward, nullable) receives them, bits_in (backward, nullable)
+// replaces the test -- the same decisions, so the same staged entries.  Both point at the
+// round's first word of this half; consecutive words are 2 apart (the halves interleave).
 template <int KW, int S = 3>
 __device__ __forceinline__ int stage_warp(const gs_rec* __restrict__ rec, const uint32_t (&jr)[KW / 32], int cnt,
-                                          int pos0, float4* s, float hx0, float hy0, int pad) {
+                                          int pos0, float4* s, float hx0, float hy0, int pad,
+                                          const uint32_t* __restrict__ bits_in = nullptr,
+                                          uint32_t* __restrict__ bits_out = nullptr) {
   constexpr int kI = KW / 32;
   const int lane = threadIdx.x & 31;
   unsigned bal[kI];
+  if (bits_in) {
 #pragma unroll
-  for (int i = 0; i < kI; i++) {
-    const int t = lane + 32 * i;
-    bool keep = false;
-    if (t < cnt) {
-      const gs_rec* r = rec + jr[i];
-      const float4 a = __ldg(&r->a), b = __ldg(&r->b);
-      const float qmax = __ldg(&r->c.w);
-      keep = box_may_hit(a.x, a.y, b.x, b.y, b.z, qmax, hx0, hy0, 7.f, 15.f);
+    for (int i = 0; i < kI; i++) {
+      const int c = cnt - 32 * i;
+      bal[i] = c <= 0 ? 0u : (__ldg(bits_in + 2 * i) & (c >= 32 ? 0xffffffffu : (1u << c) - 1u));
     }
-    bal[i] = __ballot_sync(0xffffffffu, keep);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kI; i++) {
+      const int t = lane + 32 * i;
+      bool keep = false;
+      if (t < cnt) {
+        const gs_rec* r = rec + jr[i];
+        const float4 a = __ldg(&r->a), b = __ldg(&r->b);
+        const float qmax = __ldg(&r->c.w);
+        keep = box_may_hit(a.x, a.y, b.x, b.y, b.z, qmax, hx0, hy0, 7.f, 15.f);
+      }
+      bal[i] = __ballot_sync(0xffffffffu, keep);
+    }
+    if (bits_out && lane == 0) {
+#pragma unroll
+      for (int i = 0; i < kI; i++)
+        if (32 * i < cnt) bits_out[2 * i] = bal[i];
+    }
   }
   const double rx = (double)hx0 + 3.5, ry = (double)hy0 + 7.5;
   const unsigned lt = (1u << lane) - 1u;
@@ -245,7 +268,7 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_fwd(
     const uint8_t* __restrict__ gt, float norm, float* __restrict__ out_rgb,
     float* __restrict__ T_final, int32_t* __restrict__ n_last, float* __restrict__ dL_dpix,
     double* __restrict__ loss_sum, int64_t* __restrict__ tile_cost, int cost_mode,
-    long long* __restrict__ stats) {
+    long long* __restrict__ stats, uint32_t* __restrict__ cull) {
   static_assert(kTrack || !kStats, "statistics need the stop positions");
   constexpr int kSlots = kFW + kUnroll;
   __shared__ float4 s_e[2 * 3 * kSlots];
@@ -290,7 +313,9 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_fwd(
     // 56-register cap: 18.41 -> 18.55 ms)
     uint32_t jc[kFW / 32];
     load_idx<kFW>(sorted_idx + b0, cnt, jc);
-    const int kept = stage_warp<kFW>(rec, jc, cnt, b0 - beg, s, hx0, hy0, kUnroll);
+    // this half's cull words of the round: word (beg / 32 + lb + position / 32), halves interleaved
+    uint32_t* const bo = cull ? cull + 2 * ((int64_t)(beg >> 5) + lb + ((b0 - beg) >> 5)) + wid : nullptr;
+    const int kept = stage_warp<kFW>(rec, jc, cnt, b0 - beg, s, hx0, hy0, kUnroll, nullptr, bo);
     const int kept8 = (kept + kUnroll - 1) & ~(kUnroll - 1);
     for (int k0 = 0; k0 < kept8; k0 += kUnroll) {
       if (all_done()) break;
@@ -493,7 +518,7 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_bwd(
     const int32_t* __restrict__ range, gs_geom geo, int64_t B_lo, float bg0, float bg1, float bg2,
     const float* __restrict__ dL_dpix, const float* __restrict__ T_final,
     const int32_t* __restrict__ n_last, int64_t* __restrict__ tile_cost, int cost_mode,
-    long long* __restrict__ stats, gs_gdst gdst) {
+    long long* __restrict__ stats, gs_gdst gdst, const uint32_t* __restrict__ cull) {
   // the staged entries as (A, Bq, cq, E) quadruples, so one pointer walks them
   __shared__ float4 s_e[4 * 2 * kBW];
   // per-warp buffered reduction rows (flush_rows)
@@ -548,7 +573,9 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_bwd(
     for (int i = 0; i < kBW / 32; i++) jc[i] = jn[i];
     if (bi > 0) load_idx<kBW>(sorted_idx + beg + p0 - kBW, kBW, jn);
     __syncwarp();
-    const int kept = stage_warp<kBW, 4>(rec, jc, cnt, p0, s, hx0, hy0, 1);
+    const uint32_t* const bi_ =
+        GS_CULL_REUSE && cull ? cull + 2 * ((int64_t)(beg >> 5) + lb + (p0 >> 5)) + wid : nullptr;
+    const int kept = stage_warp<kBW, 4>(rec, jc, cnt, p0, s, hx0, hy0, 1, bi_);
     const float4* ep = s + 4 * (kept - 1);  // entry k's quadruple
     for (int k = kept - 1; k >= 0; k--, ep -= 4) {
       const float4 cq = ep[2];
@@ -652,12 +679,16 @@ __global__ void k_selftest_ex2(uint32_t b_lo, uint32_t n, unsigned long long* ou
 
 }  // namespace
 
+extern "C" int64_t gs_cull_words(int64_t n_pairs, int64_t n_owned) {
+  return n_pairs < 0 || n_owned < 0 ? 0 : 2 * (n_pairs / 32 + n_owned + 1);
+}
+
 extern "C" gs_status gs_render_fwd(gs_ctx* c, const void* recv_rec, const uint32_t* sorted_idx,
                                    const int32_t* tile_range, const gs_camera* cams_h, int n_views,
                                    const int64_t* dp_h, const float* bg_h, const uint8_t* gt, int b_loss,
                                    float* out_rgb, float* T_final, int32_t* n_last, float* dL_dpix,
                                    double* loss_sum, int64_t* tile_cost, int cost_mode, int64_t* stats,
-                                   void* stream) {
+                                   uint32_t* cull_bits, void* stream) {
   if (!c) return GS_EINVAL;
   gs_status s = gs_check_batch(c, cams_h, n_views, dp_h);
   if (s != GS_OK) return s;
@@ -677,7 +708,7 @@ extern "C" gs_status gs_render_fwd(gs_ctx* c, const void* recv_rec, const uint32
                                                                         : k_render_fwd<false, GS_FWD_MINB, false>;
   kf<<<(unsigned)n_owned, kNT, 0, (cudaStream_t)stream>>>(
       (const gs_rec*)recv_rec, sorted_idx, tile_range, geo, B_lo, bg[0], bg[1], bg[2], gt, norm, out_rgb,
-      T_final, n_last, dL_dpix, loss_sum, tile_cost, cost_mode, (long long*)stats);
+      T_final, n_last, dL_dpix, loss_sum, tile_cost, cost_mode, (long long*)stats, cull_bits);
   GS_LAUNCH_CHECK(c, "render_fwd");
   return GS_OK;
 }
@@ -687,7 +718,7 @@ static gs_status render_bwd_launch(gs_ctx* c, const void* recv_rec, const uint32
                                    const int32_t* tile_range, const gs_camera* cams_h, const int64_t* dp_h,
                                    const float* bg_h, const float* dL_dpix, const float* T_final,
                                    const int32_t* n_last, const gs_gdst& gdst, int64_t* tile_cost, int cost_mode,
-                                   int64_t* stats, cudaStream_t st) {
+                                   int64_t* stats, const uint32_t* cull_bits, cudaStream_t st) {
   const int64_t B_lo = dp_h[c->rank], n_owned = dp_h[c->rank + 1] - B_lo;
   if (n_owned == 0) return GS_OK;
   GS_REQUIRE(c, tile_range && T_final && n_last && dL_dpix, "null argument");
@@ -703,7 +734,7 @@ static gs_status render_bwd_launch(gs_ctx* c, const void* recv_rec, const uint32
                   : (stats ? k_render_bwd<true, 12, true> : k_render_bwd<false, 12, true>);
   kb<<<(unsigned)n_owned, kNT, 0, st>>>((const gs_rec*)recv_rec, sorted_idx, tile_range, geo, B_lo, bg[0], bg[1],
                                         bg[2], dL_dpix, T_final, n_last, tile_cost, cost_mode, (long long*)stats,
-                                        gdst);
+                                        gdst, cull_bits);
   GS_LAUNCH_CHECK(c, "render_bwd");
   return GS_OK;
 }
@@ -713,7 +744,7 @@ extern "C" gs_status gs_render_bwd(gs_ctx* c, const void* recv_rec, int64_t n_re
                                    const gs_camera* cams_h, int n_views, const int64_t* dp_h,
                                    const float* bg_h, const float* dL_dpix, const float* T_final,
                                    const int32_t* n_last, float* dL_drec, int64_t* tile_cost, int cost_mode,
-                                   int64_t* stats, void* stream) {
+                                   int64_t* stats, const uint32_t* cull_bits, void* stream) {
   if (!c) return GS_EINVAL;
   gs_status s = gs_check_batch(c, cams_h, n_views, dp_h);
   if (s != GS_OK) return s;
@@ -729,14 +760,14 @@ extern "C" gs_status gs_render_bwd(gs_ctx* c, const void* recv_rec, int64_t n_re
   g.seg[1] = n_recv;
   g.nseg = 1;
   return render_bwd_launch(c, recv_rec, sorted_idx, tile_range, cams_h, dp_h, bg_h, dL_dpix, T_final, n_last, g,
-                           tile_cost, cost_mode, stats, st);
+                           tile_cost, cost_mode, stats, cull_bits, st);
 }
 
 extern "C" gs_status gs_render_bwd_put(gs_ctx* c, const void* recv_rec, int64_t n_recv, const uint32_t* sorted_idx,
                                        const int32_t* tile_range, const gs_camera* cams_h, int n_views,
                                        const int64_t* dp_h, const float* dL_dpix, const float* T_final,
                                        const int32_t* n_last, int64_t* tile_cost, int cost_mode, int64_t* stats,
-                                       void* stream) {
+                                       const uint32_t* cull_bits, void* stream) {
   if (!c) return GS_EINVAL;
   gs_status s = gs_check_batch(c, cams_h, n_views, dp_h);
   if (s != GS_OK) return s;
@@ -757,7 +788,7 @@ extern "C" gs_status gs_render_bwd_put(gs_ctx* c, const void* recv_rec, int64_t 
     }
   g.nseg = G;
   return render_bwd_launch(c, recv_rec, sorted_idx, tile_range, cams_h, dp_h, nullptr, dL_dpix, T_final, n_last, g,
-                           tile_cost, cost_mode, stats, (cudaStream_t)stream);
+                           tile_cost, cost_mode, stats, cull_bits, (cudaStream_t)stream);
 }
 
 extern "C" gs_status gs_selftest_ex2(gs_ctx* c, float lo, float hi, double* max_rel_err_h, void* stream) {

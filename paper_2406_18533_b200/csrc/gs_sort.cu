@@ -11,9 +11,13 @@
 //     view-local super-tile index (10 bits at 4591x3436: 2 passes of 5; 8 bits at 1080p: one
 //     pass) with one digit histogram laid out [view][digit][tile].  Each super-tile's coarse
 //     list is then in (depth, gid) order.
-//  3. Block offsets without reading any pair: every record adds its rectangle to a per-view 2D
-//     difference array (4 atomics), a 2D prefix gives each block's pair count, and an
-//     exclusive scan over the owned blocks gives tile_range.
+//  3. Block offsets without storing any pair: each super-tile's coarse list is cut into
+//     segments of kFineSeg records; per segment the hits of each of its 64 blocks are counted
+//     (ballot popcounts of the records' block masks), a running sum over the super-tile's
+//     segments gives every segment its blocks' starting ranks and every block its pair count,
+//     and an exclusive scan over the owned blocks gives tile_range.  (A per-view 2D difference
+//     array of the rectangles needs 4 atomics per record, which serialise when many records
+//     share a rectangle corner -- the screen-clamped Gaussians of street views: 44 ms of C4.)
 //  4. Fine emission: one CTA per super-tile walks its coarse list in order, 128 records at a
 //     time; each record's blocks inside the super-tile are a 64-bit mask, the in-order rank of
 //     a record among those hitting a block is a ballot popcount (plus the earlier warps'
@@ -50,6 +54,7 @@ constexpr int kEmitPairs = 1024;  // pairs per emission CTA
 constexpr int kSTShift = 3;        // super-tile side: 2^3 = 8 blocks (64 blocks: one 64-bit mask)
 constexpr int kST = 1 << kSTShift;
 constexpr int kFineThreads = 128;  // fine emission: records per chunk (4 warps)
+constexpr int kFineSeg = 2048;     // fine emission: coarse-list records per CTA (16 chunks)
 
 // The coarse grid: super-tile (sx, sy) = blocks [8 sx, 8 sx + 7] x [8 sy, 8 sy + 7] of the
 // view, view-local index sy * Cw + sx.
@@ -101,15 +106,13 @@ __device__ __forceinline__ long long seg_hidx(const seg_arg& g, int k, int d, lo
   return t0 * bins + (long long)d * nt + (t - t0);
 }
 
-// Per record: its coarse-pair count (super-tiles its tile rectangle touches), its rectangle
-// added to the view's 2D difference array diff[k][Ht + 1][Wt + 1] (the prefix sums of which
-// count each block's pairs), and per view the coarse-pair total and the owned-pair total
-// (owned = view-local block in [lo, hi): per rectangle row an interval intersection).
-// cnt[k] / own[k] over the rank's views; g.lo / g.hi are the FINE ownership bounds here.
+// Per record: its coarse-pair count (super-tiles its tile rectangle touches), its packed
+// rectangle, and per view the coarse-pair total and the owned-pair total (owned = view-local
+// block in [lo, hi): per rectangle row an interval intersection).  cnt[k] / own[k] over the
+// rank's views; g.lo / g.hi are the FINE ownership bounds here.
 __global__ void k_tile_counts(const gs_rec* __restrict__ rec, int64_t n_recv, gs_geom geo, seg_arg g,
                               int64_t* __restrict__ n_coarse, unsigned long long* __restrict__ cnt,
-                              unsigned long long* __restrict__ own, int* __restrict__ diff,
-                              uint2* __restrict__ rect8) {
+                              unsigned long long* __restrict__ own, uint2* __restrict__ rect8) {
   __shared__ unsigned long long s_c[GS_MAX_VIEWS], s_o[GS_MAX_VIEWS];
   if (threadIdx.x < GS_MAX_VIEWS) s_c[threadIdx.x] = s_o[threadIdx.x] = 0;
   __syncthreads();
@@ -131,12 +134,6 @@ __global__ void k_tile_counts(const gs_rec* __restrict__ rec, int64_t n_recv, gs
         const long long r0 = (long long)ty * geo.Wt + tx0, r1 = (long long)ty * geo.Wt + tx1 + 1;
         o += (unsigned)max(0ll, min(r1, (long long)g.hi[k]) - max(r0, (long long)g.lo[k]));
       }
-      int* D = diff + (int64_t)k * (geo.Ht + 1) * (geo.Wt + 1);
-      const int W1 = geo.Wt + 1;
-      atomicAdd(D + ty0 * W1 + tx0, 1);
-      atomicAdd(D + ty0 * W1 + tx1 + 1, -1);
-      atomicAdd(D + (ty1 + 1) * W1 + tx0, -1);
-      atomicAdd(D + (ty1 + 1) * W1 + tx1 + 1, 1);
     } else {
       k = -1;
     }
@@ -483,45 +480,6 @@ __global__ void k_seg_ranges(const uint32_t* __restrict__ keys, seg_arg g, int64
   }
 }
 
-// 2D prefix of the difference arrays, rows first: warp per row of Wt + 1 entries.
-__global__ void k_diff_rows(int* __restrict__ diff, int64_t nrows, int W1) {
-  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (r >= nrows) return;
-  int* row = diff + r * W1;
-  int carry = 0;
-  for (int x0 = 0; x0 < W1; x0 += 32) {
-    const int x = x0 + lane;
-    int v = x < W1 ? row[x] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, v, o);
-      if (lane >= o) v += y;
-    }
-    v += carry;
-    if (x < W1) row[x] = v;
-    carry = __shfl_sync(0xffffffffu, v, 31);
-  }
-}
-
-// ... then columns: thread per column x < Wt of view k = blockIdx.y; the running sum is block
-// (x, y)'s pair count, stored for owned blocks at their owned index (b - B_lo).
-__global__ void k_diff_cols(const int* __restrict__ diff, gs_geom geo, seg_arg g, int64_t* __restrict__ bcnt) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
-  if (x >= geo.Wt) return;
-  const int W1 = geo.Wt + 1;
-  const int* D = diff + (int64_t)k * (geo.Ht + 1) * W1 + x;
-  int64_t* out = bcnt + ((int64_t)(g.v_lo + k) * geo.per_view - g.B_lo);
-  const int lo = g.lo[k], hi = g.hi[k];
-  int run = 0;
-#pragma unroll 4
-  for (int y = 0; y < geo.Ht; y++) {
-    run += D[(int64_t)y * W1];
-    const int loc = y * geo.Wt + x;
-    if (loc >= lo && loc < hi) out[loc] = run;
-  }
-}
-
 __global__ void k_to_i32(const int64_t* __restrict__ in, int64_t n, int32_t* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = (int32_t)in[i];
@@ -542,8 +500,12 @@ __device__ __forceinline__ unsigned warp_transpose32(unsigned v, int lane) {
   return v;
 }
 
-// Fine emission, one CTA per (view k, super-tile): the super-tile's coarse list (crange, in
-// (depth, gid) order) in chunks of 128 records, one per thread.  A record's owned blocks
+// Fine emission, one CTA per segment of kFineSeg records of a (view k, super-tile)'s coarse
+// list (crange, in (depth, gid) order; fseg[t] = the first segment of super-tile t), in chunks
+// of 128 records, one per thread.  Each segment's block cursors start at tile_range + the
+// hits of the super-tile's earlier segments (fcnt, k_fine_count + k_fine_prefix), so the
+// segments of a long list (the horizon rows of street views reach ~10^5 records per
+// super-tile) run in parallel and each block list still comes out in order.  A record's owned blocks
 // inside the super-tile form a 64-bit mask (bit 8 j + i = block (8 sx + i, 8 sy + j)).  Each
 // warp transposes its 32 masks, so lane l holds the 32-bit sets of its lanes (= records, in
 // order) hitting block l and block l + 32; their popcounts are the warp's counts (phase 1).
@@ -559,9 +521,123 @@ struct fine_arg {
   int lo[GS_MAX_VIEWS], hi[GS_MAX_VIEWS];  // owned view-local blocks [lo, hi) of view k
   long long B_lo;
 };
+// The segment of CTA `bid`: its super-tile t (fseg[t] <= bid < fseg[t + 1], binary search)
+// and coarse-list range [cs, ce); false past the last segment.  Also the super-tile's owned
+// blocks (bit b of own_lo / own_hi: block b / b + 32, every lane computes the same mask).
+struct fine_seg {
+  int t, k, bx0, by0, cs, ce, seg;
+  unsigned own_lo, own_hi;
+};
+__device__ __forceinline__ bool find_fine_seg(int64_t bid, const int64_t* __restrict__ fseg, int nt,
+                                              const int32_t* __restrict__ crange, const gs_geom& geo,
+                                              const cgrid& cg, const fine_arg& f, fine_seg& q) {
+  if (bid >= fseg[nt]) return false;
+  int lo = 0, hi = nt;  // largest t with fseg[t] <= bid (empty super-tiles have fseg[t] == fseg[t+1])
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (fseg[mid] <= bid) lo = mid; else hi = mid;
+  }
+  q.t = lo;
+  q.seg = (int)(bid - fseg[lo]);
+  const int cs0 = crange[lo], ce0 = crange[lo + 1];
+  q.cs = cs0 + q.seg * kFineSeg;
+  q.ce = min(ce0, q.cs + kFineSeg);
+  q.k = lo / f.nST;
+  const int sidx = lo - q.k * f.nST;
+  q.bx0 = (sidx % cg.Cw) * kST;
+  q.by0 = (sidx / cg.Cw) * kST;
+  const int lane = threadIdx.x & 31;
+  bool ob[2];
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const int b = lane + 32 * h, bx = q.bx0 + (b & (kST - 1)), by = q.by0 + (b >> kSTShift);
+    const int loc = by * geo.Wt + bx;
+    ob[h] = bx < geo.Wt && by < geo.Ht && loc >= f.lo[q.k] && loc < f.hi[q.k];
+  }
+  q.own_lo = __ballot_sync(0xffffffffu, ob[0]);
+  q.own_hi = __ballot_sync(0xffffffffu, ob[1]);
+  return true;
+}
+
+// The owned blocks of the super-tile that coarse-list record i hits, as a 64-bit mask.
+__device__ __forceinline__ void fine_mask(const uint2* __restrict__ rect8, uint32_t j, const fine_seg& q,
+                                          unsigned& mlo, unsigned& mhi) {
+  int tx0, tx1, ty0, ty1, v;
+  unpack_rect(__ldg(&rect8[j]), tx0, tx1, ty0, ty1, v);
+  const int ix0 = max(tx0 - q.bx0, 0), ix1 = min(tx1 - q.bx0, kST - 1);
+  const int iy0 = max(ty0 - q.by0, 0), iy1 = min(ty1 - q.by0, kST - 1);
+  mlo = mhi = 0;
+  if (ix0 <= ix1 && iy0 <= iy1) {
+    const unsigned long long cols =
+        (unsigned long long)((0xffu << ix0) & (0xffu >> (kST - 1 - ix1))) * 0x0101010101010101ull;
+    const unsigned long long rows = (~0ull << (8 * iy0)) & (~0ull >> (8 * (kST - 1 - iy1)));
+    const unsigned long long m = cols & rows;
+    mlo = (unsigned)m & q.own_lo;
+    mhi = (unsigned)(m >> 32) & q.own_hi;
+  }
+}
+
+// Segments per super-tile: fseg[t] = ceil(len_t / kFineSeg) (then exclusively scanned).
+__global__ void k_fine_nseg(const int32_t* __restrict__ crange, int nt, int64_t* __restrict__ fseg) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nt) fseg[t] = (crange[t + 1] - crange[t] + kFineSeg - 1) / kFineSeg;
+}
+
+// Per-block hit counts of every segment: fcnt[seg][64].
+__global__ void __launch_bounds__(kFineThreads) k_fine_count(const uint2* __restrict__ rect8,
+                                                             const uint32_t* __restrict__ clist,
+                                                             const int32_t* __restrict__ crange,
+                                                             const int64_t* __restrict__ fseg, int nt, gs_geom geo,
+                                                             cgrid cg, fine_arg f, int* __restrict__ fcnt) {
+  constexpr int kB = kST * kST;
+  __shared__ int s_c[kB];
+  fine_seg q;
+  if (!find_fine_seg(blockIdx.x, fseg, nt, crange, geo, cg, f, q)) return;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < kB) s_c[tid] = 0;
+  __syncthreads();
+  int a = 0, b = 0;  // this lane's counts of blocks lane, lane + 32 (over its warp's chunks)
+  for (int c0 = q.cs; c0 < q.ce; c0 += kFineThreads) {
+    const int i = c0 + tid;
+    unsigned mlo = 0, mhi = 0;
+    if (i < q.ce) fine_mask(rect8, clist[i], q, mlo, mhi);
+    a += __popc(warp_transpose32(mlo, lane));
+    b += __popc(warp_transpose32(mhi, lane));
+  }
+  atomicAdd(&s_c[lane], a);
+  atomicAdd(&s_c[lane + 32], b);
+  __syncthreads();
+  if (tid < kB) fcnt[(int64_t)blockIdx.x * kB + tid] = s_c[tid];
+}
+
+// fcnt[seg][b] -> the hits of block b in the super-tile's earlier segments, and the block's
+// pair count (all its segments) to bcnt at its owned index (one thread per (super-tile,
+// block), sequential over the super-tile's segments; every owned block is written once).
+__global__ void k_fine_prefix(const int64_t* __restrict__ fseg, int nt, int* __restrict__ fcnt, gs_geom geo,
+                              cgrid cg, fine_arg f, int64_t* __restrict__ bcnt) {
+  constexpr int kB = kST * kST;
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (int64_t)nt * kB) return;
+  const int t = (int)(g / kB), b = (int)(g % kB);
+  const int k = t / f.nST, sidx = t - k * f.nST;
+  const int bx = (sidx % cg.Cw) * kST + (b & (kST - 1)), by = (sidx / cg.Cw) * kST + (b >> kSTShift);
+  const int loc = by * geo.Wt + bx;
+  const bool own = bx < geo.Wt && by < geo.Ht && loc >= f.lo[k] && loc < f.hi[k];
+  const int64_t s0 = fseg[t], s1 = fseg[t + 1];
+  int run = 0;
+  for (int64_t s = s0; s < s1; s++) {
+    const int x = fcnt[s * kB + b];
+    fcnt[s * kB + b] = run;
+    run += x;
+  }
+  if (own) bcnt[(int64_t)(f.v_lo + k) * geo.per_view + loc - f.B_lo] = run;
+}
+
 __global__ void __launch_bounds__(kFineThreads) k_fine(const uint2* __restrict__ rect8,
                                                        const uint32_t* __restrict__ clist,
-                                                       const int32_t* __restrict__ crange, gs_geom geo, cgrid cg,
+                                                       const int32_t* __restrict__ crange,
+                                                       const int64_t* __restrict__ fseg, int nt,
+                                                       const int* __restrict__ fcnt, gs_geom geo, cgrid cg,
                                                        fine_arg f, const int32_t* __restrict__ range,
                                                        uint32_t* __restrict__ out) {
   constexpr int kW = kFineThreads / 32, kB = kST * kST;
@@ -572,25 +648,17 @@ __global__ void __launch_bounds__(kFineThreads) k_fine(const uint2* __restrict__
   __shared__ int s_tot, s_tot_a;
   __shared__ uint32_t s_flat[kStage + 1];
   __shared__ uint8_t s_blk[kStage + 1];
-  const int bid = blockIdx.x;
-  const int cs = crange[bid], ce = crange[bid + 1];
-  if (cs >= ce) return;
-  const int k = bid / f.nST, sidx = bid - k * f.nST;
-  const int bx0 = (sidx % cg.Cw) * kST, by0 = (sidx / cg.Cw) * kST;
+  fine_seg q;
+  if (!find_fine_seg(blockIdx.x, fseg, nt, crange, geo, cg, f, q)) return;
+  const int cs = q.cs, ce = q.ce, k = q.k, bx0 = q.bx0, by0 = q.by0;
+  const unsigned own_lo = q.own_lo, own_hi = q.own_hi;
+  if (cs >= ce || (own_lo | own_hi) == 0) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  // the super-tile's owned blocks (every warp computes the same mask)
-  bool ob[2];
-#pragma unroll
-  for (int h = 0; h < 2; h++) {
-    const int b = lane + 32 * h, bx = bx0 + (b & (kST - 1)), by = by0 + (b >> kSTShift);
-    const int loc = by * geo.Wt + bx;
-    ob[h] = bx < geo.Wt && by < geo.Ht && loc >= f.lo[k] && loc < f.hi[k];
-  }
-  const unsigned own_lo = __ballot_sync(0xffffffffu, ob[0]), own_hi = __ballot_sync(0xffffffffu, ob[1]);
-  if ((own_lo | own_hi) == 0) return;
   if (tid < kB) {
     const int loc = (by0 + (tid >> kSTShift)) * geo.Wt + bx0 + (tid & (kST - 1));
-    s_cur[tid] = ob[tid >> 5] ? range[(int64_t)(f.v_lo + k) * geo.per_view + loc - f.B_lo] : 0;
+    s_cur[tid] = ((tid >> 5 ? own_hi : own_lo) >> (tid & 31) & 1u)
+                     ? range[(int64_t)(f.v_lo + k) * geo.per_view + loc - f.B_lo] + fcnt[(int64_t)blockIdx.x * kB + tid]
+                     : 0;
   }
   for (int c0 = cs; c0 < ce; c0 += kFineThreads) {
     __syncthreads();  // s_cur initialised / the previous chunk's staging written out
@@ -599,18 +667,7 @@ __global__ void __launch_bounds__(kFineThreads) k_fine(const uint2* __restrict__
     unsigned mlo = 0, mhi = 0;
     if (i < ce) {
       j = clist[i];
-      int tx0, tx1, ty0, ty1, v;
-      unpack_rect(__ldg(&rect8[j]), tx0, tx1, ty0, ty1, v);
-      const int ix0 = max(tx0 - bx0, 0), ix1 = min(tx1 - bx0, kST - 1);
-      const int iy0 = max(ty0 - by0, 0), iy1 = min(ty1 - by0, kST - 1);
-      if (ix0 <= ix1 && iy0 <= iy1) {
-        const unsigned long long cols =
-            (unsigned long long)((0xffu << ix0) & (0xffu >> (kST - 1 - ix1))) * 0x0101010101010101ull;
-        const unsigned long long rows = (~0ull << (8 * iy0)) & (~0ull >> (8 * (kST - 1 - iy1)));
-        const unsigned long long m = cols & rows;
-        mlo = (unsigned)m & own_lo;
-        mhi = (unsigned)(m >> 32) & own_hi;
-      }
+      fine_mask(rect8, j, q, mlo, mhi);
     }
     // lane l: which of the warp's records hit block l (tlo) and block l + 32 (thi)
     unsigned tlo = warp_transpose32(mlo, lane), thi = warp_transpose32(mhi, lane);
@@ -764,20 +821,16 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
   GS_REQUIRE(c, (int64_t)g.nv * nST < (1ll << 31) - 1, "too many super-tiles");
   GS_REQUIRE(c, geo.Wt < (1 << 16) && geo.Ht < (1 << 13), "image of %d x %d blocks exceeds the packed rectangle",
              geo.Wt, geo.Ht);
-  // 1. per-record coarse counts, block-count difference arrays, per-view coarse and owned-pair
-  //    totals (one host sync)
-  const int64_t dsz = (int64_t)g.nv * (geo.Ht + 1) * (geo.Wt + 1);
+  // 1. per-record coarse counts, per-view coarse and owned-pair totals (one host sync)
   int64_t* ncoarse = (int64_t*)gs_slot_get(c, SLOT_RECTILES, (n_recv + 1) * sizeof(int64_t), st);
   int64_t* ps = (int64_t*)gs_slot_get(c, SLOT_PSTART, (n_recv + 1) * sizeof(int64_t), st);
   unsigned long long* vc = (unsigned long long*)gs_slot_get(c, SLOT_COUNTS, 2 * GS_MAX_VIEWS * sizeof(int64_t), st);
-  int* diff = (int*)gs_slot_get(c, SLOT_DIFF, dsz * sizeof(int), st);
   uint2* rect8 = (uint2*)gs_slot_get(c, SLOT_RECT8, n_recv * sizeof(uint2), st);
-  if (!ncoarse || !ps || !vc || !diff || !rect8) return gs_fail(c, GS_ECUDA, "scratch");
+  if (!ncoarse || !ps || !vc || !rect8) return gs_fail(c, GS_ECUDA, "scratch");
   GS_CUDA(c, cudaMemsetAsync(vc, 0, 2 * GS_MAX_VIEWS * sizeof(int64_t), st));
-  GS_CUDA(c, cudaMemsetAsync(diff, 0, dsz * sizeof(int), st));
   ++c->launches;
   k_tile_counts<<<(unsigned)((n_recv + 256) / 256), 256, 0, st>>>(rec, n_recv, geo, g, ncoarse, vc,
-                                                                  vc + GS_MAX_VIEWS, diff, rect8);
+                                                                  vc + GS_MAX_VIEWS, rect8);
   GS_LAUNCH_CHECK(c, "tile counts");
   GS_CUDA(c, cudaMemcpyAsync(c->pinned, vc, 2 * GS_MAX_VIEWS * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GS_CUDA(c, cudaStreamSynchronize(st));
@@ -807,22 +860,11 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
     return gs_fail(c, GS_ENOTSUP, "pair total %lld exceeds int32 positions", (long long)std::max(n_pad, K));
   if (K > pair_cap) return gs_fail(c, GS_ECAPACITY, "pair capacity %lld < %lld", (long long)pair_cap, (long long)K);
   GS_REQUIRE(c, K == 0 || sorted_idx != nullptr, "null sorted_idx");
-  // 2. block offsets: 2D prefix of the difference arrays, owned counts, exclusive scan
-  int64_t* bcnt = (int64_t*)gs_slot_get(c, SLOT_BCOUNT, (n_owned + 1) * sizeof(int64_t), st);
-  if (!bcnt) return gs_fail(c, GS_ECUDA, "scratch");
-  GS_CUDA(c, cudaMemsetAsync(bcnt + n_owned, 0, sizeof(int64_t), st));
-  const int64_t nrows = (int64_t)g.nv * (geo.Ht + 1);
-  ++c->launches;
-  k_diff_rows<<<(unsigned)((nrows * 32 + 255) / 256), 256, 0, st>>>(diff, nrows, geo.Wt + 1);
-  ++c->launches;
-  k_diff_cols<<<dim3((unsigned)((geo.Wt + 127) / 128), (unsigned)g.nv), 128, 0, st>>>(diff, geo, g, bcnt);
-  GS_LAUNCH_CHECK(c, "block counts");
-  s = gs_scan_i64(c, bcnt, bcnt, n_owned + 1, 0, st);
-  if (s != GS_OK) return s;
-  ++c->launches;
-  k_to_i32<<<(unsigned)((n_owned + 256) / 256), 256, 0, st>>>(bcnt, n_owned + 1, tile_range);
-  GS_LAUNCH_CHECK(c, "block ranges");
-  if (K == 0) return GS_OK;
+  if (K == 0) {  // no owned pair: empty lists
+    GS_CUDA(c, cudaMemsetAsync(tile_range, 0, (n_owned + 1) * sizeof(int32_t), st));
+    return GS_OK;
+  }
+
   // 3. records by (view, depth): 4 stable 8-bit depth passes (A -> B -> A -> B -> A), then the
   //    view (-> B -> A, values only kept)
   const int64_t cap = std::max(n_pad, n_recv);
@@ -898,9 +940,34 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
   // 6. super-tile ranges of the coarse lists (sorted keys now in kin), then the fine emission
   ++c->launches;
   k_seg_ranges<<<(unsigned)(n_pad / 1024), 256, 0, st>>>(kin, cgs, nST, crange);
+  // fine emission over segments of kFineSeg coarse records (long lists split across CTAs)
+  const int nt = g.nv * nST;
+  const int64_t nseg_max = nt + n_full / kFineSeg + 1;  // >= sum over t of ceil(len_t / kFineSeg)
+  int64_t* fseg = (int64_t*)gs_slot_get(c, SLOT_CURSOR, ((int64_t)nt + 1) * sizeof(int64_t), st);
+  int* fcnt = (int*)gs_slot_get(c, SLOT_FSEG_CNT, nseg_max * kST * kST * sizeof(int), st);
+  if (!fseg || !fcnt) return gs_fail(c, GS_ECUDA, "fine emission scratch");
   ++c->launches;
-  k_fine<<<(unsigned)((int64_t)g.nv * nST), kFineThreads, 0, st>>>(rect8, clist, crange, geo, cg, fa, tile_range,
-                                                                   sorted_idx);
+  k_fine_nseg<<<(unsigned)((nt + 256) / 256), 256, 0, st>>>(crange, nt, fseg);
+  GS_CUDA(c, cudaMemsetAsync(fseg + nt, 0, sizeof(int64_t), st));
+  s = gs_scan_i64(c, fseg, fseg, (int64_t)nt + 1, 0, st);
+  if (s != GS_OK) return s;
+  // block pair counts -> tile_range (exclusive scan over the owned blocks)
+  int64_t* bcnt = (int64_t*)gs_slot_get(c, SLOT_BCOUNT, (n_owned + 1) * sizeof(int64_t), st);
+  if (!bcnt) return gs_fail(c, GS_ECUDA, "scratch");
+  GS_CUDA(c, cudaMemsetAsync(bcnt + n_owned, 0, sizeof(int64_t), st));
+  ++c->launches;
+  k_fine_count<<<(unsigned)nseg_max, kFineThreads, 0, st>>>(rect8, clist, crange, fseg, nt, geo, cg, fa, fcnt);
+  ++c->launches;
+  k_fine_prefix<<<(unsigned)(((int64_t)nt * kST * kST + 255) / 256), 256, 0, st>>>(fseg, nt, fcnt, geo, cg, fa,
+                                                                                   bcnt);
+  GS_LAUNCH_CHECK(c, "block counts");
+  s = gs_scan_i64(c, bcnt, bcnt, n_owned + 1, 0, st);
+  if (s != GS_OK) return s;
+  ++c->launches;
+  k_to_i32<<<(unsigned)((n_owned + 256) / 256), 256, 0, st>>>(bcnt, n_owned + 1, tile_range);
+  ++c->launches;
+  k_fine<<<(unsigned)nseg_max, kFineThreads, 0, st>>>(rect8, clist, crange, fseg, nt, fcnt, geo, cg, fa,
+                                                     tile_range, sorted_idx);
   GS_LAUNCH_CHECK(c, "bin_sort fine");
   return GS_OK;
 }

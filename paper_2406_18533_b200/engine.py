@@ -89,6 +89,7 @@ class GrendelTrainer:
         self.recv = _Buf(dev, torch.uint8, (L.RECORD_BYTES,))
         self.sorted = _Buf(dev, torch.int32)
         self.range = _Buf(dev, torch.int32)
+        self.cull = _Buf(dev, torch.int32)  # the forward's per-entry cull bits, reused by the backward
         self.T = _Buf(dev, torch.float32, (256,))
         self.nl = _Buf(dev, torch.int32, (256,))
         self.dpix = _Buf(dev, torch.float32, (3, 256))
@@ -327,6 +328,7 @@ class GrendelTrainer:
         rec("bin_sort", 1)
         # A4 render forward + fused L1
         self.T.ensure(no), self.nl.ensure(no), self.dpix.ensure(no), self.cost.ensure(no)
+        self.cull.ensure(L.cull_words(n_pairs, no))
         self.drec.ensure(n_recv), self.dsend.ensure(n_send)
         self.cost.t[:no].zero_()
         self.loss.zero_()
@@ -344,11 +346,11 @@ class GrendelTrainer:
         rec("render_fwd", 0)
         if self.loss_kind == "l1":  # L1 fused into the forward's epilogue (O13)
             L.render_fwd(ctx, recv_t, self.sorted.t, self.range.t, cams, dp, self.bg, gt, self.b, None, self.T.t,
-                         self.nl.t, self.dpix.t, self.loss, cost_t, self.cost_mode, stats, st)
+                         self.nl.t, self.dpix.t, self.loss, cost_t, self.cost_mode, stats, st, cull=self.cull.t)
         else:
             self.rgb.ensure(no)
             L.render_fwd(ctx, recv_t, self.sorted.t, self.range.t, cams, dp, self.bg, None, self.b, self.rgb.t,
-                         self.T.t, self.nl.t, None, None, cost_t, self.cost_mode, stats, st)
+                         self.T.t, self.nl.t, None, None, cost_t, self.cost_mode, stats, st, cull=self.cull.t)
         rec("render_fwd", 1)
         if self.loss_kind == "ssim":  # NEXT-1: L1 + D-SSIM in two passes around halo exchanges
             rec("loss", 0)
@@ -364,10 +366,10 @@ class GrendelTrainer:
         rec("render_bwd", 0)
         if p2p:  # A5 + A6 fused: gradient sums reduced straight into the owners' buffers
             L.render_bwd_put(ctx, recv_t, n_recv, self.sorted.t, self.range.t, cams, dp, self.dpix.t, self.T.t,
-                             self.nl.t, cost_t, self.cost_mode, stats, st)
+                             self.nl.t, cost_t, self.cost_mode, stats, st, cull=self.cull.t)
         else:
             L.render_bwd(ctx, recv_t, n_recv, self.sorted.t, self.range.t, cams, dp, self.bg, self.dpix.t,
-                         self.T.t, self.nl.t, self.drec.t, cost_t, self.cost_mode, stats, st)
+                         self.T.t, self.nl.t, self.drec.t, cost_t, self.cost_mode, stats, st, cull=self.cull.t)
         rec("render_bwd", 1)
         if paper_avg:
             self._pa_ev[1].record(torch.cuda.current_stream() if st is None else st)
@@ -475,6 +477,7 @@ class VirtualGrendel:
         self.send = _Buf(dev, torch.uint8, (L.RECORD_BYTES,))
         self.dsend = _Buf(dev, torch.float32, (L.GRAD_FLOATS,))
         self.sorted = _Buf(dev, torch.int32)
+        self.cull = _Buf(dev, torch.int32)
         self.range = _Buf(dev, torch.int32, (), self.B + 1)
         self.T = _Buf(dev, torch.float32, (256,), self.B)
         self.nl = _Buf(dev, torch.int32, (256,), self.B)
@@ -504,7 +507,7 @@ class VirtualGrendel:
             recv = self.send.t[off[r]:]
             while True:
                 try:
-                    L.bin_sort(ctx, recv, n_recv, cams, dp, self.sorted.t, self.sorted.cap, self.range.t)
+                    n_pairs = L.bin_sort(ctx, recv, n_recv, cams, dp, self.sorted.t, self.sorted.cap, self.range.t)
                     break
                 except L.CapacityError as e:
                     self.sorted.ensure(e.needed)
@@ -512,11 +515,12 @@ class VirtualGrendel:
             # PAPER_AVG: the rank's measured render time, spread by gs_rebalance_row over
             # its pixels; the kernels' per-block counters are not used
             cost = None if self.cost_mode == L.COST_PAPER_AVG else (self.row[dp[r]:] if no else self.row)
+            self.cull.ensure(L.cull_words(n_pairs, no))
             e0.record()
             L.render_fwd(ctx, recv, self.sorted.t, self.range.t, cams, dp, (0, 0, 0), gt, self.b, None, self.T.t,
-                         self.nl.t, self.dpix.t, self.loss, cost, self.cost_mode, None)
+                         self.nl.t, self.dpix.t, self.loss, cost, self.cost_mode, None, cull=self.cull.t)
             L.render_bwd(ctx, recv, n_recv, self.sorted.t, self.range.t, cams, dp, (0, 0, 0), self.dpix.t,
-                         self.T.t, self.nl.t, self.dsend.t[off[r]:], cost, self.cost_mode, None)
+                         self.T.t, self.nl.t, self.dsend.t[off[r]:], cost, self.cost_mode, None, cull=self.cull.t)
             e1.record()
             ms.append((e0, e1))
         ms_r = None

@@ -55,7 +55,9 @@ class Run:
         self.n_send = int(self.send_counts.sum())
         self.bg, self.gt, self.cost_mode = bg, gt, cost_mode
 
-    def render(self, recv, n_recv, upstream=None):
+    def render(self, recv, n_recv, upstream=None, cull=False):
+        """cull: the forward writes its per-entry cull bits and the backward reads them instead
+        of repeating the test (gs_render_fwd / gs_render_bwd cull_bits)."""
         ctx, dp = self.ctx, self.dp
         self.recv, self.n_recv = recv, n_recv
         no = int(dp[ctx.rank + 1] - dp[ctx.rank])
@@ -75,14 +77,15 @@ class Run:
         self.cost = torch.zeros(no, dtype=torch.int64, device=DEV)
         self.stats = torch.zeros(8, dtype=torch.int64, device=DEV)
         gt_t = torch.from_numpy(self.gt).to(DEV) if self.gt is not None else None
+        cb = torch.empty(L.cull_words(self.n_pairs, no), dtype=torch.int32, device=DEV) if cull else None
         L.render_fwd(ctx, recv, self.sorted, self.range, self.cams, dp, self.bg, gt_t, len(self.cams), self.rgb,
                      self.T, self.nl, self.dpix if gt_t is not None else None, self.loss, self.cost,
-                     self.cost_mode, self.stats)
+                     self.cost_mode, self.stats, cull=cb)
         if upstream is not None:
             self.dpix.copy_(torch.from_numpy(np.ascontiguousarray(upstream.transpose(0, 2, 1)).reshape(-1)).to(DEV))
         self.drec = torch.empty((max(n_recv, 1), 9), dtype=torch.float32, device=DEV)
         L.render_bwd(ctx, recv, n_recv, self.sorted, self.range, self.cams, dp, self.bg, self.dpix, self.T, self.nl,
-                     self.drec, self.cost, self.cost_mode, self.stats)
+                     self.drec, self.cost, self.cost_mode, self.stats, cull=cb)
         torch.cuda.synchronize()
         return self
 
@@ -195,14 +198,16 @@ def test_render_fwd(case):
 
 
 # ---------------------------------------------------------------- A5 backward
-def test_render_bwd_upstream(case):
+@pytest.mark.parametrize("cull", [False, True], ids=["cull-test", "cull-bits"])
+def test_render_bwd_upstream(case, cull):
     """Seeded upstream gradient on every pixel fed to both sides (the upstream is an input, so
     sign decisions of the loss cannot differ); the oracle's backward follows, per pixel, the
-    outcome path the GPU forward took."""
+    outcome path the GPU forward took.  cull-bits: the backward reads the forward's cull
+    decisions (the trainer's path) instead of repeating the test."""
     sc, cams, bg, recs, off, ent, fwd = (case[k] for k in ("scene", "cams", "bg", "recs", "off", "ent", "fwd"))
     run = Run(sc, cams, bg, None)
     up = synth.upstream_grad(11, (16, 256, 3)).astype(np.float64) * 1e-3
-    run.render(run.send, run.n_send, upstream=up.astype(np.float32))
+    run.render(run.send, run.n_send, upstream=up.astype(np.float32), cull=cull)
     flips, _ = matched(run, fwd, case["name"])
     g_or = oracle.render_bwd(recs, off, ent, 0, 16, run.W, run.H, up.astype(np.float32).astype(np.float64), bg,
                              flips=flips)

@@ -58,13 +58,16 @@ def _window_case(sc, cam, lo_frac=0.45, nblk=256, seed=0):
     rgb = torch.empty(no * 768, device=DEV)
     dpix = torch.empty(no * 768, device=DEV)
     loss = torch.zeros(1, dtype=torch.float64, device=DEV)
-    L.render_fwd(ctx, recv, srt, rng_t, [cam], dp, (0, 0, 0), gt_t, 1, rgb, T, nl, dpix, loss, None, 0, None)
+    # the forward's cull bits, read by the backward (the launch configuration the trainer and bench use)
+    cull = torch.empty(L.cull_words(npairs, no), dtype=torch.int32, device=DEV)
+    L.render_fwd(ctx, recv, srt, rng_t, [cam], dp, (0, 0, 0), gt_t, 1, rgb, T, nl, dpix, loss, None, 0, None,
+                 cull=cull)
     torch.cuda.synchronize()
     # oracle over the same window
     recs = oracle.make_records(sc, [cam], "parity")
     o_off, o_ent = oracle.tile_lists(recs, lo, hi, Wt, Ht)
     fwd = oracle.render_fwd(recs, o_off, o_ent, lo, hi, W, H, (0, 0, 0), gt[None], 1, max_paths=64)
-    return dict(ctx=ctx, dp=dp, recv=recv, n_recv=n_recv, range=rng_t, sorted=srt, npairs=npairs, T=T, nl=nl,
+    return dict(ctx=ctx, dp=dp, recv=recv, n_recv=n_recv, range=rng_t, sorted=srt, npairs=npairs, T=T, nl=nl, cull=cull,
                 rgb=rgb, dpix=dpix, recs=recs, off=o_off, ent=o_ent, fwd=fwd, no=no, lo=lo, hi=hi, W=W, H=H,
                 Wt=Wt, Ht=Ht, cam=cam, sc=sc, cnt=cnt)
 
@@ -102,7 +105,7 @@ def _check_bwd(c, flips):
     dpix = torch.from_numpy(np.ascontiguousarray(up.astype(np.float32).transpose(0, 2, 1)).reshape(-1)).to(DEV)
     drec = torch.empty((max(c["n_recv"], 1), 9), device=DEV)
     L.render_bwd(ctx, c["recv"], c["n_recv"], c["sorted"], c["range"], [c["cam"]], dp, (0, 0, 0), dpix, c["T"],
-                 c["nl"], drec, None, 0, None)
+                 c["nl"], drec, None, 0, None, cull=c["cull"])
     torch.cuda.synchronize()
     g_or = oracle.render_bwd(c["recs"], c["off"], c["ent"], c["lo"], c["hi"], c["W"], c["H"],
                              up.astype(np.float32).astype(np.float64), flips=flips)
