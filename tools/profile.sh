@@ -15,7 +15,7 @@ ncu --set full --clock-control none --import-source on -k regex:'k_render_bwd|k_
     -s 6 -c 2 -o $OUT/prof_${TAG}_${CFG}_render $B > $OUT/prof_${TAG}_${CFG}_render.log 2>&1
 # 3. projection and binning kernels in the bench command
 ncu --set full --clock-control none --import-source on \
-    -k regex:'k_project_count|k_project_write|k_radix_scatter|k_radix_hist|k_emit|k_key_ranges' \
+    -k regex:'k_project_count|k_project_write|k_radix_scatter|k_radix_hist|k_emit|k_fine|k_tile_counts|k_diff_rows|k_diff_cols' \
     -s 150 -c 20 -o $OUT/prof_${TAG}_${CFG}_bin $B > $OUT/prof_${TAG}_${CFG}_bin.log 2>&1
 # 4. the Adam kernels write all parameters, moments and gradients (~11 GB at C2), which kernel
 #    replay must save/restore: capture them on a reduced copy (4 views, 2.8M Gaussians)
