@@ -54,3 +54,29 @@ def test_host_only_calls():
     assert list(so) == [0, 3, 7, 12] and list(ro) == [0, 2, 6, 6]
     with pytest.raises(L.GSError):
         L.division_points([-1, 2], 2)
+
+
+def test_cull_words_cover_every_staged_word():
+    """gs_cull_words: the forward stores the keep ballot of list entries 32k..32k+31 of block lb
+    and half h at word 2 (range[lb] / 32 + lb + k) + h (gs_render.cu k_render_fwd); every word
+    a block's list can need (including the round's second word of a 64-entry staging round
+    that starts inside the list) lies below gs_cull_words(n_pairs, n_owned), and no two blocks
+    share a word."""
+    import paper_2406_18533_b200._lib as L
+    rng = np.random.default_rng(7)
+    for trial in range(200):
+        n_owned = int(rng.integers(1, 60))
+        lens = rng.integers(0, 300, n_owned) * (rng.random(n_owned) < 0.8)
+        rng_ = np.concatenate([[0], np.cumsum(lens)])
+        n_pairs = int(rng_[-1])
+        words = L.cull_words(n_pairs, n_owned)
+        used = set()
+        for lb in range(n_owned):
+            beg, ln = int(rng_[lb]), int(lens[lb])
+            for k in range((ln + 31) // 32):  # words written: entries 32k < len
+                for h in (0, 1):
+                    w = 2 * (beg // 32 + lb + k) + h
+                    assert w < words, (trial, lb, k, w, words)
+                    assert w not in used
+                    used.add(w)
+    assert L.cull_words(0, 0) == 2 and L.cull_words(-1, 3) == 0
