@@ -641,7 +641,7 @@ def main():
         "render_bwd": ("alu", (CENSUS["bwd_contrib"] * Ebc + CENSUS["bwd_skip"] * (Eb - Ebc)) / 1e12,
                        "T FP32-lane-op/s", fp32_peak),
         "adam": ("hbm", (1416.0 * p.n + 36.0 * counts["n_send"]) / 1e9, "GB/s", float(pk.get("hbm_gbs", 6650.0))),
-        "project": ("hbm", (236.0 * p.n + 48.0 * counts["n_send"]) / 1e9, "GB/s", float(pk.get("hbm_gbs", 6650.0))),
+        "project": ("hbm", (236.0 * p.n + 56.0 * counts["n_send"]) / 1e9, "GB/s", float(pk.get("hbm_gbs", 6650.0))),
         "bin_sort": ("hbm", (28.0 * counts["n_pairs"] + 16.0 * counts["n_recv"]) / 1e9, "GB/s",
                      float(pk.get("hbm_gbs", 6650.0))),
         "loss": ("alu", SSIM_OPS_PER_PIXEL * 256.0 * counts["n_owned"] / 1e12, "T FP32-lane-op/s", fp32_peak),
