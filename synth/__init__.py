@@ -147,8 +147,10 @@ def _chunked(kind, seed, n_total, lo, hi) -> Scene:
     if len(jobs) > 1:
         import concurrent.futures as cf
         import multiprocessing as mp
+        # spawn, not fork: the caller may hold an initialised CUDA context (GPU tests, bench),
+        # which a forked child must not touch
         with cf.ProcessPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1),
-                                    mp_context=mp.get_context("fork")) as ex:
+                                    mp_context=mp.get_context("spawn")) as ex:
             chunks = list(ex.map(_chunk_job, jobs))
     else:
         chunks = [_chunk_job(j) for j in jobs]
