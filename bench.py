@@ -392,7 +392,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-morton", action="store_true", help="keep the generator's (random) Gaussian order")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--breakdown-steps", type=int, default=2)
+    ap.add_argument("--breakdown-steps", type=int, default=5)
     ap.add_argument("--json-out", default=None)
     ap.add_argument("--densify", action="store_true",
                     help="NEXT-2: collect densification statistics every step and time one densify event at "
@@ -530,7 +530,7 @@ def main():
     value = views / (ms_max / 1000.0)
 
     # ---------------- per-call breakdown + work counters (untimed pass)
-    calls = {}
+    calls, call_lists = {}, {}
     stats = np.zeros(8, np.int64)
     counts = dict(n_send=0, n_recv=0, n_pairs=0, n_owned=0)
     # per-call times with the kernels of the timed region (no counters), then the same batches
@@ -541,7 +541,9 @@ def main():
         one_step(events=ev)
         torch.cuda.synchronize()
         for kname, v in event_ms(ev).items():
-            calls[kname] = calls.get(kname, 0.0) + v / args.breakdown_steps
+            call_lists.setdefault(kname, []).append(v)
+    # per call: the median over the breakdown steps, p10 / p90 reported beside it
+    calls = {k: float(np.median(v)) for k, v in call_lists.items()}
     k_sched[0] = k_bd
     for _ in range(args.breakdown_steps):
         one_step(stats=True)
@@ -717,6 +719,8 @@ def main():
                            "shard_layout": "random" if args.no_morton else "morton"},
                 "raster_ms_per_view": round(raster_ms_view, 3),
                 "calls_ms": {k: round(v, 3) for k, v in calls.items()},
+                "calls_ms_p10_p90": {k: [round(float(np.percentile(v, 10)), 3), round(float(np.percentile(v, 90)), 3)]
+                                     for k, v in call_lists.items()},
                 "gpu_launches": int(launches),
                 "roofline": {"bound": bound, "kernel": dom, "achieved": round(achieved, 3), "peak": peak,
                              "unit": unit, "frac": round(achieved / peak, 4), "traffic": traffic,

@@ -116,17 +116,15 @@ __device__ __forceinline__ float ref_w(const float4& a, const float4& b, const f
 // jr: the round's receive indices (load_idx); the backward loads them one round ahead, so its
 // staging waits on one level of dependent loads (the records), not two.
 // Cull bits (gs_render_fwd's cull_bits): word k of the round holds the keep ballot of entries
-// 32k .. 32k + 31; bits_out (forward, nullable) receives them, bits_in (backward, nullable)
-// replaces the test -- the same decisions, so the same staged entries.  Both point at the
-// round's first word of this half; consecutive words are 2 apart (the halves interleave).
+// 32k .. 32k + 31; bal (out) returns them to the forward, which stores them; bits_in
+// (backward, nullable: the round's first word of this half, consecutive words 2 apart as the
+// halves interleave) replaces the test -- the same decisions, so the same staged entries.
 template <int KW, int S = 3>
 __device__ __forceinline__ int stage_warp(const gs_rec* __restrict__ rec, const uint32_t (&jr)[KW / 32], int cnt,
                                           int pos0, float4* s, float hx0, float hy0, int pad,
-                                          const uint32_t* __restrict__ bits_in = nullptr,
-                                          uint32_t* __restrict__ bits_out = nullptr) {
+                                          unsigned (&bal)[KW / 32], const uint32_t* __restrict__ bits_in = nullptr) {
   constexpr int kI = KW / 32;
   const int lane = threadIdx.x & 31;
-  unsigned bal[kI];
   if (bits_in) {
 #pragma unroll
     for (int i = 0; i < kI; i++) {
@@ -145,11 +143,6 @@ __device__ __forceinline__ int stage_warp(const gs_rec* __restrict__ rec, const 
         keep = box_may_hit(a.x, a.y, b.x, b.y, b.z, qmax, hx0, hy0, 7.f, 15.f);
       }
       bal[i] = __ballot_sync(0xffffffffu, keep);
-    }
-    if (bits_out && lane == 0) {
-#pragma unroll
-      for (int i = 0; i < kI; i++)
-        if (32 * i < cnt) bits_out[2 * i] = bal[i];
     }
   }
   const double rx = (double)hx0 + 3.5, ry = (double)hy0 + 7.5;
@@ -313,9 +306,15 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_fwd(
     // 56-register cap: 18.41 -> 18.55 ms)
     uint32_t jc[kFW / 32];
     load_idx<kFW>(sorted_idx + b0, cnt, jc);
-    // this half's cull words of the round: word (beg / 32 + lb + position / 32), halves interleaved
-    uint32_t* const bo = cull ? cull + 2 * ((int64_t)(beg >> 5) + lb + ((b0 - beg) >> 5)) + wid : nullptr;
-    const int kept = stage_warp<kFW>(rec, jc, cnt, b0 - beg, s, hx0, hy0, kUnroll, nullptr, bo);
+    unsigned bal[kFW / 32];
+    const int kept = stage_warp<kFW>(rec, jc, cnt, b0 - beg, s, hx0, hy0, kUnroll, bal);
+    if (cull && lane == 0) {
+      // this half's cull words of the round: word (beg / 32 + lb + position / 32), halves interleaved
+      uint32_t* const bo = cull + 2 * ((int64_t)(beg >> 5) + lb + ((b0 - beg) >> 5)) + wid;
+#pragma unroll
+      for (int i = 0; i < kFW / 32; i++)
+        if (32 * i < cnt) bo[2 * i] = bal[i];
+    }
     const int kept8 = (kept + kUnroll - 1) & ~(kUnroll - 1);
     for (int k0 = 0; k0 < kept8; k0 += kUnroll) {
       if (all_done()) break;
@@ -575,7 +574,8 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_bwd(
     __syncwarp();
     const uint32_t* const bi_ =
         GS_CULL_REUSE && cull ? cull + 2 * ((int64_t)(beg >> 5) + lb + (p0 >> 5)) + wid : nullptr;
-    const int kept = stage_warp<kBW, 4>(rec, jc, cnt, p0, s, hx0, hy0, 1, bi_);
+    unsigned bal[kBW / 32];
+    const int kept = stage_warp<kBW, 4>(rec, jc, cnt, p0, s, hx0, hy0, 1, bal, bi_);
     const float4* ep = s + 4 * (kept - 1);  // entry k's quadruple
     for (int k = kept - 1; k >= 0; k--, ep -= 4) {
       const float4 cq = ep[2];
