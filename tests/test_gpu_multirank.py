@@ -130,11 +130,16 @@ def _check(one, many, G):
     np.testing.assert_array_equal(np.concatenate([m["nl"] for m in many]), one["nl"])
     np.testing.assert_array_equal(np.concatenate([m["cost"] for m in many]), one["cost"])  # WORK: invariant
     assert abs(sum(m["loss"] for m in many) - one["loss"]) <= 1e-6 * abs(one["loss"])
-    # P17: parameter gradients (shards concatenated) within the 1e-3 metric
+    # P17: parameter gradients (shards concatenated) against the single-rank run -- two GPU
+    # runs, so the difference is the fp32 atomic summation order: l2 within 1e-3, the max norm
+    # within 3e-3 (DESIGN.md §9 "GPU against GPU": the single-rank run against itself already
+    # differs by 5.7e-4 of the group maximum in the scale and rotation groups of this crop)
     for k in range(4):
         got = np.concatenate([m["g"][k] for m in many], axis=-2)
         want = one["g"][k]
-        assert np.abs(got - want).max() <= 1e-3 * np.abs(want).max() + 1e-30, k
+        d = got - want
+        assert np.abs(d).max() <= 3e-3 * np.abs(want).max() + 1e-30, (k, np.abs(d).max() / np.abs(want).max())
+        assert np.linalg.norm(d) <= 1e-3 * np.linalg.norm(want) + 1e-30, (k, np.linalg.norm(d) / np.linalg.norm(want))
     # A9: identical next division points on every rank = Algorithm 1 on the WORK row
     want_dp = oracle.division_points(one["cost"], G)
     for m in many:
