@@ -121,7 +121,7 @@ void gs_destroy(gs_ctx* c) {
   if (c->pinned) cudaFreeHost(c->pinned);
   for (void* q : c->p2p.opened) cudaIpcCloseMemHandle(q);
   if (c->p2p.err) cudaFree(c->p2p.err);
-  for (int k = 0; k < 3; k++)
+  for (int k = 0; k < 5; k++)
     if (c->p2p.sym[k]) cudaFree(c->p2p.sym[k]);
 #ifdef GS_WITH_NCCL
   if (c->comm) ncclCommDestroy(c->comm);
