@@ -125,8 +125,10 @@ __global__ void __launch_bounds__(kBlock) k_project_write(
     q = rot[i];
   }
   gs_cov3 cv = cov3_of(ls, q);
-  // O1 opacity, rounded to nearest from fp64 (it sets alpha and the skip threshold)
+  // O1 opacity, rounded to nearest from fp64 (it sets alpha and the skip threshold), and
+  // log2(255 o) rounded to nearest from fp64 (a record's qmax; per Gaussian, not per view)
   const float opac = __double2float_rn(1.0 / (1.0 + exp(-(double)X.w)));
+  const float qmax_o = opac > 0.f ? __double2float_rn(log2(255.0 * (double)opac)) : -1.0f;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   for (int v = 0; v < b; v++) {
@@ -157,7 +159,7 @@ __global__ void __launch_bounds__(kBlock) k_project_write(
       // qmax = log2(255 o), rounded to nearest from fp64 (alpha = o 2^-q >= 1/255 <=> q <= qmax);
       // -1 (never composited) for a zero opacity or a covariance whose fp64 determinant is not
       // positive (not reachable with the 0.3 I dilation: det >= 0.09)
-      const float qmax = (opac > 0.f && lh[0] > 0.f) ? __double2float_rn(log2(255.0 * (double)opac)) : -1.0f;
+      const float qmax = lh[0] > 0.f ? qmax_o : -1.0f;
       // O9: colour from the view direction
       float dx = X.x - cam.campos[0], dy = X.y - cam.campos[1], dz = X.z - cam.campos[2];
       float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
