@@ -232,15 +232,16 @@ __device__ __forceinline__ void q_strip(const float4& A, const float4& Bq, float
 // (identical results).  kCapFree sits 1e-4 below the cap: raw would need G > 1.0001.
 constexpr float kCapFree = 0.9899f;
 // Composite one staged entry into one pixel (O12) given its capped alpha >= 1/255.  A pixel
-// that stops gets the +inf penalty (pen: a thread is done when all its penalties are); kTrack keeps its stop
+// that stops gets the +inf penalty (pen) and counts towards ndone; kTrack keeps its stop
 // position (evaluation counts: statistics and the WORK cost mode).
 template <bool kStats, bool kTrack>
 __device__ __forceinline__ void fwd_comp(float alpha, float cr, float cg, float cb, int pos, float& T, float& C0,
-                                         float& C1, float& C2, float& pen, int& nlast, int& stop_pos,
+                                         float& C1, float& C2, float& pen, int& ndone, int& nlast, int& stop_pos,
                                          int& efc) {
   const float Tn = T * (1.0f - alpha);
   if (Tn < kTStop) {  // R3: stop before compositing this entry
     pen = __int_as_float(0x7f800000);
+    ndone++;
     if (kTrack) stop_pos = pos;
     return;
   }
@@ -282,6 +283,7 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_fwd(
   float T[kPPT], C0[kPPT], C1[kPPT], C2[kPPT];
   int nl[kPPT], sp[kPPT];
   float2 pen[kPPT / 2];  // pixel pairs; 0: live pixel, +inf: stopped or outside the image (q_strip)
+  int ndone = 0;
   unsigned inside = 0;
 #pragma unroll
   for (int j = 0; j < kPPT; j++) {
@@ -292,13 +294,10 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_fwd(
     const bool in = px < geo.W && py0 + kRS * j < geo.H;
     inside |= (unsigned)in << j;
     (j & 1 ? pen[j / 2].y : pen[j / 2].x) = in ? 0.f : __int_as_float(0x7f800000);
+    ndone += !in;
   }
   int efc = 0;
-  // done: every penalty +inf (pixels stopped or outside the image) -- no per-composite counter
-  static_assert(kPPT == 4, "all_done reads two penalty pairs");
-  auto all_done = [&]() {
-    return fminf(fminf(pen[0].x, pen[0].y), fminf(pen[1].x, pen[1].y)) == __int_as_float(0x7f800000);
-  };
+  auto all_done = [&]() { return ndone == kPPT; };
   float4* const s = s_e + wid * 3 * kSlots;  // this warp's slots
   for (int b0 = beg; b0 < end; b0 += kFW) {
     if (__all_sync(0xffffffffu, all_done())) break;
@@ -336,7 +335,7 @@ __global__ void __launch_bounds__(kNT, MINB) k_render_fwd(
             if (cj[j]) {
               const float al = fminf(kAlphaCap, __fmul_rn(Bq.y, ex2_approx(-e.q[j])));
               fwd_comp<kStats, kTrack>(al, Bq.z, Bq.w, cq.x, __float_as_int(cq.z), T[j], C0[j], C1[j], C2[j],
-                                       j & 1 ? pen[j / 2].y : pen[j / 2].x, nl[j], sp[j], efc);
+                                       j & 1 ? pen[j / 2].y : pen[j / 2].x, ndone, nl[j], sp[j], efc);
             }
         }
       }
