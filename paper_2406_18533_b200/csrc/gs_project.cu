@@ -23,6 +23,8 @@ namespace {
 // Record destinations of k_project_write: the record at send-order position pos with
 // destination d goes to d_[d][pos] (all d_ = the send buffer for gs_project; for the fused
 // NEXT-3 path d_[d] = d's receive buffer + put_base[d] - send_off[d]).
+constexpr int kPList = 8;  // records per thread listed per round (k_project_write)
+
 struct gs_outs {
   gs_rec* d[GS_MAX_WORLD];
 };
@@ -89,6 +91,8 @@ __global__ void __launch_bounds__(kBlock) k_project_write(
     gs_devouts dv) {
   __shared__ int s_cnt[kWarps * kMaxBuckets];
   __shared__ gs_rec* s_out[GS_MAX_WORLD];  // kDev: destination d's base for this rank's records
+  __shared__ int64_t s_pos[kPList * kBlock];  // per-thread send positions of its records
+  __shared__ uint16_t s_vd[kPList * kBlock];  // and their (view, destination)
   if constexpr (kDev) {
     // every destination's records: this rank's bucket for d starts at put[d] = sum over
     // s < rank of C[s][d] in d's buffer and at soff[d] = sum over d' < d of C[rank][d'] in the
@@ -131,71 +135,94 @@ __global__ void __launch_bounds__(kBlock) k_project_write(
   const float qmax_o = opac > 0.f ? __double2float_rn(log2(255.0 * (double)opac)) : -1.0f;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  for (int v = 0; v < b; v++) {
-    if (!view_in_union(u, v, b, G)) continue;  // warp-uniform
-    bool mine = i < n && view_in_mask(m, v, b, G);
-    gs_rec rec;
-    if (mine) {
-      const gs_dcam& cam = cams.c[v];
-      gs_memb mb = membership(cv, X.x, X.y, X.z, cam, geo.Wt, geo.Ht);
-      // conic = inverse of the 2D covariance (O6), carried as its Cholesky factor prescaled by
-      // sqrt(0.5 log2 e) (conic = L L^T): l11 = sqrt(c / det), l21 = -b / sqrt(det c),
-      // l22 = 1 / sqrt(c), evaluated in fp64 from the fp32 covariance (the products of fp32
-      // values are exact in fp64) and stored as hi + lo, each rounded to nearest
-      float lh[3] = {0.f, 0.f, 0.f}, ll[3] = {0.f, 0.f, 0.f};
-      {
-        const double a64 = mb.a, b64 = mb.b, c64 = mb.c;
-        const double det = a64 * c64 - b64 * b64;
-        if (det > 0.0) {
-          const double sc = sqrt(c64), sd = sqrt(det);
-          const double L[3] = {kLScale64 * sc / sd, -kLScale64 * b64 / (sd * sc), kLScale64 / sc};
-#pragma unroll
-          for (int k = 0; k < 3; k++) {
-            lh[k] = __double2float_rn(L[k]);
-            ll[k] = __double2float_rn(L[k] - (double)lh[k]);
+  // Phase A (warp-uniform over the union of the warp's buckets, view outer, destination
+  // inner): each lane lists the send positions of its own records in that order.  Phase B
+  // (per lane, divergent): walks its own list, forms the record of each of its views once and
+  // stores it at each destination's position -- a warp no longer steps through every view any
+  // lane sees.  Lists longer than kPList go in rounds (warp-uniform count).
+  int n_mine = 0;
+  for (int w = 0; w < NW; w++) n_mine += i < n ? __popc(m[w]) : 0;
+  const int rounds = (__reduce_max_sync(0xffffffffu, n_mine) + kPList - 1) / kPList;
+  for (int r = 0; r < rounds; r++) {
+    int cnt = 0;
+    for (int v = 0; v < b; v++) {
+      if (!view_in_union(u, v, b, G)) continue;  // warp-uniform
+      for (int d = 0; d < G; d++) {
+        const int k = d * b + v;
+        if (!get_bit(u, k)) continue;  // warp-uniform
+        const bool bit = i < n && get_bit(m, k);
+        const unsigned bal = __ballot_sync(0xffffffffu, bit);
+        if (bit) {
+          const int slot = cnt - r * kPList;
+          if (slot >= 0 && slot < kPList) {
+            s_pos[slot * kBlock + threadIdx.x] =
+                base[(int64_t)k * ncta + blockIdx.x] + warp_prefix(s_cnt, wid, nb, k) + __popc(bal & lt);
+            s_vd[slot * kBlock + threadIdx.x] = (uint16_t)(v | d << 8);
           }
+          cnt++;
         }
       }
-      // qmax = log2(255 o), rounded to nearest from fp64 (alpha = o 2^-q >= 1/255 <=> q <= qmax);
-      // -1 (never composited) for a zero opacity or a covariance whose fp64 determinant is not
-      // positive (not reachable with the 0.3 I dilation: det >= 0.09)
-      const float qmax = lh[0] > 0.f ? qmax_o : -1.0f;
-      // O9: colour from the view direction
-      float dx = X.x - cam.campos[0], dy = X.y - cam.campos[1], dz = X.z - cam.campos[2];
-      float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
-      float Y[16];
-      sh_basis(dx * inv, dy * inv, dz * inv, Y);
-      float col[3];
-      col[0] = col[1] = col[2] = 0.5f;
-      bool shf = true;
-#pragma unroll
-      for (int k = 0; k < 12; k++) {  // SH planes read only for visible (i, v)
-        const float4 s4 = sh[(int64_t)k * n + i];
-        shf = shf && isfinite(s4.x) && isfinite(s4.y) && isfinite(s4.z) && isfinite(s4.w);
-        const float e[4] = {s4.x, s4.y, s4.z, s4.w};
-#pragma unroll
-        for (int j = 0; j < 4; j++) col[(4 * k + j) % 3] = fmaf(Y[(4 * k + j) / 3], e[j], col[(4 * k + j) % 3]);
-      }
-#pragma unroll
-      for (int ch = 0; ch < 3; ch++) col[ch] = fmaxf(col[ch], 0.0f);
-      // SH coefficients are read here only (visible Gaussians): reported by the next call's sync
-      if (!shf) atomicMin(bad, (unsigned long long)(gid_base + i));
-      unsigned meta = (unsigned)((gid_base + i) * 32 + v);
-      rec.a = make_float4(mb.mx, mb.my, mb.depth, mb.r);
-      rec.b = make_float4(lh[0], lh[1], lh[2], opac);
-      rec.c = make_float4(col[0], col[1], col[2], qmax);
-      rec.d = make_float4(ll[0], ll[1], ll[2], __uint_as_float(meta));
     }
-    for (int d = 0; d < G; d++) {
-      int k = d * b + v;
-      if (!get_bit(u, k)) continue;  // warp-uniform
-      bool bit = i < n && get_bit(m, k);
-      unsigned bal = __ballot_sync(0xffffffffu, bit);
-      if (bit) {
-        int64_t pos = base[(int64_t)k * ncta + blockIdx.x] + warp_prefix(s_cnt, wid, nb, k) +
-                      __popc(bal & lt);
-        (kDev ? s_out[d] : outs.d[d])[pos] = rec;  // own send buffer, or (NEXT-3) d's receive buffer
+    const int nl = min(kPList, max(0, cnt - r * kPList));
+    gs_rec rec;
+    int cur = -1;
+    for (int j = 0; j < nl; j++) {
+      const int vd = s_vd[j * kBlock + threadIdx.x], v = vd & 0xff, d = vd >> 8;
+      if (v != cur) {
+        cur = v;
+        const gs_dcam& cam = cams.c[v];
+        gs_memb mb = membership(cv, X.x, X.y, X.z, cam, geo.Wt, geo.Ht);
+        // conic = inverse of the 2D covariance (O6), carried as its Cholesky factor prescaled by
+        // sqrt(0.5 log2 e) (conic = L L^T): l11 = sqrt(c / det), l21 = -b / sqrt(det c),
+        // l22 = 1 / sqrt(c), evaluated in fp64 from the fp32 covariance (the products of fp32
+        // values are exact in fp64) and stored as hi + lo, each rounded to nearest
+        float lh[3] = {0.f, 0.f, 0.f}, ll[3] = {0.f, 0.f, 0.f};
+        {
+          const double a64 = mb.a, b64 = mb.b, c64 = mb.c;
+          const double det = a64 * c64 - b64 * b64;
+          if (det > 0.0) {
+            const double sc = sqrt(c64), sd = sqrt(det);
+            const double L[3] = {kLScale64 * sc / sd, -kLScale64 * b64 / (sd * sc), kLScale64 / sc};
+#pragma unroll
+            for (int k = 0; k < 3; k++) {
+              lh[k] = __double2float_rn(L[k]);
+              ll[k] = __double2float_rn(L[k] - (double)lh[k]);
+            }
+          }
+        }
+        // qmax = log2(255 o), rounded to nearest from fp64 (alpha = o 2^-q >= 1/255 <=> q <= qmax);
+        // -1 (never composited) for a zero opacity or a covariance whose fp64 determinant is not
+        // positive (not reachable with the 0.3 I dilation: det >= 0.09)
+        const float qmax = lh[0] > 0.f ? qmax_o : -1.0f;
+        // O9: colour from the view direction
+        float dx = X.x - cam.campos[0], dy = X.y - cam.campos[1], dz = X.z - cam.campos[2];
+        float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
+        float Y[16];
+        sh_basis(dx * inv, dy * inv, dz * inv, Y);
+        float col[3];
+        col[0] = col[1] = col[2] = 0.5f;
+        bool shf = true;
+#pragma unroll
+        for (int k = 0; k < 12; k++) {  // SH planes read only for visible (i, v)
+          const float4 s4 = sh[(int64_t)k * n + i];
+          shf = shf && isfinite(s4.x) && isfinite(s4.y) && isfinite(s4.z) && isfinite(s4.w);
+          const float e[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+          for (int jj = 0; jj < 4; jj++)
+            col[(4 * k + jj) % 3] = fmaf(Y[(4 * k + jj) / 3], e[jj], col[(4 * k + jj) % 3]);
+        }
+#pragma unroll
+        for (int ch = 0; ch < 3; ch++) col[ch] = fmaxf(col[ch], 0.0f);
+        // SH coefficients are read here only (visible Gaussians): reported by the next call's sync
+        if (!shf) atomicMin(bad, (unsigned long long)(gid_base + i));
+        unsigned meta = (unsigned)((gid_base + i) * 32 + v);
+        rec.a = make_float4(mb.mx, mb.my, mb.depth, mb.r);
+        rec.b = make_float4(lh[0], lh[1], lh[2], opac);
+        rec.c = make_float4(col[0], col[1], col[2], qmax);
+        rec.d = make_float4(ll[0], ll[1], ll[2], __uint_as_float(meta));
       }
+      // own send buffer, or (NEXT-3) d's receive buffer
+      (kDev ? s_out[d] : outs.d[d])[s_pos[j * kBlock + threadIdx.x]] = rec;
     }
   }
 }
