@@ -110,11 +110,15 @@ __device__ __forceinline__ long long seg_hidx(const seg_arg& g, int k, int d, lo
 // rectangle, and per view the coarse-pair total and the owned-pair total (owned = view-local
 // block in [lo, hi): per rectangle row an interval intersection).  cnt[k] / own[k] over the
 // rank's views; g.lo / g.hi are the FINE ownership bounds here.
+// nrec[k]: records of view k; unord: set when a record's view is below its predecessor's
+// (the receive buffer is then not view-contiguous and the records take the general sort).
 __global__ void k_tile_counts(const gs_rec* __restrict__ rec, int64_t n_recv, gs_geom geo, seg_arg g,
                               int64_t* __restrict__ n_coarse, unsigned long long* __restrict__ cnt,
-                              unsigned long long* __restrict__ own, uint2* __restrict__ rect8) {
+                              unsigned long long* __restrict__ own, uint2* __restrict__ rect8,
+                              unsigned long long* __restrict__ nrec, unsigned long long* __restrict__ unord) {
   __shared__ unsigned long long s_c[GS_MAX_VIEWS], s_o[GS_MAX_VIEWS];
-  if (threadIdx.x < GS_MAX_VIEWS) s_c[threadIdx.x] = s_o[threadIdx.x] = 0;
+  __shared__ unsigned s_r[GS_MAX_VIEWS];
+  if (threadIdx.x < GS_MAX_VIEWS) s_c[threadIdx.x] = s_o[threadIdx.x] = 0, s_r[threadIdx.x] = 0;
   __syncthreads();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned t = 0, o = 0;
@@ -122,6 +126,8 @@ __global__ void k_tile_counts(const gs_rec* __restrict__ rec, int64_t n_recv, gs
   if (j < n_recv) {
     const float4 a = rec[j].a;
     const int v = (int)(__float_as_uint(rec[j].d.w) & 31u);
+    if (j > 0 && (int)(__float_as_uint(rec[j - 1].d.w) & 31u) > v) atomicOr(unord, 1ull);
+    if (v - g.v_lo >= 0 && v - g.v_lo < g.nv) atomicAdd(&s_r[v - g.v_lo], 1u);
     k = v - g.v_lo;
     int tx0, tx1, ty0, ty1;
     const bool ok = k >= 0 && k < g.nv && rect_of(a.x, a.y, a.w, geo.Wt, geo.Ht, tx0, tx1, ty0, ty1);
@@ -152,6 +158,7 @@ __global__ void k_tile_counts(const gs_rec* __restrict__ rec, int64_t n_recv, gs
     atomicAdd(&cnt[threadIdx.x], s_c[threadIdx.x]);
     if (s_o[threadIdx.x]) atomicAdd(&own[threadIdx.x], s_o[threadIdx.x]);
   }
+  if (threadIdx.x < GS_MAX_VIEWS && s_r[threadIdx.x]) atomicAdd(&nrec[threadIdx.x], (unsigned long long)s_r[threadIdx.x]);
 }
 
 __global__ void k_depth_keys(const gs_rec* __restrict__ rec, int64_t n, uint32_t* __restrict__ keys,
@@ -160,6 +167,21 @@ __global__ void k_depth_keys(const gs_rec* __restrict__ rec, int64_t n, uint32_t
   if (j >= n) return;
   keys[j] = __float_as_uint(rec[j].a.z);  // depth > 0: the bit pattern orders like the value
   vals[j] = (uint32_t)j;
+}
+
+// View-contiguous records (the receive buffer of one rank's own views): depth keys laid out
+// in per-view segments padded to radix tiles (padded position p of segment k holds record
+// kcum[k] + p - seg[k], or the sentinel 0xffffffff -- above every depth's bits -- past the
+// view's records), so four segmented stable passes sort each view by depth with no view pass.
+__global__ void k_depth_keys_seg(const gs_rec* __restrict__ rec, seg_arg r, uint32_t* __restrict__ keys,
+                                 uint32_t* __restrict__ vals) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= r.seg[r.nv]) return;
+  const int k = seg_of_tile(r, p / kRadixTile);
+  const int64_t o = p - r.seg[k], nk = r.kcum[k + 1] - r.kcum[k];
+  const int64_t j = r.kcum[k] + o;
+  keys[p] = o < nk ? __float_as_uint(rec[j].a.z) : 0xffffffffu;
+  vals[p] = o < nk ? (uint32_t)j : 0u;
 }
 
 // view keys of the depth-ordered records (the last, stable, record pass groups them by view)
@@ -769,6 +791,31 @@ gs_status radix_pass(gs_ctx* c, const uint32_t* kin, const uint32_t* vin, uint32
   return GS_OK;
 }
 
+// One stable segmented 8-bit pass over n_pad padded elements (layout of g); last: values
+// to vout at their compact positions (sentinels dropped).  Scratch: SLOT_RADIX_HIST.
+gs_status seg_radix_pass(gs_ctx* c, const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
+                         int64_t n_pad, int shift, const seg_arg& g, bool last, int64_t vcap, cudaStream_t st) {
+  if (n_pad == 0) return GS_OK;
+  const int bins = 256;
+  const int64_t ntl = n_pad / kRadixTile;
+  unsigned long long* hist =
+      (unsigned long long*)gs_slot_get(c, SLOT_RADIX_HIST, (size_t)bins * ntl * sizeof(int64_t), st);
+  if (!hist) return gs_fail(c, GS_ECUDA, "radix histogram scratch");
+  ++c->launches;
+  k_radix_hist<true><<<(unsigned)ntl, kRadixThreads, 0, st>>>(kin, n_pad, shift, 8, ntl, g, hist);
+  gs_status s = gs_scan_i64(c, (const int64_t*)hist, (int64_t*)hist, (int64_t)bins * ntl, 0, st);
+  if (s != GS_OK) return s;
+  ++c->launches;
+  if (last)
+    k_radix_scatter<true, true><<<(unsigned)ntl, kRadixThreads, kScatterSmem, st>>>(kin, vin, kout, vout, n_pad, shift,
+                                                                                    8, ntl, g, hist, vcap);
+  else
+    k_radix_scatter<true, false><<<(unsigned)ntl, kRadixThreads, kScatterSmem, st>>>(kin, vin, kout, vout, n_pad,
+                                                                                     shift, 8, ntl, g, hist, 0);
+  GS_LAUNCH_CHECK(c, "segmented radix pass");
+  return GS_OK;
+}
+
 }  // namespace
 
 extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv, const gs_camera* cams_h,
@@ -824,15 +871,17 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
   // 1. per-record coarse counts, per-view coarse and owned-pair totals (one host sync)
   int64_t* ncoarse = (int64_t*)gs_slot_get(c, SLOT_RECTILES, (n_recv + 1) * sizeof(int64_t), st);
   int64_t* ps = (int64_t*)gs_slot_get(c, SLOT_PSTART, (n_recv + 1) * sizeof(int64_t), st);
-  unsigned long long* vc = (unsigned long long*)gs_slot_get(c, SLOT_COUNTS, 2 * GS_MAX_VIEWS * sizeof(int64_t), st);
+  // per view: coarse pairs, owned pairs, records; then the view-order flag
+  unsigned long long* vc = (unsigned long long*)gs_slot_get(c, SLOT_COUNTS, (3 * GS_MAX_VIEWS + 1) * sizeof(int64_t), st);
   uint2* rect8 = (uint2*)gs_slot_get(c, SLOT_RECT8, n_recv * sizeof(uint2), st);
   if (!ncoarse || !ps || !vc || !rect8) return gs_fail(c, GS_ECUDA, "scratch");
-  GS_CUDA(c, cudaMemsetAsync(vc, 0, 2 * GS_MAX_VIEWS * sizeof(int64_t), st));
+  GS_CUDA(c, cudaMemsetAsync(vc, 0, (3 * GS_MAX_VIEWS + 1) * sizeof(int64_t), st));
   ++c->launches;
   k_tile_counts<<<(unsigned)((n_recv + 256) / 256), 256, 0, st>>>(rec, n_recv, geo, g, ncoarse, vc,
-                                                                  vc + GS_MAX_VIEWS, rect8);
+                                                                  vc + GS_MAX_VIEWS, rect8, vc + 2 * GS_MAX_VIEWS,
+                                                                  vc + 3 * GS_MAX_VIEWS);
   GS_LAUNCH_CHECK(c, "tile counts");
-  GS_CUDA(c, cudaMemcpyAsync(c->pinned, vc, 2 * GS_MAX_VIEWS * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(c, cudaMemcpyAsync(c->pinned, vc, (3 * GS_MAX_VIEWS + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GS_CUDA(c, cudaStreamSynchronize(st));
   // coarse segments: every super-tile key is "owned" ([0, nST)); the sentinel pads
   seg_arg cgs = g;
@@ -865,23 +914,53 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
     return GS_OK;
   }
 
-  // 3. records by (view, depth): 4 stable 8-bit depth passes (A -> B -> A -> B -> A), then the
-  //    view (-> B -> A, values only kept)
-  const int64_t cap = std::max(n_pad, n_recv);
+  // 3. records by (view, depth): view-contiguous records in 4 segmented stable 8-bit depth
+  //    passes; otherwise 4 stable depth passes (A -> B -> A -> B -> A), then the view (-> B -> A,
+  //    values only kept)
+  // view-contiguous records (one rank's own receive buffer at G = 1 is bucketed by view): the
+  // records' own per-view segments, sorted by depth in 4 segmented passes
+  seg_arg rs = g;
+  bool vseg = c->pinned[3 * GS_MAX_VIEWS] == 0;
+  {
+    int64_t tot = 0;
+    rs.seg[0] = 0;
+    rs.kcum[0] = 0;
+    for (int k = 0; k < g.nv; k++) {
+      const int64_t nk = c->pinned[2 * GS_MAX_VIEWS + k];
+      rs.seg[k + 1] = rs.seg[k] + (nk + kRadixTile - 1) / kRadixTile * kRadixTile;
+      rs.kcum[k + 1] = rs.kcum[k] + nk;
+      tot += nk;
+    }
+    rs.sentinel = 0xffffffffu;
+    vseg = vseg && tot == n_recv && g.nv > 1;  // every record in an owned view (else: general path)
+  }
+  const int64_t cap = std::max(std::max(n_pad, n_recv), vseg ? (int64_t)rs.seg[g.nv] : 0);
   uint32_t* A = (uint32_t*)gs_slot_get(c, SLOT_KEYS, 2 * cap * sizeof(uint32_t), st);
   uint32_t* Bf = (uint32_t*)gs_slot_get(c, SLOT_KEYS_TMP, 2 * cap * sizeof(uint32_t), st);
   uint32_t* clist = (uint32_t*)gs_slot_get(c, SLOT_CLIST, std::max<int64_t>(n_full, 1) * sizeof(uint32_t), st);
   int32_t* crange = (int32_t*)gs_slot_get(c, SLOT_CRANGE, ((int64_t)g.nv * nST + 1) * sizeof(int32_t), st);
   if (!A || !Bf || !clist || !crange) return gs_fail(c, GS_ECUDA, "radix scratch (%lld pairs)", (long long)cap);
   uint32_t *ka = A, *va = A + cap, *kb = Bf, *vb = Bf + cap;
-  ++c->launches;
-  k_depth_keys<<<(unsigned)((n_recv + 255) / 256), 256, 0, st>>>(rec, n_recv, ka, va);
-  for (int p = 0; p < 4; p++) {
-    s = (p & 1) ? radix_pass(c, kb, vb, ka, va, n_recv, 8 * p, 8, g, st)
-                : radix_pass(c, ka, va, kb, vb, n_recv, 8 * p, 8, g, st);
-    if (s != GS_OK) return s;
+  if (vseg) {
+    const int64_t np_ = rs.seg[g.nv];
+    ++c->launches;
+    k_depth_keys_seg<<<(unsigned)((np_ + 255) / 256), 256, 0, st>>>(rec, rs, ka, va);
+    // A -> B -> A -> B, the last pass writing the values compact into va (sentinels dropped)
+    for (int p = 0; p < 4; p++) {
+      s = (p & 1) ? seg_radix_pass(c, kb, vb, ka, va, np_, 8 * p, rs, p == 3, n_recv, st)
+                  : seg_radix_pass(c, ka, va, kb, vb, np_, 8 * p, rs, false, 0, st);
+      if (s != GS_OK) return s;
+    }
+  } else {
+    ++c->launches;
+    k_depth_keys<<<(unsigned)((n_recv + 255) / 256), 256, 0, st>>>(rec, n_recv, ka, va);
+    for (int p = 0; p < 4; p++) {
+      s = (p & 1) ? radix_pass(c, kb, vb, ka, va, n_recv, 8 * p, 8, g, st)
+                  : radix_pass(c, ka, va, kb, vb, n_recv, 8 * p, 8, g, st);
+      if (s != GS_OK) return s;
+    }
   }
-  if (g.nv > 1) {
+  if (!vseg && g.nv > 1) {
     ++c->launches;
     k_view_keys<<<(unsigned)((n_recv + 255) / 256), 256, 0, st>>>(rec, va, n_recv, g.v_lo, ka);
     s = radix_pass(c, ka, va, kb, vb, n_recv, 0, 32 - __builtin_clz((unsigned)(g.nv - 1)), g, st);
