@@ -115,7 +115,8 @@ __device__ __forceinline__ long long seg_hidx(const seg_arg& g, int k, int d, lo
 __global__ void k_tile_counts(const gs_rec* __restrict__ rec, int64_t n_recv, gs_geom geo, seg_arg g,
                               int64_t* __restrict__ n_coarse, unsigned long long* __restrict__ cnt,
                               unsigned long long* __restrict__ own, uint2* __restrict__ rect8,
-                              unsigned long long* __restrict__ nrec, unsigned long long* __restrict__ unord) {
+                              unsigned long long* __restrict__ nrec, unsigned long long* __restrict__ unord,
+                              uint32_t* __restrict__ dbits) {
   __shared__ unsigned long long s_c[GS_MAX_VIEWS], s_o[GS_MAX_VIEWS];
   __shared__ unsigned s_r[GS_MAX_VIEWS];
   if (threadIdx.x < GS_MAX_VIEWS) s_c[threadIdx.x] = s_o[threadIdx.x] = 0, s_r[threadIdx.x] = 0;
@@ -125,6 +126,7 @@ __global__ void k_tile_counts(const gs_rec* __restrict__ rec, int64_t n_recv, gs
   int k = -1;
   if (j < n_recv) {
     const float4 a = rec[j].a;
+    dbits[j] = __float_as_uint(a.z);  // depth > 0: the bit pattern orders like the value
     const int v = (int)(__float_as_uint(rec[j].d.w) & 31u);
     if (j > 0 && (int)(__float_as_uint(rec[j - 1].d.w) & 31u) > v) atomicOr(unord, 1ull);
     if (v - g.v_lo >= 0 && v - g.v_lo < g.nv) atomicAdd(&s_r[v - g.v_lo], 1u);
@@ -161,11 +163,11 @@ __global__ void k_tile_counts(const gs_rec* __restrict__ rec, int64_t n_recv, gs
   if (threadIdx.x < GS_MAX_VIEWS && s_r[threadIdx.x]) atomicAdd(&nrec[threadIdx.x], (unsigned long long)s_r[threadIdx.x]);
 }
 
-__global__ void k_depth_keys(const gs_rec* __restrict__ rec, int64_t n, uint32_t* __restrict__ keys,
+__global__ void k_depth_keys(const uint32_t* __restrict__ dbits, int64_t n, uint32_t* __restrict__ keys,
                              uint32_t* __restrict__ vals) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
-  keys[j] = __float_as_uint(rec[j].a.z);  // depth > 0: the bit pattern orders like the value
+  keys[j] = dbits[j];
   vals[j] = (uint32_t)j;
 }
 
@@ -173,14 +175,14 @@ __global__ void k_depth_keys(const gs_rec* __restrict__ rec, int64_t n, uint32_t
 // in per-view segments padded to radix tiles (padded position p of segment k holds record
 // kcum[k] + p - seg[k], or the sentinel 0xffffffff -- above every depth's bits -- past the
 // view's records), so four segmented stable passes sort each view by depth with no view pass.
-__global__ void k_depth_keys_seg(const gs_rec* __restrict__ rec, seg_arg r, uint32_t* __restrict__ keys,
+__global__ void k_depth_keys_seg(const uint32_t* __restrict__ dbits, seg_arg r, uint32_t* __restrict__ keys,
                                  uint32_t* __restrict__ vals) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= r.seg[r.nv]) return;
   const int k = seg_of_tile(r, p / kRadixTile);
   const int64_t o = p - r.seg[k], nk = r.kcum[k + 1] - r.kcum[k];
   const int64_t j = r.kcum[k] + o;
-  keys[p] = o < nk ? __float_as_uint(rec[j].a.z) : 0xffffffffu;
+  keys[p] = o < nk ? dbits[j] : 0xffffffffu;
   vals[p] = o < nk ? (uint32_t)j : 0u;
 }
 
@@ -870,6 +872,8 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
              geo.Wt, geo.Ht);
   // 1. per-record coarse counts, per-view coarse and owned-pair totals (one host sync)
   int64_t* ncoarse = (int64_t*)gs_slot_get(c, SLOT_RECTILES, (n_recv + 1) * sizeof(int64_t), st);
+  // ps: the depth bits of the records (k_tile_counts -> the depth keys), later the coarse pair
+  // starts in (view, depth) order (k_gather_tiles)
   int64_t* ps = (int64_t*)gs_slot_get(c, SLOT_PSTART, (n_recv + 1) * sizeof(int64_t), st);
   // per view: coarse pairs, owned pairs, records; then the view-order flag
   unsigned long long* vc = (unsigned long long*)gs_slot_get(c, SLOT_COUNTS, (3 * GS_MAX_VIEWS + 1) * sizeof(int64_t), st);
@@ -879,7 +883,7 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
   ++c->launches;
   k_tile_counts<<<(unsigned)((n_recv + 256) / 256), 256, 0, st>>>(rec, n_recv, geo, g, ncoarse, vc,
                                                                   vc + GS_MAX_VIEWS, rect8, vc + 2 * GS_MAX_VIEWS,
-                                                                  vc + 3 * GS_MAX_VIEWS);
+                                                                  vc + 3 * GS_MAX_VIEWS, (uint32_t*)ps);
   GS_LAUNCH_CHECK(c, "tile counts");
   GS_CUDA(c, cudaMemcpyAsync(c->pinned, vc, (3 * GS_MAX_VIEWS + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GS_CUDA(c, cudaStreamSynchronize(st));
@@ -944,7 +948,7 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
   if (vseg) {
     const int64_t np_ = rs.seg[g.nv];
     ++c->launches;
-    k_depth_keys_seg<<<(unsigned)((np_ + 255) / 256), 256, 0, st>>>(rec, rs, ka, va);
+    k_depth_keys_seg<<<(unsigned)((np_ + 255) / 256), 256, 0, st>>>((const uint32_t*)ps, rs, ka, va);
     // A -> B -> A -> B, the last pass writing the values compact into va (sentinels dropped)
     for (int p = 0; p < 4; p++) {
       s = (p & 1) ? seg_radix_pass(c, kb, vb, ka, va, np_, 8 * p, rs, p == 3, n_recv, st)
@@ -953,7 +957,7 @@ extern "C" gs_status gs_bin_sort(gs_ctx* c, const void* recv_rec, int64_t n_recv
     }
   } else {
     ++c->launches;
-    k_depth_keys<<<(unsigned)((n_recv + 255) / 256), 256, 0, st>>>(rec, n_recv, ka, va);
+    k_depth_keys<<<(unsigned)((n_recv + 255) / 256), 256, 0, st>>>((const uint32_t*)ps, n_recv, ka, va);
     for (int p = 0; p < 4; p++) {
       s = (p & 1) ? radix_pass(c, kb, vb, ka, va, n_recv, 8 * p, 8, g, st)
                   : radix_pass(c, ka, va, kb, vb, n_recv, 8 * p, 8, g, st);
