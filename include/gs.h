@@ -170,7 +170,10 @@ gs_status gs_exchange(gs_ctx* ctx, const void* send_rec, const int64_t* send_cou
  * of its view inside its tile rectangle gets the record; each block's list is sorted by
  * (depth, gid) (R7; unique keys, so the order is deterministic).  Outputs:
  *   tile_range[n_owned+1] (int32 offsets into sorted_idx), sorted_idx[n_pairs] (uint32
- *   receive indices).  *n_pairs_h = pair count (host sync).  GS_ECAPACITY if > pair_cap. */
+ *   receive indices).  *n_pairs_h = pair count (host sync).  GS_ECAPACITY if > pair_cap.
+ * Depth ties keep receive order, so records of one view must arrive in ascending gid (the
+ * exchange's ascending-source-rank order guarantees it).  Any view order is accepted; a
+ * buffer whose views never decrease (a rank's own buckets) takes the segmented record sort. */
 gs_status gs_bin_sort(gs_ctx* ctx, const void* recv_rec, int64_t n_recv, const gs_camera* cams_h,
                       int n_views, const int64_t* dp_h, uint32_t* sorted_idx, int64_t pair_cap,
                       int32_t* tile_range, int64_t* n_pairs_h, void* stream);
