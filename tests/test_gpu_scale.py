@@ -185,3 +185,68 @@ def test_full_c2_sampled_blocks():
             np.testing.assert_allclose(dpx[firm], np.sign(res[firm]) / (3.0 * W * H * 16), rtol=1e-6)
             assert np.all(np.isin(np.round(dpx * (3.0 * W * H * 16)), [-1, 0, 1]))  # every pixel: a valid sign
             assert tr.range.t[lb + 1].item() - tr.range.t[lb].item() == len(ent)
+
+
+def _projection_case(cfg):
+    if cfg == "C2":  # the bench batch
+        pool = synth.cameras_rubble(64)
+        return synth.scene_rubble(11_200_000), [pool[i] for i in synth.batch_schedule(64, 16, 1, 2)[0]]
+    if cfg == "C1":
+        pool = synth.cameras_garden(64)
+        return synth.scene_garden(5_000_000), [pool[i] for i in synth.batch_schedule(64, 4, 1, 1)[0]]
+    pool = synth.cameras_city(128)  # C4: 4 street (pool 0..63) + 4 aerial (64..127) views
+    return synth.scene_city(24_000_000), [pool[i] for i in (3, 17, 40, 61, 66, 80, 101, 127)]
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C1", "C4"])
+def test_full_projection_every_record(cfg):
+    """Full-scene projection, every (Gaussian, view) of a batch (C2: 11.2M Gaussians x the 16
+    bench views of 4591x3436; C1: 5M x 4 views of 1080p; C4: 24M x 8 views, street and aerial)
+    (P:103 step 1; O1-O8, R10): the set of records equals the oracle's visible (gid, view)
+    pairs, in (view, gid) send order; each record's mean2d and depth bit-exact and radius exact
+    (the fp32 membership chain); its conic (from the double-float Cholesky factor) within 1e-6
+    of the oracle's fp64 inverse of the same fp32 covariance.  The oracle runs the views on
+    host threads (the C calls release the GIL)."""
+    import concurrent.futures as cf
+    import os
+    from tests.gsutil import conic_of
+    sc, cams = _projection_case(cfg)
+    nv = len(cams)
+    ctx = L.Context(0, 0, 1)
+    p = _params(sc)
+    B = nv * ((cams[0].width + 15) // 16) * ((cams[0].height + 15) // 16)
+    dp = np.array([0, B], np.int64)
+    idx = torch.empty(L.project_index_bytes(ctx, p.n, nv), dtype=torch.uint8, device=DEV)
+    try:
+        cnt = L.project(ctx, p, cams, dp, None, 0, idx)
+    except L.CapacityError as e:
+        cnt = e.counts
+    send = torch.empty((int(cnt.sum()) + 1, L.RECORD_BYTES), dtype=torch.uint8, device=DEV)
+    cnt = L.project(ctx, p, cams, dp, send, int(cnt.sum()), idx)
+    d = decode_records(send[: int(cnt.sum())])
+    del send
+    # the records of view v are one contiguous run (bucket (0, v)), in ascending gid
+    assert np.all(np.diff(d["view"]) >= 0)
+    starts = np.searchsorted(d["view"], np.arange(nv + 1))
+
+    def check(v):
+        mb = oracle.membership(sc, cams[v])
+        sl = slice(starts[v], starts[v + 1])
+        want = np.nonzero(mb["vis"])[0]
+        np.testing.assert_array_equal(d["gid"][sl], want)
+        for k in ("mx", "my", "depth"):
+            np.testing.assert_array_equal(d[k][sl].view(np.uint32), mb[k][want].view(np.uint32))
+        np.testing.assert_array_equal(d["radius"][sl].astype(np.int64), mb["radius"][want])
+        cov = mb["cov"][want].astype(np.float64)
+        det = cov[:, 0] * cov[:, 2] - cov[:, 1] * cov[:, 1]
+        ref = np.stack([cov[:, 2], -cov[:, 1], cov[:, 0]], 1) / det[:, None]
+        got = conic_of({k2: d[k2][sl] for k2 in ("l11", "l21", "l22", "l11_lo", "l21_lo", "l22_lo")})
+        # (A, B, C) of L L^T against the inverse of the covariance, per record
+        scale = np.abs(ref).max(1, keepdims=True)
+        assert np.all(np.abs(got - ref) <= 1e-6 * scale), v
+        return len(want)
+
+    with cf.ThreadPoolExecutor(min(8, os.cpu_count() or 1)) as ex:
+        n_vis = list(ex.map(check, range(nv)))
+    assert sum(n_vis) == int(cnt.sum())
+    print(cfg, "records per view:", n_vis)
