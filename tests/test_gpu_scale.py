@@ -250,3 +250,72 @@ def test_full_projection_every_record(cfg):
         n_vis = list(ex.map(check, range(nv)))
     assert sum(n_vis) == int(cnt.sum())
     print(cfg, "records per view:", n_vis)
+
+
+def test_full_c2_batch_every_pixel():
+    """The bench configuration (11.2M Gaussians, 16 views of 4591x3436, G = 1) through the step
+    driver; EVERY pixel of the batch (16 x 61,705 blocks, 252.7M pixels) against the oracle,
+    recomputed in chunks of blocks on host threads: n_last exact and T within 1e-4 on one of
+    the oracle's outcome paths (R16), every block's list length exact, dL/dpix the sign of the
+    residual wherever the colour is firm."""
+    import concurrent.futures as cf
+    import os
+    from paper_2406_18533_b200.engine import GrendelTrainer
+    sc = synth.scene_rubble(11_200_000)
+    pool = synth.cameras_rubble(64)
+    cams = [pool[i] for i in synth.batch_schedule(64, 16, 1, 2)[0]]
+    W, H = cams[0].width, cams[0].height
+    gt = np.stack([synth.gt_image(2, c) for c in cams])
+    ctx = L.Context(0, 0, 1)
+    p = _params(sc)
+    tr = GrendelTrainer(ctx, p, W, H, 16, 64, cost_mode=L.COST_WORK, rebalance=False)
+    tr.step(cams, torch.from_numpy(gt).to(DEV))
+    torch.cuda.synchronize()
+    Wt, Ht = (W + 15) // 16, (H + 15) // 16
+    pv = Wt * Ht
+    norm = 3.0 * W * H * 16
+    T_b, nl_b, dpx_b = tr.T.t[:16 * pv].cpu().numpy(), tr.nl.t[:16 * pv].cpu().numpy(), tr.dpix.t[:16 * pv].cpu().numpy()
+    rng_b = tr.range.t[:16 * pv + 1].cpu().numpy().astype(np.int64)
+
+    def chunk(b0):
+        b1 = min(b0 + 512, pv)
+        off, ent = oracle.tile_lists(recs, b0, b1, Wt, Ht)
+        f = oracle.render_fwd(recs, off, ent, b0, b1, W, H, (0, 0, 0), gt[v][None], 16, max_paths=16)
+        T, nl = T_all[b0:b1], nl_all[b0:b1]
+        P = f["flips"].shape[2]
+        valid = np.arange(P)[None, None, :] < f["n_paths"][..., None]
+        ok = (valid & (f["path_nl"] == nl[..., None]) & (np.abs(f["path_T"] - T[..., None]) <= 1e-4)).any(-1)
+        n_over = int(((f["flags"] >> 16) & 1).sum())
+        lens_ok = np.array_equal(np.diff(rng_all[b0:b1 + 1]), np.diff(off))
+        # dL/dpix: the sign of the nominal residual wherever it is firm (single path, |res| > 1e-4)
+        blk = np.arange(b0, b1)
+        ty, tx = blk // Wt, blk % Wt
+        py = ty[:, None] * 16 + np.arange(256)[None, :] // 16
+        px = tx[:, None] * 16 + np.arange(256)[None, :] % 16
+        inside = (px < W) & (py < H)
+        gb = np.zeros((b1 - b0, 256, 3))
+        gb[inside] = gt[v][py[inside], px[inside]] / 255.0
+        res = f["c"] - gb
+        firm = (f["n_paths"] == 1)[..., None] & inside[..., None] & (np.abs(res) > 1e-4)
+        dpx = dpx_all[b0:b1].reshape(b1 - b0, 3, 256).transpose(0, 2, 1)
+        sign_ok = np.allclose(dpx[firm] * norm, np.sign(res[firm]), atol=1e-5)
+        multi = int((f["n_paths"] > 1).sum())
+        return int((~ok).sum()), n_over, lens_ok, sign_ok, multi
+
+    n_px = n_multi = 0
+    with cf.ThreadPoolExecutor(min(16, os.cpu_count() or 1)) as ex:
+        for v in range(16):
+            T_all, nl_all = T_b[v * pv:(v + 1) * pv], nl_b[v * pv:(v + 1) * pv]
+            dpx_all, rng_all = dpx_b[v * pv:(v + 1) * pv], rng_b[v * pv:(v + 1) * pv + 1]
+            recs = oracle.make_records(sc, [cams[v]], "parity")
+            res = list(ex.map(chunk, range(0, pv, 512)))
+            bad, over, multi = sum(r[0] for r in res), sum(r[1] for r in res), sum(r[4] for r in res)
+            print("view %d: %d pixels, %d with more than one valid outcome (%.1e), %d matching none, overflow %d" %
+                  (v, pv * 256, multi, multi / (pv * 256), bad, over))
+            assert over == 0 and bad == 0, v
+            assert all(r[2] for r in res), ("list lengths", v)
+            assert all(r[3] for r in res), ("dL/dpix signs", v)
+            n_px += pv * 256
+            n_multi += multi
+    print("batch: %d pixels, %.1e with more than one valid outcome" % (n_px, n_multi / n_px))
+    assert n_multi <= 1e-3 * n_px
