@@ -256,8 +256,8 @@ def test_full_c2_batch_every_pixel():
     """The bench configuration (11.2M Gaussians, 16 views of 4591x3436, G = 1) through the step
     driver; EVERY pixel of the batch (16 x 61,705 blocks, 252.7M pixels) against the oracle,
     recomputed in chunks of blocks on host threads: n_last exact and T within 1e-4 on one of
-    the oracle's outcome paths (R16), every block's list length exact, dL/dpix the sign of the
-    residual wherever the colour is firm."""
+    the oracle's outcome paths (R16), every block's list bit-exact (O11), dL/dpix the sign of
+    the residual wherever the colour is firm."""
     import concurrent.futures as cf
     import os
     from paper_2406_18533_b200.engine import GrendelTrainer
@@ -276,6 +276,9 @@ def test_full_c2_batch_every_pixel():
     norm = 3.0 * W * H * 16
     T_b, nl_b, dpx_b = tr.T.t[:16 * pv].cpu().numpy(), tr.nl.t[:16 * pv].cpu().numpy(), tr.dpix.t[:16 * pv].cpu().numpy()
     rng_b = tr.range.t[:16 * pv + 1].cpu().numpy().astype(np.int64)
+    # the Z-buffer: every block's list as gids (receive index -> gid through the send buffer)
+    gid_of = decode_records(tr.send.t[:tr.last["n_send"]])["gid"]
+    srt_b = tr.sorted.t[:int(rng_b[-1])].cpu().numpy().view(np.uint32)
 
     def chunk(b0):
         b1 = min(b0 + 512, pv)
@@ -286,7 +289,9 @@ def test_full_c2_batch_every_pixel():
         valid = np.arange(P)[None, None, :] < f["n_paths"][..., None]
         ok = (valid & (f["path_nl"] == nl[..., None]) & (np.abs(f["path_T"] - T[..., None]) <= 1e-4)).any(-1)
         n_over = int(((f["flags"] & oracle.FLAG_OVERFLOW) != 0).sum())
-        lens_ok = np.array_equal(np.diff(rng_all[b0:b1 + 1]), np.diff(off))
+        # O11: the chunk's lists bit-exact (same records in the same (depth, gid) order)
+        lens_ok = np.array_equal(np.diff(rng_all[b0:b1 + 1]), np.diff(off)) and np.array_equal(
+            gid_of[srt_b[rng_all[b0]:rng_all[b1]]], recs.rec_i[ent, 0])
         # dL/dpix: the sign of the nominal residual wherever it is firm (single path, |res| > 1e-4)
         blk = np.arange(b0, b1)
         ty, tx = blk // Wt, blk % Wt
@@ -313,7 +318,7 @@ def test_full_c2_batch_every_pixel():
             print("view %d: %d pixels, %d with more than one valid outcome (%.1e), %d matching none, overflow %d" %
                   (v, pv * 256, multi, multi / (pv * 256), bad, over))
             assert over == 0 and bad == 0, v
-            assert all(r[2] for r in res), ("list lengths", v)
+            assert all(r[2] for r in res), ("block lists", v)
             assert all(r[3] for r in res), ("dL/dpix signs", v)
             n_px += pv * 256
             n_multi += multi
