@@ -24,12 +24,11 @@ struct gs_slot {
 enum {
   SLOT_SCAN = 0,      // scan partials
   SLOT_PROJ_TMP,      // projection per-destination totals
-  SLOT_DIFF,          // (unused)
-  SLOT_COUNTS,        // bin_sort per-block counts (int64)
+  SLOT_COUNTS,        // bin_sort per-view coarse / owned-pair / record counts + view-order flag
   SLOT_CURSOR,        // bin_sort fine emission: first segment of each super-tile (int64)
-  SLOT_KEYS,          // bin_sort (depth, recv idx) keys
-  SLOT_KEYS_TMP,      // merge ping-pong for long lists
-  SLOT_LARGE,         // list of long blocks + counters
+  SLOT_KEYS,          // bin_sort radix keys + values (ping)
+  SLOT_KEYS_TMP,      // bin_sort radix keys + values (pong)
+  SLOT_LARGE,         // bin_sort first record of every emission CTA
   SLOT_ROW,           // rebalance cost row (all blocks of the batch)
   SLOT_ET,            // rebalance ET of next batch
   SLOT_CT,            // rebalance prefix sums
@@ -37,7 +36,7 @@ enum {
   SLOT_COUNT_GATHER,  // exchange count matrix
   SLOT_RECTILES,      // bin_sort per-record coarse counts
   SLOT_RADIX_HIST,    // bin_sort radix per-tile digit histograms -> offsets
-  SLOT_PSTART,        // bin_sort pair starts in depth order
+  SLOT_PSTART,        // bin_sort records' depth bits, then coarse-pair starts in (view, depth) order
   SLOT_HALO_SEND,     // halo exchange: packed blocks to send
   SLOT_HALO_IDX,      // halo exchange: owned-block indices to pack
   SLOT_DENSIFY,       // densify keep flags [4][n]
