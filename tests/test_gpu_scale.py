@@ -252,30 +252,46 @@ def test_full_projection_every_record(cfg):
     print(cfg, "records per view:", n_vis)
 
 
-def test_full_c2_batch_every_pixel():
-    """The bench configuration (11.2M Gaussians, 16 views of 4591x3436, G = 1) through the step
-    driver; EVERY pixel of the batch (16 x 61,705 blocks, 252.7M pixels) against the oracle,
-    recomputed in chunks of blocks on host threads: n_last exact and T within 1e-4 on one of
-    the oracle's outcome paths (R16), every block's list bit-exact (O11), dL/dpix the sign of
-    the residual wherever the colour is firm."""
+def _batch_case(cfg):
+    """(scene, the config's first bench batch, ground-truth seed, views to check)."""
+    if cfg == "C2":
+        pool = synth.cameras_rubble(64)
+        return (synth.scene_rubble(11_200_000), [pool[i] for i in synth.batch_schedule(64, 16, 1, 2)[0]], 2,
+                list(range(16)))
+    if cfg == "C1":
+        pool = synth.cameras_garden(64)
+        return synth.scene_garden(5_000_000), [pool[i] for i in synth.batch_schedule(64, 4, 1, 1)[0]], 1, [0, 1, 2, 3]
+    pool = synth.cameras_city(128)  # C4: 16 street + 16 aerial, as bench.py batches them
+    st = synth.batch_schedule(64, 16, 1, 4)[0]
+    ae = synth.batch_schedule(64, 16, 1, 5)[0]
+    return synth.scene_city(24_000_000), [pool[i] for i in st + [64 + a for a in ae]], 4, [0, 1, 16, 17]
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C1", "C4"])
+def test_full_batch_every_pixel(cfg):
+    """A bench batch through the step driver at full size (C2: 11.2M Gaussians, 16 views of
+    4591x3436 -- 252.7M pixels, every view; C1: 5M, 4 views of 1080p, every view; C4: 24M,
+    32 views of 1080p, two street and two aerial views checked), EVERY pixel of the checked
+    views against the oracle, recomputed in chunks of blocks on host threads: n_last exact
+    and T within 1e-4 on one of the oracle's outcome paths (R16), every block's list
+    bit-exact (O11), dL/dpix the sign of the residual wherever the colour is firm."""
     import concurrent.futures as cf
     import os
     from paper_2406_18533_b200.engine import GrendelTrainer
-    sc = synth.scene_rubble(11_200_000)
-    pool = synth.cameras_rubble(64)
-    cams = [pool[i] for i in synth.batch_schedule(64, 16, 1, 2)[0]]
+    sc, cams, gseed, check = _batch_case(cfg)
+    nv = len(cams)
     W, H = cams[0].width, cams[0].height
-    gt = np.stack([synth.gt_image(2, c) for c in cams])
+    gt = np.stack([synth.gt_image(gseed, c) for c in cams])
     ctx = L.Context(0, 0, 1)
     p = _params(sc)
-    tr = GrendelTrainer(ctx, p, W, H, 16, 64, cost_mode=L.COST_WORK, rebalance=False)
+    tr = GrendelTrainer(ctx, p, W, H, nv, 128, cost_mode=L.COST_WORK, rebalance=False)
     tr.step(cams, torch.from_numpy(gt).to(DEV))
     torch.cuda.synchronize()
     Wt, Ht = (W + 15) // 16, (H + 15) // 16
     pv = Wt * Ht
-    norm = 3.0 * W * H * 16
-    T_b, nl_b, dpx_b = tr.T.t[:16 * pv].cpu().numpy(), tr.nl.t[:16 * pv].cpu().numpy(), tr.dpix.t[:16 * pv].cpu().numpy()
-    rng_b = tr.range.t[:16 * pv + 1].cpu().numpy().astype(np.int64)
+    norm = 3.0 * W * H * nv
+    T_b, nl_b, dpx_b = tr.T.t[:nv * pv].cpu().numpy(), tr.nl.t[:nv * pv].cpu().numpy(), tr.dpix.t[:nv * pv].cpu().numpy()
+    rng_b = tr.range.t[:nv * pv + 1].cpu().numpy().astype(np.int64)
     # the Z-buffer: every block's list as gids (receive index -> gid through the send buffer)
     gid_of = decode_records(tr.send.t[:tr.last["n_send"]])["gid"]
     srt_b = tr.sorted.t[:int(rng_b[-1])].cpu().numpy().view(np.uint32)
@@ -283,7 +299,7 @@ def test_full_c2_batch_every_pixel():
     def chunk(b0):
         b1 = min(b0 + 512, pv)
         off, ent = oracle.tile_lists(recs, b0, b1, Wt, Ht)
-        f = oracle.render_fwd(recs, off, ent, b0, b1, W, H, (0, 0, 0), gt[v][None], 16, max_paths=16)
+        f = oracle.render_fwd(recs, off, ent, b0, b1, W, H, (0, 0, 0), gt[v][None], nv, max_paths=16)
         T, nl = T_all[b0:b1], nl_all[b0:b1]
         P = f["flips"].shape[2]
         valid = np.arange(P)[None, None, :] < f["n_paths"][..., None]
@@ -309,7 +325,7 @@ def test_full_c2_batch_every_pixel():
 
     n_px = n_multi = 0
     with cf.ThreadPoolExecutor(min(16, os.cpu_count() or 1)) as ex:
-        for v in range(16):
+        for v in check:
             T_all, nl_all = T_b[v * pv:(v + 1) * pv], nl_b[v * pv:(v + 1) * pv]
             dpx_all, rng_all = dpx_b[v * pv:(v + 1) * pv], rng_b[v * pv:(v + 1) * pv + 1]
             recs = oracle.make_records(sc, [cams[v]], "parity")
@@ -322,8 +338,8 @@ def test_full_c2_batch_every_pixel():
             assert all(r[3] for r in res), ("dL/dpix signs", v)
             n_px += pv * 256
             n_multi += multi
-    print("batch: %d pixels, %.1e with more than one valid outcome" % (n_px, n_multi / n_px))
-    assert n_multi <= 1e-3 * n_px
+    print("%s: %d pixels, %.1e with more than one valid outcome" % (cfg, n_px, n_multi / n_px))
+    assert n_multi <= (1e-2 if cfg == "C4" else 1e-3) * n_px
 
 
 def test_full_c2_record_grads_two_views():
