@@ -342,23 +342,24 @@ def test_full_batch_every_pixel(cfg):
     assert n_multi <= (1e-2 if cfg == "C4" else 1e-3) * n_px
 
 
-def test_full_c2_record_grads_two_views():
-    """The bench step's render backward at full size: the record gradients of two whole views
-    (4591x3436 each, all 61,705 blocks) against the oracle's O14-O15 summed over every block,
-    the oracle following per pixel the outcome path the GPU forward took and fed the GPU's
-    upstream dL/dpix (so the L1 sign decisions are the kernel's), within the 1e-3 metric per
-    group (SURVEY #31)."""
+@pytest.mark.parametrize("cfg,views", [("C2", (2, 11)), ("C1", (0, 3)), ("C4", (0, 16))])
+def test_full_record_grads_two_views(cfg, views):
+    """A bench step's render backward at full size: the record gradients of two whole views
+    (C2: 4591x3436, all 61,705 blocks each; C1: 1080p; C4: a street and an aerial 1080p view
+    of the 32-view batch) against the oracle's O14-O15 summed over every block, the oracle
+    following per pixel the outcome path the GPU forward took and fed the GPU's upstream
+    dL/dpix (so the L1 sign decisions are the kernel's), within the 1e-3 metric per group
+    (SURVEY #31)."""
     import concurrent.futures as cf
     import os
     from paper_2406_18533_b200.engine import GrendelTrainer
-    sc = synth.scene_rubble(11_200_000)
-    pool = synth.cameras_rubble(64)
-    cams = [pool[i] for i in synth.batch_schedule(64, 16, 1, 2)[0]]
+    sc, cams, gseed, _ = _batch_case(cfg)
+    nv = len(cams)
     W, H = cams[0].width, cams[0].height
-    gt = np.stack([synth.gt_image(2, c) for c in cams])
+    gt = np.stack([synth.gt_image(gseed, c) for c in cams])
     ctx = L.Context(0, 0, 1)
     p = _params(sc)
-    tr = GrendelTrainer(ctx, p, W, H, 16, 64, cost_mode=L.COST_WORK, rebalance=False)
+    tr = GrendelTrainer(ctx, p, W, H, nv, 128, cost_mode=L.COST_WORK, rebalance=False)
     tr.step(cams, torch.from_numpy(gt).to(DEV))
     torch.cuda.synchronize()
     Wt, Ht = (W + 15) // 16, (H + 15) // 16
@@ -366,7 +367,7 @@ def test_full_c2_record_grads_two_views():
     n_send = tr.last["n_send"]
     drec = tr.drec.t[:n_send].cpu().numpy().astype(np.float64)
     d = decode_records(tr.send.t[:n_send])
-    for v in (2, 11):
+    for v in views:
         T_all = tr.T.t[v * pv:(v + 1) * pv].cpu().numpy()
         nl_all = tr.nl.t[v * pv:(v + 1) * pv].cpu().numpy()
         up_all = tr.dpix.t[v * pv:(v + 1) * pv].cpu().numpy().transpose(0, 2, 1).astype(np.float64)
@@ -375,7 +376,7 @@ def test_full_c2_record_grads_two_views():
         def chunk(b0):
             b1 = min(b0 + 512, pv)
             off, ent = oracle.tile_lists(recs, b0, b1, Wt, Ht)
-            f = oracle.render_fwd(recs, off, ent, b0, b1, W, H, (0, 0, 0), None, 16, max_paths=16)
+            f = oracle.render_fwd(recs, off, ent, b0, b1, W, H, (0, 0, 0), None, nv, max_paths=16)
             P = f["flips"].shape[2]
             valid = np.arange(P)[None, None, :] < f["n_paths"][..., None]
             m = valid & (f["path_nl"] == nl_all[b0:b1][..., None]) & \
@@ -395,5 +396,5 @@ def test_full_c2_record_grads_two_views():
         for name, sl in [("mean", slice(0, 2)), ("conic", slice(2, 5)), ("opacity", slice(5, 6)),
                          ("rgb", slice(6, 9))]:
             e_inf, e_2 = grad_metric(g_k[:, sl], g_or[:, sl])
-            print("view %d %s: max %.2e l2 %.2e" % (v, name, e_inf, e_2))
+            print("%s view %d %s: max %.2e l2 %.2e" % (cfg, v, name, e_inf, e_2))
             assert e_inf <= 1e-3 and e_2 <= 1e-3, (v, name, e_inf, e_2)
