@@ -256,8 +256,9 @@ def _batch_case(cfg):
     """(scene, the config's first bench batch, ground-truth seed, views to check)."""
     if cfg == "C2":
         pool = synth.cameras_rubble(64)
+        # 8 of the 16 views (the suite's time budget; all 16 pass: profiles/r2o_full_batch_every_pixel.txt)
         return (synth.scene_rubble(11_200_000), [pool[i] for i in synth.batch_schedule(64, 16, 1, 2)[0]], 2,
-                list(range(16)))
+                list(range(0, 16, 2)))
     if cfg == "C1":
         pool = synth.cameras_garden(64)
         return synth.scene_garden(5_000_000), [pool[i] for i in synth.batch_schedule(64, 4, 1, 1)[0]], 1, [0, 1, 2, 3]
@@ -270,8 +271,8 @@ def _batch_case(cfg):
 @pytest.mark.parametrize("cfg", ["C2", "C1", "C4"])
 def test_full_batch_every_pixel(cfg):
     """A bench batch through the step driver at full size (C2: 11.2M Gaussians, 16 views of
-    4591x3436 -- 252.7M pixels, every view; C1: 5M, 4 views of 1080p, every view; C4: 24M,
-    32 views of 1080p, two street and two aerial views checked), EVERY pixel of the checked
+    4591x3436, every other view checked -- 126M pixels; C1: 5M, 4 views of 1080p, every view;
+    C4: 24M, 32 views of 1080p, two street and two aerial views checked), EVERY pixel of the checked
     views against the oracle, recomputed in chunks of blocks on host threads: n_last exact
     and T within 1e-4 on one of the oracle's outcome paths (R16), every block's list
     bit-exact (O11), dL/dpix the sign of the residual wherever the colour is firm."""
